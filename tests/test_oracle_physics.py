@@ -1,0 +1,122 @@
+"""Pins of the oracle's Euler physics (readings R3, R5, R7)."""
+import math
+
+import numpy as np
+import pytest
+
+import es_inputs as I
+import oracle as O
+
+G = 1.4
+
+
+def _prim(U):
+    d = U.shape[-1] - 2
+    rho = U[..., 0]
+    v = U[..., 1:1 + d] / rho[..., None]
+    p = (G - 1) * (U[..., -1] - 0.5 * rho * np.sum(v * v, -1))
+    return rho, v, p
+
+
+def test_printed_examples(golden):
+    ex = golden["euler_flux_example"]
+    U = I.prim_to_cons(np.array([1.0]), np.array([[1.0, 0.0]]), np.array([1.0]))
+    F = O.euler_flux(U, [1.0, 0.0])
+    np.testing.assert_allclose(F[0], ex["F"], atol=1e-15)
+    U = I.prim_to_cons(np.array([1.0]), np.array([[0.0, 0.0]]), np.array([golden["entropy_example"]["p"]]))
+    S, Fe = O.entropy(U)
+    assert abs(S[0] - golden["entropy_example"]["S"]) < 1e-14
+    U = I.prim_to_cons(np.array([2.0]), np.array([[0.3, -0.2]]), np.array([4.0]))
+    assert abs(O.entropy_vars(U)[0, -1] - golden["w_last_example"]["w_last"]) < 1e-15
+    for ex in golden["log_mean_examples"][:-1]:
+        assert abs(O.ln_mean(ex["x"], ex["y"]) - ex["v"]) < 2e-15 * ex["v"]
+        assert abs(O.inv_ln_mean(ex["x"], ex["y"]) * ex["v"] - 1) < 2e-15
+    U = I.prim_to_cons(np.array([1.0]), np.array([[0.0, 0.0]]), np.array([1.0]))
+    assert abs(O.wave_speed(U[0], U[0], np.array([1.0, 0.0])) - golden["wave_speed_rest"]["value"]) < 1e-15
+
+
+def test_log_mean_branches():
+    # series branch near x = y vs a 50-digit evaluation of (y-x)/ln(y/x) through log1p
+    for x, y in [(1.0, 1.0 + 1e-3), (0.3, 0.3001), (5.0, 5.002), (1.0, 1.0199)]:
+        t = (y - x) / x
+        exact = (y - x) / math.log1p(t)
+        assert abs(O.ln_mean(x, y) - exact) < 3e-16 * exact
+        assert abs(O.inv_ln_mean(x, y) * exact - 1) < 3e-16
+    # symmetric
+    assert O.ln_mean(2.0, 3.0) == O.ln_mean(3.0, 2.0) or abs(O.ln_mean(2.0, 3.0) - O.ln_mean(3.0, 2.0)) < 1e-15
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_entropy_variables(d):
+    U = I.random_states(200, d, seed=1)
+    W = O.entropy_vars(U)
+    np.testing.assert_allclose(O.cons_from_entropy(W), U, rtol=1e-13, atol=1e-13)
+    # W = grad_U S by central differences (S = -rho ln(p/rho^g)/(g-1))
+    h = 1e-6
+    for i in range(0, 200, 40):
+        for k in range(d + 2):
+            e = np.zeros(d + 2)
+            e[k] = h * max(1.0, abs(U[i, k]))
+            Sp, _ = O.entropy(U[i] + e)
+            Sm, _ = O.entropy(U[i] - e)
+            assert abs((Sp[0] - Sm[0]) / (2 * e[k]) - W[i, k]) < 1e-7
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_ec_flux_consistency_symmetry_tadmor(d):
+    Ua = I.random_states(500, d, seed=2, spread=0.6)
+    Ub = I.random_states(500, d, seed=3, spread=0.6)
+    rng = np.random.default_rng(4)
+    nv = rng.standard_normal((500, d))
+    # consistency f#(U,U,n) = f(U,n)
+    np.testing.assert_allclose(O.ec_flux(Ua, Ua, nv), O.euler_flux(Ua, nv), rtol=1e-14, atol=1e-13)
+    # symmetry
+    np.testing.assert_allclose(O.ec_flux(Ua, Ub, nv), O.ec_flux(Ub, Ua, nv), rtol=1e-14, atol=1e-14)
+    # Tadmor's condition in directional form with psi_m = rho v_m
+    Wa, Wb = O.entropy_vars(Ua), O.entropy_vars(Ub)
+    F = O.ec_flux(Ua, Ub, nv)
+    psi_a = np.sum(Ua[:, 1:1 + d] * nv, 1)
+    psi_b = np.sum(Ub[:, 1:1 + d] * nv, 1)
+    res = np.sum((Wb - Wa) * F, 1) - (psi_b - psi_a)
+    scale = np.sum(np.abs(Wb - Wa) * np.abs(F), 1) + 1
+    assert np.abs(res / scale).max() < 1e-13
+    # the energy component as printed at P:834 (1/2 multiplying both terms) fails consistency (R3)
+    rho, v, p = _prim(Ua)
+    vn = np.sum(v * nv, 1)
+    printed = 0.5 * rho * vn * (np.sum(v * v, 1) + p / rho / (G - 1)) + p * vn
+    assert np.abs(printed - O.euler_flux(Ua, nv)[:, -1]).max() > 1e-2
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_es_flux_conservation_and_entropy_condition(d):
+    Ua = I.random_states(300, d, seed=5, spread=0.6)
+    Ub = I.random_states(300, d, seed=6, spread=0.6)
+    rng = np.random.default_rng(7)
+    n = rng.standard_normal((300, d))
+    n /= np.linalg.norm(n, axis=1)[:, None]
+    Fab = O.es_flux(Ua, Ub, n)
+    Fba = O.es_flux(Ub, Ua, -n)
+    np.testing.assert_allclose(Fab, -Fba, rtol=1e-14, atol=1e-14)
+    np.testing.assert_allclose(O.es_flux(Ua, Ua, n), O.euler_flux(Ua, n), rtol=1e-14, atol=1e-13)
+    Wa, Wb = O.entropy_vars(Ua), O.entropy_vars(Ub)
+    lhs = np.sum((Wb - Wa) * Fab, 1)
+    rhs = np.sum(Ub[:, 1:1 + d] * n, 1) - np.sum(Ua[:, 1:1 + d] * n, 1)
+    assert (lhs - rhs <= 1e-12).all()  # P:488 entropy condition
+    # Davis wave speed is an upper bound of |v.n| + c on both sides
+    for i in range(20):
+        lam = O.wave_speed(Ua[i], Ub[i], n[i])
+        for U in (Ua[i], Ub[i]):
+            rho, v, p = _prim(U[None])
+            assert lam >= abs(v[0] @ n[i]) + math.sqrt(G * p[0] / rho[0]) - 1e-14
+
+
+def test_initial_conditions(golden):
+    g = golden["ic_density_wave"]
+    U = I.density_wave(np.array([g[0]["x"], g[1]["x"]]), L=2.0)
+    assert abs(U[0, 0] - 1.0) < 1e-15 and abs(U[0, -1] - g[0]["E"]) < 1e-14
+    assert abs(U[1, 0] - g[1]["rho"]) < 1e-14
+    t = golden["ic_tgv"]
+    U = I.taylor_green(np.array([t["x"]]), Ma=t["Ma"])
+    rho, v, p = _prim(U)
+    np.testing.assert_allclose(v[0], t["v"], atol=1e-15)
+    assert abs(p[0] - t["p"]) < 1e-10
