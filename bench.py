@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native ES modal DSEM right-hand side (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl reference]
+
+A *step* is one classical RK4 step of the whole hot path (4 right-hand sides: entropy projection,
+line-wise flux differencing, facet correction, interface flux, lifting, weight-adjusted inverse,
+fused stage update) over the configuration's mesh.  The default workload is BASELINE.json config
+C5: 3D Euler, curved tetrahedra, p = 8, 32^3 x 6 = 196 608 elements, Taylor-Green vortex Ma 0.1,
+entropy-stable interface flux.  Multi-GPU (torchrun): elements are partitioned into contiguous
+slabs, face-trace halos go over NCCL; the timing is the max over ranks (CUDA events).
+
+value = EC two-point flux evaluations per second, whole job (line-wise volume + facet-correction
+pairs actually evaluated).  DOF.RHS/s and the Eq.-num_fluxes-equivalent rate
+are reported alongside.  Inputs are synthetic (analytic initial data projected by the library).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (dim, M, p, L, warp, initial state, interface flux, description)
+    "C1": (2, 4, 2, 1.0, "none", "vortex", 1, "2D Euler p=2 affine triangles, 32 elements, isentropic vortex, ES"),
+    "C2": (2, 32, 4, 2.0, "bj", "density_wave", 1, "2D Euler p=4 curved triangles, 2048 elements, density wave, ES"),
+    "C3": (2, 64, 10, 2.0, "bj", "vortex", 1, "2D Euler p=10 curved triangles, 8192 elements, isentropic vortex, ES"),
+    "C4": (3, 16, 4, 2 * math.pi, "bj", "tgv", 0, "3D Euler p=4 curved tetrahedra, 24576 elements, TGV Ma0.1, EC"),
+    "C5": (3, 32, 8, 2 * math.pi, "bj", "tgv", 1,
+           "3D Euler p=8 curved tetrahedra, 196608 elements, TGV Ma0.1, ES, RK4 step"),
+}
+
+# ---- algorithmic FP64 operation counts: +,-,*,/,sqrt,log,exp = 1 flop ----
+FLUX_FLOPS = {2: 67, 3: 81}            # Ranocha EC flux, Taylor branch of both log means
+VOL_NORMAL_FLOPS = {2: 12, 3: 24}      # n_ij from the line operators and averaged metrics
+FAC_NORMAL_FLOPS = {2: 10, 3: 21}      # <J n> of the facet correction
+ACC_FLOPS = {2: 8, 3: 10}              # -F to node i, +F to node j (or C^T 1)
+IFACE_FLOPS = {2: 110, 3: 140}         # EC flux + Davis wave speed + LF jump + B J_f scaling
+
+
+def counts(dim, p):
+    n = p + 1
+    if dim == 2:
+        vol, fac, eq56 = p * n * n, 3 * n * n, 3 * n * n * (p + 2) // 2
+        iface = 3 * n
+        Np, Nq = n * (n + 1) // 2, n * n
+        sf = Np * n + n * n * n  # MACs per sum-factorised V (or V^T) apply, one variable
+    else:
+        vol, fac, eq56 = 3 * p * n ** 3 // 2, 3 * n ** 3 + n ** 4, 4 * n ** 4
+        iface = 4 * n * n
+        Np, Nq = n * (n + 1) * (n + 2) // 6, n ** 3
+        sf = Np * n + (n * (n + 1) // 2) * n * n + n ** 4
+    return dict(vol=vol, fac=fac, eq56=eq56, iface=iface, Np=Np, Nq=Nq, sf=sf)
+
+
+def rhs_kernel_flops(dim, p):
+    """algorithmic flops of the flux-differencing kernel (K2) per element and RHS"""
+    c = counts(dim, p)
+    nc = dim + 2
+    f = c["vol"] * (FLUX_FLOPS[dim] + VOL_NORMAL_FLOPS[dim] + ACC_FLOPS[dim])
+    f += c["fac"] * (FLUX_FLOPS[dim] + FAC_NORMAL_FLOPS[dim] + ACC_FLOPS[dim])
+    f += c["iface"] * IFACE_FLOPS[dim]
+    f += 2 * 3 * nc * c["sf"]  # V^T, V, V^T of the weight-adjusted inverse
+    f += nc * c["Nq"] * (2 * (dim + 1) + 1)  # lifting R^T s and W/J~ scaling
+    return f
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def fp64_peak_tflops(sm_mhz=None):
+    """FP64 CUDA-core peak from the unit counts: 148 SMs x 64 DFMA/clk x 2 flop x clock
+    (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz)."""
+    mhz = sm_mhz or measured_peaks().get("sm_max_mhz", 1965.0)
+    return 148 * 64 * 2 * mhz * 1e6 / 1e12
+
+
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (200 ms)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        sm, mx, reasons = [], 1965.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower() in ("active", "yes", "1"):
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def initial_state(ctx, torch, kind, d, L):
+    import es_inputs as I
+    x = torch.empty((ctx.nloc, ctx.Nq, d), dtype=torch.float64, device="cuda")
+    ctx.node_coords(x)
+    ctx.synchronize()
+    xn = x.cpu().numpy()
+    un = {"tgv": lambda: I.taylor_green(xn, Ma=0.1), "density_wave": lambda: I.density_wave(xn, L),
+          "vortex": lambda: I.isentropic_vortex(xn, L)}[kind]()
+    um = torch.empty((ctx.nloc, d + 2, ctx.Np), dtype=torch.float64, device="cuda")
+    ctx.project_nodal(torch.from_numpy(np.ascontiguousarray(un)).cuda(), um)
+    ctx.synchronize()
+    return um, xn, un
+
+
+def cfl_dt(xn, un, d, L, M, p, cfl=0.1, gamma=1.4):
+    """R16: dt = CFL h / ((2p+1) max(|v| + c)) from the initial nodal state, h = L/M."""
+    rho = un[..., 0]
+    v = un[..., 1:1 + d] / rho[..., None]
+    pr = (gamma - 1) * (un[..., -1] - 0.5 * rho * np.sum(v * v, -1))
+    smax = float(np.max(np.sqrt(np.sum(v * v, -1)) + np.sqrt(gamma * pr / rho)))
+    return cfl * (L / M) / ((2 * p + 1) * smax)
+
+
+def cpu_baseline(cfg, budget_s=20.0):
+    """The oracle as it stands (test infrastructure), timed on this host's cores on a bounded
+    sample of the workload's elements; returns flux evals/s of the oracle's line-wise RHS."""
+    import es_inputs as I
+    import oracle as O
+    dim, M, p, L, warp, kind, fm, _ = CONFIGS[cfg]
+    mesh = I.split_cartesian(dim, M, L)
+    w = {"bj": I.bj_warp(dim, L, M), "none": None}.get(warp)
+    u = I.modal_state_from_centroids(mesh, p, kind, seed=0, amp=1e-3)
+    ne = len(mesh["elem_vertices"])
+    cores = os.cpu_count() or 1
+    nsample = min(ne, 8 * cores)
+    sample = np.arange(nsample, dtype=np.int64)
+    om = O.Mesh(mesh, p, warp=w, active=sample)
+    t0 = time.perf_counter()
+    _, st = om.rhs(u, flux_mode=fm, variant=1, elems=sample, nthreads=cores)
+    dt1 = time.perf_counter() - t0
+    reps = max(1, min(20, int(budget_s / max(dt1, 1e-3))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        _, st = om.rhs(u, flux_mode=fm, variant=1, elems=sample, nthreads=cores)
+    dt = (time.perf_counter() - t0) / reps
+    evals = st.volume_pairs + st.facet_pairs
+    return {"value": evals / dt, "unit": "flux_evals/s", "cores": cores, "kind": "oracle",
+            "sample": f"{cfg}: one RHS (line-wise variant, projection of sample + neighbours) on the first "
+                      f"{nsample} of {ne} elements, OpenMP {cores} threads, mean of {reps}",
+            "seconds_per_rhs_sample": dt}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as the reference arm, on this arm's config/metric/unit."""
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return 0
+    cfg = args.config
+    cb = None
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(cfg, budget_s=2.0)
+        if i >= args.warmup:
+            vals.append(r["value"])
+        cb = r
+    value = statistics.mean(vals)
+    line = {"metric": "EC two-point flux evals/s", "value": value, "unit": "flux_evals/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_rhs_sample"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": CONFIGS[cfg][7], "sample": cb["sample"]},
+            "cpu_baseline": {"value": value, "unit": "flux_evals/s", "cores": cb["cores"], "kind": "oracle",
+                             "sample": cb["sample"]},
+            "e2e": {"value": value, "unit": "flux_evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run(args):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = _dist_env()
+    if world != args.gpus:
+        world = max(world, 1)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import es_inputs as I
+    import paper_2312_07874_b200 as es
+    dim, M, p, L, warp, kind, fm, desc = CONFIGS[args.config]
+    mesh = I.split_cartesian(dim, M, L)
+    w = {"bj": I.bj_warp(dim, L, M), "none": None}.get(warp)
+    nccl_id = None
+    if world > 1:
+        import ctypes
+        lib = ctypes.CDLL("libnccl.so.2")
+
+        class Uid(ctypes.Structure):
+            _fields_ = [("internal", ctypes.c_char * 128)]
+        uid = Uid()
+        if rank == 0:
+            lib.ncclGetUniqueId(ctypes.byref(uid))
+        t = torch.frombuffer(bytearray(uid.internal if rank == 0 else bytes(128)), dtype=torch.uint8).cuda()
+        dist.broadcast(t, 0)
+        nccl_id = bytes(t.cpu().numpy().tobytes())
+    stream = torch.cuda.Stream()
+    t_setup = time.perf_counter()
+    ctx = es.Context(mesh, p, warp=w, interface_flux=fm, rank=rank, world=world, nccl_id=nccl_id,
+                     stream=stream.cuda_stream, device=local)
+    t_setup = time.perf_counter() - t_setup
+    um, xn, un = initial_state(ctx, torch, kind, dim, L)
+    dt = cfl_dt(xn, un, dim, L, M, p)
+    if world > 1:
+        dtt = torch.tensor([dt], device="cuda", dtype=torch.float64)
+        dist.all_reduce(dtt, op=dist.ReduceOp.MIN)
+        dt = float(dtt.item())
+    ctx.set_state(um)
+    ctx.synchronize()
+    c = counts(dim, p)
+    ne = len(mesh["elem_vertices"])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            ctx.step(dt, 1)
+    ctx.synchronize()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ctx.reset_launch_count()
+    ctx.timing_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        ctx.step(dt, 1)
+    e1.record(stream)
+    ctx.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    k2_ms, k2_n = ctx.timing_read(1)
+    k1_ms, k1_n = ctx.timing_read(0)
+    launches = ctx.launch_count()
+    ctx.timing_enable(False)
+    if world > 1:
+        tt = torch.tensor([ms, k2_ms / max(k2_n, 1)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt[0].item())
+    ms_step = ms / args.steps
+    rhs_per_step = 4
+    evals_step = rhs_per_step * ne * (c["vol"] + c["fac"])
+    value = evals_step / (ms_step * 1e-3)
+    dof = ne * c["Np"] * (dim + 2)
+    # ---- end to end through the public API with host buffers ----
+    state = torch.empty_like(um)
+    ctx.get_state(state)
+    ctx.synchronize()
+    host_in = state.cpu().pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    dev = torch.empty_like(um)
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    esteps = max(1, min(args.steps, 3))
+    with torch.cuda.stream(stream):
+        for _ in range(esteps):
+            dev.copy_(host_in, non_blocking=True)
+            ctx.set_state(dev)
+            ctx.step(dt, 1)
+            ctx.get_state(dev)
+            host_out.copy_(dev, non_blocking=True)
+    e3.record(stream)
+    ctx.synchronize()
+    barrier()
+    e2e_ms = e2.elapsed_time(e3) / esteps
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt[0].item())
+    e2e_value = evals_step / (e2e_ms * 1e-3)
+    nbytes = host_in.numel() * 8
+    # ---- roofline of the dominant kernel (K2) ----
+    k2_avg_ms = k2_ms / max(k2_n, 1)
+    elems_per_launch = ne / world if world == 1 else ne / world / 2  # interior/boundary split
+    k2_flops = rhs_kernel_flops(dim, p) * (ne / world) / (k2_n / max(1, args.steps * 4))
+    achieved = k2_flops / (k2_avg_ms * 1e-3) / 1e12
+    peak = fp64_peak_tflops()
+    line = {
+        "metric": "EC two-point flux evals/s", "value": value, "unit": "flux_evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {desc}", "n_elements": ne, "p": p, "dim": dim,
+                   "dof": dof, "dt": dt, "l2": "inputs larger than L2 (no flush needed)" if dof * 8 > 126e6 else
+                   "inputs smaller than L2",
+                   "parallelism": f"element partition over {world} GPU(s), NCCL face-trace halo",
+                   "setup_s": t_setup},
+        "dof_rhs_per_s": dof * rhs_per_step / (ms_step * 1e-3),
+        "rhs_per_s": rhs_per_step / (ms_step * 1e-3),
+        "eq56_equivalent_evals_per_s": rhs_per_step * ne * c["eq56"] / (ms_step * 1e-3),
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "rhs_kernel (K2)",
+                     "kernel_ms_avg": k2_avg_ms, "kernel_share_of_step": k2_ms / args.steps / ms_step,
+                     "projection_kernel_ms_avg": k1_ms / max(k1_n, 1),
+                     "peak_basis": "148 SM x 64 DFMA/clk x 2 x sm_max_mhz (DESIGN.md 6)"},
+        "e2e": {"value": e2e_value, "unit": "flux_evals/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                "api": "cudaMemcpyAsync(pinned->device) + es_set_state + es_step + es_get_state + copy back"},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args.config)
+            line["cpu_baseline"].pop("seconds_per_rhs_sample", None)
+        except Exception as ex:  # pragma: no cover
+            line["cpu_baseline"] = {"error": str(ex)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,141 @@
+/*
+ * es.h -- C ABI of the B200-native (sm_100a) entropy-stable modal DSEM right-hand side.
+ *
+ * Method: Montoya & Zingg, arXiv 2312.07874 (PAPER.md, cited as P:<line> [label]).
+ *   es_rhs evaluates d u~/dt = M~^{-1} V^T r (P:446 [eq:dudt_modal]) with r the entropy-stable
+ *   flux-differencing residual of P:520 [eq:entropy_stable] including the facet correction of P:525
+ *   [eq:facet_correction], for the compressible Euler equations with Ranocha's
+ *   entropy-conservative two-point flux (energy term per DESIGN.md reading R3) in the volume
+ *   and facet-correction terms and the EC or ES (EC + local Lax-Friedrichs with Davis wave speed,
+ *   P:491) interface flux.  Volume fluxes are evaluated line by line in collapsed coordinates
+ *   (P:572), one evaluation per node pair on each eta_k line.
+ *
+ * Conventions (all functions):
+ *   - reals are IEEE FP64; arrays are C-contiguous;
+ *   - modal arrays are the LOCAL block u[k_local][e][i]: element k_local in [0, n_local), conserved
+ *     variable e in {rho, rho v_1..rho v_d, E} (N_c = d+2), PKD mode i in [0, N_p*) in the
+ *     alpha1-major nested order (for a1 in 0..p: for a2 in 0..p-a1: [for a3 in 0..p-a1-a2]);
+ *   - "device pointer" = CUDA global memory of the context's device (e.g. torch tensor data_ptr());
+ *     "host pointer" = ordinary or pinned host memory;
+ *   - the caller owns every buffer it passes; the library copies what it keeps and owns all of its
+ *     device allocations (geometry, tables, traces, RK state);
+ *   - every function returns es_status; no C++ exception crosses the ABI.  After ES_ERR_CUDA or
+ *     ES_ERR_NCCL the context is poisoned: every later call returns the same code.  Output buffers
+ *     are undefined after a failed call.  es_last_error() returns a context-owned message;
+ *   - calls on one context are not thread safe; one context per process / GPU;
+ *   - es_rhs / es_step are asynchronous on the context stream unless opt.check_admissibility.
+ */
+#ifndef ES_B200_H
+#define ES_B200_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ES_OK = 0,
+  ES_ERR_CONFIG = 2,        /* unsupported (dim, p) or inconsistent options */
+  ES_ERR_INADMISSIBLE = 3,  /* rho <= 0 or p <= 0 at a projected node */
+  ES_ERR_VERIFY = 4,        /* mesh check failed: J~ <= 0, unmatched face */
+  ES_ERR_ARG = -1,          /* null / out-of-range argument */
+  ES_ERR_CUDA = -5,
+  ES_ERR_NCCL = -6,
+  ES_ERR_OOM = -7
+} es_status;
+
+typedef struct es_context es_context;
+
+/* Periodic conforming simplicial mesh.  Copied during es_setup. */
+typedef struct {
+  int dim;                          /* 2 (triangles) or 3 (tetrahedra) */
+  int64_t n_elements;               /* global element count N_e */
+  const int64_t* elem_vertices;     /* host [N_e][dim+1] periodic global vertex ids in CANONICAL
+                                       order: ascending id, first two swapped if the corner simplex
+                                       is negatively oriented (R11) */
+  const double* elem_vertex_coords; /* host [N_e][dim+1][dim] unwrapped corner coordinates */
+  const double* period;             /* host [dim] periodic lengths (fully periodic meshes) */
+} es_mesh;
+
+/* Geometry map (P:327 [eq:poly_mapping]): called ONCE by es_setup with the affine images of the
+ * degree-p equispaced lattice mapping nodes of the local elements, x_in host [n][dim] -> x_out host
+ * [n][dim].  The returned positions define the isoparametric mapping.  */
+typedef void (*es_map_fn)(void* user, int64_t n, const double* x_in, double* x_out);
+
+typedef struct {
+  double gamma;                         /* ratio of specific heats (1.4) */
+  int interface_flux;                   /* 0 = entropy conservative, 1 = entropy stable */
+  int rank, world;                      /* local elements [rank*N_e/world, (rank+1)*N_e/world) */
+  const unsigned char* nccl_unique_id;  /* 128-byte ncclUniqueId (world > 1), broadcast by caller */
+  void* cuda_stream;                    /* cudaStream_t to launch on; NULL = a library stream */
+  int device;                           /* CUDA device ordinal */
+  int check_admissibility;              /* 1: es_rhs synchronises and returns ES_ERR_INADMISSIBLE */
+} es_options;
+
+/* Builds tables, geometry (exact metrics in 2D, conservative curl metrics in 3D, P:345-364;
+ * Jacobian interpolant P:448-452), connectivity and the halo plan; uploads everything to the
+ * device.  p in [1, 10] for dim 2 and [1, 8] for dim 3 (q = p).  */
+es_status es_setup(es_context** ctx, const es_mesh* mesh, int p, es_map_fn map, void* map_user,
+                   const es_options* opt);
+void es_destroy(es_context* ctx);
+const char* es_last_error(const es_context* ctx);
+
+/* Sizes: N_p*, N_q, N_qf per facet, local element count and first global element. */
+es_status es_sizes(const es_context* ctx, int* Np, int* Nq, int* Nqf, int64_t* n_local,
+                   int64_t* first_element);
+
+/* d u~/dt for the local block: u_modal, dudt_modal device pointers [n_local][N_c][N_p*].
+ * Includes the face-trace halo exchange (NCCL) when world > 1. */
+es_status es_rhs(es_context* ctx, const double* u_modal, double* dudt_modal);
+/* Same, with HOST buffers: host->device copy, es_rhs, device->host copy, synchronised. */
+es_status es_rhs_host(es_context* ctx, const double* u_modal_host, double* dudt_modal_host);
+
+/* Library-owned RK state: copy in/out (device pointers, [n_local][N_c][N_p*]). */
+es_status es_set_state(es_context* ctx, const double* u_modal);
+es_status es_get_state(es_context* ctx, double* u_modal);
+/* nsteps classical RK4 steps of size dt on the library state (R17). */
+es_status es_step(es_context* ctx, double dt, int nsteps);
+
+/* Entropy production sum_k sum_e w^T r = d/dt sum_k 1^T W J~ s, global over ranks,
+ * its absolute scale sum |w_i r_i| (computed modally as sum |w~_i (V^T r)_i|), and the global
+ * conservation residuals sum_k 1^T r^(e), conservation[N_c].  u_modal: device pointer.
+ * Synchronous; includes an ncclAllReduce when world > 1.  Any output pointer may be NULL. */
+es_status es_entropy_production(es_context* ctx, const double* u_modal, double* rate,
+                                double* abs_scale, double* conservation);
+
+/* Two-point flux evaluations per element and RHS (integers, exact): line-wise volume pairs,
+ * facet-correction pairs, the Eq. num_fluxes count, interface evaluations per element. */
+es_status es_flux_counts(const es_context* ctx, int64_t* volume_pairs_per_el,
+                         int64_t* facet_pairs_per_el, int64_t* eq56_per_el,
+                         double* interface_per_el);
+
+/* Physical coordinates of the volume quadrature nodes, device pointer [n_local][N_q][dim]. */
+es_status es_node_coords(es_context* ctx, double* x_dev);
+/* Reference L2 projection u~ = V^T W u (M = I): u_nodal device [n_local][N_q][N_c] ->
+ * u_modal device [n_local][N_c][N_p*].  (Initial data; R18.) */
+es_status es_project_nodal(es_context* ctx, const double* u_nodal, double* u_modal);
+
+/* Geometry of one local element copied to HOST buffers (tests): G [N_q][dim][dim] (G_lm),
+ * Jn [N_f][N_qf][dim] = G^T nhat at facet nodes, Jt [N_q] = J~.  NULL = skip. */
+es_status es_element_geometry(es_context* ctx, int64_t local_element, double* G, double* Jn,
+                              double* Jt);
+
+/* Synchronise the context stream (and report asynchronous CUDA errors). */
+es_status es_synchronize(es_context* ctx);
+/* Stream the context launches on (cudaStream_t as void*). */
+void* es_stream(const es_context* ctx);
+
+/* Kernel launch accounting: number of library kernels launched since the last reset. */
+int64_t es_launch_count(const es_context* ctx);
+void es_reset_launch_count(es_context* ctx);
+
+/* Per-launch timing of the flux-differencing kernel (CUDA events on the context stream):
+ * es_timing_enable(ctx, 1) starts recording; es_timing_read returns the summed milliseconds and
+ * the number of launches of each kernel class since enabling: 0 = trace/projection kernel,
+ * 1 = flux-differencing + surface + inverse-mass kernel. */
+es_status es_timing_enable(es_context* ctx, int on);
+es_status es_timing_read(es_context* ctx, int kernel_class, double* total_ms, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

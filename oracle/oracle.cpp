@@ -29,27 +29,30 @@ const double PI = 3.14159265358979323846;
 // 1D: normalised Jacobi polynomials, computed with the three-term recurrence for the
 // orthonormal family (Hesthaven & Warburton App. A, cited at P:144).
 // ------------------------------------------------------------------------------------------------
-struct JacobiRec {
+template <class T>
+struct JacobiRecT {
   // P_{i+1} = ((x - bn[i]) P_i - ao[i] P_{i-1}) / an[i]
-  double p0, c1;
-  vector<double> an, bn, ao;
+  T p0, c1;
+  vector<T> an, bn, ao;
 };
+using JacobiRec = JacobiRecT<double>;
 
-JacobiRec jacobi_rec(int nmax, double a, double b) {
-  JacobiRec r;
-  r.p0 = std::sqrt(std::pow(2.0, -a - b - 1.0) * std::tgamma(a + b + 2.0) /
-                   (std::tgamma(a + 1.0) * std::tgamma(b + 1.0)));
-  r.c1 = std::sqrt((a + b + 3.0) / ((a + 1.0) * (b + 1.0)));
-  double aold = 2.0 / (2.0 + a + b) * std::sqrt((a + 1.0) * (b + 1.0) / (a + b + 3.0));
-  r.an.assign(nmax + 1, 0.0);
-  r.bn.assign(nmax + 1, 0.0);
-  r.ao.assign(nmax + 1, 0.0);
+template <class T>
+JacobiRecT<T> jacobi_recT(int nmax, T a, T b) {
+  JacobiRecT<T> r;
+  r.p0 = std::sqrt(std::pow((T)2.0, -a - b - (T)1.0) * std::tgamma(a + b + (T)2.0) /
+                   (std::tgamma(a + (T)1.0) * std::tgamma(b + (T)1.0)));
+  r.c1 = std::sqrt((a + b + (T)3.0) / ((a + (T)1.0) * (b + (T)1.0)));
+  T aold = (T)2.0 / ((T)2.0 + a + b) * std::sqrt((a + (T)1.0) * (b + (T)1.0) / (a + b + (T)3.0));
+  r.an.assign(nmax + 1, (T)0.0);
+  r.bn.assign(nmax + 1, (T)0.0);
+  r.ao.assign(nmax + 1, (T)0.0);
   for (int i = 1; i <= nmax; ++i) {
-    double h1 = 2.0 * i + a + b;
-    double anew = 2.0 / (h1 + 2.0) *
-                  std::sqrt((i + 1.0) * (i + 1.0 + a + b) * (i + 1.0 + a) * (i + 1.0 + b) /
-                            ((h1 + 1.0) * (h1 + 3.0)));
-    double bnew = -(a * a - b * b) / (h1 * (h1 + 2.0));
+    T h1 = (T)2.0 * i + a + b;
+    T anew = (T)2.0 / (h1 + (T)2.0) *
+             std::sqrt(((T)i + 1) * ((T)i + 1 + a + b) * ((T)i + 1 + a) * ((T)i + 1 + b) /
+                       ((h1 + (T)1.0) * (h1 + (T)3.0)));
+    T bnew = -(a * a - b * b) / (h1 * (h1 + (T)2.0));
     r.an[i] = anew;
     r.bn[i] = bnew;
     r.ao[i] = aold;
@@ -57,6 +60,7 @@ JacobiRec jacobi_rec(int nmax, double a, double b) {
   }
   return r;
 }
+JacobiRec jacobi_rec(int nmax, double a, double b) { return jacobi_recT<double>(nmax, a, b); }
 
 double jacobi(int n, double a, double b, double x) {
   JacobiRec r = jacobi_rec(n, a, b);
@@ -196,25 +200,25 @@ double pkd_eta(int d, const int* al, const double* e) {
 // tri:  phi = sqrt2 2^a1 H_a1^(0,0)(s,t) P_a2^(2a1+1,0)(xi2),  t=(1-xi2)/2, s=(1+xi1)-t
 // tet:  phi = 2 sqrt2 4^a1 2^a2 H_a1^(0,0)(s1,t1) H_a2^(2a1+1,0)(s2,t2) P_a3^(2a1+2a2+2,0)(xi3),
 //       t1=(-xi2-xi3)/2, s1=(1+xi1)-t1, t2=(1-xi3)/2, s2=(1+xi2)-t2.
-void homog(int n, double a, double b, double s, const double* ds, double t, const double* dt, int d,
-           double& H, double* dH) {
-  JacobiRec r = jacobi_rec(n + 1, a, b);
-  double Hm = r.p0, dHm[3] = {0, 0, 0};
+template <class T>
+void homog(int n, T a, T b, T s, const T* ds, T t, const T* dt, int d, T& H, T* dH) {
+  JacobiRecT<T> r = jacobi_recT<T>(n + 1, a, b);
+  T Hm = r.p0, dHm[3] = {0, 0, 0};
   if (n == 0) {
     H = Hm;
     for (int k = 0; k < d; ++k) dH[k] = 0.0;
     return;
   }
-  double c = r.p0 * r.c1;
-  double Hc = c * ((a + b + 2.0) * s / 2.0 + (a - b) * t / 2.0);
-  double dHc[3];
-  for (int k = 0; k < d; ++k) dHc[k] = c * ((a + b + 2.0) * ds[k] / 2.0 + (a - b) * dt[k] / 2.0);
+  T c = r.p0 * r.c1;
+  T Hc = c * ((a + b + (T)2.0) * s / (T)2.0 + (a - b) * t / (T)2.0);
+  T dHc[3];
+  for (int k = 0; k < d; ++k) dHc[k] = c * ((a + b + (T)2.0) * ds[k] / (T)2.0 + (a - b) * dt[k] / (T)2.0);
   for (int i = 1; i < n; ++i) {
-    double Hn = ((s - r.bn[i] * t) * Hc - r.ao[i] * t * t * Hm) / r.an[i];
-    double dHn[3];
+    T Hn = ((s - r.bn[i] * t) * Hc - r.ao[i] * t * t * Hm) / r.an[i];
+    T dHn[3];
     for (int k = 0; k < d; ++k)
       dHn[k] = ((ds[k] - r.bn[i] * dt[k]) * Hc + (s - r.bn[i] * t) * dHc[k] -
-                r.ao[i] * (2.0 * t * dt[k] * Hm + t * t * dHm[k])) /
+                r.ao[i] * ((T)2.0 * t * dt[k] * Hm + t * t * dHm[k])) /
                r.an[i];
     Hm = Hc;
     Hc = Hn;
@@ -227,30 +231,44 @@ void homog(int n, double a, double b, double s, const double* ds, double t, cons
   for (int k = 0; k < d; ++k) dH[k] = dHc[k];
 }
 
-void pkd_cart(int d, const int* al, const double* x, double& v, double* g) {
+template <class T>
+T jacobiT(int n, T a, T b, T x) {
+  T H, dH[1];
+  T one = 1.0, zero = 0.0;
+  homog<T>(n, a, b, x, &one, one, &zero, 1, H, dH);
+  return H;
+}
+template <class T>
+T jacobi_derivT(int n, T a, T b, T x) {
+  if (n == 0) return 0.0;
+  return std::sqrt((T)n * ((T)n + a + b + (T)1.0)) * jacobiT<T>(n - 1, a + (T)1.0, b + (T)1.0, x);
+}
+
+template <class T>
+void pkd_cart(int d, const int* al, const T* x, T& v, T* g) {
   if (d == 2) {
-    double t = (1.0 - x[1]) / 2.0, s = (1.0 + x[0]) - t;
-    double dt[2] = {0.0, -0.5}, ds[2] = {1.0, 0.5};
-    double H, dH[2];
-    homog(al[0], 0, 0, s, ds, t, dt, 2, H, dH);
-    double P = jacobi(al[1], 2.0 * al[0] + 1.0, 0, x[1]);
-    double dP = jacobi_deriv(al[1], 2.0 * al[0] + 1.0, 0, x[1]);
-    double c = std::sqrt(2.0) * std::pow(2.0, al[0]);
+    T t = ((T)1.0 - x[1]) / (T)2.0, s = ((T)1.0 + x[0]) - t;
+    T dt[2] = {0.0, -0.5}, ds[2] = {1.0, 0.5};
+    T H, dH[2];
+    homog<T>(al[0], 0, 0, s, ds, t, dt, 2, H, dH);
+    T P = jacobiT<T>(al[1], (T)2.0 * al[0] + (T)1.0, 0, x[1]);
+    T dP = jacobi_derivT<T>(al[1], (T)2.0 * al[0] + (T)1.0, 0, x[1]);
+    T c = std::sqrt((T)2.0) * std::pow((T)2.0, (T)al[0]);
     v = c * H * P;
     g[0] = c * dH[0] * P;
     g[1] = c * (dH[1] * P + H * dP);
   } else {
-    double t1 = (-x[1] - x[2]) / 2.0, s1 = (1.0 + x[0]) - t1;
-    double dt1[3] = {0.0, -0.5, -0.5}, ds1[3] = {1.0, 0.5, 0.5};
-    double t2 = (1.0 - x[2]) / 2.0, s2 = (1.0 + x[1]) - t2;
-    double dt2[3] = {0.0, 0.0, -0.5}, ds2[3] = {0.0, 1.0, 0.5};
-    double H1, dH1[3], H2, dH2[3];
-    homog(al[0], 0, 0, s1, ds1, t1, dt1, 3, H1, dH1);
-    homog(al[1], 2.0 * al[0] + 1.0, 0, s2, ds2, t2, dt2, 3, H2, dH2);
-    double a3 = 2.0 * al[0] + 2.0 * al[1] + 2.0;
-    double P = jacobi(al[2], a3, 0, x[2]);
-    double dP = jacobi_deriv(al[2], a3, 0, x[2]);
-    double c = 2.0 * std::sqrt(2.0) * std::pow(4.0, al[0]) * std::pow(2.0, al[1]);
+    T t1 = (-x[1] - x[2]) / (T)2.0, s1 = ((T)1.0 + x[0]) - t1;
+    T dt1[3] = {0.0, -0.5, -0.5}, ds1[3] = {1.0, 0.5, 0.5};
+    T t2 = ((T)1.0 - x[2]) / (T)2.0, s2 = ((T)1.0 + x[1]) - t2;
+    T dt2[3] = {0.0, 0.0, -0.5}, ds2[3] = {0.0, 1.0, 0.5};
+    T H1, dH1[3], H2, dH2[3];
+    homog<T>(al[0], 0, 0, s1, ds1, t1, dt1, 3, H1, dH1);
+    homog<T>(al[1], (T)2.0 * al[0] + (T)1.0, 0, s2, ds2, t2, dt2, 3, H2, dH2);
+    T a3 = (T)2.0 * al[0] + (T)2.0 * al[1] + (T)2.0;
+    T P = jacobiT<T>(al[2], a3, 0, x[2]);
+    T dP = jacobi_derivT<T>(al[2], a3, 0, x[2]);
+    T c = (T)2.0 * std::sqrt((T)2.0) * std::pow((T)4.0, (T)al[0]) * std::pow((T)2.0, (T)al[1]);
     v = c * H1 * H2 * P;
     for (int k = 0; k < 3; ++k) g[k] = c * (dH1[k] * H2 * P + H1 * dH2[k] * P);
     g[2] += c * H1 * H2 * dP;
@@ -547,7 +565,8 @@ void es_flux(int d, double g, const double* Ua, const double* Ub, const double* 
 // ------------------------------------------------------------------------------------------------
 // small dense linear algebra: Gaussian elimination with partial pivoting, A X = B (in place)
 // ------------------------------------------------------------------------------------------------
-bool solve_dense(int N, vector<double> A, vector<double>& X, int nrhs) {
+template <class T>
+bool solve_dense(int N, vector<T> A, vector<T>& X, int nrhs) {
   for (int k = 0; k < N; ++k) {
     int piv = k;
     for (int i = k + 1; i < N; ++i)
@@ -558,7 +577,7 @@ bool solve_dense(int N, vector<double> A, vector<double>& X, int nrhs) {
       for (int j = 0; j < nrhs; ++j) std::swap(X[(size_t)k * nrhs + j], X[(size_t)piv * nrhs + j]);
     }
     for (int i = k + 1; i < N; ++i) {
-      double f = A[(size_t)i * N + k] / A[(size_t)k * N + k];
+      T f = A[(size_t)i * N + k] / A[(size_t)k * N + k];
       if (f == 0.0) continue;
       for (int j = k; j < N; ++j) A[(size_t)i * N + j] -= f * A[(size_t)k * N + j];
       for (int j = 0; j < nrhs; ++j) X[(size_t)i * nrhs + j] -= f * X[(size_t)k * nrhs + j];
@@ -566,7 +585,7 @@ bool solve_dense(int N, vector<double> A, vector<double>& X, int nrhs) {
   }
   for (int k = N - 1; k >= 0; --k) {
     for (int j = 0; j < nrhs; ++j) {
-      double s = X[(size_t)k * nrhs + j];
+      T s = X[(size_t)k * nrhs + j];
       for (int i = k + 1; i < N; ++i) s -= A[(size_t)k * N + i] * X[(size_t)i * nrhs + j];
       X[(size_t)k * nrhs + j] = s / A[(size_t)k * N + k];
     }
@@ -605,47 +624,54 @@ void lattice(int d, int N, vector<double>& xi, vector<double>& lam) {
   }
 }
 
+// Geometry is evaluated in extended precision (long double, 64-bit significand): the equispaced
+// lattice interpolation and differentiation of degree q+1 amplify rounding by ~1e3 (reading R25),
+// so the oracle's metric terms are computed well below double-precision rounding and then rounded.
+typedef long double LD;
+
 // polynomial interpolant on a lattice in the PKD basis: coefficients for nrhs fields
 struct Interp {
   int d, N, M;
   vector<int> al;
-  vector<double> xi;  // lattice points
-  vector<double> Vl;  // [M][M]
+  vector<LD> xi;  // lattice points
+  vector<LD> Vl;  // [M][M]
 };
 Interp make_interp(int d, int N) {
   Interp I;
   I.d = d;
   I.N = N;
-  vector<double> lam;
-  lattice(d, N, I.xi, lam);
+  vector<double> lam, xid;
+  lattice(d, N, xid, lam);
+  // exact lattice coordinates -1 + 2 i/N in long double
+  I.xi.assign(xid.size(), 0.0L);
+  for (size_t k = 0; k < xid.size(); ++k) I.xi[k] = std::nearbyint((xid[k] + 1.0) * N / 2.0) * 2.0L / N - 1.0L;
   I.al = multi_indices(d, N);
   I.M = (int)I.al.size() / d;
-  I.Vl.assign((size_t)I.M * I.M, 0.0);
-  double g[3];
+  I.Vl.assign((size_t)I.M * I.M, 0.0L);
+  LD g[3];
   for (int i = 0; i < I.M; ++i)
-    for (int k = 0; k < I.M; ++k) pkd_cart(d, &I.al[k * d], &I.xi[i * d], I.Vl[(size_t)i * I.M + k], g);
+    for (int k = 0; k < I.M; ++k) pkd_cart<LD>(d, &I.al[k * d], &I.xi[i * d], I.Vl[(size_t)i * I.M + k], g);
   return I;
 }
 // evaluate sum_k c[k][j] phi_k(x) and its gradient; c [M][nrhs]
-void interp_eval(const Interp& I, const vector<double>& c, int nrhs, const double* x, double* val,
-                 double* grad /*[nrhs][d]*/) {
+void interp_eval(const Interp& I, const vector<LD>& c, int nrhs, const LD* x, LD* val, LD* grad /*[nrhs][d]*/) {
   int d = I.d;
   for (int j = 0; j < nrhs; ++j) {
     val[j] = 0.0;
     for (int k = 0; k < d; ++k) grad[j * d + k] = 0.0;
   }
-  double v, g[3];
+  LD v, g[3];
   for (int k = 0; k < I.M; ++k) {
-    pkd_cart(d, &I.al[k * d], x, v, g);
+    pkd_cart<LD>(d, &I.al[k * d], x, v, g);
     for (int j = 0; j < nrhs; ++j) {
-      double ck = c[(size_t)k * nrhs + j];
+      LD ck = c[(size_t)k * nrhs + j];
       val[j] += ck * v;
       for (int l = 0; l < d; ++l) grad[j * d + l] += ck * g[l];
     }
   }
 }
 
-double det_d(int d, const double* A) {
+LD det_d(int d, const LD* A) {
   if (d == 2) return A[0] * A[3] - A[1] * A[2];
   return A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
          A[2] * (A[3] * A[7] - A[4] * A[6]);
@@ -687,39 +713,38 @@ void facet_verts(int d, int z, int* vs) {
   }
 }
 
-// geometry of one element (P:322-364 metric terms, P:448-452 Jacobian interpolant)
+// geometry of one element (P:322-364 metric terms, P:448-452 Jacobian interpolant), evaluated in
+// long double and rounded to double at the end (R25)
 bool element_geometry(ora_mesh& m, int64_t el, const double* xmap /*[Npg][d]*/, const Interp& Ipg,
                       const Interp* Icurl) {
   const Ref& r = m.ref;
   int d = m.d, Nq = r.Nq, Nf = r.Nf, Nqf = r.Nqf;
   // interpolation coefficients of the mapping (P:327-331 [eq:poly_mapping])
-  vector<double> cx(xmap, xmap + (size_t)Ipg.M * d);
-  if (!solve_dense(Ipg.M, Ipg.Vl, cx, d)) return false;
+  vector<LD> cx(xmap, xmap + (size_t)Ipg.M * d);
+  if (!solve_dense<LD>(Ipg.M, Ipg.Vl, cx, d)) return false;
   vector<double> G((size_t)Nq * d * d), Gf((size_t)Nf * Nqf * d * d), Jt(Nq), Jn((size_t)Nf * Nqf * d),
       xq((size_t)Nq * d);
-  double val[3], A[9];
-  auto gradx = [&](const double* x, double* vals, double* Aout) {
+  LD val[3], A[9];
+  auto gradx = [&](const LD* x, LD* vals, LD* Aout) {
     // Aout[mm*d + l] = d x_mm / d xi_l
-    double grad[9];
+    LD grad[9];
     interp_eval(Ipg, cx, d, x, vals, grad);
     for (int i = 0; i < d * d; ++i) Aout[i] = grad[i];
   };
-  auto metric_at = [&](const double* x, double* Gout) {
-    if (d == 2) {
-      // exact metric terms = adjugate of the Jacobian, SURVEY App. B
-      gradx(x, val, A);
-      Gout[0] = A[3];   // G_11 = dx2/dxi2
-      Gout[1] = -A[1];  // G_12 = -dx1/dxi2
-      Gout[2] = -A[2];  // G_21 = -dx2/dxi1
-      Gout[3] = A[0];   // G_22 = dx1/dxi1
-    }
+  auto metric_at = [&](const LD* x, LD* Gout) {
+    // exact metric terms = adjugate of the Jacobian, SURVEY App. B
+    gradx(x, val, A);
+    Gout[0] = A[3];   // G_11 = dx2/dxi2
+    Gout[1] = -A[1];  // G_12 = -dx1/dxi2
+    Gout[2] = -A[2];  // G_21 = -dx2/dxi1
+    Gout[3] = A[0];   // G_22 = dx1/dxi1
   };
   // conservative curl metrics in 3D (P:349-356 [eq:metric_interpolants, eq:conservative_curl]),
   // column reading R4: G_{:,1} = -curl r1, G_{:,2} = curl r2, G_{:,3} = curl r3.
-  vector<double> cr;  // [Mcurl][9] coefficients of r1, r2, r3 (each 3 components)
+  vector<LD> cr;  // [Mcurl][9] coefficients of r1, r2, r3 (each 3 components)
   if (d == 3) {
     int Mc = Icurl->M;
-    cr.assign((size_t)Mc * 9, 0.0);
+    cr.assign((size_t)Mc * 9, 0.0L);
     for (int i = 0; i < Mc; ++i) {
       gradx(&Icurl->xi[i * 3], val, A);
       // r1 = x3 grad x2, r2 = x3 grad x1, r3 = x1 grad x2
@@ -729,67 +754,77 @@ bool element_geometry(ora_mesh& m, int64_t el, const double* xmap /*[Npg][d]*/, 
         cr[(size_t)i * 9 + 6 + l] = val[0] * A[1 * 3 + l];
       }
     }
-    if (!solve_dense(Mc, Icurl->Vl, cr, 9)) return false;
+    if (!solve_dense<LD>(Mc, Icurl->Vl, cr, 9)) return false;
   }
-  auto curl_metric_at = [&](const double* x, double* Gout) {
-    double v9[9], g27[27];
+  auto curl_metric_at = [&](const LD* x, LD* Gout) {
+    LD v9[9], g27[27];
     interp_eval(*Icurl, cr, 9, x, v9, g27);
     // g27[(field)*3 + l] = d field / d xi_l, field = 3*rk + comp
     auto dr = [&](int rk, int comp, int l) { return g27[(3 * rk + comp) * 3 + l]; };
     for (int rk = 0; rk < 3; ++rk) {
-      double c0 = dr(rk, 2, 1) - dr(rk, 1, 2);
-      double c1 = dr(rk, 0, 2) - dr(rk, 2, 0);
-      double c2 = dr(rk, 1, 0) - dr(rk, 0, 1);
-      double s = (rk == 0) ? -1.0 : 1.0;
+      LD c0 = dr(rk, 2, 1) - dr(rk, 1, 2);
+      LD c1 = dr(rk, 0, 2) - dr(rk, 2, 0);
+      LD c2 = dr(rk, 1, 0) - dr(rk, 0, 1);
+      LD s = (rk == 0) ? -1.0L : 1.0L;
       Gout[0 * 3 + rk] = s * c0;
       Gout[1 * 3 + rk] = s * c1;
       Gout[2 * 3 + rk] = s * c2;
     }
   };
+  auto to_ld = [&](const double* x, LD* y) {
+    for (int k = 0; k < d; ++k) y[k] = x[k];
+  };
   for (int i = 0; i < Nq; ++i) {
-    const double* x = &r.xi[i * d];
+    LD x[3], Gl[9], xv[3], gr[9];
+    to_ld(&r.xi[i * d], x);
     if (d == 2)
-      metric_at(x, &G[(size_t)i * 4]);
+      metric_at(x, Gl);
     else
-      curl_metric_at(x, &G[(size_t)i * 9]);
-    double grad[9];
-    interp_eval(Ipg, cx, d, x, &xq[(size_t)i * d], grad);
+      curl_metric_at(x, Gl);
+    for (int k = 0; k < d * d; ++k) G[(size_t)i * d * d + k] = (double)Gl[k];
+    interp_eval(Ipg, cx, d, x, xv, gr);
+    for (int k = 0; k < d; ++k) xq[(size_t)i * d + k] = (double)xv[k];
   }
   for (int z = 0; z < Nf; ++z)
     for (int f = 0; f < Nqf; ++f) {
-      const double* x = &r.xif[((size_t)z * Nqf + f) * d];
-      double* Go = &Gf[((size_t)z * Nqf + f) * d * d];
+      LD x[3], Gl[9];
+      to_ld(&r.xif[((size_t)z * Nqf + f) * d], x);
       if (d == 2)
-        metric_at(x, Go);
+        metric_at(x, Gl);
       else
-        curl_metric_at(x, Go);
+        curl_metric_at(x, Gl);
+      double* Go = &Gf[((size_t)z * Nqf + f) * d * d];
+      for (int k = 0; k < d * d; ++k) Go[k] = (double)Gl[k];
       // J n = G^T nhat (P:361 [eq:nanson]); facet metric evaluated at the facet node (R8)
       for (int mm = 0; mm < d; ++mm) {
-        double s = 0.0;
-        for (int l = 0; l < d; ++l) s += Go[l * d + mm] * r.nhat[z * d + l];
-        Jn[((size_t)z * Nqf + f) * d + mm] = s;
+        LD s = 0.0;
+        for (int l = 0; l < d; ++l) s += Gl[l * d + mm] * (LD)r.nhat[z * d + l];
+        Jn[((size_t)z * Nqf + f) * d + mm] = (double)s;
       }
     }
   // Jacobian interpolant of degree p_g (P:448-452 [eq:jacobian_approx])
-  vector<double> cj(Ipg.M);
+  vector<LD> cj(Ipg.M);
   for (int i = 0; i < Ipg.M; ++i) {
     gradx(&Ipg.xi[i * d], val, A);
     cj[i] = det_d(d, A);
-    if (!(cj[i] > 0.0)) {
+    if (!(cj[i] > 0.0L)) {
       fprintf(stderr, "oracle: J <= 0 at mapping node %d of element %lld\n", i, (long long)el);
       return false;
     }
   }
-  if (!solve_dense(Ipg.M, Ipg.Vl, cj, 1)) return false;
+  if (!solve_dense<LD>(Ipg.M, Ipg.Vl, cj, 1)) return false;
   for (int i = 0; i < Nq; ++i) {
-    double v1, g1[3];
-    interp_eval(Ipg, cj, 1, &r.xi[i * d], &v1, g1);
-    Jt[i] = v1;
-    if (!(v1 > 0.0)) {
+    LD x[3], v1, g1[3];
+    to_ld(&r.xi[i * d], x);
+    interp_eval(Ipg, cj, 1, x, &v1, g1);
+    Jt[i] = (double)v1;
+    if (!(v1 > 0.0L)) {
       fprintf(stderr, "oracle: J~ <= 0 at volume node %d of element %lld\n", i, (long long)el);
       return false;
     }
   }
+  for (int i = 0; i < Nq; ++i)  // back to global coordinates (R25)
+    for (int k = 0; k < d; ++k) xq[(size_t)i * d + k] += m.evx[((size_t)el * (d + 1) + 0) * d + k];
   m.G[el] = G;
   m.Gf[el] = Gf;
   m.Jt[el] = Jt;
@@ -1008,6 +1043,12 @@ ora_mesh* ora_mesh_create(int d, int p, int64_t ne, const int64_t* elem_vertices
     map(user, (int64_t)alist.size() * Npg, xin.data(), xout.data());
   else
     xout = xin;
+  // geometry in element-local coordinates x - X_1 (reading R25: G, J and J~ are invariant under a
+  // translation of the map -- for the curl form because curl I_{q+1}[c grad x_k] = c curl grad x_k
+  // = 0 exactly, grad x_k being in P_{p-1} -- and local coordinates avoid cancellation of size L/h)
+  for (size_t a = 0; a < alist.size(); ++a)
+    for (int i = 0; i < Npg; ++i)
+      for (int k = 0; k < d; ++k) xout[((size_t)a * Npg + i) * d + k] -= m->evx[(alist[a] * nv + 0) * d + k];
   bool ok = true;
 #pragma omp parallel for schedule(dynamic, 4)
   for (int64_t a = 0; a < (int64_t)alist.size(); ++a) {

@@ -1,0 +1,217 @@
+"""Python binding of the B200-native ES modal DSEM library (include/es.h).
+
+Argument marshalling only: every step of the right-hand side runs in the sm_100a kernels of
+libes_b200.so.  There is no CPU fallback -- importing this package fails loudly when the CUDA
+library is missing.  PyTorch is used by callers for device memory and streams; this module only
+passes raw pointers.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libes_b200.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "es.h")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(no CPU fallback exists)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_dp = ctypes.POINTER(ctypes.c_double)
+_lp = ctypes.POINTER(ctypes.c_int64)
+_vp = ctypes.c_void_p
+
+ES_OK, ES_ERR_CONFIG, ES_ERR_INADMISSIBLE, ES_ERR_VERIFY = 0, 2, 3, 4
+ES_ERR_ARG, ES_ERR_CUDA, ES_ERR_NCCL, ES_ERR_OOM = -1, -5, -6, -7
+
+es_map_fn = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, _dp, _dp)
+
+
+class es_mesh(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int), ("n_elements", ctypes.c_int64), ("elem_vertices", _lp),
+                ("elem_vertex_coords", _dp), ("period", _dp)]
+
+
+class es_options(ctypes.Structure):
+    _fields_ = [("gamma", ctypes.c_double), ("interface_flux", ctypes.c_int), ("rank", ctypes.c_int),
+                ("world", ctypes.c_int), ("nccl_unique_id", ctypes.c_char_p), ("cuda_stream", _vp),
+                ("device", ctypes.c_int), ("check_admissibility", ctypes.c_int)]
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_i = ctypes.c_int
+es_setup = _sig("es_setup", _i, ctypes.POINTER(_vp), ctypes.POINTER(es_mesh), _i, es_map_fn, _vp,
+                ctypes.POINTER(es_options))
+es_destroy = _sig("es_destroy", None, _vp)
+es_last_error = _sig("es_last_error", ctypes.c_char_p, _vp)
+es_sizes = _sig("es_sizes", _i, _vp, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i),
+                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64))
+es_rhs = _sig("es_rhs", _i, _vp, _vp, _vp)
+es_rhs_host = _sig("es_rhs_host", _i, _vp, _vp, _vp)
+es_set_state = _sig("es_set_state", _i, _vp, _vp)
+es_get_state = _sig("es_get_state", _i, _vp, _vp)
+es_step = _sig("es_step", _i, _vp, ctypes.c_double, _i)
+es_entropy_production = _sig("es_entropy_production", _i, _vp, _vp, _dp, _dp, _dp)
+es_flux_counts = _sig("es_flux_counts", _i, _vp, _lp, _lp, _lp, _dp)
+es_node_coords = _sig("es_node_coords", _i, _vp, _vp)
+es_project_nodal = _sig("es_project_nodal", _i, _vp, _vp, _vp)
+es_element_geometry = _sig("es_element_geometry", _i, _vp, ctypes.c_int64, _dp, _dp, _dp)
+es_synchronize = _sig("es_synchronize", _i, _vp)
+es_stream = _sig("es_stream", _vp, _vp)
+es_launch_count = _sig("es_launch_count", ctypes.c_int64, _vp)
+es_reset_launch_count = _sig("es_reset_launch_count", None, _vp)
+es_timing_enable = _sig("es_timing_enable", _i, _vp, _i)
+es_timing_read = _sig("es_timing_read", _i, _vp, _i, _dp, _lp)
+
+
+def declared_symbols():
+    """Every function name declared in include/es.h."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(es_[a-z_]+)\s*\(", txt)) - {"es_map_fn"})
+
+
+class ESError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"es error {code}: {msg}")
+        self.code = code
+
+
+def _ptr(t):
+    """data pointer of a torch tensor or numpy array"""
+    if hasattr(t, "data_ptr"):
+        return ctypes.c_void_p(t.data_ptr())
+    return ctypes.c_void_p(t.ctypes.data)
+
+
+class Context:
+    """Thin owner of an es_context.  `mesh` is a dict with elem_vertices, elem_vertex_coords, period
+    (e.g. es_inputs.split_cartesian); `warp` a callable [n,d] -> [n,d] (the geometry map)."""
+
+    def __init__(self, mesh, p, warp=None, gamma=1.4, interface_flux=1, rank=0, world=1, nccl_id=None,
+                 stream=None, device=0, check_admissibility=0):
+        self.d = int(mesh["d"]) if "d" in mesh else int(np.asarray(mesh["period"]).size)
+        self._ev = np.ascontiguousarray(mesh["elem_vertices"], dtype=np.int64)
+        self._evx = np.ascontiguousarray(mesh["elem_vertex_coords"], dtype=np.float64)
+        self._per = np.ascontiguousarray(mesh["period"], dtype=np.float64)
+        self.p = p
+        self.ne = len(self._ev)
+        d = self.d
+        err = []
+
+        def cb(user, n, xin, xout):
+            try:
+                xi = np.ctypeslib.as_array(xin, shape=(n * d,)).reshape(n, d)
+                xo = np.ctypeslib.as_array(xout, shape=(n * d,)).reshape(n, d)
+                xo[:] = warp(xi) if warp is not None else xi
+            except Exception as ex:  # pragma: no cover
+                err.append(ex)
+        self._cb = es_map_fn(cb)
+        m = es_mesh(d, self.ne, self._ev.ctypes.data_as(_lp), self._evx.ctypes.data_as(_dp),
+                    self._per.ctypes.data_as(_dp))
+        self._nccl_id = nccl_id
+        o = es_options(gamma, interface_flux, rank, world, nccl_id, stream, device, check_admissibility)
+        h = _vp()
+        rc = es_setup(ctypes.byref(h), ctypes.byref(m), p, self._cb, None, ctypes.byref(o))
+        self.h = h
+        if err:
+            raise err[0]
+        if rc != ES_OK:
+            msg = es_last_error(h).decode() if h else ""
+            raise ESError(rc, msg)
+        Np, Nq, Nqf = _i(), _i(), _i()
+        nloc, first = ctypes.c_int64(), ctypes.c_int64()
+        es_sizes(h, ctypes.byref(Np), ctypes.byref(Nq), ctypes.byref(Nqf), ctypes.byref(nloc), ctypes.byref(first))
+        self.Np, self.Nq, self.Nqf = Np.value, Nq.value, Nqf.value
+        self.nloc, self.first = nloc.value, first.value
+        self.Nc = d + 2
+        self.shape = (self.nloc, self.Nc, self.Np)
+
+    def _check(self, rc):
+        if rc != ES_OK:
+            raise ESError(rc, es_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            es_destroy(self.h)
+        self.h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- device-pointer API (torch CUDA tensors) --
+    def rhs(self, u, dudt):
+        self._check(es_rhs(self.h, _ptr(u), _ptr(dudt)))
+
+    def rhs_host(self, u_host, dudt_host):
+        self._check(es_rhs_host(self.h, _ptr(u_host), _ptr(dudt_host)))
+
+    def set_state(self, u):
+        self._check(es_set_state(self.h, _ptr(u)))
+
+    def get_state(self, u):
+        self._check(es_get_state(self.h, _ptr(u)))
+
+    def step(self, dt, nsteps=1):
+        self._check(es_step(self.h, float(dt), int(nsteps)))
+
+    def entropy_production(self, u):
+        r, a = ctypes.c_double(), ctypes.c_double()
+        cons = (ctypes.c_double * 5)()
+        self._check(es_entropy_production(self.h, _ptr(u), ctypes.byref(r), ctypes.byref(a),
+                                          ctypes.cast(cons, _dp)))
+        return r.value, a.value, np.array(cons[:self.Nc])
+
+    def flux_counts(self):
+        v, f, e = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        i = ctypes.c_double()
+        self._check(es_flux_counts(self.h, ctypes.byref(v), ctypes.byref(f), ctypes.byref(e), ctypes.byref(i)))
+        return dict(volume=v.value, facet=f.value, eq56=e.value, interface=i.value)
+
+    def node_coords(self, x):
+        self._check(es_node_coords(self.h, _ptr(x)))
+
+    def project_nodal(self, un, um):
+        self._check(es_project_nodal(self.h, _ptr(un), _ptr(um)))
+
+    def element_geometry(self, k):
+        d = self.d
+        G = np.zeros((self.Nq, d, d))
+        Jn = np.zeros((d + 1, self.Nqf, d))
+        Jt = np.zeros(self.Nq)
+        self._check(es_element_geometry(self.h, k, G.ctypes.data_as(_dp), Jn.ctypes.data_as(_dp),
+                                        Jt.ctypes.data_as(_dp)))
+        return dict(G=G, Jn=Jn, Jt=Jt)
+
+    def synchronize(self):
+        self._check(es_synchronize(self.h))
+
+    def stream(self):
+        return es_stream(self.h)
+
+    def launch_count(self):
+        return es_launch_count(self.h)
+
+    def reset_launch_count(self):
+        es_reset_launch_count(self.h)
+
+    def timing_enable(self, on=True):
+        self._check(es_timing_enable(self.h, 1 if on else 0))
+
+    def timing_read(self, cls):
+        t, n = ctypes.c_double(), ctypes.c_int64()
+        self._check(es_timing_read(self.h, cls, ctypes.byref(t), ctypes.byref(n)))
+        return t.value, n.value

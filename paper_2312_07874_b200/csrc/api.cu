@@ -1,0 +1,614 @@
+// api.cpp -- the C ABI declared in include/es.h: context, setup, RHS / RK4 / entropy drivers,
+// NCCL face-trace halo exchange.  Product code (no CPU fallback: every step runs in the kernels).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "es.h"
+#include "geometry.cuh"
+#include "internal.h"
+#include "kernels.cuh"
+
+namespace esb {
+cudaError_t launch_project_2d(int n, const DevRef& R, const ProjArgs& A, cudaStream_t st);
+cudaError_t launch_project_3d(int n, const DevRef& R, const ProjArgs& A, cudaStream_t st);
+cudaError_t launch_rhs_2d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
+cudaError_t launch_rhs_3d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
+cudaError_t launch_projnodal_2d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st);
+cudaError_t launch_projnodal_3d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st);
+}  // namespace esb
+
+using namespace esb;
+
+struct TimedEvent {
+  cudaEvent_t a, b;
+  int cls;
+};
+
+struct es_context {
+  std::string err;
+  es_status poisoned = ES_OK;
+  int d = 0, p = 0, n = 0, Nq = 0, Nqf = 0, Nf = 0, Np = 0, NC = 0;
+  int64_t ne = 0, first = 0, nloc = 0, nslots = 0;
+  double gamma = 1.4, c0 = 0.0;
+  int es = 1, check_adm = 0, rank = 0, world = 1, device = 0;
+  cudaStream_t stream = nullptr, comm_stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev_packed = nullptr, ev_comm = nullptr;
+  RefTables T;
+  MeshPlan plan;
+  DevRef R{};
+  void* d_tables = nullptr;
+  double *geo_vol = nullptr, *geo_face = nullptr, *xq = nullptr, *jt = nullptr;
+  double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr;
+  int64_t *face_slot = nullptr, *d_interior = nullptr, *d_boundary = nullptr, *d_send = nullptr;
+  int* face_reflect = nullptr;
+  int* bad = nullptr;
+  double *U = nullptr, *ACC = nullptr, *US = nullptr, *hin = nullptr, *hout = nullptr, *send_buf = nullptr;
+  ncclComm_t comm = nullptr;
+  int64_t launches = 0;
+  bool timing = false;
+  std::vector<TimedEvent> tev;
+  std::vector<cudaEvent_t> ev_pool;
+};
+
+namespace {
+
+es_status fail(es_context* c, es_status s, const std::string& m) {
+  if (c) {
+    c->err = m;
+    if (s == ES_ERR_CUDA || s == ES_ERR_NCCL) c->poisoned = s;
+  }
+  return s;
+}
+#define CK(x)                                                                                     \
+  do {                                                                                            \
+    cudaError_t _e = (x);                                                                         \
+    if (_e != cudaSuccess)                                                                        \
+      return fail(c, _e == cudaErrorMemoryAllocation ? ES_ERR_OOM : ES_ERR_CUDA,                  \
+                  std::string(#x) + ": " + cudaGetErrorString(_e));                               \
+  } while (0)
+#define NK(x)                                                                                     \
+  do {                                                                                            \
+    ncclResult_t _r = (x);                                                                        \
+    if (_r != ncclSuccess) return fail(c, ES_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
+#define POISON_CHECK()                            \
+  do {                                            \
+    if (!c) return ES_ERR_ARG;                    \
+    if (c->poisoned != ES_OK) return c->poisoned; \
+  } while (0)
+
+cudaEvent_t get_event(es_context* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+template <class T>
+cudaError_t upload(T** dst, const std::vector<T>& v) {
+  if (v.empty()) {
+    *dst = nullptr;
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaMalloc((void**)dst, v.size() * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+// pack the reference tables into one device allocation
+es_status upload_tables(es_context* c) {
+  const RefTables& t = c->T;
+  std::vector<char> blob;
+  std::vector<std::pair<size_t, int>> offs;  // (offset, kind)
+  auto add_d = [&](const std::vector<double>& v) {
+    size_t off = (blob.size() + 255) / 256 * 256;
+    blob.resize(off + std::max<size_t>(v.size(), 1) * sizeof(double), 0);
+    if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(double));
+    return off;
+  };
+  auto add_i = [&](const std::vector<int>& v) {
+    size_t off = (blob.size() + 255) / 256 * 256;
+    blob.resize(off + std::max<size_t>(v.size(), 1) * sizeof(int), 0);
+    if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(int));
+    return off;
+  };
+  std::vector<int> mode_pr(t.Np), mode_last(t.Np);
+  for (size_t pr = 0; pr < t.pair_off.size(); ++pr) {
+    int cnt = (pr + 1 < t.pair_off.size() ? t.pair_off[pr + 1] : t.Np) - t.pair_off[pr];
+    for (int k = 0; k < cnt; ++k) {
+      mode_pr[t.pair_off[pr] + k] = (int)pr;
+      mode_last[t.pair_off[pr] + k] = k;
+    }
+  }
+  size_t o_eta = add_d(t.eta), o_w = add_d(t.w), o_eta3 = add_d(t.eta3), o_w3 = add_d(t.w3);
+  size_t o_q1 = add_d(t.skQ1), o_a1 = add_d(t.skA1), o_a2 = add_d(t.skA2), o_a3 = add_d(t.skA3), o_a4 = add_d(t.skA4);
+  size_t o_lL = add_d(t.lL), o_lR = add_d(t.lR), o_l3 = add_d(t.l3L), o_li4 = add_d(t.lint4);
+  size_t o_p1 = add_d(t.psi1), o_p2 = add_d(t.psi2), o_p3 = add_d(t.psi3);
+  size_t o_pa1 = add_i(t.pair_a1), o_pa2 = add_i(t.pair_a2), o_poff = add_i(t.pair_off), o_mpr = add_i(mode_pr),
+         o_ml = add_i(mode_last);
+  size_t o_B = add_d(t.Bf), o_nh = add_d(t.nhat), o_W = add_d(t.Wvol);
+  char* d = nullptr;
+  CK(cudaMalloc((void**)&d, blob.size()));
+  CK(cudaMemcpy(d, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+  c->d_tables = d;
+  auto P = [&](size_t o) { return (const double*)(d + o); };
+  auto I = [&](size_t o) { return (const int*)(d + o); };
+  c->R = DevRef{P(o_eta), P(o_w), P(o_eta3), P(o_w3), P(o_q1), P(o_a1), P(o_a2), P(o_a3), P(o_a4),
+                P(o_lL), P(o_lR), P(o_l3), P(o_li4), P(o_p1), P(o_p2), P(o_p3),
+                I(o_pa1), I(o_pa2), I(o_poff), I(o_mpr), I(o_ml), P(o_B), P(o_nh), P(o_W)};
+  return ES_OK;
+}
+
+cudaError_t run_project(es_context* c, const double* u, int64_t n, const int64_t* list, double* wt) {
+  ProjArgs A{n, list, u, c->geo_vol, c->prim, c->trace, wt, c->bad, c->gamma};
+  c->launches++;
+  return c->d == 2 ? launch_project_2d(c->n, c->R, A, c->stream) : launch_project_3d(c->n, c->R, A, c->stream);
+}
+
+cudaError_t run_rhs(es_context* c, RhsArgs A, int64_t n, const int64_t* list) {
+  A.n_elem = n;
+  A.elem_list = list;
+  if (n <= 0) return cudaSuccess;
+  TimedEvent te{};
+  if (c->timing) {
+    te = {get_event(c), get_event(c), 1};
+    cudaEventRecord(te.a, c->stream);
+  }
+  c->launches++;
+  cudaError_t e = c->d == 2 ? launch_rhs_2d(c->n, c->R, A, c->stream) : launch_rhs_3d(c->n, c->R, A, c->stream);
+  if (c->timing) {
+    cudaEventRecord(te.b, c->stream);
+    c->tev.push_back(te);
+  }
+  return e;
+}
+
+RhsArgs base_rhs_args(es_context* c) {
+  RhsArgs A{};
+  A.prim = c->prim;
+  A.trace = c->trace;
+  A.geo_vol = c->geo_vol;
+  A.geo_face = c->geo_face;
+  A.face_slot = c->face_slot;
+  A.face_reflect = c->face_reflect;
+  A.gamma = c->gamma;
+  A.es = c->es;
+  A.c0 = c->c0;
+  return A;
+}
+
+// one right-hand side: projection, halo exchange overlapped with interior elements, then the
+// boundary elements
+es_status rhs_pass(es_context* c, const double* u, RhsArgs A, double* wt) {
+  TimedEvent te{};
+  if (c->timing) {
+    te = {get_event(c), get_event(c), 0};
+    cudaEventRecord(te.a, c->stream);
+  }
+  CK(run_project(c, u, c->nloc, nullptr, wt));
+  if (c->timing) {
+    cudaEventRecord(te.b, c->stream);
+    c->tev.push_back(te);
+  }
+  if (c->world == 1) {
+    CK(run_rhs(c, A, c->nloc, nullptr));
+    return ES_OK;
+  }
+  const int per_face = c->NC * c->Nqf;
+  const int64_t nsend = (int64_t)c->plan.send_slots.size();
+  CK(launch_pack(c->trace, c->d_send, nsend, per_face, c->send_buf, c->stream));
+  c->launches++;
+  CK(cudaEventRecord(c->ev_packed, c->stream));
+  CK(cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
+  NK(ncclGroupStart());
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    if (c->plan.send_count[r] > 0)
+      NK(ncclSend(c->send_buf + c->plan.send_offset[r] * per_face, (size_t)(c->plan.send_count[r] * per_face),
+                  ncclDouble, r, c->comm, c->comm_stream));
+    if (c->plan.recv_count[r] > 0)
+      NK(ncclRecv(c->trace + (c->nloc * c->Nf + c->plan.recv_offset[r]) * per_face,
+                  (size_t)(c->plan.recv_count[r] * per_face), ncclDouble, r, c->comm, c->comm_stream));
+  }
+  NK(ncclGroupEnd());
+  CK(cudaEventRecord(c->ev_comm, c->comm_stream));
+  CK(run_rhs(c, A, (int64_t)c->plan.interior.size(), c->d_interior));
+  CK(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
+  CK(run_rhs(c, A, (int64_t)c->plan.boundary.size(), c->d_boundary));
+  return ES_OK;
+}
+
+es_status check_bad(es_context* c) {
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (h) {
+    CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
+    return fail(c, ES_ERR_INADMISSIBLE, "inadmissible state (rho <= 0 or p <= 0) at a projected node");
+  }
+  return ES_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* es_last_error(const es_context* c) { return c ? c->err.c_str() : "null context"; }
+
+void es_destroy(es_context* c) {
+  if (!c) return;
+  if (c->device >= 0) cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : {(void*)c->d_tables, (void*)c->geo_vol, (void*)c->geo_face, (void*)c->xq, (void*)c->jt,
+                  (void*)c->prim, (void*)c->trace, (void*)c->wt, (void*)c->part, (void*)c->red,
+                  (void*)c->face_slot, (void*)c->d_interior, (void*)c->d_boundary, (void*)c->d_send,
+                  (void*)c->face_reflect, (void*)c->bad, (void*)c->U, (void*)c->ACC, (void*)c->US,
+                  (void*)c->hin, (void*)c->hout, (void*)c->send_buf})
+    if (p) cudaFree(p);
+  for (auto& t : c->tev) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->ev_packed) cudaEventDestroy(c->ev_packed);
+  if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, void* user,
+                   const es_options* opt) {
+  if (!out || !mesh || !opt || !mesh->elem_vertices || !mesh->elem_vertex_coords) return ES_ERR_ARG;
+  *out = nullptr;
+  es_context* c = new es_context();
+  *out = c;
+  c->d = mesh->dim;
+  c->p = p;
+  c->gamma = opt->gamma;
+  c->es = opt->interface_flux ? 1 : 0;
+  c->check_adm = opt->check_admissibility;
+  c->rank = opt->rank;
+  c->world = opt->world < 1 ? 1 : opt->world;
+  c->device = opt->device;
+  if (c->d != 2 && c->d != 3) return fail(c, ES_ERR_CONFIG, "dim must be 2 or 3");
+  if (!(c->gamma > 1.0)) return fail(c, ES_ERR_CONFIG, "gamma must exceed 1");
+  if (c->rank < 0 || c->rank >= c->world) return fail(c, ES_ERR_ARG, "rank out of range");
+  if (c->world > 1 && !opt->nccl_unique_id) return fail(c, ES_ERR_ARG, "world > 1 needs nccl_unique_id");
+  std::string err;
+  if (!build_ref_tables(c->d, p, c->T, err)) return fail(c, ES_ERR_CONFIG, err);
+  c->n = c->T.n;
+  c->Nq = c->T.Nq;
+  c->Nqf = c->T.Nqf;
+  c->Nf = c->T.Nf;
+  c->Np = c->T.Np;
+  c->NC = c->d + 2;
+  c->c0 = c->d == 2 ? 1.0 / std::sqrt(2.0) : std::sqrt(0.75);
+  c->ne = mesh->n_elements;
+  if (c->ne < c->world) return fail(c, ES_ERR_CONFIG, "fewer elements than ranks");
+  if (!build_mesh_plan(c->d, c->ne, mesh->elem_vertices, c->rank, c->world, c->plan, err))
+    return fail(c, ES_ERR_VERIFY, err);
+  c->first = c->plan.first;
+  c->nloc = c->plan.nloc;
+  c->nslots = c->nloc * c->Nf + c->plan.n_halo;
+  CK(cudaSetDevice(c->device));
+  if (opt->cuda_stream) {
+    c->stream = (cudaStream_t)opt->cuda_stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
+  es_status s = upload_tables(c);
+  if (s != ES_OK) return s;
+  // ---- mapping nodes: affine images of the degree-p lattice, then the user map ----
+  const int d = c->d, nv = d + 1, Npg = c->T.Npg;
+  std::vector<double> xin((size_t)c->nloc * Npg * d), xmap(xin.size());
+  for (int64_t k = 0; k < c->nloc; ++k) {
+    const double* X = mesh->elem_vertex_coords + (size_t)(c->first + k) * nv * d;
+    for (int i = 0; i < Npg; ++i)
+      for (int m = 0; m < d; ++m) {
+        double s2 = 0.0;
+        for (int v = 0; v < nv; ++v) s2 += c->T.lat_bary[(size_t)i * nv + v] * X[v * d + m];
+        xin[((size_t)k * Npg + i) * d + m] = s2;
+      }
+  }
+  if (map)
+    map(user, c->nloc * Npg, xin.data(), xmap.data());
+  else
+    xmap = xin;
+  // element-local coordinates (R25): metric terms are translation invariant, and local
+  // coordinates avoid a cancellation of order (L/h)^2 in the curl-form metrics
+  std::vector<double> shift((size_t)c->nloc * d);
+  for (int64_t k = 0; k < c->nloc; ++k)
+    for (int m = 0; m < d; ++m) {
+      shift[(size_t)k * d + m] = mesh->elem_vertex_coords[(size_t)(c->first + k) * nv * d + m];
+      for (int i = 0; i < Npg; ++i) xmap[((size_t)k * Npg + i) * d + m] -= shift[(size_t)k * d + m];
+    }
+  double* d_shift = nullptr;
+  CK(upload(&d_shift, shift));
+  // ---- geometry on the device ----
+  double* d_xmap = nullptr;
+  CK(upload(&d_xmap, xmap));
+  const int NG = d * d, NF = c->Nf * c->Nqf;
+  CK(cudaMalloc((void**)&c->geo_vol, (size_t)c->nloc * (NG + 2) * c->Nq * sizeof(double)));
+  CK(cudaMalloc((void**)&c->geo_face, (size_t)c->nloc * NF * d * sizeof(double)));
+  CK(cudaMalloc((void**)&c->xq, (size_t)c->nloc * c->Nq * d * sizeof(double)));
+  CK(cudaMalloc((void**)&c->jt, (size_t)c->nloc * c->Nq * sizeof(double)));
+  CK(cudaMalloc((void**)&c->bad, sizeof(int)));
+  CK(cudaMemset(c->bad, 0, sizeof(int)));
+  std::vector<double*> mats(8, nullptr);
+  const std::vector<double>* srcs[8] = {&c->T.LmapV, &c->T.DmapV, &c->T.DmapF, &c->T.DmapM,
+                                        &c->T.LmapC, &c->T.DmapC, &c->T.DcurlV, &c->T.DcurlF};
+  for (int k = 0; k < 8; ++k) CK(upload(&mats[k], *srcs[k]));
+  const double* lo[8];
+  for (int k = 0; k < 8; ++k) lo[k] = mats[k] ? mats[k] + srcs[k]->size() / 2 : nullptr;  // [hi | lo]
+  GeoArgs g{d, Npg, c->T.Ncl, c->Nq, NF, c->Nqf, d_xmap, mats[0], mats[1], mats[2], mats[3], mats[4], mats[5],
+            mats[6], mats[7], lo[0], lo[1], lo[2], lo[3], lo[4], lo[5], lo[6], lo[7],
+            c->R.Wvol, c->R.nhat, d_shift, c->geo_vol, c->geo_face, c->xq, c->jt, c->bad};
+  CK(launch_geometry(g, c->nloc, c->stream));
+  c->launches++;
+  int hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(d_xmap);
+  cudaFree(d_shift);
+  for (auto m : mats)
+    if (m) cudaFree(m);
+  if (hbad) return fail(c, ES_ERR_VERIFY, "non-positive Jacobian (J at a mapping node or J~ at a volume node)");
+  // ---- connectivity, lists, face check ----
+  CK(upload(&c->face_slot, c->plan.face_slot));
+  CK(upload(&c->face_reflect, c->plan.face_reflect));
+  CK(upload(&c->d_interior, c->plan.interior));
+  CK(upload(&c->d_boundary, c->plan.boundary));
+  CK(upload(&c->d_send, c->plan.send_slots));
+  unsigned long long* d_mm = nullptr;
+  CK(cudaMalloc((void**)&d_mm, sizeof(unsigned long long)));
+  CK(cudaMemset(d_mm, 0, sizeof(unsigned long long)));
+  FaceCheckArgs fa{d, c->n, c->Nqf, c->nloc, c->geo_face, c->R.Bf, c->face_slot, c->face_reflect, d_mm};
+  CK(launch_face_check(fa, c->stream));
+  unsigned long long hmm = 0;
+  CK(cudaMemcpyAsync(&hmm, d_mm, sizeof(hmm), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(d_mm);
+  double mism;
+  std::memcpy(&mism, &hmm, sizeof(double));
+  if (!(mism < 1e-8))
+    return fail(c, ES_ERR_VERIFY, "face normals / weights do not match across faces (rel " + std::to_string(mism) + ")");
+  // ---- work buffers ----
+  const size_t nmod = (size_t)c->nloc * c->NC * c->Np;
+  CK(cudaMalloc((void**)&c->prim, (size_t)c->nloc * c->NC * c->Nq * sizeof(double)));
+  CK(cudaMalloc((void**)&c->trace, (size_t)c->nslots * c->NC * c->Nqf * sizeof(double)));
+  CK(cudaMalloc((void**)&c->wt, nmod * sizeof(double)));
+  CK(cudaMalloc((void**)&c->part, (size_t)c->nloc * (2 + c->NC) * sizeof(double)));
+  CK(cudaMalloc((void**)&c->red, 8 * sizeof(double)));
+  CK(cudaMalloc((void**)&c->U, nmod * sizeof(double)));
+  CK(cudaMalloc((void**)&c->ACC, nmod * sizeof(double)));
+  CK(cudaMalloc((void**)&c->US, nmod * sizeof(double)));
+  CK(cudaMemset(c->U, 0, nmod * sizeof(double)));
+  if (c->world > 1) {
+    const size_t nsend = c->plan.send_slots.size();
+    CK(cudaMalloc((void**)&c->send_buf, std::max<size_t>(nsend, 1) * c->NC * c->Nqf * sizeof(double)));
+    ncclUniqueId id;
+    std::memcpy(&id, opt->nccl_unique_id, sizeof(id));
+    NK(ncclCommInitRank(&c->comm, c->world, id, c->rank));
+  }
+  return ES_OK;
+}
+
+es_status es_sizes(const es_context* c, int* Np, int* Nq, int* Nqf, int64_t* nloc, int64_t* first) {
+  if (!c) return ES_ERR_ARG;
+  if (Np) *Np = c->Np;
+  if (Nq) *Nq = c->Nq;
+  if (Nqf) *Nqf = c->Nqf;
+  if (nloc) *nloc = c->nloc;
+  if (first) *first = c->first;
+  return ES_OK;
+}
+
+es_status es_rhs(es_context* c, const double* u, double* dudt) {
+  POISON_CHECK();
+  if (!u || !dudt) return fail(c, ES_ERR_ARG, "null buffer");
+  CK(cudaSetDevice(c->device));
+  RhsArgs A = base_rhs_args(c);
+  A.mode = 0;
+  A.out = dudt;
+  es_status s = rhs_pass(c, u, A, nullptr);
+  if (s != ES_OK) return s;
+  if (c->check_adm) return check_bad(c);
+  return ES_OK;
+}
+
+es_status es_rhs_host(es_context* c, const double* uh, double* duh) {
+  POISON_CHECK();
+  if (!uh || !duh) return fail(c, ES_ERR_ARG, "null buffer");
+  CK(cudaSetDevice(c->device));
+  const size_t bytes = (size_t)c->nloc * c->NC * c->Np * sizeof(double);
+  if (!c->hin) {
+    CK(cudaMalloc((void**)&c->hin, bytes));
+    CK(cudaMalloc((void**)&c->hout, bytes));
+  }
+  CK(cudaMemcpyAsync(c->hin, uh, bytes, cudaMemcpyHostToDevice, c->stream));
+  es_status s = es_rhs(c, c->hin, c->hout);
+  if (s != ES_OK) return s;
+  CK(cudaMemcpyAsync(duh, c->hout, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return ES_OK;
+}
+
+es_status es_set_state(es_context* c, const double* u) {
+  POISON_CHECK();
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(c->U, u, (size_t)c->nloc * c->NC * c->Np * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  return ES_OK;
+}
+es_status es_get_state(es_context* c, double* u) {
+  POISON_CHECK();
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(u, c->U, (size_t)c->nloc * c->NC * c->Np * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  return ES_OK;
+}
+
+es_status es_step(es_context* c, double dt, int nsteps) {
+  POISON_CHECK();
+  CK(cudaSetDevice(c->device));
+  for (int st = 0; st < nsteps; ++st) {
+    for (int s = 0; s < 4; ++s) {  // classical RK4 (R17), stage update fused in the RHS epilogue
+      RhsArgs A = base_rhs_args(c);
+      A.mode = 1 + s;
+      A.dt = dt;
+      A.u0 = c->U;
+      A.acc = c->ACC;
+      A.ustage = c->US;
+      A.out = c->U;
+      es_status r = rhs_pass(c, s == 0 ? c->U : c->US, A, nullptr);
+      if (r != ES_OK) return r;
+    }
+  }
+  if (c->check_adm) return check_bad(c);
+  return ES_OK;
+}
+
+es_status es_entropy_production(es_context* c, const double* u, double* rate, double* abs_scale,
+                                 double* cons) {
+  POISON_CHECK();
+  CK(cudaSetDevice(c->device));
+  const size_t nmod = (size_t)c->nloc * c->NC * c->Np;
+  double* scratch = c->ACC;  // the RK accumulator is free between steps
+  (void)nmod;
+  RhsArgs A = base_rhs_args(c);
+  A.mode = 5;
+  A.out = scratch;
+  A.wt = c->wt;
+  A.part = c->part;
+  es_status s = rhs_pass(c, u, A, c->wt);
+  if (s != ES_OK) return s;
+  const int w = 2 + c->NC;
+  CK(launch_reduce_parts(c->part, c->nloc, w, c->red, c->stream));
+  c->launches++;
+  if (c->world > 1) NK(ncclAllReduce(c->red, c->red, w, ncclDouble, ncclSum, c->comm, c->stream));
+  double h[8] = {0};
+  CK(cudaMemcpyAsync(h, c->red, w * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (rate) *rate = h[0];
+  if (abs_scale) *abs_scale = h[1];
+  if (cons)
+    for (int v = 0; v < c->NC; ++v) cons[v] = h[2 + v];
+  return check_bad(c);
+}
+
+es_status es_flux_counts(const es_context* c, int64_t* vol, int64_t* fac, int64_t* eq56, double* iface) {
+  if (!c) return ES_ERR_ARG;
+  int64_t n = c->n, q = c->p;
+  if (c->d == 2) {
+    if (vol) *vol = q * n * n;                 // two eta-line directions, n(n-1)/2 pairs per line
+    if (fac) *fac = 3 * n * n;                 // n volume nodes per facet node, 3 facets
+    if (eq56) *eq56 = 3 * n * n * (q + 2) / 2; // sum_l nnz(S^(l))/2 + sum nnz(R^T B)
+    if (iface) *iface = 3.0 * n;               // per element side
+  } else {
+    if (vol) *vol = 3 * q * n * n * n / 2;
+    if (fac) *fac = 3 * n * n * n + n * n * n * n;
+    if (eq56) *eq56 = 4 * n * n * n * n;
+    if (iface) *iface = 4.0 * n * n;
+  }
+  return ES_OK;
+}
+
+es_status es_node_coords(es_context* c, double* x) {
+  POISON_CHECK();
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(x, c->xq, (size_t)c->nloc * c->Nq * c->d * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  return ES_OK;
+}
+
+es_status es_project_nodal(es_context* c, const double* un, double* um) {
+  POISON_CHECK();
+  CK(cudaSetDevice(c->device));
+  c->launches++;
+  CK(c->d == 2 ? launch_projnodal_2d(c->n, c->R, c->nloc, un, um, c->stream)
+               : launch_projnodal_3d(c->n, c->R, c->nloc, un, um, c->stream));
+  return ES_OK;
+}
+
+es_status es_element_geometry(es_context* c, int64_t k, double* G, double* Jn, double* Jt) {
+  POISON_CHECK();
+  if (k < 0 || k >= c->nloc) return fail(c, ES_ERR_ARG, "element out of range");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  const int d = c->d, NG = d * d, Nq = c->Nq, Nqf = c->Nqf, Nf = c->Nf;
+  if (G) {
+    std::vector<double> gv((size_t)NG * Nq);
+    CK(cudaMemcpy(gv.data(), c->geo_vol + (size_t)k * (NG + 2) * Nq, gv.size() * 8, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < Nq; ++i)
+      for (int q = 0; q < NG; ++q) G[(size_t)i * NG + q] = gv[(size_t)q * Nq + i];
+  }
+  if (Jn) {
+    std::vector<double> gf((size_t)Nf * d * Nqf);
+    CK(cudaMemcpy(gf.data(), c->geo_face + (size_t)k * Nf * d * Nqf, gf.size() * 8, cudaMemcpyDeviceToHost));
+    for (int z = 0; z < Nf; ++z)
+      for (int f = 0; f < Nqf; ++f)
+        for (int m = 0; m < d; ++m) Jn[((size_t)z * Nqf + f) * d + m] = gf[((size_t)z * d + m) * Nqf + f];
+  }
+  if (Jt) CK(cudaMemcpy(Jt, c->jt + (size_t)k * Nq, (size_t)Nq * 8, cudaMemcpyDeviceToHost));
+  return ES_OK;
+}
+
+es_status es_synchronize(es_context* c) {
+  POISON_CHECK();
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaGetLastError());
+  return ES_OK;
+}
+
+void* es_stream(const es_context* c) { return c ? (void*)c->stream : nullptr; }
+int64_t es_launch_count(const es_context* c) { return c ? c->launches : 0; }
+void es_reset_launch_count(es_context* c) {
+  if (c) c->launches = 0;
+}
+
+es_status es_timing_enable(es_context* c, int on) {
+  POISON_CHECK();
+  CK(cudaStreamSynchronize(c->stream));
+  for (auto& t : c->tev) {
+    c->ev_pool.push_back(t.a);
+    c->ev_pool.push_back(t.b);
+  }
+  c->tev.clear();
+  c->timing = on != 0;
+  return ES_OK;
+}
+
+es_status es_timing_read(es_context* c, int cls, double* total_ms, int64_t* launches) {
+  POISON_CHECK();
+  CK(cudaStreamSynchronize(c->stream));
+  double tot = 0.0;
+  int64_t cnt = 0;
+  for (auto& t : c->tev) {
+    if (t.cls != cls) continue;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, t.a, t.b));
+    tot += ms;
+    ++cnt;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = cnt;
+  return ES_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,40 @@
+// geometry.cuh -- setup / utility kernel interfaces (product code)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace esb {
+
+struct GeoArgs {
+  int dim, Npg, Ncl, Nq, NF, Nqf;
+  const double* xmap;   // [ne][Npg][dim] mapping-node positions
+  // reference matrices as double-double pairs (hi, lo) built in long double (R25)
+  const double *LmapV, *DmapV, *DmapF, *DmapM, *LmapC, *DmapC, *DcurlV, *DcurlF;
+  const double *LmapV_lo, *DmapV_lo, *DmapF_lo, *DmapM_lo, *LmapC_lo, *DmapC_lo, *DcurlV_lo, *DcurlF_lo;
+  const double* Wvol;   // [Nq]
+  const double* nhat;   // [Nf][3]
+  const double* shift;  // [ne][dim] local-coordinate origin added back to xq (R25)
+  double* geo_vol;      // [ne][dim*dim+2][Nq]
+  double* geo_face;     // [ne][Nf][dim][Nqf]
+  double* xq;           // [ne][Nq][dim]
+  double* jt_out;       // optional [ne][Nq]
+  int* bad;
+};
+
+struct FaceCheckArgs {
+  int dim, n, Nqf;
+  int64_t nloc;
+  const double* geo_face;
+  const double* Bf;
+  const int64_t* face_slot;
+  const int* face_reflect;
+  unsigned long long* max_mismatch;
+};
+
+cudaError_t launch_geometry(const GeoArgs& g, int64_t ne, cudaStream_t st);
+cudaError_t launch_face_check(const FaceCheckArgs& a, cudaStream_t st);
+cudaError_t launch_pack(const double* trace, const int64_t* slots, int64_t nsend, int per_face, double* buf,
+                        cudaStream_t st);
+cudaError_t launch_reduce_parts(const double* part, int64_t ne, int w, double* out, cudaStream_t st);
+
+}  // namespace esb

@@ -1,0 +1,25 @@
+// kernels_3d.cu -- tetrahedron instantiations (q = p = N-1 in [1, 8]) of the kernels in kernels.cuh
+#include "kernels.cuh"
+
+namespace esb {
+#include "launch.inc"
+
+#define ES_CASES(F, ...) \
+  switch (n) {           \
+    case 2: return F<3, 2>(__VA_ARGS__);  \
+    case 3: return F<3, 3>(__VA_ARGS__);  \
+    case 4: return F<3, 4>(__VA_ARGS__);  \
+    case 5: return F<3, 5>(__VA_ARGS__);  \
+    case 6: return F<3, 6>(__VA_ARGS__);  \
+    case 7: return F<3, 7>(__VA_ARGS__);  \
+    case 8: return F<3, 8>(__VA_ARGS__);  \
+    case 9: return F<3, 9>(__VA_ARGS__);  \
+    default: return cudaErrorInvalidValue; \
+  }
+
+cudaError_t launch_project_3d(int n, const DevRef& R, const ProjArgs& A, cudaStream_t st) { ES_CASES(do_project, R, A, st) }
+cudaError_t launch_rhs_3d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st) { ES_CASES(do_rhs, R, A, st) }
+cudaError_t launch_projnodal_3d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st) {
+  ES_CASES(do_projnodal, R, ne, un, um, st)
+}
+}  // namespace esb

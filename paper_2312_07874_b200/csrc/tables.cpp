@@ -1,0 +1,457 @@
+// tables.cpp -- host construction of the reference tables used by the sm_100a kernels.
+//
+// Independent of oracle/: nodes by Golub-Welsch (implicit-QL eigenvalues of the Jacobi matrix)
+// polished by Newton on the monic recurrence, weights by the Gauss-Christoffel formula, Lagrange
+// data by the barycentric formula, and PKD gradients by forward-mode dual numbers.
+// Citations: P:<line> = PAPER.md.
+#include <quadmath.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+
+namespace esb {
+namespace {
+
+// ---------------- monic Jacobi recurrence p_{k+1} = (x - al_k) p_k - be_k p_{k-1} ----------------
+struct Monic {
+  std::vector<double> al, be;  // be[0] = mu0 = int (1-x)^a (1+x)^b
+};
+Monic monic_coeffs(int N, double a, double b) {
+  Monic m;
+  m.al.resize(N + 1);
+  m.be.resize(N + 1);
+  for (int k = 0; k <= N; ++k) {
+    double s = 2.0 * k + a + b;
+    m.al[k] = (k == 0) ? (b - a) / (a + b + 2.0) : (b * b - a * a) / (s * (s + 2.0));
+    if (k == 0)
+      m.be[k] = std::exp((a + b + 1.0) * std::log(2.0) + std::lgamma(a + 1.0) + std::lgamma(b + 1.0) -
+                         std::lgamma(a + b + 2.0));
+    else if (k == 1)
+      m.be[k] = 4.0 * (1.0 + a) * (1.0 + b) / ((2.0 + a + b) * (2.0 + a + b) * (3.0 + a + b));
+    else
+      m.be[k] = 4.0 * k * (k + a) * (k + b) * (k + a + b) / (s * s * (s + 1.0) * (s - 1.0));
+  }
+  return m;
+}
+
+// normalised Jacobi value via the orthonormal recurrence derived from the monic one
+double pnorm(int n, double a, double b, double x) {
+  Monic m = monic_coeffs(n + 1, a, b);
+  double pm = 0.0, pc = 1.0 / sqrt(m.be[0]);
+  for (int k = 0; k < n; ++k) {
+    double pn = ((x - m.al[k]) * pc - (k > 0 ? sqrt(m.be[k]) * pm : 0.0)) / sqrt(m.be[k + 1]);
+    pm = pc;
+    pc = pn;
+  }
+  return pc;
+}
+
+// symmetric tridiagonal eigen-decomposition (implicit QL with Wilkinson-type shifts)
+bool tridiag_eig(std::vector<double>& dg, std::vector<double> e, int n, std::vector<double>& z) {
+  z.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) z[(size_t)i * n + i] = 1.0;
+  e.resize(n, 0.0);
+  e[n - 1] = 0.0;
+  for (int l = 0; l < n; ++l) {
+    int iter = 0, m;
+    do {
+      for (m = l; m < n - 1; ++m) {
+        double dd = std::fabs(dg[m]) + std::fabs(dg[m + 1]);
+        if (std::fabs(e[m]) <= 1e-300 + 2.2e-16 * dd) break;
+      }
+      if (m != l) {
+        if (iter++ == 100) return false;
+        double g = (dg[l + 1] - dg[l]) / (2.0 * e[l]);
+        double r = std::hypot(g, 1.0);
+        g = dg[m] - dg[l] + e[l] / (g + std::copysign(r, g));
+        double s = 1.0, c = 1.0, pp = 0.0;
+        int i;
+        bool early = false;
+        for (i = m - 1; i >= l; --i) {
+          double f = s * e[i], bb = c * e[i];
+          r = std::hypot(f, g);
+          e[i + 1] = r;
+          if (r == 0.0) {
+            dg[i + 1] -= pp;
+            e[m] = 0.0;
+            early = true;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = dg[i + 1] - pp;
+          r = (dg[i] - g) * s + 2.0 * c * bb;
+          pp = s * r;
+          dg[i + 1] = g + pp;
+          g = c * r - bb;
+          for (int k = 0; k < n; ++k) {
+            double t = z[(size_t)k * n + i + 1];
+            z[(size_t)k * n + i + 1] = s * z[(size_t)k * n + i] + c * t;
+            z[(size_t)k * n + i] = c * z[(size_t)k * n + i] - s * t;
+          }
+        }
+        if (early) continue;
+        dg[l] -= pp;
+        e[l] = g;
+        e[m] = 0.0;
+      }
+    } while (m != l);
+  }
+  return true;
+}
+
+// Gauss rule w.r.t. (1-x)^a (1+x)^b with N nodes: Golub-Welsch, Newton polish,
+// Gauss-Christoffel weights  w_i = ||p_{N-1}||^2 / (p_{N-1}(x_i) p_N'(x_i)).
+bool gauss_rule(int N, double a, double b, std::vector<double>& x, std::vector<double>& w) {
+  Monic m = monic_coeffs(N + 1, a, b);
+  std::vector<double> dg(N), e(N, 0.0), z;
+  for (int k = 0; k < N; ++k) dg[k] = m.al[k];
+  for (int k = 0; k + 1 < N; ++k) e[k] = sqrt(m.be[k + 1]);
+  if (!tridiag_eig(dg, e, N, z)) return false;
+  x = dg;
+  std::sort(x.begin(), x.end());
+  double norm2 = m.be[0];
+  for (int k = 1; k < N; ++k) norm2 *= m.be[k];
+  w.resize(N);
+  for (int i = 0; i < N; ++i) {
+    double xi = x[i];
+    double pN = 0, dpN = 0, pN1 = 0;
+    for (int it = 0; it < 3; ++it) {
+      double p0 = 1.0, d0 = 0.0, p1 = xi - m.al[0], d1 = 1.0;
+      if (N == 1) {
+        p1 = xi - m.al[0];
+        d1 = 1.0;
+        p0 = 1.0;
+      }
+      for (int k = 1; k < N; ++k) {
+        double p2 = (xi - m.al[k]) * p1 - m.be[k] * p0;
+        double d2 = p1 + (xi - m.al[k]) * d1 - m.be[k] * d0;
+        p0 = p1;
+        d0 = d1;
+        p1 = p2;
+        d1 = d2;
+      }
+      pN = p1;
+      dpN = d1;
+      pN1 = p0;
+      if (it < 2) xi -= pN / dpN;
+    }
+    x[i] = xi;
+    w[i] = norm2 / (pN1 * dpN);
+  }
+  return true;
+}
+
+// barycentric Lagrange data on nodes x
+std::vector<double> bary_weights(const std::vector<double>& x) {
+  int n = (int)x.size();
+  std::vector<double> lam(n, 1.0);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < n; ++k)
+      if (k != j) lam[j] /= (x[j] - x[k]);
+  return lam;
+}
+std::vector<double> lagrange_at(const std::vector<double>& x, double t) {
+  int n = (int)x.size();
+  std::vector<double> lam = bary_weights(x), l(n, 0.0);
+  for (int j = 0; j < n; ++j)
+    if (t == x[j]) {
+      l[j] = 1.0;
+      return l;
+    }
+  double den = 0.0;
+  for (int j = 0; j < n; ++j) den += lam[j] / (t - x[j]);
+  for (int j = 0; j < n; ++j) l[j] = lam[j] / (t - x[j]) / den;
+  return l;
+}
+std::vector<double> diff_matrix(const std::vector<double>& x) {  // D[i][j] = l_j'(x_i)
+  int n = (int)x.size();
+  std::vector<double> lam = bary_weights(x), D((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int j = 0; j < n; ++j)
+      if (j != i) {
+        D[(size_t)i * n + j] = lam[j] / lam[i] / (x[i] - x[j]);
+        s += D[(size_t)i * n + j];
+      }
+    D[(size_t)i * n + i] = -s;
+  }
+  return D;
+}
+std::vector<double> skew_of(const std::vector<double>& X, int n) {
+  std::vector<double> S((size_t)n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) S[(size_t)i * n + j] = 0.5 * (X[(size_t)i * n + j] - X[(size_t)j * n + i]);
+  return S;
+}
+
+// ---------------- geometry tables in binary128 ----------------
+// The geometry of an element is built from Lagrange interpolants on the equispaced barycentric
+// lattice of degree N (R10).  For that lattice the Lagrange basis has Silvester's closed form
+//   l_alpha(lam) = prod_k prod_{j < alpha_k} (N lam_k - j) / (j + 1),   |alpha| = N,
+// so the tables need no Vandermonde inverse.  They are evaluated in binary128 and stored as
+// double-double pairs because the device sums them against data with cancellation (R25).
+typedef __float128 LD;
+
+// equispaced barycentric lattice of degree N (R10): reference coords [M][d], barycentric [M][d+1]
+template <class T>
+void lattice_nodes(int d, int N, std::vector<T>& xi, std::vector<double>& bary) {
+  xi.clear();
+  bary.clear();
+  if (d == 2) {
+    for (int i = 0; i <= N; ++i)
+      for (int j = 0; j <= N - i; ++j) {
+        double l2 = double(i) / N, l3 = double(j) / N;
+        bary.insert(bary.end(), {1.0 - l2 - l3, l2, l3});
+        xi.insert(xi.end(), {(T)(2 * i) / N - 1, (T)(2 * j) / N - 1});
+      }
+  } else {
+    for (int i = 0; i <= N; ++i)
+      for (int j = 0; j <= N - i; ++j)
+        for (int k = 0; k <= N - i - j; ++k) {
+          double l2 = double(i) / N, l3 = double(j) / N, l4 = double(k) / N;
+          bary.insert(bary.end(), {1.0 - l2 - l3 - l4, l2, l3, l4});
+          xi.insert(xi.end(), {(T)(2 * i) / N - 1, (T)(2 * j) / N - 1, (T)(2 * k) / N - 1});
+        }
+  }
+}
+
+// Lagrange basis (and gradients) of the degree-N lattice evaluated at points X[npts][d] (reference
+// coordinates), stored as double-double pairs: out = [hi block | lo block]
+void lattice_basis(int d, int N, const std::vector<double>& X, int npts, std::vector<double>* L,
+                   std::vector<double>* Dg /*[d][npts][M]*/) {
+  std::vector<double> lxi, lb;
+  lattice_nodes<double>(d, N, lxi, lb);
+  const int nb = d + 1, M = (int)lb.size() / nb;
+  std::vector<int> alpha((size_t)M * nb);
+  for (int i = 0; i < M; ++i)
+    for (int k = 0; k < nb; ++k) alpha[(size_t)i * nb + k] = (int)std::lround(lb[(size_t)i * nb + k] * N);
+  size_t nL = (size_t)npts * M, nD = (size_t)d * npts * M;
+  if (L) L->assign(2 * nL, 0.0);
+  if (Dg) Dg->assign(2 * nD, 0.0);
+  auto put = [](std::vector<double>& out, size_t n, size_t idx, LD v) {
+    double hi = (double)v;
+    out[idx] = hi;
+    out[n + idx] = (double)(v - (LD)hi);
+  };
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int x = 0; x < npts; ++x) {
+    // barycentric coordinates: lam_{k+1} = (1 + xi_k)/2, lam_1 = 1 - sum; d lam_{k+1}/d xi_l = delta/2,
+    // d lam_1 / d xi_l = -1/2
+    LD lam[4];
+    LD sum = 0;
+    for (int k = 0; k < d; ++k) {
+      lam[k + 1] = ((LD)1 + (LD)X[(size_t)x * d + k]) / (LD)2;
+      sum += lam[k + 1];
+    }
+    lam[0] = (LD)1 - sum;
+    for (int i = 0; i < M; ++i) {
+      const int* al = &alpha[(size_t)i * nb];
+      LD f[4], df[4];  // factor prod_{j<a}(N lam - j)/(j+1) and its derivative w.r.t. lam
+      for (int k = 0; k < nb; ++k) {
+        LD v = 1, dv = 0;
+        for (int j = 0; j < al[k]; ++j) {
+          LD t = ((LD)N * lam[k] - (LD)j) / (LD)(j + 1);
+          dv = dv * t + v * (LD)N / (LD)(j + 1);
+          v = v * t;
+        }
+        f[k] = v;
+        df[k] = dv;
+      }
+      LD val = 1;
+      for (int k = 0; k < nb; ++k) val *= f[k];
+      if (L) put(*L, nL, (size_t)x * M + i, val);
+      if (Dg) {
+        for (int l = 0; l < d; ++l) {
+          // d/dxi_l = 1/2 (d/dlam_{l+1} - d/dlam_0)
+          LD g = 0;
+          for (int k = 0; k < nb; ++k) {
+            if (k != l + 1 && k != 0) continue;
+            LD prod = df[k];
+            for (int kk = 0; kk < nb; ++kk)
+              if (kk != k) prod *= f[kk];
+            g += (k == 0) ? -prod : prod;
+          }
+          put(*Dg, nD, ((size_t)l * npts + x) * M + i, g / (LD)2);
+        }
+      }
+    }
+  }
+}
+
+void collapse(int d, const double* e, double* x) {
+  if (d == 2) {
+    x[0] = 0.5 * (1.0 + e[0]) * (1.0 - e[1]) - 1.0;
+    x[1] = e[1];
+  } else {  // P:263 with the (1-eta3) factor (R1)
+    x[0] = 0.25 * (1.0 + e[0]) * (1.0 - e[1]) * (1.0 - e[2]) - 1.0;
+    x[1] = 0.5 * (1.0 + e[1]) * (1.0 - e[2]) - 1.0;
+    x[2] = e[2];
+  }
+}
+
+}  // namespace
+
+bool build_ref_tables(int d, int p, RefTables& t, std::string& err) {
+  if (!((d == 2 && p >= 1 && p <= 10) || (d == 3 && p >= 1 && p <= 8))) {
+    err = "unsupported (dim, p)";
+    return false;
+  }
+  t.d = d;
+  t.p = p;
+  int n = p + 1;
+  t.n = n;
+  t.Nq = d == 2 ? n * n : n * n * n;
+  t.Nf = d + 1;
+  t.Nqf = d == 2 ? n : n * n;
+  t.Np = d == 2 ? (p + 1) * (p + 2) / 2 : (p + 1) * (p + 2) * (p + 3) / 6;
+  if (!gauss_rule(n, 0.0, 0.0, t.eta, t.w) || !gauss_rule(n, 1.0, 0.0, t.eta3, t.w3)) {
+    err = "Gauss rule construction failed";
+    return false;
+  }
+  const auto& e = t.eta;
+  const auto& w = t.w;
+  const auto& e3 = t.eta3;
+  const auto& w3 = t.w3;
+  // 1D line operators: X = diag(weight) D, S-line = skew(X)
+  std::vector<double> D = diff_matrix(e), D3 = diff_matrix(e3);
+  std::vector<double> Q1(n * n), A1(n * n), A2(n * n), A3(n * n), A4(n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      Q1[i * n + j] = w[i] * D[i * n + j];
+      A1[i * n + j] = w[i] * (1.0 + e[i]) / 2.0 * D[i * n + j];
+      A2[i * n + j] = w[i] * (1.0 - e[i]) / 2.0 * D[i * n + j];
+      A3[i * n + j] = w[i] * (1.0 - e[i] * e[i]) / 4.0 * D[i * n + j];
+      A4[i * n + j] = w3[i] * (1.0 - e3[i]) * D3[i * n + j];
+    }
+  t.skQ1 = skew_of(Q1, n);
+  t.skA1 = skew_of(A1, n);
+  t.skA2 = skew_of(A2, n);
+  t.skA3 = skew_of(A3, n);
+  t.skA4 = skew_of(A4, n);
+  t.lL = lagrange_at(e, -1.0);
+  t.lR = lagrange_at(e, 1.0);
+  t.l3L = lagrange_at(e3, -1.0);
+  t.lint4.assign(n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    std::vector<double> l = lagrange_at(e, e3[j]);
+    for (int b = 0; b < n; ++b) t.lint4[j * n + b] = l[b];
+  }
+  // PKD principal-function tables
+  t.psi1.assign(n * n, 0.0);
+  t.psi2.assign((size_t)n * n * n, 0.0);
+  t.psi3.assign((size_t)n * n * n, 0.0);
+  for (int a1 = 0; a1 <= p; ++a1)
+    for (int a = 0; a < n; ++a) t.psi1[a1 * n + a] = std::sqrt(2.0) * pnorm(a1, 0.0, 0.0, e[a]);
+  for (int a1 = 0; a1 <= p; ++a1)
+    for (int a2 = 0; a2 <= p - a1; ++a2)
+      for (int b = 0; b < n; ++b)
+        t.psi2[((size_t)a1 * n + a2) * n + b] = std::pow(1.0 - e[b], a1) * pnorm(a2, 2.0 * a1 + 1.0, 0.0, e[b]);
+  if (d == 3)
+    for (int s = 0; s <= p; ++s)
+      for (int a3 = 0; a3 <= p - s; ++a3)
+        for (int c = 0; c < n; ++c)
+          t.psi3[((size_t)s * n + a3) * n + c] =
+              2.0 * std::pow(1.0 - e3[c], s) * pnorm(a3, 2.0 * s + 2.0, 0.0, e3[c]);
+  // modal order (ABI): a1-major nested
+  t.pair_a1.clear();
+  t.pair_a2.clear();
+  t.pair_off.clear();
+  int off = 0;
+  for (int a1 = 0; a1 <= p; ++a1) {
+    if (d == 2) {
+      t.pair_a1.push_back(a1);
+      t.pair_a2.push_back(0);
+      t.pair_off.push_back(off);
+      off += p - a1 + 1;
+    } else {
+      for (int a2 = 0; a2 <= p - a1; ++a2) {
+        t.pair_a1.push_back(a1);
+        t.pair_a2.push_back(a2);
+        t.pair_off.push_back(off);
+        off += p - a1 - a2 + 1;
+      }
+    }
+  }
+  if (off != t.Np) {
+    err = "modal count mismatch";
+    return false;
+  }
+  // nodes and weights
+  t.Wvol.assign(t.Nq, 0.0);
+  t.xi_vol.assign((size_t)t.Nq * d, 0.0);
+  t.Bf.assign((size_t)t.Nf * t.Nqf, 0.0);
+  t.xi_face.assign((size_t)t.Nf * t.Nqf * d, 0.0);
+  t.nhat.assign((size_t)t.Nf * 3, 0.0);
+  if (d == 2) {
+    for (int b = 0; b < n; ++b)
+      for (int a = 0; a < n; ++a) {
+        int i = a + n * b;
+        double et[2] = {e[a], e[b]};
+        collapse(2, et, &t.xi_vol[i * 2]);
+        t.Wvol[i] = w[a] * w[b] * (1.0 - e[b]) / 2.0;
+      }
+    for (int f = 0; f < n; ++f) {
+      double f1[2] = {e[f], -1.0}, f2[2] = {1.0, e[f]}, f3[2] = {-1.0, e[f]};
+      collapse(2, f1, &t.xi_face[(0 * n + f) * 2]);
+      collapse(2, f2, &t.xi_face[(1 * n + f) * 2]);
+      collapse(2, f3, &t.xi_face[(2 * n + f) * 2]);
+      t.Bf[0 * n + f] = w[f];
+      t.Bf[1 * n + f] = std::sqrt(2.0) * w[f];
+      t.Bf[2 * n + f] = w[f];
+    }
+    double r2 = std::sqrt(0.5);
+    double nh[9] = {0, -1, 0, r2, r2, 0, -1, 0, 0};
+    std::memcpy(t.nhat.data(), nh, sizeof(nh));
+  } else {
+    for (int c = 0; c < n; ++c)
+      for (int b = 0; b < n; ++b)
+        for (int a = 0; a < n; ++a) {
+          int i = a + n * b + n * n * c;
+          double et[3] = {e[a], e[b], e3[c]};
+          collapse(3, et, &t.xi_vol[i * 3]);
+          t.Wvol[i] = w[a] * w[b] * w3[c] * (1.0 - e[b]) * (1.0 - e3[c]) / 8.0;
+        }
+    int Nqf = t.Nqf;
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        int f = i + n * j;
+        double f1[3] = {e[i], -1.0, e3[j]}, f2[3] = {1.0, e[i], e3[j]}, f3[3] = {-1.0, e[i], e3[j]},
+               f4[3] = {e[i], e3[j], -1.0};
+        collapse(3, f1, &t.xi_face[(0 * Nqf + f) * 3]);
+        collapse(3, f2, &t.xi_face[(1 * Nqf + f) * 3]);
+        collapse(3, f3, &t.xi_face[(2 * Nqf + f) * 3]);
+        collapse(3, f4, &t.xi_face[(3 * Nqf + f) * 3]);
+        double ww = w[i] * w3[j];
+        t.Bf[0 * Nqf + f] = 0.5 * ww;
+        t.Bf[1 * Nqf + f] = std::sqrt(3.0) / 2.0 * ww;
+        t.Bf[2 * Nqf + f] = 0.5 * ww;
+        t.Bf[3 * Nqf + f] = 0.5 * ww;
+      }
+    double r3 = 1.0 / std::sqrt(3.0);
+    double nh[12] = {0, -1, 0, r3, r3, r3, -1, 0, 0, 0, 0, -1};
+    std::memcpy(t.nhat.data(), nh, sizeof(nh));
+  }
+  // geometry interpolation matrices (P:327 mapping of degree p_g = p, P:349 curl lattice q+1)
+  std::vector<double> lxi;
+  lattice_nodes<double>(d, p, lxi, t.lat_bary);
+  t.Npg = (int)t.lat_bary.size() / (d + 1);
+  lattice_basis(d, p, t.xi_vol, t.Nq, &t.LmapV, d == 2 ? &t.DmapV : nullptr);
+  lattice_basis(d, p, lxi, t.Npg, nullptr, &t.DmapM);
+  if (d == 2) {
+    lattice_basis(d, p, t.xi_face, t.Nf * t.Nqf, nullptr, &t.DmapF);
+  } else {
+    std::vector<double> cxi, cb;
+    lattice_nodes<double>(d, p + 1, cxi, cb);
+    t.Ncl = (int)cb.size() / (d + 1);
+    lattice_basis(d, p, cxi, t.Ncl, &t.LmapC, &t.DmapC);
+    lattice_basis(d, p + 1, t.xi_vol, t.Nq, nullptr, &t.DcurlV);
+    lattice_basis(d, p + 1, t.xi_face, t.Nf * t.Nqf, nullptr, &t.DcurlF);
+  }
+  return true;
+}
+
+}  // namespace esb

@@ -1,0 +1,52 @@
+"""CPU checks of the product boundary: the C-ABI library builds, loads, and exports every symbol
+that include/es.h declares (no compute calls without a GPU)."""
+import ctypes
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def es():
+    from tools.build import build_lib
+    build_lib()
+    import paper_2312_07874_b200 as es
+    return es
+
+
+def test_library_exports_every_declared_symbol(es):
+    names = es.declared_symbols()
+    assert len(names) >= 18
+    lib = ctypes.CDLL(es.LIB_PATH)
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", es.LIB_PATH], capture_output=True, text=True).stdout
+    for n in names:
+        assert f" T {n}" in out, n
+
+
+def test_library_is_sm100a(es):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", es.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_oracle_not_linked_into_product(es):
+    out = subprocess.run(["ldd", es.LIB_PATH], capture_output=True, text=True).stdout
+    assert "oracle" not in out
+    src = os.path.join(ROOT, "paper_2312_07874_b200")
+    for dirpath, _, files in os.walk(src):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h", ".inc")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "oracle.h" not in txt and "liboracle" not in txt, f
+
+
+def test_setup_rejects_bad_arguments_without_gpu(es):
+    # argument validation happens before any CUDA call
+    h = ctypes.c_void_p()
+    rc = es.es_setup(ctypes.byref(h), None, 2, es.es_map_fn(0), None, None)
+    assert rc == es.ES_ERR_ARG

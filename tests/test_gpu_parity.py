@@ -1,0 +1,224 @@
+"""GPU <-> oracle parity of the sm_100a ES modal DSEM right-hand side (B200 required).
+
+Tolerance (BASELINE.json north_star, reading R20): per conserved variable e,
+    max_{k,i} |du_gpu - du_ora| / max_{k,i} |du_ora| <= 1e-11,
+free-stream states use an absolute bound relative to the flux scale.  Integer flux counts must match
+exactly.  Inputs are seeded and identical for both sides: modal coefficients are produced by the
+oracle's projection of the analytic initial data (small meshes) or by es_inputs directly (full-size
+meshes), never by the CUDA path.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import es_inputs as I
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+@pytest.fixture(scope="module")
+def es():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2312_07874_b200 as es
+    return es
+
+
+def _L(d):
+    return 2.0 if d == 2 else 2.0 * math.pi
+
+
+def _warp(kind, d, L, M):
+    return {"paper": I.paper_warp(d, L), "bj": I.bj_warp(d, L, M), "none": None}[kind]
+
+
+def _ic(kind, x, d, L):
+    if kind == "tgv":
+        return I.taylor_green(x, Ma=0.1)
+    if kind == "tgv3":
+        return I.taylor_green(x, Ma=0.3)
+    if kind == "wave":
+        return I.density_wave(x, L)
+    if kind == "vortex":
+        return I.isentropic_vortex(x, L)
+    return I.free_stream(x, d)
+
+
+def _setup(es, d, M, p, warp, ic, fm, seed=1):
+    L = _L(d)
+    mesh = I.split_cartesian(d, M, L)
+    w = _warp(warp, d, L, M)
+    om = O.Mesh(mesh, p, warp=w)
+    u = om.project(_ic(ic, om.node_coords(), d, L))
+    u = I.perturb_modal(u, d, p, seed=seed, amp=1e-2)
+    ctx = es.Context(mesh, p, warp=w, interface_flux=fm)
+    return mesh, om, ctx, u
+
+
+def _relerr(a, b):
+    d = a.shape[1]
+    out = []
+    for v in range(d):
+        out.append(np.abs(a[:, v] - b[:, v]).max() / max(np.abs(b[:, v]).max(), 1e-300))
+    return np.array(out)
+
+
+def _gpu_rhs(ctx, u):
+    ut = torch.from_numpy(u).cuda()
+    du = torch.empty_like(ut)
+    ctx.rhs(ut, du)
+    ctx.synchronize()
+    return du.cpu().numpy()
+
+
+CASES = [
+    # d, M, p, warp, ic, flux mode
+    (2, 4, 2, "none", "vortex", 1),    # C1 geometry (affine), p = 2
+    (2, 3, 3, "paper", "wave", 1),     # even line length
+    (2, 4, 4, "bj", "wave", 1),        # C2 family
+    (2, 3, 4, "paper", "vortex", 0),   # EC
+    (2, 3, 6, "paper", "wave", 1),
+    (2, 3, 10, "bj", "vortex", 1),     # C3 degree
+    (3, 3, 2, "paper", "tgv3", 1),
+    (3, 3, 3, "paper", "tgv3", 1),     # even line length
+    (3, 3, 4, "bj", "tgv", 0),         # C4 family, EC
+    (3, 3, 4, "paper", "tgv3", 1),
+    (3, 3, 6, "paper", "tgv3", 1),
+    (3, 3, 8, "bj", "tgv", 1),         # C5 degree
+]
+
+
+@pytest.mark.parametrize("d,M,p,warp,ic,fm", CASES)
+def test_rhs_parity(es, d, M, p, warp, ic, fm):
+    mesh, om, ctx, u = _setup(es, d, M, p, warp, ic, fm)
+    ref, st = om.rhs(u, flux_mode=fm, variant=1)
+    got = _gpu_rhs(ctx, u)
+    err = _relerr(got, ref)
+    assert (err <= TOL).all(), err
+    c = ctx.flux_counts()
+    assert c["volume"] * om.ne == st.volume_pairs
+    assert c["facet"] * om.ne == st.facet_pairs
+
+
+def test_free_stream_gpu(es):
+    for d, p in ((2, 4), (3, 3)):
+        L = _L(d)
+        mesh = I.split_cartesian(d, 3, L)
+        w = I.paper_warp(d, L)
+        om = O.Mesh(mesh, p, warp=w)
+        u = om.project(I.free_stream(om.node_coords(), d))
+        ctx = es.Context(mesh, p, warp=w, interface_flux=1)
+        got = _gpu_rhs(ctx, u)
+        assert np.abs(got).max() < 1e-10
+
+
+@pytest.mark.parametrize("d,p", [(2, 3), (3, 3)])
+def test_geometry_and_nodes_parity(es, d, p):
+    L = _L(d)
+    mesh = I.split_cartesian(d, 3, L)
+    w = I.paper_warp(d, L)
+    om = O.Mesh(mesh, p, warp=w)
+    ctx = es.Context(mesh, p, warp=w)
+    x = torch.empty((ctx.nloc, ctx.Nq, d), dtype=torch.float64, device="cuda")
+    ctx.node_coords(x)
+    xg = x.cpu().numpy()
+    for e in (0, 7, om.ne - 1):
+        go = om.geometry(e)
+        gg = ctx.element_geometry(e)
+        assert np.abs(gg["G"] - go["G"]).max() < 1e-12 * np.abs(go["G"]).max()
+        assert np.abs(gg["Jn"] - go["Jn"]).max() < 1e-12 * np.abs(go["Jn"]).max()
+        assert np.abs(gg["Jt"] - go["Jt"]).max() < 1e-12 * np.abs(go["Jt"]).max()
+        assert np.abs(xg[e] - go["xq"]).max() < 1e-12 * L
+    # projection of nodal data (R18)
+    un = I.density_wave(xg, L) if d == 2 else I.taylor_green(xg, 0.3)
+    um = torch.empty((ctx.nloc, d + 2, ctx.Np), dtype=torch.float64, device="cuda")
+    ctx.project_nodal(torch.from_numpy(np.ascontiguousarray(un)).cuda(), um)
+    ref = om.project(un)
+    assert np.abs(um.cpu().numpy() - ref).max() < 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("d,p,fm", [(2, 3, 1), (3, 2, 0), (3, 3, 1)])
+def test_entropy_production_parity(es, d, p, fm):
+    mesh, om, ctx, u = _setup(es, d, 3, p, "paper", "wave" if d == 2 else "tgv3", fm)
+    ref, st = om.rhs(u, flux_mode=fm, variant=1)
+    rate, scale, cons = ctx.entropy_production(torch.from_numpy(u).cuda())
+    if fm == 0:
+        assert abs(rate) < 1e-12 * st.entropy_abs
+    else:
+        assert rate < 0 and abs(rate - st.entropy_rate) < 1e-10 * st.entropy_abs
+    assert np.abs(cons).max() < 1e-12 * om.ne * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("d,p", [(2, 2), (3, 2)])
+def test_rk4_steps_parity(es, d, p):
+    # C1-style: 10 RK4 steps on the library state vs the oracle's RK4 (R17)
+    mesh, om, ctx, u = _setup(es, d, 4 if d == 2 else 3, p, "none" if d == 2 else "paper",
+                              "vortex" if d == 2 else "tgv3", 1)
+    dt = 1e-3
+    ref = om.rk4(u, dt, 10, flux_mode=1)
+    ut = torch.from_numpy(u).cuda()
+    ctx.set_state(ut)
+    ctx.step(dt, 10)
+    out = torch.empty_like(ut)
+    ctx.get_state(out)
+    ctx.synchronize()
+    got = out.cpu().numpy()
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err < 1e-13, err
+    # the update itself: compare the increments
+    inc = _relerr(got - u, ref - u)
+    assert (inc < 1e-10).all(), inc
+
+
+def test_host_entry_point_matches_device(es):
+    mesh, om, ctx, u = _setup(es, 2, 4, 4, "bj", "wave", 1)
+    got = _gpu_rhs(ctx, u)
+    out = np.zeros_like(u)
+    ctx.rhs_host(np.ascontiguousarray(u), out)
+    assert np.array_equal(out, got)  # bitwise: same kernels, same inputs
+    again = _gpu_rhs(ctx, u)
+    assert np.array_equal(again, got)  # deterministic
+
+
+def test_inadmissible_state_flagged(es):
+    L = 2.0
+    mesh = I.split_cartesian(2, 3, L)
+    ctx = es.Context(mesh, 2, check_admissibility=1)
+    om = O.Mesh(mesh, 2)
+    u = om.project(I.density_wave(om.node_coords(), L))
+    u[3, 0, :] *= -1.0  # negative density in element 3
+    ut = torch.from_numpy(u).cuda()
+    with pytest.raises(es.ESError) as ex:
+        ctx.rhs(ut, torch.empty_like(ut))
+    assert ex.value.code == es.ES_ERR_INADMISSIBLE
+
+
+FULL = [
+    # BASELINE configs at full size, sampled elements checked against the oracle
+    ("C2", 2, 32, 4, "bj", "density_wave", 1),
+    ("C3", 2, 64, 10, "bj", "vortex", 1),
+    ("C4", 3, 16, 4, "bj", "tgv", 0),
+    ("C5", 3, 32, 8, "bj", "tgv", 1),
+]
+
+
+@pytest.mark.parametrize("name,d,M,p,warp,kind,fm", FULL)
+def test_full_size_sampled_parity(es, name, d, M, p, warp, kind, fm):
+    L = _L(d)
+    mesh = I.split_cartesian(d, M, L)
+    w = _warp(warp, d, L, M)
+    u = I.modal_state_from_centroids(mesh, p, kind, seed=3, amp=1e-2)
+    ctx = es.Context(mesh, p, warp=w, interface_flux=fm)
+    got = _gpu_rhs(ctx, u)
+    ne = len(mesh["elem_vertices"])
+    rng = np.random.default_rng(11)
+    sample = np.unique(np.concatenate([[0, ne - 1, ne // 2], rng.integers(0, ne, 5)]))
+    om = O.Mesh(mesh, p, warp=w, active=sample)
+    ref, st = om.rhs(u, flux_mode=fm, variant=1, elems=sample)
+    err = _relerr(got[sample], ref[sample])
+    assert (err <= TOL).all(), (name, err)

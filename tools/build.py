@@ -56,6 +56,8 @@ def build_lib(force=False, jobs=8):
             o = os.path.join(bdir, f + ".o")
             cmd = [NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                    *inc, "-c", p, "-o", o]
+            if f == "api.cu":
+                cmd = [NVCC, *ARCH, "-std=c++17", "-O2", "-Xcompiler", "-fPIC", *inc, "-c", p, "-o", o]
         elif f.endswith(".cpp"):
             o = os.path.join(bdir, f + ".o")
             cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-fopenmp", *inc, "-I", "/usr/local/cuda/include",
@@ -71,7 +73,7 @@ def build_lib(force=False, jobs=8):
             procs = []
     _wait(procs)
     _run([NVCC, *ARCH, "-shared", "-o", LIB_SO, *objs, "-Xcompiler", "-fopenmp",
-          "-L/usr/local/cuda/lib64", "-lcudart", "-lnccl"])
+          "-L/usr/local/cuda/lib64", "-lcudart", "-lnccl", "-lquadmath"])
     return LIB_SO
 
 
