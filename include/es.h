@@ -119,6 +119,21 @@ es_status es_project_nodal(es_context* ctx, const double* u_nodal, double* u_mod
 es_status es_element_geometry(es_context* ctx, int64_t local_element, double* G, double* Jn,
                               double* Jt);
 
+/* Host-only (no GPU needed): the reference tables the kernels use for (dim, p), copied to the host
+ * buffer out (capacity cap doubles); *n receives the length.  Names: "eta","w","eta3","w3" [n];
+ * "skQ1","skA1","skA2","skA3","skA4" [n][n] skew line operators; "lL","lR","l3L" [n];
+ * "lint4" [n][n]; "psi1" [n][n], "psi2","psi3" [n][n][n]; "Wvol" [N_q]; "Bf" [N_f][N_qf];
+ * "xi_vol" [N_q][dim].  Returns ES_ERR_ARG for an unknown name or too small a buffer. */
+es_status es_ref_table(int dim, int p, const char* name, double* out, int64_t cap, int64_t* n);
+
+/* Host-only: connectivity and halo plan of rank `rank` of `world` (no GPU).  face_slot [n_local][N_f]
+ * (trace slot of the neighbour face: local slots e*N_f+z, halo slots n_local*N_f + h),
+ * face_reflect [n_local][N_f], send_slots [n_send], send_count/recv_count [world]; any output may be
+ * NULL; *n_send, *n_halo receive the sizes. */
+es_status es_plan(int dim, int64_t n_elements, const int64_t* elem_vertices, int rank, int world,
+                  int64_t* face_slot, int* face_reflect, int64_t* send_slots, int64_t* send_count,
+                  int64_t* recv_count, int64_t* n_send, int64_t* n_halo);
+
 /* Synchronise the context stream (and report asynchronous CUDA errors). */
 es_status es_synchronize(es_context* ctx);
 /* Stream the context launches on (cudaStream_t as void*). */

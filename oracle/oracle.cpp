@@ -62,6 +62,25 @@ JacobiRecT<T> jacobi_recT(int nmax, T a, T b) {
 }
 JacobiRec jacobi_rec(int nmax, double a, double b) { return jacobi_recT<double>(nmax, a, b); }
 
+template <class T>
+T jacobi_val(int n, T a, T b, T x) {
+  JacobiRecT<T> r = jacobi_recT<T>(n, a, b);
+  T pm = r.p0;
+  if (n == 0) return pm;
+  T pc = r.p0 * ((a + b + (T)2) * x / (T)2 + (a - b) / (T)2) * r.c1;
+  for (int i = 1; i < n; ++i) {
+    T pn = ((x - r.bn[i]) * pc - r.ao[i] * pm) / r.an[i];
+    pm = pc;
+    pc = pn;
+  }
+  return pc;
+}
+template <class T>
+T jacobi_der(int n, T a, T b, T x) {
+  if (n == 0) return 0;
+  return std::sqrt((T)n * ((T)n + a + b + (T)1)) * jacobi_val<T>(n - 1, a + (T)1, b + (T)1, x);
+}
+
 double jacobi(int n, double a, double b, double x) {
   JacobiRec r = jacobi_rec(n, a, b);
   double pm = r.p0;
@@ -84,47 +103,58 @@ double jacobi_deriv(int n, double a, double b, double x) {
 // Gauss rule ("Gauss: P_{q+1}^(a,b)(eta) = 0"): Newton iteration with polynomial deflation
 // (Karniadakis & Sherwin App. B, cited at P:160); weights from the Christoffel numbers of the
 // orthonormal family, w_i = 1 / sum_{k<=q} P_k(x_i)^2, equal to int l_i (1-x)^a (1+x)^b.
-void gauss_jacobi(int q, double a, double b, vector<double>& x, vector<double>& w) {
+// All reference tables are computed in long double and rounded once to FP64 (reading R26).
+typedef long double LD;
+template <class T>
+void gauss_jacobiT(int q, T a, T b, vector<T>& x, vector<T>& w) {
   int N = q + 1;
-  x.assign(N, 0.0);
-  w.assign(N, 0.0);
+  x.assign(N, (T)0);
+  w.assign(N, (T)0);
   for (int k = 0; k < N; ++k) {
-    double r = -std::cos((2.0 * k + 1.0) * PI / (2.0 * N));
-    if (k > 0) r = 0.5 * (r + x[k - 1]);
+    T r = -std::cos(((T)2 * k + (T)1) * (T)PI / ((T)2 * N));
+    if (k > 0) r = (r + x[k - 1]) / (T)2;
     for (int it = 0; it < 200; ++it) {
-      double s = 0.0;
-      for (int j = 0; j < k; ++j) s += 1.0 / (r - x[j]);
-      double P = jacobi(N, a, b, r);
-      double dP = jacobi_deriv(N, a, b, r);
-      double delta = -P / (dP - s * P);
+      T s = 0;
+      for (int j = 0; j < k; ++j) s += (T)1 / (r - x[j]);
+      T P = jacobi_val<T>(N, a, b, r);
+      T dP = jacobi_der<T>(N, a, b, r);
+      T delta = -P / (dP - s * P);
       r += delta;
-      if (std::fabs(delta) < 1e-16) break;
+      if (std::fabs(delta) < (T)1e-19 * ((T)1 + std::fabs(r))) break;
     }
     x[k] = r;
   }
   std::sort(x.begin(), x.end());
   for (int i = 0; i < N; ++i) {
-    double s = 0.0;
+    T s = 0;
     for (int k = 0; k < N; ++k) {
-      double pk = jacobi(k, a, b, x[i]);
+      T pk = jacobi_val<T>(k, a, b, x[i]);
       s += pk * pk;
     }
-    w[i] = 1.0 / s;
+    w[i] = (T)1 / s;
   }
+}
+void gauss_jacobi(int q, double a, double b, vector<double>& x, vector<double>& w) {
+  vector<LD> xl, wl;
+  gauss_jacobiT<LD>(q, a, b, xl, wl);
+  x.assign(xl.begin(), xl.end());
+  w.assign(wl.begin(), wl.end());
 }
 
 // Lagrange polynomials (P:153-155 [eq:lagrange]) and their derivatives, by the product formula.
-double lagrange(const vector<double>& nd, int j, double x) {
-  double v = 1.0;
+template <class T>
+T lagrange(const vector<T>& nd, int j, T x) {
+  T v = 1;
   for (size_t k = 0; k < nd.size(); ++k)
     if ((int)k != j) v *= (x - nd[k]) / (nd[j] - nd[k]);
   return v;
 }
-double lagrange_deriv(const vector<double>& nd, int j, double x) {
-  double s = 0.0;
+template <class T>
+T lagrange_deriv(const vector<T>& nd, int j, T x) {
+  T s = 0;
   for (size_t k = 0; k < nd.size(); ++k) {
     if ((int)k == j) continue;
-    double t = 1.0 / (nd[j] - nd[k]);
+    T t = (T)1 / (nd[j] - nd[k]);
     for (size_t m = 0; m < nd.size(); ++m)
       if ((int)m != j && m != k) t *= (x - nd[m]) / (nd[j] - nd[m]);
     s += t;
@@ -153,13 +183,14 @@ struct Ref {
 
 // Tetrahedral collapsed map with the corrected first component (R1):
 // xi1 = 1/4 (1+eta1)(1-eta2)(1-eta3) - 1   (P:263 prints (1-eta2)(1-eta2)).
-void chi(int d, const double* e, double* x) {
+template <class T>
+void chi(int d, const T* e, T* x) {
   if (d == 2) {  // P:183 [eq:tri_mapping]
-    x[0] = 0.5 * (1.0 + e[0]) * (1.0 - e[1]) - 1.0;
+    x[0] = (T)0.5 * ((T)1 + e[0]) * ((T)1 - e[1]) - (T)1;
     x[1] = e[1];
   } else {  // P:263 [eq:tet_mapping], R1
-    x[0] = 0.25 * (1.0 + e[0]) * (1.0 - e[1]) * (1.0 - e[2]) - 1.0;
-    x[1] = 0.5 * (1.0 + e[1]) * (1.0 - e[2]) - 1.0;
+    x[0] = (T)0.25 * ((T)1 + e[0]) * ((T)1 - e[1]) * ((T)1 - e[2]) - (T)1;
+    x[1] = (T)0.5 * ((T)1 + e[1]) * ((T)1 - e[2]) - (T)1;
     x[2] = e[2];
   }
 }
@@ -185,12 +216,13 @@ vector<int> multi_indices(int d, int p) {
 
 // PKD basis function from the principal functions (P:378-389 [eq:principal_functions,
 // eq:modal_basis_2d/3d]), evaluated at collapsed coordinates eta.
-double pkd_eta(int d, const int* al, const double* e) {
-  double v = std::sqrt(2.0) * jacobi(al[0], 0, 0, e[0]);
-  v *= std::pow(1.0 - e[1], al[0]) * jacobi(al[1], 2.0 * al[0] + 1.0, 0, e[1]);
+template <class T>
+T pkd_eta(int d, const int* al, const T* e) {
+  T v = std::sqrt((T)2) * jacobi_val<T>(al[0], 0, 0, e[0]);
+  v *= std::pow((T)1 - e[1], (T)al[0]) * jacobi_val<T>(al[1], (T)2 * al[0] + (T)1, 0, e[1]);
   if (d == 3)
-    v *= 2.0 * std::pow(1.0 - e[2], al[0] + al[1]) *
-         jacobi(al[2], 2.0 * al[0] + 2.0 * al[1] + 2.0, 0, e[2]);
+    v *= (T)2 * std::pow((T)1 - e[2], (T)(al[0] + al[1])) *
+         jacobi_val<T>(al[2], (T)2 * al[0] + (T)2 * al[1] + (T)2, 0, e[2]);
   return v;
 }
 
@@ -276,6 +308,7 @@ void pkd_cart(int d, const int* al, const T* x, T& v, T* g) {
 }
 
 Ref build_ref(int d, int q, int p) {
+  // every table is evaluated in long double and rounded once to FP64 (reading R26)
   Ref r;
   r.d = d;
   r.q = q;
@@ -285,89 +318,86 @@ Ref build_ref(int d, int q, int p) {
   r.Nf = d + 1;
   r.Nqf = (d == 2) ? n : n * n;
   r.p = p;
-  gauss_jacobi(q, 0, 0, r.eta1, r.w1);
-  gauss_jacobi(q, 1, 0, r.eta3, r.w3);
-  r.eta.assign(r.Nq * d, 0.0);
-  r.xi.assign(r.Nq * d, 0.0);
-  r.W.assign(r.Nq, 0.0);
-  r.xif.assign(r.Nf * r.Nqf * d, 0.0);
-  r.B.assign(r.Nf * r.Nqf, 0.0);
-  r.nhat.assign(r.Nf * d, 0.0);
-  const vector<double>& e = r.eta1;
-  const vector<double>& w = r.w1;
-  const vector<double>& e3 = r.eta3;
-  const vector<double>& w3 = r.w3;
+  const int Nq = r.Nq, Nqf = r.Nqf, Nf = r.Nf;
+  vector<LD> e, w, e3, w3;
+  gauss_jacobiT<LD>(q, 0, 0, e, w);
+  gauss_jacobiT<LD>(q, 1, 0, e3, w3);
+  r.eta1.assign(e.begin(), e.end());
+  r.w1.assign(w.begin(), w.end());
+  r.eta3.assign(e3.begin(), e3.end());
+  r.w3.assign(w3.begin(), w3.end());
+  vector<LD> eta((size_t)Nq * d), xi((size_t)Nq * d), W(Nq), xif((size_t)Nf * Nqf * d), B((size_t)Nf * Nqf),
+      nhat((size_t)Nf * d);
   auto sg = [&](int a, int b, int c) { return a + n * b + n * n * c; };  // sigma (R9)
   if (d == 2) {
     // P:205 [eq:tri_quadrature]
     for (int b = 0; b < n; ++b)
       for (int a = 0; a < n; ++a) {
         int i = sg(a, b, 0);
-        double et[2] = {e[a], e[b]};
-        r.eta[i * 2] = e[a];
-        r.eta[i * 2 + 1] = e[b];
-        chi(2, et, &r.xi[i * 2]);
-        r.W[i] = (1.0 - e[b]) / 2.0 * w[a] * w[b];
+        LD et[2] = {e[a], e[b]};
+        eta[i * 2] = e[a];
+        eta[i * 2 + 1] = e[b];
+        chi<LD>(2, et, &xi[i * 2]);
+        W[i] = ((LD)1 - e[b]) / (LD)2 * w[a] * w[b];
       }
     // P:208-212 [eq:tri_facet_quadrature_nodes]
     for (int i = 0; i < n; ++i) {
-      double e1[2] = {e[i], -1.0}, e2[2] = {1.0, e[i]}, e3v[2] = {-1.0, e[i]};
-      chi(2, e1, &r.xif[(0 * n + i) * 2]);
-      chi(2, e2, &r.xif[(1 * n + i) * 2]);
-      chi(2, e3v, &r.xif[(2 * n + i) * 2]);
-      r.B[0 * n + i] = w[i];
-      r.B[1 * n + i] = std::sqrt(2.0) * w[i];
-      r.B[2 * n + i] = w[i];
+      LD f1[2] = {e[i], -1}, f2[2] = {1, e[i]}, f3[2] = {-1, e[i]};
+      chi<LD>(2, f1, &xif[(0 * n + i) * 2]);
+      chi<LD>(2, f2, &xif[(1 * n + i) * 2]);
+      chi<LD>(2, f3, &xif[(2 * n + i) * 2]);
+      B[0 * n + i] = w[i];
+      B[1 * n + i] = std::sqrt((LD)2) * w[i];
+      B[2 * n + i] = w[i];
     }
     // outward unit normals of the facets P:176-178
-    double nh[6] = {0.0, -1.0, 1.0 / std::sqrt(2.0), 1.0 / std::sqrt(2.0), -1.0, 0.0};
-    for (int k = 0; k < 6; ++k) r.nhat[k] = nh[k];
+    LD r2 = (LD)1 / std::sqrt((LD)2);
+    LD nh[6] = {0, -1, r2, r2, -1, 0};
+    for (int k = 0; k < 6; ++k) nhat[k] = nh[k];
   } else {
     // P:267 [eq:tet_quadrature]
     for (int c = 0; c < n; ++c)
       for (int b = 0; b < n; ++b)
         for (int a = 0; a < n; ++a) {
           int i = sg(a, b, c);
-          double et[3] = {e[a], e[b], e3[c]};
-          for (int k = 0; k < 3; ++k) r.eta[i * 3 + k] = et[k];
-          chi(3, et, &r.xi[i * 3]);
-          r.W[i] = (1.0 - e[b]) * (1.0 - e3[c]) / 8.0 * w[a] * w[b] * w3[c];
+          LD et[3] = {e[a], e[b], e3[c]};
+          for (int k = 0; k < 3; ++k) eta[i * 3 + k] = et[k];
+          chi<LD>(3, et, &xi[i * 3]);
+          W[i] = ((LD)1 - e[b]) * ((LD)1 - e3[c]) / (LD)8 * w[a] * w[b] * w3[c];
         }
     // P:271-283 [eq:tet_facet_quadrature_nodes, eq:tet_facet_quadrature_weights]
     for (int j = 0; j < n; ++j)
       for (int i = 0; i < n; ++i) {
         int f = i + n * j;  // sigma_f (R9)
-        double f1[3] = {e[i], -1.0, e3[j]}, f2[3] = {1.0, e[i], e3[j]},
-               f3[3] = {-1.0, e[i], e3[j]}, f4[3] = {e[i], e3[j], -1.0};
-        chi(3, f1, &r.xif[(0 * r.Nqf + f) * 3]);
-        chi(3, f2, &r.xif[(1 * r.Nqf + f) * 3]);
-        chi(3, f3, &r.xif[(2 * r.Nqf + f) * 3]);
-        chi(3, f4, &r.xif[(3 * r.Nqf + f) * 3]);
-        r.B[0 * r.Nqf + f] = 0.5 * w[i] * w3[j];
-        r.B[1 * r.Nqf + f] = std::sqrt(3.0) / 2.0 * w[i] * w3[j];
-        r.B[2 * r.Nqf + f] = 0.5 * w[i] * w3[j];
-        r.B[3 * r.Nqf + f] = 0.5 * w[i] * w3[j];
+        LD f1[3] = {e[i], -1, e3[j]}, f2[3] = {1, e[i], e3[j]}, f3[3] = {-1, e[i], e3[j]}, f4[3] = {e[i], e3[j], -1};
+        chi<LD>(3, f1, &xif[(0 * Nqf + f) * 3]);
+        chi<LD>(3, f2, &xif[(1 * Nqf + f) * 3]);
+        chi<LD>(3, f3, &xif[(2 * Nqf + f) * 3]);
+        chi<LD>(3, f4, &xif[(3 * Nqf + f) * 3]);
+        B[0 * Nqf + f] = w[i] * w3[j] / (LD)2;
+        B[1 * Nqf + f] = std::sqrt((LD)3) / (LD)2 * w[i] * w3[j];
+        B[2 * Nqf + f] = w[i] * w3[j] / (LD)2;
+        B[3 * Nqf + f] = w[i] * w3[j] / (LD)2;
       }
     // outward unit normals of the facets P:257-258
-    double s3 = 1.0 / std::sqrt(3.0);
-    double nh[12] = {0, -1, 0, s3, s3, s3, -1, 0, 0, 0, 0, -1};
-    for (int k = 0; k < 12; ++k) r.nhat[k] = nh[k];
+    LD s3 = (LD)1 / std::sqrt((LD)3);
+    LD nh[12] = {0, -1, 0, s3, s3, s3, -1, 0, 0, 0, 0, -1};
+    for (int k = 0; k < 12; ++k) nhat[k] = nh[k];
   }
   // derivative operators P:218-221 [eq:d_2d] and P:286-289 [eq:d_3d] (R2: delta_{a3 b3})
-  int Nq = r.Nq;
-  r.D.assign((size_t)d * Nq * Nq, 0.0);
-  auto Dm = [&](int m, int i, int j) -> double& { return r.D[((size_t)m * Nq + i) * Nq + j]; };
+  vector<LD> D((size_t)d * Nq * Nq, (LD)0);
+  auto Dm = [&](int m, int i, int j) -> LD& { return D[((size_t)m * Nq + i) * Nq + j]; };
   if (d == 2) {
     for (int b = 0; b < n; ++b)
       for (int a = 0; a < n; ++a)
         for (int bb = 0; bb < n; ++bb)
           for (int aa = 0; aa < n; ++aa) {
             int i = sg(a, b, 0), j = sg(aa, bb, 0);
-            double dl1 = lagrange_deriv(e, aa, e[a]);
-            double dl2 = lagrange_deriv(e, bb, e[b]);
-            double d_ab = (b == bb) ? 1.0 : 0.0, d_aa = (a == aa) ? 1.0 : 0.0;
-            Dm(0, i, j) = 2.0 / (1.0 - e[b]) * dl1 * d_ab;
-            Dm(1, i, j) = (1.0 + e[a]) / (1.0 - e[b]) * dl1 * d_ab + d_aa * dl2;
+            LD dl1 = lagrange_deriv<LD>(e, aa, e[a]);
+            LD dl2 = lagrange_deriv<LD>(e, bb, e[b]);
+            LD d_ab = (b == bb) ? 1 : 0, d_aa = (a == aa) ? 1 : 0;
+            Dm(0, i, j) = (LD)2 / ((LD)1 - e[b]) * dl1 * d_ab;
+            Dm(1, i, j) = ((LD)1 + e[a]) / ((LD)1 - e[b]) * dl1 * d_ab + d_aa * dl2;
           }
   } else {
     for (int c = 0; c < n; ++c)
@@ -377,32 +407,29 @@ Ref build_ref(int d, int q, int p) {
             for (int bb = 0; bb < n; ++bb)
               for (int aa = 0; aa < n; ++aa) {
                 int i = sg(a, b, c), j = sg(aa, bb, cc);
-                double d1 = (a == aa) ? 1.0 : 0.0, d2 = (b == bb) ? 1.0 : 0.0,
-                       d3 = (c == cc) ? 1.0 : 0.0;
-                if (d1 == 0.0 && d2 == 0.0) continue;  // no term couples such nodes
-                double dl1 = lagrange_deriv(e, aa, e[a]);
-                double dl2 = lagrange_deriv(e, bb, e[b]);
-                double dl3 = lagrange_deriv(e3, cc, e3[c]);
-                double den = (1.0 - e[b]) * (1.0 - e3[c]);
-                Dm(0, i, j) = 4.0 / den * dl1 * d2 * d3;
-                Dm(1, i, j) = 2.0 * (1.0 + e[a]) / den * dl1 * d2 * d3 +
-                              2.0 / (1.0 - e3[c]) * d1 * dl2 * d3;
-                Dm(2, i, j) = 2.0 * (1.0 + e[a]) / den * dl1 * d2 * d3 +
-                              (1.0 + e[b]) / (1.0 - e3[c]) * d1 * dl2 * d3 + d1 * d2 * dl3;
+                LD d1 = (a == aa) ? 1 : 0, d2 = (b == bb) ? 1 : 0, d3 = (c == cc) ? 1 : 0;
+                if (d1 == 0 && d2 == 0) continue;  // no term couples such nodes
+                LD dl1 = lagrange_deriv<LD>(e, aa, e[a]);
+                LD dl2 = lagrange_deriv<LD>(e, bb, e[b]);
+                LD dl3 = lagrange_deriv<LD>(e3, cc, e3[c]);
+                LD den = ((LD)1 - e[b]) * ((LD)1 - e3[c]);
+                Dm(0, i, j) = (LD)4 / den * dl1 * d2 * d3;
+                Dm(1, i, j) = (LD)2 * ((LD)1 + e[a]) / den * dl1 * d2 * d3 + (LD)2 / ((LD)1 - e3[c]) * d1 * dl2 * d3;
+                Dm(2, i, j) = (LD)2 * ((LD)1 + e[a]) / den * dl1 * d2 * d3 +
+                              ((LD)1 + e[b]) / ((LD)1 - e3[c]) * d1 * dl2 * d3 + d1 * d2 * dl3;
               }
   }
   // extrapolation operators P:223-227 [eq:r_2d] and P:292-297 [eq:r_3d]
-  int Nqf = r.Nqf, Nf = r.Nf;
-  r.R.assign((size_t)Nf * Nqf * Nq, 0.0);
-  auto Rz = [&](int z, int f, int j) -> double& { return r.R[((size_t)z * Nqf + f) * Nq + j]; };
+  vector<LD> R((size_t)Nf * Nqf * Nq, (LD)0);
+  auto Rz = [&](int z, int f, int j) -> LD& { return R[((size_t)z * Nqf + f) * Nq + j]; };
   if (d == 2) {
     for (int i = 0; i < n; ++i)
       for (int bb = 0; bb < n; ++bb)
         for (int aa = 0; aa < n; ++aa) {
           int j = sg(aa, bb, 0);
-          Rz(0, i, j) = lagrange(e, aa, e[i]) * lagrange(e, bb, -1.0);
-          Rz(1, i, j) = lagrange(e, aa, 1.0) * lagrange(e, bb, e[i]);
-          Rz(2, i, j) = lagrange(e, aa, -1.0) * lagrange(e, bb, e[i]);
+          Rz(0, i, j) = lagrange<LD>(e, aa, e[i]) * lagrange<LD>(e, bb, -1);
+          Rz(1, i, j) = lagrange<LD>(e, aa, 1) * lagrange<LD>(e, bb, e[i]);
+          Rz(2, i, j) = lagrange<LD>(e, aa, -1) * lagrange<LD>(e, bb, e[i]);
         }
   } else {
     for (int a2 = 0; a2 < n; ++a2)
@@ -411,40 +438,51 @@ Ref build_ref(int d, int q, int p) {
           for (int bb = 0; bb < n; ++bb)
             for (int aa = 0; aa < n; ++aa) {
               int f = a1 + n * a2, j = sg(aa, bb, cc);
-              Rz(0, f, j) = lagrange(e, aa, e[a1]) * lagrange(e, bb, -1.0) * lagrange(e3, cc, e3[a2]);
-              Rz(1, f, j) = lagrange(e, aa, 1.0) * lagrange(e, bb, e[a1]) * lagrange(e3, cc, e3[a2]);
-              Rz(2, f, j) = lagrange(e, aa, -1.0) * lagrange(e, bb, e[a1]) * lagrange(e3, cc, e3[a2]);
-              Rz(3, f, j) = lagrange(e, aa, e[a1]) * lagrange(e, bb, e3[a2]) * lagrange(e3, cc, -1.0);
+              Rz(0, f, j) = lagrange<LD>(e, aa, e[a1]) * lagrange<LD>(e, bb, -1) * lagrange<LD>(e3, cc, e3[a2]);
+              Rz(1, f, j) = lagrange<LD>(e, aa, 1) * lagrange<LD>(e, bb, e[a1]) * lagrange<LD>(e3, cc, e3[a2]);
+              Rz(2, f, j) = lagrange<LD>(e, aa, -1) * lagrange<LD>(e, bb, e[a1]) * lagrange<LD>(e3, cc, e3[a2]);
+              Rz(3, f, j) = lagrange<LD>(e, aa, e[a1]) * lagrange<LD>(e, bb, e3[a2]) * lagrange<LD>(e3, cc, -1);
             }
   }
   // Q = W D, E = sum_z nhat_m R^T B R (P:131 [eq:e_decomp]), S = Q - E/2
-  r.Q.assign((size_t)d * Nq * Nq, 0.0);
-  r.E.assign((size_t)d * Nq * Nq, 0.0);
-  r.S.assign((size_t)d * Nq * Nq, 0.0);
+  vector<LD> Q((size_t)d * Nq * Nq, (LD)0), E((size_t)d * Nq * Nq, (LD)0), S((size_t)d * Nq * Nq, (LD)0);
   for (int m = 0; m < d; ++m) {
     for (int i = 0; i < Nq; ++i)
-      for (int j = 0; j < Nq; ++j) r.Q[((size_t)m * Nq + i) * Nq + j] = r.W[i] * Dm(m, i, j);
+      for (int j = 0; j < Nq; ++j) Q[((size_t)m * Nq + i) * Nq + j] = W[i] * Dm(m, i, j);
     for (int z = 0; z < Nf; ++z) {
-      double nm = r.nhat[z * d + m];
-      if (nm == 0.0) continue;
+      LD nm = nhat[z * d + m];
+      if (nm == 0) continue;
       for (int f = 0; f < Nqf; ++f) {
-        double bf = r.B[z * Nqf + f];
+        LD bf = B[z * Nqf + f];
         for (int i = 0; i < Nq; ++i) {
-          double ri = Rz(z, f, i);
-          if (ri == 0.0) continue;
-          for (int j = 0; j < Nq; ++j) r.E[((size_t)m * Nq + i) * Nq + j] += nm * ri * bf * Rz(z, f, j);
+          LD ri = Rz(z, f, i);
+          if (ri == 0) continue;
+          for (int j = 0; j < Nq; ++j) E[((size_t)m * Nq + i) * Nq + j] += nm * ri * bf * Rz(z, f, j);
         }
       }
     }
     for (size_t k = 0; k < (size_t)Nq * Nq; ++k)
-      r.S[(size_t)m * Nq * Nq + k] = r.Q[(size_t)m * Nq * Nq + k] - 0.5 * r.E[(size_t)m * Nq * Nq + k];
+      S[(size_t)m * Nq * Nq + k] = Q[(size_t)m * Nq * Nq + k] - E[(size_t)m * Nq * Nq + k] / (LD)2;
   }
   // generalised Vandermonde V_ij = phi_j(xi_i) (P:372-374 [eq:modal_to_nodal])
   r.alpha = multi_indices(d, p);
   r.Np = (int)r.alpha.size() / d;
-  r.V.assign((size_t)Nq * r.Np, 0.0);
+  vector<LD> V((size_t)Nq * r.Np);
   for (int i = 0; i < Nq; ++i)
-    for (int k = 0; k < r.Np; ++k) r.V[(size_t)i * r.Np + k] = pkd_eta(d, &r.alpha[k * d], &r.eta[i * d]);
+    for (int k = 0; k < r.Np; ++k) V[(size_t)i * r.Np + k] = pkd_eta<LD>(d, &r.alpha[k * d], &eta[i * d]);
+  auto rd = [](const vector<LD>& v) { return vector<double>(v.begin(), v.end()); };
+  r.eta = rd(eta);
+  r.xi = rd(xi);
+  r.W = rd(W);
+  r.xif = rd(xif);
+  r.B = rd(B);
+  r.nhat = rd(nhat);
+  r.D = rd(D);
+  r.Q = rd(Q);
+  r.E = rd(E);
+  r.S = rd(S);
+  r.R = rd(R);
+  r.V = rd(V);
   return r;
 }
 

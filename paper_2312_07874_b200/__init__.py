@@ -73,6 +73,47 @@ es_launch_count = _sig("es_launch_count", ctypes.c_int64, _vp)
 es_reset_launch_count = _sig("es_reset_launch_count", None, _vp)
 es_timing_enable = _sig("es_timing_enable", _i, _vp, _i)
 es_timing_read = _sig("es_timing_read", _i, _vp, _i, _dp, _lp)
+es_ref_table = _sig("es_ref_table", _i, _i, _i, ctypes.c_char_p, _dp, ctypes.c_int64, _lp)
+_ip = ctypes.POINTER(ctypes.c_int)
+es_plan = _sig("es_plan", _i, _i, ctypes.c_int64, _lp, _i, _i, _lp, _ip, _lp, _lp, _lp, _lp, _lp)
+
+
+def ref_table(dim, p, name):
+    """Host-only copy of one reference table the kernels use (see es_ref_table)."""
+    n = ctypes.c_int64()
+    rc = es_ref_table(dim, p, name.encode(), None, 0, ctypes.byref(n))
+    if rc != ES_OK:
+        raise ESError(rc, f"unknown table {name}")
+    out = np.zeros(n.value)
+    rc = es_ref_table(dim, p, name.encode(), out.ctypes.data_as(_dp), n.value, ctypes.byref(n))
+    if rc != ES_OK:
+        raise ESError(rc, name)
+    return out
+
+
+def plan(dim, elem_vertices, rank, world):
+    """Host-only connectivity / halo plan of one rank (see es_plan)."""
+    ev = np.ascontiguousarray(elem_vertices, dtype=np.int64)
+    ne = len(ev)
+    nf = dim + 1
+    first, nloc = ne * rank // world, ne * (rank + 1) // world - ne * rank // world
+    ns, nh = ctypes.c_int64(), ctypes.c_int64()
+    rc = es_plan(dim, ne, ev.ctypes.data_as(_lp), rank, world, None, None, None, None, None,
+                 ctypes.byref(ns), ctypes.byref(nh))
+    if rc != ES_OK:
+        raise ESError(rc, "plan failed")
+    fs = np.zeros((nloc, nf), np.int64)
+    fr = np.zeros((nloc, nf), np.int32)
+    ss = np.zeros(max(ns.value, 1), np.int64)
+    sc = np.zeros(world, np.int64)
+    rcnt = np.zeros(world, np.int64)
+    rc = es_plan(dim, ne, ev.ctypes.data_as(_lp), rank, world, fs.ctypes.data_as(_lp),
+                 fr.ctypes.data_as(_ip), ss.ctypes.data_as(_lp), sc.ctypes.data_as(_lp),
+                 rcnt.ctypes.data_as(_lp), ctypes.byref(ns), ctypes.byref(nh))
+    if rc != ES_OK:
+        raise ESError(rc, "plan failed")
+    return dict(first=first, nloc=nloc, face_slot=fs, face_reflect=fr, send_slots=ss[:ns.value],
+                send_count=sc, recv_count=rcnt, n_halo=nh.value)
 
 
 def declared_symbols():

@@ -568,6 +568,58 @@ es_status es_element_geometry(es_context* c, int64_t k, double* G, double* Jn, d
   return ES_OK;
 }
 
+es_status es_ref_table(int dim, int p, const char* name, double* out, int64_t cap, int64_t* n) {
+  if (!name) return ES_ERR_ARG;
+  RefTables t;
+  std::string err;
+  if (!build_ref_tables(dim, p, t, err)) return ES_ERR_CONFIG;
+  std::string nm(name);
+  const std::vector<double>* v = nullptr;
+  if (nm == "eta") v = &t.eta;
+  else if (nm == "w") v = &t.w;
+  else if (nm == "eta3") v = &t.eta3;
+  else if (nm == "w3") v = &t.w3;
+  else if (nm == "skQ1") v = &t.skQ1;
+  else if (nm == "skA1") v = &t.skA1;
+  else if (nm == "skA2") v = &t.skA2;
+  else if (nm == "skA3") v = &t.skA3;
+  else if (nm == "skA4") v = &t.skA4;
+  else if (nm == "lL") v = &t.lL;
+  else if (nm == "lR") v = &t.lR;
+  else if (nm == "l3L") v = &t.l3L;
+  else if (nm == "lint4") v = &t.lint4;
+  else if (nm == "psi1") v = &t.psi1;
+  else if (nm == "psi2") v = &t.psi2;
+  else if (nm == "psi3") v = &t.psi3;
+  else if (nm == "Wvol") v = &t.Wvol;
+  else if (nm == "Bf") v = &t.Bf;
+  else if (nm == "xi_vol") v = &t.xi_vol;
+  if (!v) return ES_ERR_ARG;
+  if (n) *n = (int64_t)v->size();
+  if (out) {
+    if (cap < (int64_t)v->size()) return ES_ERR_ARG;
+    std::memcpy(out, v->data(), v->size() * sizeof(double));
+  }
+  return ES_OK;
+}
+
+es_status es_plan(int dim, int64_t ne, const int64_t* ev, int rank, int world, int64_t* face_slot,
+                  int* face_reflect, int64_t* send_slots, int64_t* send_count, int64_t* recv_count,
+                  int64_t* n_send, int64_t* n_halo) {
+  if (!ev || world < 1 || rank < 0 || rank >= world || (dim != 2 && dim != 3)) return ES_ERR_ARG;
+  MeshPlan plan;
+  std::string err;
+  if (!build_mesh_plan(dim, ne, ev, rank, world, plan, err)) return ES_ERR_VERIFY;
+  if (face_slot) std::memcpy(face_slot, plan.face_slot.data(), plan.face_slot.size() * sizeof(int64_t));
+  if (face_reflect) std::memcpy(face_reflect, plan.face_reflect.data(), plan.face_reflect.size() * sizeof(int));
+  if (send_slots) std::memcpy(send_slots, plan.send_slots.data(), plan.send_slots.size() * sizeof(int64_t));
+  if (send_count) std::memcpy(send_count, plan.send_count.data(), plan.send_count.size() * sizeof(int64_t));
+  if (recv_count) std::memcpy(recv_count, plan.recv_count.data(), plan.recv_count.size() * sizeof(int64_t));
+  if (n_send) *n_send = (int64_t)plan.send_slots.size();
+  if (n_halo) *n_halo = plan.n_halo;
+  return ES_OK;
+}
+
 es_status es_synchronize(es_context* c) {
   POISON_CHECK();
   CK(cudaSetDevice(c->device));

@@ -15,6 +15,9 @@
 namespace esb {
 namespace {
 
+typedef __float128 Q;  // every table is evaluated in binary128 and rounded once (R26)
+inline Q qsqrt(Q x) { return sqrtq(x); }
+
 // ---------------- monic Jacobi recurrence p_{k+1} = (x - al_k) p_k - be_k p_{k-1} ----------------
 struct Monic {
   std::vector<double> al, be;  // be[0] = mu0 = int (1-x)^a (1+x)^b
@@ -43,6 +46,37 @@ double pnorm(int n, double a, double b, double x) {
   double pm = 0.0, pc = 1.0 / sqrt(m.be[0]);
   for (int k = 0; k < n; ++k) {
     double pn = ((x - m.al[k]) * pc - (k > 0 ? sqrt(m.be[k]) * pm : 0.0)) / sqrt(m.be[k + 1]);
+    pm = pc;
+    pc = pn;
+  }
+  return pc;
+}
+
+struct MonicQ {
+  std::vector<Q> al, be;
+};
+MonicQ monic_q(int N, Q a, Q b) {
+  MonicQ m;
+  m.al.resize(N + 1);
+  m.be.resize(N + 1);
+  for (int k = 0; k <= N; ++k) {
+    Q s = (Q)2 * k + a + b;
+    m.al[k] = (k == 0) ? (b - a) / (a + b + (Q)2) : (b * b - a * a) / (s * (s + (Q)2));
+    if (k == 0)
+      m.be[k] = expq((a + b + (Q)1) * logq((Q)2) + lgammaq(a + (Q)1) + lgammaq(b + (Q)1) - lgammaq(a + b + (Q)2));
+    else if (k == 1)
+      m.be[k] = (Q)4 * ((Q)1 + a) * ((Q)1 + b) / (((Q)2 + a + b) * ((Q)2 + a + b) * ((Q)3 + a + b));
+    else
+      m.be[k] = (Q)4 * k * (k + a) * (k + b) * (k + a + b) / (s * s * (s + (Q)1) * (s - (Q)1));
+  }
+  return m;
+}
+// normalised Jacobi value in binary128
+Q pnorm_q(int n, Q a, Q b, Q x) {
+  MonicQ m = monic_q(n + 1, a, b);
+  Q pm = 0, pc = (Q)1 / qsqrt(m.be[0]);
+  for (int k = 0; k < n; ++k) {
+    Q pn = ((x - m.al[k]) * pc - (k > 0 ? qsqrt(m.be[k]) * pm : (Q)0)) / qsqrt(m.be[k + 1]);
     pm = pc;
     pc = pn;
   }
@@ -103,32 +137,29 @@ bool tridiag_eig(std::vector<double>& dg, std::vector<double> e, int n, std::vec
   return true;
 }
 
-// Gauss rule w.r.t. (1-x)^a (1+x)^b with N nodes: Golub-Welsch, Newton polish,
-// Gauss-Christoffel weights  w_i = ||p_{N-1}||^2 / (p_{N-1}(x_i) p_N'(x_i)).
-bool gauss_rule(int N, double a, double b, std::vector<double>& x, std::vector<double>& w) {
+// Gauss rule w.r.t. (1-x)^a (1+x)^b with N nodes: Golub-Welsch eigenvalues as
+// starting values, Newton on the monic recurrence in binary128, Gauss-Christoffel weights
+//   w_i = ||p_{N-1}||^2 / (p_{N-1}(x_i) p_N'(x_i)).
+bool gauss_rule(int N, double a, double b, std::vector<Q>& x, std::vector<Q>& w) {
   Monic m = monic_coeffs(N + 1, a, b);
   std::vector<double> dg(N), e(N, 0.0), z;
   for (int k = 0; k < N; ++k) dg[k] = m.al[k];
-  for (int k = 0; k + 1 < N; ++k) e[k] = sqrt(m.be[k + 1]);
+  for (int k = 0; k + 1 < N; ++k) e[k] = std::sqrt(m.be[k + 1]);
   if (!tridiag_eig(dg, e, N, z)) return false;
-  x = dg;
-  std::sort(x.begin(), x.end());
-  double norm2 = m.be[0];
-  for (int k = 1; k < N; ++k) norm2 *= m.be[k];
+  std::sort(dg.begin(), dg.end());
+  MonicQ mq = monic_q(N + 1, a, b);
+  Q norm2 = mq.be[0];
+  for (int k = 1; k < N; ++k) norm2 *= mq.be[k];
+  x.resize(N);
   w.resize(N);
   for (int i = 0; i < N; ++i) {
-    double xi = x[i];
-    double pN = 0, dpN = 0, pN1 = 0;
-    for (int it = 0; it < 3; ++it) {
-      double p0 = 1.0, d0 = 0.0, p1 = xi - m.al[0], d1 = 1.0;
-      if (N == 1) {
-        p1 = xi - m.al[0];
-        d1 = 1.0;
-        p0 = 1.0;
-      }
+    Q xi = dg[i];
+    Q pN = 0, dpN = 0, pN1 = 0;
+    for (int it = 0; it < 6; ++it) {
+      Q p0 = 1, d0 = 0, p1 = xi - mq.al[0], d1 = 1;
       for (int k = 1; k < N; ++k) {
-        double p2 = (xi - m.al[k]) * p1 - m.be[k] * p0;
-        double d2 = p1 + (xi - m.al[k]) * d1 - m.be[k] * d0;
+        Q p2 = (xi - mq.al[k]) * p1 - mq.be[k] * p0;
+        Q d2 = p1 + (xi - mq.al[k]) * d1 - mq.be[k] * d0;
         p0 = p1;
         d0 = d1;
         p1 = p2;
@@ -137,7 +168,7 @@ bool gauss_rule(int N, double a, double b, std::vector<double>& x, std::vector<d
       pN = p1;
       dpN = d1;
       pN1 = p0;
-      if (it < 2) xi -= pN / dpN;
+      if (it < 5) xi -= pN / dpN;
     }
     x[i] = xi;
     w[i] = norm2 / (pN1 * dpN);
@@ -145,33 +176,33 @@ bool gauss_rule(int N, double a, double b, std::vector<double>& x, std::vector<d
   return true;
 }
 
-// barycentric Lagrange data on nodes x
-std::vector<double> bary_weights(const std::vector<double>& x) {
+// barycentric Lagrange data on nodes x (binary128)
+std::vector<Q> bary_weights(const std::vector<Q>& x) {
   int n = (int)x.size();
-  std::vector<double> lam(n, 1.0);
+  std::vector<Q> lam(n, (Q)1);
   for (int j = 0; j < n; ++j)
     for (int k = 0; k < n; ++k)
       if (k != j) lam[j] /= (x[j] - x[k]);
   return lam;
 }
-std::vector<double> lagrange_at(const std::vector<double>& x, double t) {
+std::vector<Q> lagrange_at(const std::vector<Q>& x, Q t) {
   int n = (int)x.size();
-  std::vector<double> lam = bary_weights(x), l(n, 0.0);
+  std::vector<Q> lam = bary_weights(x), l(n, (Q)0);
   for (int j = 0; j < n; ++j)
     if (t == x[j]) {
-      l[j] = 1.0;
+      l[j] = 1;
       return l;
     }
-  double den = 0.0;
+  Q den = 0;
   for (int j = 0; j < n; ++j) den += lam[j] / (t - x[j]);
   for (int j = 0; j < n; ++j) l[j] = lam[j] / (t - x[j]) / den;
   return l;
 }
-std::vector<double> diff_matrix(const std::vector<double>& x) {  // D[i][j] = l_j'(x_i)
+std::vector<Q> diff_matrix(const std::vector<Q>& x) {  // D[i][j] = l_j'(x_i)
   int n = (int)x.size();
-  std::vector<double> lam = bary_weights(x), D((size_t)n * n, 0.0);
+  std::vector<Q> lam = bary_weights(x), D((size_t)n * n, (Q)0);
   for (int i = 0; i < n; ++i) {
-    double s = 0.0;
+    Q s = 0;
     for (int j = 0; j < n; ++j)
       if (j != i) {
         D[(size_t)i * n + j] = lam[j] / lam[i] / (x[i] - x[j]);
@@ -181,11 +212,16 @@ std::vector<double> diff_matrix(const std::vector<double>& x) {  // D[i][j] = l_
   }
   return D;
 }
-std::vector<double> skew_of(const std::vector<double>& X, int n) {
+std::vector<double> skew_of(const std::vector<Q>& X, int n) {
   std::vector<double> S((size_t)n * n);
   for (int i = 0; i < n; ++i)
-    for (int j = 0; j < n; ++j) S[(size_t)i * n + j] = 0.5 * (X[(size_t)i * n + j] - X[(size_t)j * n + i]);
+    for (int j = 0; j < n; ++j) S[(size_t)i * n + j] = (double)((X[(size_t)i * n + j] - X[(size_t)j * n + i]) / (Q)2);
   return S;
+}
+std::vector<double> rnd(const std::vector<Q>& v) {
+  std::vector<double> o(v.size());
+  for (size_t i = 0; i < v.size(); ++i) o[i] = (double)v[i];
+  return o;
 }
 
 // ---------------- geometry tables in binary128 ----------------
@@ -195,7 +231,6 @@ std::vector<double> skew_of(const std::vector<double>& X, int n) {
 // so the tables need no Vandermonde inverse.  They are evaluated in binary128 and stored as
 // double-double pairs because the device sums them against data with cancellation (R25).
 typedef __float128 LD;
-
 // equispaced barycentric lattice of degree N (R10): reference coords [M][d], barycentric [M][d+1]
 template <class T>
 void lattice_nodes(int d, int N, std::vector<T>& xi, std::vector<double>& bary) {
@@ -308,54 +343,56 @@ bool build_ref_tables(int d, int p, RefTables& t, std::string& err) {
   t.Nf = d + 1;
   t.Nqf = d == 2 ? n : n * n;
   t.Np = d == 2 ? (p + 1) * (p + 2) / 2 : (p + 1) * (p + 2) * (p + 3) / 6;
-  if (!gauss_rule(n, 0.0, 0.0, t.eta, t.w) || !gauss_rule(n, 1.0, 0.0, t.eta3, t.w3)) {
+  std::vector<Q> e, w, e3, w3;  // binary128 rules; rounded copies go to the device
+  if (!gauss_rule(n, 0.0, 0.0, e, w) || !gauss_rule(n, 1.0, 0.0, e3, w3)) {
     err = "Gauss rule construction failed";
     return false;
   }
-  const auto& e = t.eta;
-  const auto& w = t.w;
-  const auto& e3 = t.eta3;
-  const auto& w3 = t.w3;
+  t.eta = rnd(e);
+  t.w = rnd(w);
+  t.eta3 = rnd(e3);
+  t.w3 = rnd(w3);
   // 1D line operators: X = diag(weight) D, S-line = skew(X)
-  std::vector<double> D = diff_matrix(e), D3 = diff_matrix(e3);
-  std::vector<double> Q1(n * n), A1(n * n), A2(n * n), A3(n * n), A4(n * n);
+  std::vector<Q> D = diff_matrix(e), D3 = diff_matrix(e3);
+  std::vector<Q> Q1(n * n), A1(n * n), A2(n * n), A3(n * n), A4(n * n);
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j) {
       Q1[i * n + j] = w[i] * D[i * n + j];
-      A1[i * n + j] = w[i] * (1.0 + e[i]) / 2.0 * D[i * n + j];
-      A2[i * n + j] = w[i] * (1.0 - e[i]) / 2.0 * D[i * n + j];
-      A3[i * n + j] = w[i] * (1.0 - e[i] * e[i]) / 4.0 * D[i * n + j];
-      A4[i * n + j] = w3[i] * (1.0 - e3[i]) * D3[i * n + j];
+      A1[i * n + j] = w[i] * ((Q)1 + e[i]) / (Q)2 * D[i * n + j];
+      A2[i * n + j] = w[i] * ((Q)1 - e[i]) / (Q)2 * D[i * n + j];
+      A3[i * n + j] = w[i] * ((Q)1 - e[i] * e[i]) / (Q)4 * D[i * n + j];
+      A4[i * n + j] = w3[i] * ((Q)1 - e3[i]) * D3[i * n + j];
     }
   t.skQ1 = skew_of(Q1, n);
   t.skA1 = skew_of(A1, n);
   t.skA2 = skew_of(A2, n);
   t.skA3 = skew_of(A3, n);
   t.skA4 = skew_of(A4, n);
-  t.lL = lagrange_at(e, -1.0);
-  t.lR = lagrange_at(e, 1.0);
-  t.l3L = lagrange_at(e3, -1.0);
+  t.lL = rnd(lagrange_at(e, (Q)-1));
+  t.lR = rnd(lagrange_at(e, (Q)1));
+  t.l3L = rnd(lagrange_at(e3, (Q)-1));
   t.lint4.assign(n * n, 0.0);
   for (int j = 0; j < n; ++j) {
-    std::vector<double> l = lagrange_at(e, e3[j]);
-    for (int b = 0; b < n; ++b) t.lint4[j * n + b] = l[b];
+    std::vector<Q> l = lagrange_at(e, e3[j]);
+    for (int b = 0; b < n; ++b) t.lint4[j * n + b] = (double)l[b];
   }
   // PKD principal-function tables
   t.psi1.assign(n * n, 0.0);
   t.psi2.assign((size_t)n * n * n, 0.0);
   t.psi3.assign((size_t)n * n * n, 0.0);
   for (int a1 = 0; a1 <= p; ++a1)
-    for (int a = 0; a < n; ++a) t.psi1[a1 * n + a] = std::sqrt(2.0) * pnorm(a1, 0.0, 0.0, e[a]);
+    for (int a = 0; a < n; ++a) t.psi1[a1 * n + a] = (double)(qsqrt((Q)2) * pnorm_q(a1, 0, 0, e[a]));
   for (int a1 = 0; a1 <= p; ++a1)
     for (int a2 = 0; a2 <= p - a1; ++a2)
       for (int b = 0; b < n; ++b)
-        t.psi2[((size_t)a1 * n + a2) * n + b] = std::pow(1.0 - e[b], a1) * pnorm(a2, 2.0 * a1 + 1.0, 0.0, e[b]);
+        t.psi2[((size_t)a1 * n + a2) * n + b] =
+            (double)(powq((Q)1 - e[b], (Q)a1) * pnorm_q(a2, (Q)(2 * a1 + 1), 0, e[b]));
   if (d == 3)
     for (int s = 0; s <= p; ++s)
       for (int a3 = 0; a3 <= p - s; ++a3)
         for (int c = 0; c < n; ++c)
           t.psi3[((size_t)s * n + a3) * n + c] =
-              2.0 * std::pow(1.0 - e3[c], s) * pnorm(a3, 2.0 * s + 2.0, 0.0, e3[c]);
+              (double)((Q)2 * powq((Q)1 - e3[c], (Q)s) * pnorm_q(a3, (Q)(2 * s + 2), 0, e3[c]));
   // modal order (ABI): a1-major nested
   t.pair_a1.clear();
   t.pair_a2.clear();
@@ -386,24 +423,34 @@ bool build_ref_tables(int d, int p, RefTables& t, std::string& err) {
   t.Bf.assign((size_t)t.Nf * t.Nqf, 0.0);
   t.xi_face.assign((size_t)t.Nf * t.Nqf * d, 0.0);
   t.nhat.assign((size_t)t.Nf * 3, 0.0);
+  auto collapse_q = [&](const Q* et, double* x) {  // P:183 / P:263 (R1), rounded
+    if (d == 2) {
+      x[0] = (double)(((Q)1 + et[0]) * ((Q)1 - et[1]) / (Q)2 - (Q)1);
+      x[1] = (double)et[1];
+    } else {
+      x[0] = (double)(((Q)1 + et[0]) * ((Q)1 - et[1]) * ((Q)1 - et[2]) / (Q)4 - (Q)1);
+      x[1] = (double)(((Q)1 + et[1]) * ((Q)1 - et[2]) / (Q)2 - (Q)1);
+      x[2] = (double)et[2];
+    }
+  };
   if (d == 2) {
     for (int b = 0; b < n; ++b)
       for (int a = 0; a < n; ++a) {
         int i = a + n * b;
-        double et[2] = {e[a], e[b]};
-        collapse(2, et, &t.xi_vol[i * 2]);
-        t.Wvol[i] = w[a] * w[b] * (1.0 - e[b]) / 2.0;
+        Q et[2] = {e[a], e[b]};
+        collapse_q(et, &t.xi_vol[i * 2]);
+        t.Wvol[i] = (double)(w[a] * w[b] * ((Q)1 - e[b]) / (Q)2);
       }
     for (int f = 0; f < n; ++f) {
-      double f1[2] = {e[f], -1.0}, f2[2] = {1.0, e[f]}, f3[2] = {-1.0, e[f]};
-      collapse(2, f1, &t.xi_face[(0 * n + f) * 2]);
-      collapse(2, f2, &t.xi_face[(1 * n + f) * 2]);
-      collapse(2, f3, &t.xi_face[(2 * n + f) * 2]);
-      t.Bf[0 * n + f] = w[f];
-      t.Bf[1 * n + f] = std::sqrt(2.0) * w[f];
-      t.Bf[2 * n + f] = w[f];
+      Q f1[2] = {e[f], -1}, f2[2] = {1, e[f]}, f3[2] = {-1, e[f]};
+      collapse_q(f1, &t.xi_face[(0 * n + f) * 2]);
+      collapse_q(f2, &t.xi_face[(1 * n + f) * 2]);
+      collapse_q(f3, &t.xi_face[(2 * n + f) * 2]);
+      t.Bf[0 * n + f] = (double)w[f];
+      t.Bf[1 * n + f] = (double)(qsqrt((Q)2) * w[f]);
+      t.Bf[2 * n + f] = (double)w[f];
     }
-    double r2 = std::sqrt(0.5);
+    double r2 = (double)((Q)1 / qsqrt((Q)2));
     double nh[9] = {0, -1, 0, r2, r2, 0, -1, 0, 0};
     std::memcpy(t.nhat.data(), nh, sizeof(nh));
   } else {
@@ -411,27 +458,26 @@ bool build_ref_tables(int d, int p, RefTables& t, std::string& err) {
       for (int b = 0; b < n; ++b)
         for (int a = 0; a < n; ++a) {
           int i = a + n * b + n * n * c;
-          double et[3] = {e[a], e[b], e3[c]};
-          collapse(3, et, &t.xi_vol[i * 3]);
-          t.Wvol[i] = w[a] * w[b] * w3[c] * (1.0 - e[b]) * (1.0 - e3[c]) / 8.0;
+          Q et[3] = {e[a], e[b], e3[c]};
+          collapse_q(et, &t.xi_vol[i * 3]);
+          t.Wvol[i] = (double)(w[a] * w[b] * w3[c] * ((Q)1 - e[b]) * ((Q)1 - e3[c]) / (Q)8);
         }
     int Nqf = t.Nqf;
     for (int j = 0; j < n; ++j)
       for (int i = 0; i < n; ++i) {
         int f = i + n * j;
-        double f1[3] = {e[i], -1.0, e3[j]}, f2[3] = {1.0, e[i], e3[j]}, f3[3] = {-1.0, e[i], e3[j]},
-               f4[3] = {e[i], e3[j], -1.0};
-        collapse(3, f1, &t.xi_face[(0 * Nqf + f) * 3]);
-        collapse(3, f2, &t.xi_face[(1 * Nqf + f) * 3]);
-        collapse(3, f3, &t.xi_face[(2 * Nqf + f) * 3]);
-        collapse(3, f4, &t.xi_face[(3 * Nqf + f) * 3]);
-        double ww = w[i] * w3[j];
-        t.Bf[0 * Nqf + f] = 0.5 * ww;
-        t.Bf[1 * Nqf + f] = std::sqrt(3.0) / 2.0 * ww;
-        t.Bf[2 * Nqf + f] = 0.5 * ww;
-        t.Bf[3 * Nqf + f] = 0.5 * ww;
+        Q f1[3] = {e[i], -1, e3[j]}, f2[3] = {1, e[i], e3[j]}, f3[3] = {-1, e[i], e3[j]}, f4[3] = {e[i], e3[j], -1};
+        collapse_q(f1, &t.xi_face[(0 * Nqf + f) * 3]);
+        collapse_q(f2, &t.xi_face[(1 * Nqf + f) * 3]);
+        collapse_q(f3, &t.xi_face[(2 * Nqf + f) * 3]);
+        collapse_q(f4, &t.xi_face[(3 * Nqf + f) * 3]);
+        Q ww = w[i] * w3[j];
+        t.Bf[0 * Nqf + f] = (double)(ww / (Q)2);
+        t.Bf[1 * Nqf + f] = (double)(qsqrt((Q)3) / (Q)2 * ww);
+        t.Bf[2 * Nqf + f] = (double)(ww / (Q)2);
+        t.Bf[3 * Nqf + f] = (double)(ww / (Q)2);
       }
-    double r3 = 1.0 / std::sqrt(3.0);
+    double r3 = (double)((Q)1 / qsqrt((Q)3));
     double nh[12] = {0, -1, 0, r3, r3, r3, -1, 0, 0, 0, 0, -1};
     std::memcpy(t.nhat.data(), nh, sizeof(nh));
   }
