@@ -1,5 +1,6 @@
 // kernels_2d.cu -- triangle instantiations (q = p = N-1 in [1, 10]) of the kernels in kernels.cuh
 #include "kernels.cuh"
+#include "rhs2.cuh"
 
 namespace esb {
 #include "launch.inc"

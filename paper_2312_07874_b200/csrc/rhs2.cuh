@@ -1,0 +1,658 @@
+// rhs2.cuh -- K2 v2: warp-synchronous line-wise flux differencing (product code).
+//
+// Each warp owns whole eta_k lines ("line groups" of N lanes, floor(32/N) lines per warp).  For one
+// direction k a lane keeps its node's entropy-projected state and metric rows in registers, pairs
+// with the node (pos+s) mod N of its line for s = 1..floor(N/2) (every unordered pair exactly once,
+// P:572), subtracts F from its own accumulator and receives the partner's +F by a warp shuffle.
+// The facet-correction pairs whose extrapolation runs along the same lines are done in
+// the same pass; their facet-side sums C^T 1 use deterministic segmented shuffle trees.  Only three
+// block barriers separate the direction passes.  Interface flux, lifting and the weight-adjusted
+// inverse follow as in K2 v1.
+#pragma once
+#include "kernels.cuh"
+
+namespace esb {
+
+template <int DIM, int N>
+struct Lw {  // line-group layout
+  using S = Sz<DIM, N>;
+  static constexpr int LPW = 32 / N;                         // lines per warp slot
+  static constexpr int NL = DIM == 2 ? N : N * N;            // lines per direction
+  static constexpr int SLOTS = (NL + LPW - 1) / LPW;         // warp slots per direction
+  static constexpr int NW = SLOTS <= 12 ? SLOTS : (SLOTS % 9 == 0 ? 9 : (SLOTS % 8 == 0 ? 8 : 12));
+  static constexpr int NT = NW * 32;
+  static constexpr int NS = N / 2;                            // shifts
+  static constexpr int VB = 2;  // volume pair jobs per flux batch (ILP vs registers)
+};
+
+template <int DIM, int N>
+struct Rhs2Smem {
+  using S = Sz<DIM, N>;
+  static constexpr int PR = (DIM + 3) * S::Nq;  // rho, v, p, beta
+  static constexpr int GG = S::NG * S::Nq;      // G_lm
+  static constexpr int RR = S::NC * S::Nq;      // nodal residual r
+  static constexpr int PT = DIM == 3 ? S::NC * N * N * N : 0;  // facet-4 partial sums [v][j][a][c]
+  static constexpr int FP = (S::NC + 1) * S::NF;  // facet states (rho, v, p, beta)
+  static constexpr int FJ = DIM * S::NF;
+  static constexpr int CT = S::NC * S::NF;
+  static constexpr int TB = 5 * N * N + 6 * N + N * N + S::NF;
+  static constexpr int PS = psi_smem_doubles<DIM, N>();
+  static constexpr int o_pr = 0, o_g = o_pr + PR, o_r = o_g + GG, o_pt = o_r + RR, o_fp = o_pt + PT,
+                       o_fj = o_fp + FP, o_ct = o_fj + FJ, o_tb = o_ct + CT, o_ps = o_tb + TB, total = o_ps + PS;
+  static_assert(t1_size<DIM, N>() + t2_size<DIM, N>() <= PR + GG, "transform scratch");
+  static_assert(S::NC * S::Np <= PT + FP + FJ + CT, "modal scratch");
+};
+
+template <int DIM, int N>
+__host__ __device__ constexpr size_t rhs2_smem_doubles() {
+  return Rhs2Smem<DIM, N>::total;
+}
+
+// logarithmic mean and its reciprocal (reading R5); one reciprocal each.  In the Taylor
+// branch 1/P(f2) is evaluated as 1/(2(1+g)) = (1 - g + g^2 - g^3)/2, truncation g^4 < 2e-18.
+__device__ __forceinline__ double ln_mean_v2(double x, double y) {
+  double s = x + y;
+  double is = __drcp_rn(s);
+  double u = (x - y) * is;
+  double f2 = u * u;
+  if (f2 < 1e-4) {
+    double g = f2 * (1.0 / 3.0 + f2 * (1.0 / 5.0 + f2 * (1.0 / 7.0)));
+    return s * (0.5 * (1.0 + g * (-1.0 + g * (1.0 - g))));
+  }
+  return (y - x) / log(y / x);
+}
+__device__ __forceinline__ double inv_ln_mean_v2(double x, double y) {
+  double s = x + y;
+  double is = __drcp_rn(s);
+  double u = (x - y) * is;
+  double f2 = u * u;
+  if (f2 < 1e-4) return (2.0 + f2 * (2.0 / 3.0 + f2 * (2.0 / 5.0 + f2 * (2.0 / 7.0)))) * is;
+  return log(y / x) / (y - x);
+}
+
+struct NodeState {
+  double r, v[3], p, b;
+};
+
+// Ranocha EC flux in direction n (R3)
+template <int DIM>
+__device__ __forceinline__ void ec_flux_v2(const NodeState& A, const NodeState& B, const double* n,
+                                           double gm1inv, double* F) {
+  double rho_ln = ln_mean_v2(A.r, B.r);
+  double ib_ln = inv_ln_mean_v2(A.b, B.b);
+  double vn = 0.0, van = 0.0, vbn = 0.0, vdot = 0.0, vav[DIM];
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) {
+    vav[m] = 0.5 * (A.v[m] + B.v[m]);
+    vn += vav[m] * n[m];
+    van += A.v[m] * n[m];
+    vbn += B.v[m] * n[m];
+    vdot += A.v[m] * B.v[m];
+  }
+  double pav = 0.5 * (A.p + B.p);
+  double fr = rho_ln * vn;
+  F[0] = fr;
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) F[1 + m] = fr * vav[m] + pav * n[m];
+  F[DIM + 1] = fr * (0.5 * vdot + ib_ln * gm1inv) + 0.5 * (A.p * vbn + B.p * van);
+}
+
+// deterministic sum over the N lanes of a line group; the group's first lane gets the total
+template <int N>
+__device__ __forceinline__ double group_sum(double x, int a) {
+#pragma unroll
+  for (int o = 1; o < N; o <<= 1) {
+    double t = __shfl_down_sync(0xffffffffu, x, o);
+    if (a + o < N) x += t;
+  }
+  return x;
+}
+
+// reciprocal: hardware approximation refined by three Newton steps (no special-case branch;
+// arguments are positive and normal); within 1 ulp of 1/s
+__device__ __forceinline__ double rcp_nr(double s) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+  double e = fma(-s, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-s, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-s, r, 1.0);
+  return fma(r, e, r);
+}
+
+// one pair job: the other state lives in shared memory at base[q * stride + idx] (q = rho, v, p,
+// beta), n is the (scaled) direction, coef multiplies the flux
+template <int DIM>
+struct Job {
+  const double* base;
+  int stride, idx;
+  double n[DIM];
+  double coef;
+};
+
+// B Ranocha fluxes (R3) of `me` with the job states, straight-line in the common case: both
+// log means take the Taylor branch; a warp-uniform fallback recomputes the members that need the
+// log branch (R5).  F[b][v] = coef_b f#(me, other_b, n_b).
+template <int DIM, int B>
+__device__ __forceinline__ void flux_batch(const NodeState& me, const Job<DIM>* jb, double gm1inv,
+                                           double (*F)[DIM + 2]) {
+  NodeState o[B];
+  double rl[B], ib[B], f2r[B], f2b[B];
+  bool need = false;
+#pragma unroll
+  for (int t = 0; t < B; ++t) {
+    const double* q = jb[t].base + jb[t].idx;
+    const int st = jb[t].stride;
+    o[t].r = q[0];
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) o[t].v[m] = q[(1 + m) * st];
+    o[t].p = q[(DIM + 1) * st];
+    o[t].b = q[(DIM + 2) * st];
+  }
+#pragma unroll
+  for (int t = 0; t < B; ++t) {
+    const double sr = me.r + o[t].r, isr = rcp_nr(sr), ur = (me.r - o[t].r) * isr;
+    f2r[t] = ur * ur;
+    const double g = f2r[t] * (1.0 / 3.0 + f2r[t] * (1.0 / 5.0 + f2r[t] * (1.0 / 7.0)));
+    rl[t] = sr * (0.5 * (1.0 + g * (-1.0 + g * (1.0 - g))));
+    const double sb = me.b + o[t].b, isb = rcp_nr(sb), ub = (me.b - o[t].b) * isb;
+    f2b[t] = ub * ub;
+    ib[t] = (2.0 + f2b[t] * (2.0 / 3.0 + f2b[t] * (2.0 / 5.0 + f2b[t] * (2.0 / 7.0)))) * isb;
+    need |= (f2r[t] >= 1e-4) | (f2b[t] >= 1e-4);
+  }
+  if (__any_sync(0xffffffffu, need)) {
+#pragma unroll
+    for (int t = 0; t < B; ++t) {
+      if (f2r[t] >= 1e-4) rl[t] = (o[t].r - me.r) / log(o[t].r / me.r);
+      if (f2b[t] >= 1e-4) ib[t] = log(o[t].b / me.b) / (o[t].b - me.b);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < B; ++t) {
+    const double* n = jb[t].n;
+    double vn = 0.0, van = 0.0, vbn = 0.0, vdot = 0.0, vav[DIM];
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) {
+      vav[m] = 0.5 * (me.v[m] + o[t].v[m]);
+      vn += vav[m] * n[m];
+      van += me.v[m] * n[m];
+      vbn += o[t].v[m] * n[m];
+      vdot += me.v[m] * o[t].v[m];
+    }
+    const double pav = 0.5 * (me.p + o[t].p);
+    const double c = jb[t].coef;
+    const double fr = rl[t] * vn;
+    F[t][0] = c * fr;
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) F[t][1 + m] = c * (fr * vav[m] + pav * n[m]);
+    F[t][DIM + 1] = c * (fr * (0.5 * vdot + ib[t] * gm1inv) + 0.5 * (me.p * vbn + o[t].p * van));
+  }
+}
+
+template <int DIM, int N>
+__global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsArgs A) {
+  using S = Sz<DIM, N>;
+  using W = Lw<DIM, N>;
+  using L = Rhs2Smem<DIM, N>;
+  constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf, NT = W::NT, NS = W::NS;
+  extern __shared__ double sm[];
+  double* sP = sm + L::o_pr;   // [DIM+3][Nq]: rho, v_1..v_d, p, beta
+  double* sG = sm + L::o_g;    // [NG][Nq]: G_lm at (l*DIM+m)
+  double* sR = sm + L::o_r;    // [NC][Nq] nodal residual
+  double* pt = sm + L::o_pt;   // [NC][N(j)][N(a)][N(c)] facet-4 partials
+  double* fP = sm + L::o_fp;   // [NC+1][NF] facet states rho, v, p, beta
+  double* fJ = sm + L::o_fj;   // [DIM][NF] J n
+  double* ct = sm + L::o_ct;   // [NC][NF] C^T 1, then s = B J_f f* - C^T 1
+  double* tb = sm + L::o_tb;
+  double* tQ1 = tb;
+  double* tA1 = tQ1 + N * N;
+  double* tA2 = tA1 + N * N;
+  double* tA3 = tA2 + N * N;
+  double* tA4 = tA3 + N * N;
+  double* tw = tA4 + N * N;
+  double* tw3 = tw + N;
+  double* teta = tw3 + N;
+  double* tlL = teta + N;
+  double* tlR = tlL + N;
+  double* tl3 = tlR + N;
+  double* tli4 = tl3 + N;
+  double* tB = tli4 + N * N;
+
+  const PsiS T = stage_psi<DIM, N>(R, sm + L::o_ps);
+  const int64_t e = A.elem_list ? A.elem_list[blockIdx.x] : (int64_t)blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
+  // ---- stage tables, states and metrics in shared memory ----
+  for (int k = tid; k < N * N; k += NT) {
+    tQ1[k] = R.skQ1[k];
+    tA1[k] = R.skA1[k];
+    tA2[k] = R.skA2[k];
+    if constexpr (DIM == 3) {
+      tA3[k] = R.skA3[k];
+      tA4[k] = R.skA4[k];
+      tli4[k] = R.lint4[k];
+    }
+  }
+  for (int k = tid; k < N; k += NT) {
+    tw[k] = R.w[k];
+    tw3[k] = R.w3[k];
+    teta[k] = R.eta[k];
+    tlL[k] = R.lL[k];
+    tlR[k] = R.lR[k];
+    if constexpr (DIM == 3) tl3[k] = R.l3L[k];
+  }
+  for (int k = tid; k < NF; k += NT) tB[k] = R.Bf[k];
+  const double* pe = A.prim + (size_t)e * NC * Nq;
+  for (int k = tid; k < NC * Nq; k += NT) sP[k] = pe[k];
+  const double* gv = A.geo_vol + (size_t)e * S::NGV * Nq;
+  for (int k = tid; k < S::NG * Nq; k += NT) sG[k] = gv[k];
+  for (int k = tid; k < NC * NF; k += NT) {
+    int v = k / NF, fz = k % NF;
+    fP[k] = A.trace[(((size_t)e * S::Nf + fz / Nqf) * NC + v) * Nqf + fz % Nqf];
+  }
+  const double* gf = A.geo_face + (size_t)e * S::Nf * DIM * Nqf;
+  for (int k = tid; k < DIM * NF; k += NT) {
+    int m = (k / Nqf) % DIM, z = k / (DIM * Nqf), f = k % Nqf;
+    fJ[m * NF + z * Nqf + f] = gf[k];
+  }
+  __syncthreads();
+  for (int i = tid; i < Nq; i += NT) sP[(DIM + 2) * Nq + i] = sP[i] / sP[(DIM + 1) * Nq + i];
+  for (int fz = tid; fz < NF; fz += NT) fP[NC * NF + fz] = fP[fz] / fP[(DIM + 1) * NF + fz];
+  __syncthreads();
+
+  auto state_at = [&](int i) {
+    NodeState s;
+    s.r = sP[i];
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) s.v[m] = sP[(1 + m) * Nq + i];
+    s.p = sP[(DIM + 1) * Nq + i];
+    s.b = sP[(DIM + 2) * Nq + i];
+    return s;
+  };
+  auto fstate_at = [&](int fz) {
+    NodeState s;
+    s.r = fP[fz];
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) s.v[m] = fP[(1 + m) * NF + fz];
+    s.p = fP[(DIM + 1) * NF + fz];
+    s.b = fP[NC * NF + fz];
+    return s;
+  };
+  auto Gat = [&](int l, int m, int i) { return sG[(l * DIM + m) * Nq + i]; };
+
+  const int grp = lane / N, pos = lane - grp * N;
+  const bool lane_ok = grp < W::LPW;
+
+  // ---- three direction passes ----
+#pragma unroll 1
+  for (int k = 0; k < DIM; ++k) {
+    const int stride = k == 0 ? 1 : (k == 1 ? N : N * N);
+#pragma unroll 1
+    for (int slot = warp; slot < W::SLOTS; slot += W::NW) {
+      const int Lidx = slot * W::LPW + grp;
+      const bool valid = lane_ok && Lidx < W::NL;
+      const int l0 = valid ? Lidx % N : 0, l1 = valid ? Lidx / N : 0;
+      // node coordinates (a, b, c) and index
+      int ca, cb, cc;
+      if (k == 0) {
+        ca = pos;
+        cb = l0;
+        cc = l1;
+      } else if (k == 1) {
+        ca = l0;
+        cb = pos;
+        cc = l1;
+      } else {
+        ca = l0;
+        cb = l1;
+        cc = pos;
+      }
+      if constexpr (DIM == 2) cc = 0;
+      const int i = ca + N * cb + N * N * cc;
+      NodeState me = state_at(valid ? i : 0);
+      double gl[3][3];  // own metric rows g^(l)
+#pragma unroll
+      for (int l = 0; l < DIM; ++l)
+#pragma unroll
+        for (int m = 0; m < DIM; ++m) gl[l][m] = Gat(l, m, valid ? i : 0);
+      double acc[NC];
+#pragma unroll
+      for (int v = 0; v < NC; ++v) acc[v] = 0.0;
+
+      // -- volume pairs on this line: shifts in batches of VB (ILP), exchanged by shuffles --
+#pragma unroll
+      for (int s0 = 1; s0 <= NS; s0 += W::VB) {
+        Job<DIM> jv[W::VB];
+#pragma unroll
+        for (int t = 0; t < W::VB; ++t) {
+          const int s = s0 + t;
+          int pos2 = pos + (s <= NS ? s : 0);
+          if (pos2 >= N) pos2 -= N;
+          const int j = valid ? i + (pos2 - pos) * stride : 0;
+          const int ix = pos * N + pos2;
+          Job<DIM>& jb = jv[t];
+          jb.base = sP;
+          jb.stride = Nq;
+          jb.idx = j;
+          const bool half = (N % 2 == 0) && (s == NS);
+          jb.coef = (valid && s <= NS && !(half && pos >= N / 2)) ? 1.0 : 0.0;
+          if constexpr (DIM == 2) {
+            if (k == 0) {
+              const double cl = tw[cb], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
+#pragma unroll
+              for (int m = 0; m < 2; ++m) jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * (gl[1][m] + Gat(1, m, j));
+            } else {
+              const double a2 = tw[ca] * tA2[ix];
+#pragma unroll
+              for (int m = 0; m < 2; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j));
+            }
+          } else {
+            if (k == 0) {
+              const double cl = 0.5 * tw[cb] * tw3[cc], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
+#pragma unroll
+              for (int m = 0; m < 3; ++m)
+                jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * ((gl[1][m] + gl[2][m]) + (Gat(1, m, j) + Gat(2, m, j)));
+            } else if (k == 1) {
+              const double cl = 0.5 * tw[ca] * tw3[cc], a2 = cl * tA2[ix], a3 = cl * tA3[ix];
+#pragma unroll
+              for (int m = 0; m < 3; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j)) + a3 * (gl[2][m] + Gat(2, m, j));
+            } else {
+              const double a4 = 0.125 * tw[ca] * tw[cb] * (1.0 - teta[cb]) * tA4[ix];
+#pragma unroll
+              for (int m = 0; m < 3; ++m) jb.n[m] = a4 * (gl[2][m] + Gat(2, m, j));
+            }
+          }
+        }
+        double Fs[W::VB][NC];
+        flux_batch<DIM, W::VB>(me, jv, gm1inv, Fs);
+#pragma unroll
+        for (int t = 0; t < W::VB; ++t) {
+          const int s = s0 + t;
+          if (s > NS) break;
+          const bool half = (N % 2 == 0) && (s == NS);
+          int pos0 = pos - s;
+          if (pos0 < 0) pos0 += N;
+          const int src = grp * N + pos0;
+          const bool recv = valid && !(half && pos < N / 2);
+#pragma unroll
+          for (int v = 0; v < NC; ++v) {
+            double tt = __shfl_sync(0xffffffffu, Fs[t][v], src);
+            acc[v] -= Fs[t][v];
+            if (recv) acc[v] += tt;
+          }
+        }
+      }
+
+      // -- facet-correction pairs along the same lines --
+      // a facet job: state of facet node fz, normal (G_i^T nhat + J n_f)/2, coefficient (R^T B)_if
+      auto fjob = [&](Job<DIM>& jb, int z, int f, double coef, const double* gtn) {
+        const int fz = z * Nqf + f;
+        jb.base = fP;
+        jb.stride = NF;
+        jb.idx = fz;
+        jb.coef = valid ? coef : 0.0;
+#pragma unroll
+        for (int m = 0; m < DIM; ++m) jb.n[m] = 0.5 * (gtn[m] + fJ[m * NF + fz]);
+      };
+      // facet-side sums over the line group; the first lane of the group writes C^T 1
+      auto line_sum = [&](const double* Fc, double* dst) {
+#pragma unroll
+        for (int v = 0; v < NC; ++v) {
+          acc[v] -= Fc[v];
+          double sum = group_sum<N>(Fc[v], pos);
+          if (valid && pos == 0 && dst) dst[v] = sum;
+        }
+      };
+      if constexpr (DIM == 2) {
+        Job<DIM> jf[3];
+        if (k == 0) {  // eta1 = +1 (facet 2) and eta1 = -1 (facet 3): facet node b
+          const double r2 = 0.70710678118654752440;
+          double gtn[2] = {(gl[0][0] + gl[1][0]) * r2, (gl[0][1] + gl[1][1]) * r2};
+          double gtn3[2] = {-gl[0][0], -gl[0][1]};
+          fjob(jf[0], 1, cb, tlR[ca] * tB[1 * Nqf + cb], gtn);
+          fjob(jf[1], 2, cb, tlL[ca] * tB[2 * Nqf + cb], gtn3);
+          double Fc[2][NC];
+          flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
+          double d1[NC], d2[NC];
+          line_sum(Fc[0], d1);
+          line_sum(Fc[1], d2);
+          if (valid && pos == 0)
+#pragma unroll
+            for (int v = 0; v < NC; ++v) {
+              ct[v * NF + 1 * Nqf + cb] = d1[v];
+              ct[v * NF + 2 * Nqf + cb] = d2[v];
+            }
+        } else {  // eta2 = -1 (facet 1): facet node a
+          double gtn[2] = {-gl[1][0], -gl[1][1]};
+          fjob(jf[0], 0, ca, tlL[cb] * tB[0 * Nqf + ca], gtn);
+          double Fc[1][NC];
+          flux_batch<DIM, 1>(me, jf, gm1inv, Fc);
+          double d1[NC];
+          line_sum(Fc[0], d1);
+          if (valid && pos == 0)
+#pragma unroll
+            for (int v = 0; v < NC; ++v) ct[v * NF + ca] = d1[v];
+        }
+      } else {
+        if (k == 0) {  // facets 2 and 3 (eta1 = +1 / -1): facet node (b, c)
+          const double r3 = 0.57735026918962576451;
+          const int f = cb + N * cc;
+          double gtn[3], gtn3[3];
+#pragma unroll
+          for (int m = 0; m < 3; ++m) {
+            gtn[m] = (gl[0][m] + gl[1][m] + gl[2][m]) * r3;
+            gtn3[m] = -gl[0][m];
+          }
+          Job<DIM> jf[2];
+          fjob(jf[0], 1, f, tlR[ca] * tB[1 * Nqf + f], gtn);
+          fjob(jf[1], 2, f, tlL[ca] * tB[2 * Nqf + f], gtn3);
+          double Fc[2][NC];
+          flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
+          double d1[NC], d2[NC];
+          line_sum(Fc[0], d1);
+          line_sum(Fc[1], d2);
+          if (valid && pos == 0)
+#pragma unroll
+            for (int v = 0; v < NC; ++v) {
+              ct[v * NF + 1 * Nqf + f] = d1[v];
+              ct[v * NF + 2 * Nqf + f] = d2[v];
+            }
+        } else if (k == 1) {  // facet 1 (eta2 = -1): node (a, c); facet 4 (eta3 = -1): nodes (a, j)
+          const int f = ca + N * cc;
+          double gtn[3] = {-gl[1][0], -gl[1][1], -gl[1][2]};
+          double gt4[3] = {-gl[2][0], -gl[2][1], -gl[2][2]};
+          constexpr int JB = 2;  // jobs per batch: facet 1 and the N facet-4 nodes
+#pragma unroll 1
+          for (int j0 = -1; j0 < N; j0 += JB) {
+            Job<DIM> jq[JB];
+#pragma unroll
+            for (int t = 0; t < JB; ++t) {
+              const int jf = j0 + t;
+              if (jf < 0) {
+                fjob(jq[t], 0, f, tlL[cb] * tB[0 * Nqf + f], gtn);
+              } else {
+                const int jj = jf < N ? jf : N - 1;
+                const int f4 = ca + N * jj;
+                fjob(jq[t], 3, f4, jf < N ? tli4[jj * N + cb] * tl3[cc] * tB[3 * Nqf + f4] : 0.0, gt4);
+              }
+            }
+            double Fb[JB][NC];
+            flux_batch<DIM, JB>(me, jq, gm1inv, Fb);
+#pragma unroll
+            for (int t = 0; t < JB; ++t) {
+              const int jf = j0 + t;
+              double dd[NC];
+              line_sum(Fb[t], dd);  // sum over b on the (a, c) line
+              if (valid && pos == 0) {
+                if (jf < 0) {
+#pragma unroll
+                  for (int v = 0; v < NC; ++v) ct[v * NF + f] = dd[v];
+                } else if (jf < N) {
+#pragma unroll
+                  for (int v = 0; v < NC; ++v) pt[((v * N + jf) * N + ca) * N + cc] = dd[v];
+                }
+              }
+            }
+          }
+        }
+      }
+      // -- residual of this pass (exclusive owner of node i within the pass) --
+      if (valid) {
+#pragma unroll
+        for (int v = 0; v < NC; ++v) {
+          if (k == 0)
+            sR[v * Nq + i] = acc[v];
+          else
+            sR[v * Nq + i] += acc[v];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
+    for (int it = tid; it < NC * N * N; it += NT) {
+      const int v = it / (N * N), jf = (it / N) % N, a = it % N;
+      double s = 0.0;
+      for (int c = 0; c < N; ++c) s += pt[((v * N + jf) * N + a) * N + c];
+      ct[v * NF + 3 * Nqf + a + N * jf] = s;
+    }
+    __syncthreads();
+  }
+
+  // ---- interface flux and s = B J_f f* - C^T 1 ----
+  for (int fz = tid; fz < NF; fz += NT) {
+    int z = fz / Nqf, f = fz % Nqf;
+    int64_t slot = A.face_slot[e * S::Nf + z];
+    int rf = A.face_reflect[e * S::Nf + z];
+    int fo;
+    if constexpr (DIM == 2)
+      fo = rf ? N - 1 - f : f;
+    else
+      fo = rf ? (N - 1 - f % N) + N * (f / N) : f;
+    const double* tp = A.trace + (size_t)slot * NC * Nqf;
+    NodeState up, um = fstate_at(fz);
+    up.r = tp[fo];
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) up.v[m] = tp[(1 + m) * Nqf + fo];
+    up.p = tp[(DIM + 1) * Nqf + fo];
+    up.b = up.r / up.p;
+    double Jn[DIM], Jf = 0.0;
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) {
+      Jn[m] = fJ[m * NF + fz];
+      Jf += Jn[m] * Jn[m];
+    }
+    Jf = sqrt(Jf);
+    double nu[DIM];
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) nu[m] = Jn[m] / Jf;
+    double F[NC];
+    ec_flux_v2<DIM>(um, up, nu, gm1inv, F);
+    if (A.es) {  // local Lax-Friedrichs with Davis's wave speed
+      double vnm = 0.0, vnp = 0.0;
+#pragma unroll
+      for (int m = 0; m < DIM; ++m) {
+        vnm += um.v[m] * nu[m];
+        vnp += up.v[m] * nu[m];
+      }
+      double lam = fmax(fabs(vnm), fabs(vnp)) + fmax(sqrt(g * um.p / um.r), sqrt(g * up.p / up.r));
+      double Um[NC], Up[NC];
+      cons_of<DIM>(um.r, um.v, um.p, gm1inv, Um);
+      cons_of<DIM>(up.r, up.v, up.p, gm1inv, Up);
+#pragma unroll
+      for (int v = 0; v < NC; ++v) F[v] -= 0.5 * lam * (Up[v] - Um[v]);
+    }
+    double bj = tB[fz] * Jf;
+#pragma unroll
+    for (int v = 0; v < NC; ++v) ct[v * NF + fz] = bj * F[v] - ct[v * NF + fz];
+  }
+  __syncthreads();
+
+  // ---- lifting r -= R^T s ----
+  for (int i = tid; i < Nq; i += NT) {
+    int a = i % N, b = (i / N) % N, c = DIM == 3 ? i / (N * N) : 0;
+#pragma unroll
+    for (int v = 0; v < NC; ++v) {
+      const double* sv = ct + v * NF;
+      double t;
+      if constexpr (DIM == 2) {
+        t = tlL[b] * sv[a] + tlR[a] * sv[Nqf + b] + tlL[a] * sv[2 * Nqf + b];
+      } else {
+        t = tlL[b] * sv[a + N * c] + tlR[a] * sv[Nqf + b + N * c] + tlL[a] * sv[2 * Nqf + b + N * c];
+        double t4 = 0.0;
+        for (int jf = 0; jf < N; ++jf) t4 += tli4[jf * N + b] * sv[3 * Nqf + a + N * jf];
+        t += tl3[c] * t4;
+      }
+      sR[v * Nq + i] -= t;
+    }
+  }
+  __syncthreads();
+
+  // ---- d u~/dt = V^T W/J~ V (V^T r) ----
+  double* T1 = sm + L::o_pr;
+  double* T2 = T1 + t1_size<DIM, N>();
+  double* um = sm + L::o_pt;
+  nodal_to_modal<DIM, N, NC>(T, sR, um, T1, T2);
+  if (A.mode == 5) {  // entropy production sum w~ . (V^T r) and conservation (V^T r)_0 / c0
+    double loc = 0.0, la = 0.0;
+    for (int k = tid; k < NC * Np; k += NT) {
+      double t = A.wt[(size_t)e * NC * Np + k] * um[k];
+      loc += t;
+      la += fabs(t);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      loc += __shfl_down_sync(0xffffffffu, loc, o);
+      la += __shfl_down_sync(0xffffffffu, la, o);
+    }
+    __shared__ double red[2][W::NW];
+    if (lane == 0) {
+      red[0][warp] = loc;
+      red[1][warp] = la;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int wv = 0; wv < W::NW; ++wv) {
+        s0 += red[0][wv];
+        s1 += red[1][wv];
+      }
+      double* pe2 = A.part + (size_t)e * (2 + NC);
+      pe2[0] = s0;
+      pe2[1] = s1;
+      for (int v = 0; v < NC; ++v) pe2[2 + v] = um[v * Np] / A.c0;
+    }
+  }
+  modal_to_nodal<DIM, N, NC>(T, um, sR, T1, T2);
+  for (int it = tid; it < NC * Nq; it += NT) sR[it] *= gv[(S::NG + 1) * Nq + it % Nq];
+  __syncthreads();
+  nodal_to_modal<DIM, N, NC>(T, sR, um, T1, T2);
+  const size_t base = (size_t)e * NC * Np;
+  const double dt = A.dt;
+  for (int kk = tid; kk < NC * Np; kk += NT) {
+    double du = um[kk];
+    switch (A.mode) {
+      case 0:
+      case 5:
+        A.out[base + kk] = du;
+        break;
+      case 1:  // classical RK4 stage 1 (R17)
+        A.acc[base + kk] = A.u0[base + kk] + (dt / 6.0) * du;
+        A.ustage[base + kk] = A.u0[base + kk] + (0.5 * dt) * du;
+        break;
+      case 2:
+        A.acc[base + kk] += (dt / 3.0) * du;
+        A.ustage[base + kk] = A.u0[base + kk] + (0.5 * dt) * du;
+        break;
+      case 3:
+        A.acc[base + kk] += (dt / 3.0) * du;
+        A.ustage[base + kk] = A.u0[base + kk] + dt * du;
+        break;
+      case 4:
+        A.out[base + kk] = A.acc[base + kk] + (dt / 6.0) * du;
+        break;
+    }
+  }
+}
+
+}  // namespace esb

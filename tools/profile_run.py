@@ -1,11 +1,12 @@
-"""Small driver for ncu: C5-shaped element work (tet p=8, TGV, ES) on an M^3 x 6 mesh."""
+"""Small driver for ncu: the bench workload's element work (projected analytic initial state) on a
+smaller mesh.  usage: python tools/profile_run.py [dim M p reps]"""
 import math
 import sys
 
-import numpy as np
 import torch
 
 sys.path.insert(0, ".")
+import bench
 import es_inputs as I
 import paper_2312_07874_b200 as es
 
@@ -16,7 +17,7 @@ reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 L = 2 * math.pi if d == 3 else 2.0
 mesh = I.split_cartesian(d, M, L)
 ctx = es.Context(mesh, p, warp=I.bj_warp(d, L, M), interface_flux=1)
-u = torch.from_numpy(I.modal_state_from_centroids(mesh, p, "tgv" if d == 3 else "vortex", seed=1)).cuda()
+u, xn, un = bench.initial_state(ctx, torch, "tgv" if d == 3 else "vortex", d, L)
 du = torch.empty_like(u)
 for _ in range(reps):
     ctx.rhs(u, du)
