@@ -13,6 +13,19 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
+def nccl_dir():
+    """torch's bundled NCCL (2.28): linking the same libnccl.so.2 torch loads keeps one NCCL per
+    process whichever of torch / libes_b200.so is loaded first."""
+    try:
+        import nvidia.nccl
+        d = os.path.dirname(nvidia.nccl.__file__) if nvidia.nccl.__file__ else list(nvidia.nccl.__path__)[0]
+        if os.path.exists(os.path.join(d, "lib", "libnccl.so.2")):
+            return d
+    except Exception:
+        pass
+    return None
+
+
 def _run(cmd):
     print("+", " ".join(cmd), flush=True)
     subprocess.check_call(cmd, cwd=ROOT)
@@ -50,6 +63,9 @@ def build_lib(force=False, jobs=8):
     objs = []
     procs = []
     inc = ["-I", os.path.join(ROOT, "include"), "-I", c]
+    nd = nccl_dir()
+    if nd:
+        inc = ["-I", os.path.join(nd, "include")] + inc
     for f in sorted(os.listdir(c)):
         p = os.path.join(c, f)
         if f.endswith(".cu"):
@@ -72,8 +88,11 @@ def build_lib(force=False, jobs=8):
             _wait(procs)
             procs = []
     _wait(procs)
+    nccl_link = ["-lnccl"]
+    if nd:
+        nccl_link = ["-L" + os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib")]
     _run([NVCC, *ARCH, "-shared", "-o", LIB_SO, *objs, "-Xcompiler", "-fopenmp",
-          "-L/usr/local/cuda/lib64", "-lcudart", "-lnccl", "-lquadmath"])
+          "-L/usr/local/cuda/lib64", "-lcudart", *nccl_link, "-lquadmath"])
     return LIB_SO
 
 
