@@ -346,7 +346,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   double* d_xmap = nullptr;
   CK(upload(&d_xmap, xmap));
   const int NG = d * d, NF = c->Nf * c->Nqf;
-  CK(cudaMalloc((void**)&c->geo_vol, (size_t)c->nloc * (NG + 2) * c->Nq * sizeof(double)));
+  CK(cudaMalloc((void**)&c->geo_vol, (size_t)c->nloc * even_up((NG + 2) * c->Nq) * sizeof(double)));
   CK(cudaMalloc((void**)&c->geo_face, (size_t)c->nloc * NF * d * sizeof(double)));
   CK(cudaMalloc((void**)&c->xq, (size_t)c->nloc * c->Nq * d * sizeof(double)));
   CK(cudaMalloc((void**)&c->jt, (size_t)c->nloc * c->Nq * sizeof(double)));
@@ -358,7 +358,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   for (int k = 0; k < 8; ++k) CK(upload(&mats[k], *srcs[k]));
   const double* lo[8];
   for (int k = 0; k < 8; ++k) lo[k] = mats[k] ? mats[k] + srcs[k]->size() / 2 : nullptr;  // [hi | lo]
-  GeoArgs g{d, Npg, c->T.Ncl, c->Nq, NF, c->Nqf, d_xmap, mats[0], mats[1], mats[2], mats[3], mats[4], mats[5],
+  GeoArgs g{d, Npg, c->T.Ncl, c->Nq, NF, c->Nqf, even_up((NG + 2) * c->Nq), d_xmap, mats[0], mats[1], mats[2], mats[3], mats[4], mats[5],
             mats[6], mats[7], lo[0], lo[1], lo[2], lo[3], lo[4], lo[5], lo[6], lo[7],
             c->R.Wvol, c->R.nhat, d_shift, c->geo_vol, c->geo_face, c->xq, c->jt, c->bad};
   CK(launch_geometry(g, c->nloc, c->stream));
@@ -392,7 +392,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
     return fail(c, ES_ERR_VERIFY, "face normals / weights do not match across faces (rel " + std::to_string(mism) + ")");
   // ---- work buffers ----
   const size_t nmod = (size_t)c->nloc * c->NC * c->Np;
-  CK(cudaMalloc((void**)&c->prim, (size_t)c->nloc * c->NC * c->Nq * sizeof(double)));
+  CK(cudaMalloc((void**)&c->prim, (size_t)c->nloc * even_up(c->NC * c->Nq) * sizeof(double)));
   CK(cudaMalloc((void**)&c->trace, (size_t)c->nslots * c->NC * c->Nqf * sizeof(double)));
   CK(cudaMalloc((void**)&c->wt, nmod * sizeof(double)));
   CK(cudaMalloc((void**)&c->part, (size_t)c->nloc * (2 + c->NC) * sizeof(double)));
@@ -553,7 +553,7 @@ es_status es_element_geometry(es_context* c, int64_t k, double* G, double* Jn, d
   const int d = c->d, NG = d * d, Nq = c->Nq, Nqf = c->Nqf, Nf = c->Nf;
   if (G) {
     std::vector<double> gv((size_t)NG * Nq);
-    CK(cudaMemcpy(gv.data(), c->geo_vol + (size_t)k * (NG + 2) * Nq, gv.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(gv.data(), c->geo_vol + (size_t)k * even_up((NG + 2) * Nq), gv.size() * 8, cudaMemcpyDeviceToHost));
     for (int i = 0; i < Nq; ++i)
       for (int q = 0; q < NG; ++q) G[(size_t)i * NG + q] = gv[(size_t)q * Nq + i];
   }

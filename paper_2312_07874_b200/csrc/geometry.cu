@@ -141,7 +141,7 @@ __global__ void geometry_kernel(GeoArgs g) {
       for (int m = 0; m < d; ++m) x[m] = dd_add(x[m], dd_mul(c, dd{xs[i * d + m], 0.0}));
     }
     if (!(jt.hi > 0.0)) atomicOr(g.bad, 2);
-    double* gv = g.geo_vol + (size_t)e * (NG + 2) * Nq;
+    double* gv = g.geo_vol + (size_t)e * g.gv_stride;
     for (int k = 0; k < NG; ++k) gv[k * Nq + X] = G[k];
     double W = __ldg(&g.Wvol[X]);
     gv[NG * Nq + X] = W * jt.hi;

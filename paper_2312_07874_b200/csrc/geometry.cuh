@@ -7,6 +7,7 @@ namespace esb {
 
 struct GeoArgs {
   int dim, Npg, Ncl, Nq, NF, Nqf;
+  int gv_stride;        // doubles per element in geo_vol (even: 16-byte aligned element blocks)
   const double* xmap;   // [ne][Npg][dim] mapping-node positions
   // reference matrices as double-double pairs (hi, lo) built in long double (R25)
   const double *LmapV, *DmapV, *DmapF, *DmapM, *LmapC, *DmapC, *DcurlV, *DcurlF;
@@ -14,7 +15,7 @@ struct GeoArgs {
   const double* Wvol;   // [Nq]
   const double* nhat;   // [Nf][3]
   const double* shift;  // [ne][dim] local-coordinate origin added back to xq (R25)
-  double* geo_vol;      // [ne][dim*dim+2][Nq]
+  double* geo_vol;      // [ne][gv_stride]: [dim*dim+2][Nq] then padding
   double* geo_face;     // [ne][Nf][dim][Nqf]
   double* xq;           // [ne][Nq][dim]
   double* jt_out;       // optional [ne][Nq]

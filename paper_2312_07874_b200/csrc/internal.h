@@ -72,6 +72,10 @@ struct MeshPlan {
 bool build_mesh_plan(int d, int64_t ne, const int64_t* ev, int rank, int world, MeshPlan& plan,
                      std::string& err);
 
+// per-element strides of the device arrays, rounded up to an even number of doubles so that every
+// element block is 16-byte aligned for bulk (TMA) copies
+inline int even_up(int x) { return (x + 1) & ~1; }
+
 // element range of a rank
 inline void rank_range(int64_t ne, int rank, int world, int64_t& first, int64_t& count) {
   first = ne * rank / world;

@@ -27,6 +27,8 @@ struct Sz {
   static constexpr int NC = DIM + 2;
   static constexpr int NG = DIM * DIM;
   static constexpr int NGV = NG + 2;  // G_lm, W J~, W / J~
+  static constexpr int GVS = (NGV * Nq + 1) & ~1;  // geo_vol element stride (even, 16-B aligned)
+  static constexpr int PRS = (NC * Nq + 1) & ~1;   // prim element stride
   static constexpr int KPT = (Nq + 383) / 384;
   static constexpr int NT = ((Nq + KPT - 1) / KPT + 31) / 32 * 32;
 };
@@ -45,8 +47,8 @@ struct ProjArgs {
   int64_t n_elem;
   const int64_t* elem_list;  // optional element subset
   const double* u;           // [nloc][NC][Np] modal stage input
-  const double* geo_vol;     // [nloc][NGV][Nq]
-  double* prim;              // [nloc][NC][Nq]   entropy-projected primitive (rho, v, p)
+  const double* geo_vol;     // [nloc][GVS]: [NGV][Nq] + pad
+  double* prim;              // [nloc][PRS]: [NC][Nq] + pad, entropy-projected primitive (rho, v, p)
   double* trace;             // [slots][NC][Nqf] entropy-projected primitive at facet nodes
   double* wt;                // optional [nloc][NC][Np] projected entropy variables w~
   int* bad;                  // admissibility flag
@@ -392,7 +394,7 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT) project_kernel(DevRef R, ProjA
   const int64_t e = A.elem_list ? A.elem_list[blockIdx.x] : (int64_t)blockIdx.x;
   const int tid = threadIdx.x, nt = blockDim.x;
   const double g = A.gamma, gm1 = g - 1.0, gm1inv = 1.0 / gm1;
-  const double* gv = A.geo_vol + (size_t)e * S::NGV * Nq;
+  const double* gv = A.geo_vol + (size_t)e * S::GVS;
   for (int k = tid; k < NC * Np; k += nt) um[k] = A.u[(size_t)e * NC * Np + k];
   __syncthreads();
   modal_to_nodal<DIM, N, NC>(T, um, X, T1, T2);  // u = V u~
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT) project_kernel(DevRef R, ProjA
     for (int v = 0; v < NC; ++v) w[v] = X[v * Nq + i];
     bad |= Uofw(w, o);
 #pragma unroll
-    for (int v = 0; v < NC; ++v) A.prim[((size_t)e * NC + v) * Nq + i] = o[v];
+    for (int v = 0; v < NC; ++v) A.prim[(size_t)e * S::PRS + v * Nq + i] = o[v];
   }
   for (int fz = tid; fz < NF; fz += nt) {
     double w[NC], o[NC];

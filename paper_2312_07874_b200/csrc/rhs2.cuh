@@ -1,13 +1,14 @@
-// rhs2.cuh -- K2 v2: warp-synchronous line-wise flux differencing (product code).
+// rhs2.cuh -- K2 (v4): warp-synchronous line-wise flux differencing (product code).
 //
 // Each warp owns whole eta_k lines ("line groups" of N lanes, floor(32/N) lines per warp).  For one
 // direction k a lane keeps its node's entropy-projected state and metric rows in registers, pairs
 // with the node (pos+s) mod N of its line for s = 1..floor(N/2) (every unordered pair exactly once,
 // P:572), subtracts F from its own accumulator and receives the partner's +F by a warp shuffle.
 // The facet-correction pairs whose extrapolation runs along the same lines are done in
-// the same pass; their facet-side sums C^T 1 use deterministic segmented shuffle trees.  Only three
-// block barriers separate the direction passes.  Interface flux, lifting and the weight-adjusted
-// inverse follow as in K2 v1.
+// the same pass; their facet-side sums C^T 1 go through a per-warp shared-memory scratch and are
+// summed in a fixed order (deterministic, no atomics).  The element's states, metric terms, traces
+// and facet normals arrive by bulk asynchronous copies (cp.async.bulk, TMA engine) completing on an
+// mbarrier.  Interface flux, lifting and the weight-adjusted inverse follow in the same CTA.
 #pragma once
 #include "kernels.cuh"
 
@@ -25,22 +26,33 @@ struct Lw {  // line-group layout
   static constexpr int VB = 2;  // volume pair jobs per flux batch (ILP vs registers)
 };
 
+__host__ __device__ constexpr int ev2(int x) { return (x + 1) & ~1; }
+
 template <int DIM, int N>
 struct Rhs2Smem {
   using S = Sz<DIM, N>;
-  static constexpr int PR = (DIM + 3) * S::Nq;  // rho, v, p, beta
-  static constexpr int GG = S::NG * S::Nq;      // G_lm
-  static constexpr int RR = S::NC * S::Nq;      // nodal residual r
+  using W = Lw<DIM, N>;
+  static constexpr int PR = ev2((DIM + 3) * S::Nq);  // rho, v, p, beta   (bulk copy of prim: PRS)
+  static constexpr int GG = ev2(S::NG * S::Nq);      // G_lm              (bulk copy)
+  static constexpr int RR = S::NC * S::Nq;           // nodal residual r
   static constexpr int PT = DIM == 3 ? S::NC * N * N * N : 0;  // facet-4 partial sums [v][j][a][c]
-  static constexpr int FP = (S::NC + 1) * S::NF;  // facet states (rho, v, p, beta)
-  static constexpr int FJ = DIM * S::NF;
-  static constexpr int CT = S::NC * S::NF;
+  static constexpr int FP = S::Nf * S::NC * S::Nqf;  // facet states [z][rho, v, p][f] (bulk copy)
+  static constexpr int FB = S::NF;                   // facet beta = rho / p
+  static constexpr int FJ = S::Nf * DIM * S::Nqf;    // J n at facet nodes [z][m][f] (bulk copy)
+  static constexpr int CT = S::NC * S::NF;           // C^T 1, then s = B J_f f* - C^T 1
+  static constexpr int SC = W::NW * S::NC * 32;      // per-warp reduction scratch
   static constexpr int TB = 5 * N * N + 6 * N + N * N + S::NF;
-  static constexpr int PS = psi_smem_doubles<DIM, N>();
-  static constexpr int o_pr = 0, o_g = o_pr + PR, o_r = o_g + GG, o_pt = o_r + RR, o_fp = o_pt + PT,
-                       o_fj = o_fp + FP, o_ct = o_fj + FJ, o_tb = o_ct + CT, o_ps = o_tb + TB, total = o_ps + PS;
-  static_assert(t1_size<DIM, N>() + t2_size<DIM, N>() <= PR + GG, "transform scratch");
-  static_assert(S::NC * S::Np <= PT + FP + FJ + CT, "modal scratch");
+  static constexpr int o_pr = 0, o_g = o_pr + PR, o_r = ev2(o_g + GG), o_pt = ev2(o_r + RR), o_fp = ev2(o_pt + PT),
+                       o_fb = ev2(o_fp + FP), o_fj = ev2(o_fb + FB), o_ct = ev2(o_fj + FJ), o_sc = ev2(o_ct + CT),
+                       o_tb = ev2(o_sc + SC), o_end = ev2(o_tb + TB);
+  // epilogue: transform scratch reuses the state / metric region, and so do the psi tables when
+  // they fit there (3D); otherwise they get their own region
+  static constexpr int o_t1 = 0, o_t2 = o_t1 + t1_size<DIM, N>(), o_ps0 = ev2(o_t2 + t2_size<DIM, N>());
+  static constexpr bool PS_IN = o_ps0 + psi_smem_doubles<DIM, N>() <= PR + GG;
+  static constexpr int o_ps = PS_IN ? o_ps0 : o_end;
+  static constexpr int total = PS_IN ? o_end : o_end + psi_smem_doubles<DIM, N>();
+  static_assert(o_t2 + t2_size<DIM, N>() <= PR + GG, "epilogue scratch");
+  static_assert(S::PRS <= PR, "prim copy");
 };
 
 template <int DIM, int N>
@@ -97,43 +109,39 @@ __device__ __forceinline__ void ec_flux_v2(const NodeState& A, const NodeState& 
   F[DIM + 1] = fr * (0.5 * vdot + ib_ln * gm1inv) + 0.5 * (A.p * vbn + B.p * van);
 }
 
-// deterministic sum over the N lanes of a line group; the group's first lane gets the total
-template <int N>
-__device__ __forceinline__ double group_sum(double x, int a) {
-#pragma unroll
-  for (int o = 1; o < N; o <<= 1) {
-    double t = __shfl_down_sync(0xffffffffu, x, o);
-    if (a + o < N) x += t;
-  }
-  return x;
+// warp shuffle of a double as two 32-bit halves (no register moves around inline asm)
+__device__ __forceinline__ double shfl_d(double x, int src) {
+  int lo = __double2loint(x), hi = __double2hiint(x);
+  lo = __shfl_sync(0xffffffffu, lo, src);
+  hi = __shfl_sync(0xffffffffu, hi, src);
+  return __hiloint2double(hi, lo);
 }
 
-// reciprocal: hardware approximation refined by three Newton steps (no special-case branch;
-// arguments are positive and normal); within 1 ulp of 1/s
+// reciprocal: hardware approximation refined by two Newton steps (quadratic convergence from the
+// ~2^-23 seed; arguments are positive and normal)
 __device__ __forceinline__ double rcp_nr(double s) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
   double e = fma(-s, r, 1.0);
   r = fma(r, e, r);
   e = fma(-s, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-s, r, 1.0);
   return fma(r, e, r);
 }
 
-// one pair job: the other state lives in shared memory at base[q * stride + idx] (q = rho, v, p,
-// beta), n is the (scaled) direction, coef multiplies the flux
+// one pair job: the other state lives in shared memory at base[q * stride + idx] (q = rho, v, p)
+// and bb[idx] (beta); n is the direction, already scaled by the operator coefficient (f# is linear
+// in n), zero for masked jobs -- which makes F exactly zero
 template <int DIM>
 struct Job {
   const double* base;
+  const double* bb;
   int stride, idx;
   double n[DIM];
-  double coef;
 };
 
 // B Ranocha fluxes (R3) of `me` with the job states, straight-line in the common case: both
 // log means take the Taylor branch; a warp-uniform fallback recomputes the members that need the
-// log branch (R5).  F[b][v] = coef_b f#(me, other_b, n_b).
+// log branch (R5).  F[b][v] = f#(me, other_b, n_b).
 template <int DIM, int B>
 __device__ __forceinline__ void flux_batch(const NodeState& me, const Job<DIM>* jb, double gm1inv,
                                            double (*F)[DIM + 2]) {
@@ -148,7 +156,7 @@ __device__ __forceinline__ void flux_batch(const NodeState& me, const Job<DIM>* 
 #pragma unroll
     for (int m = 0; m < DIM; ++m) o[t].v[m] = q[(1 + m) * st];
     o[t].p = q[(DIM + 1) * st];
-    o[t].b = q[(DIM + 2) * st];
+    o[t].b = jb[t].bb[jb[t].idx];
   }
 #pragma unroll
   for (int t = 0; t < B; ++t) {
@@ -181,13 +189,35 @@ __device__ __forceinline__ void flux_batch(const NodeState& me, const Job<DIM>* 
       vdot += me.v[m] * o[t].v[m];
     }
     const double pav = 0.5 * (me.p + o[t].p);
-    const double c = jb[t].coef;
     const double fr = rl[t] * vn;
-    F[t][0] = c * fr;
+    F[t][0] = fr;
 #pragma unroll
-    for (int m = 0; m < DIM; ++m) F[t][1 + m] = c * (fr * vav[m] + pav * n[m]);
-    F[t][DIM + 1] = c * (fr * (0.5 * vdot + ib[t] * gm1inv) + 0.5 * (me.p * vbn + o[t].p * van));
+    for (int m = 0; m < DIM; ++m) F[t][1 + m] = fr * vav[m] + pav * n[m];
+    F[t][DIM + 1] = fr * (0.5 * vdot + ib[t] * gm1inv) + 0.5 * (me.p * vbn + o[t].p * van);
   }
+}
+
+// ---- bulk asynchronous copies (TMA engine) global -> shared, completing on an mbarrier ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 template <int DIM, int N>
@@ -196,15 +226,17 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
   using W = Lw<DIM, N>;
   using L = Rhs2Smem<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf, NT = W::NT, NS = W::NS;
-  extern __shared__ double sm[];
-  double* sP = sm + L::o_pr;   // [DIM+3][Nq]: rho, v_1..v_d, p, beta
-  double* sG = sm + L::o_g;    // [NG][Nq]: G_lm at (l*DIM+m)
-  double* sR = sm + L::o_r;    // [NC][Nq] nodal residual
-  double* pt = sm + L::o_pt;   // [NC][N(j)][N(a)][N(c)] facet-4 partials
-  double* fP = sm + L::o_fp;   // [NC+1][NF] facet states rho, v, p, beta
-  double* fJ = sm + L::o_fj;   // [DIM][NF] J n
-  double* ct = sm + L::o_ct;   // [NC][NF] C^T 1, then s = B J_f f* - C^T 1
-  double* tb = sm + L::o_tb;
+  extern __shared__ __align__(16) double smk2[];
+  __shared__ uint64_t mbar;
+  double* sP = smk2 + L::o_pr;  // [DIM+3][Nq]: rho, v_1..v_d, p, beta
+  double* sG = smk2 + L::o_g;   // [NG][Nq]: G_lm at (l*DIM+m)
+  double* sR = smk2 + L::o_r;   // [NC][Nq] nodal residual
+  double* pt = smk2 + L::o_pt;  // [NC][N(j)][N(a)][N(c)] facet-4 partials
+  double* fP = smk2 + L::o_fp;  // [Nf][NC][Nqf] facet states rho, v, p
+  double* fB = smk2 + L::o_fb;  // [Nf*Nqf] facet beta
+  double* fJ = smk2 + L::o_fj;  // [Nf][DIM][Nqf] J n
+  double* ct = smk2 + L::o_ct;  // [NC][NF] C^T 1, then s = B J_f f* - C^T 1
+  double* tb = smk2 + L::o_tb;
   double* tQ1 = tb;
   double* tA1 = tQ1 + N * N;
   double* tA2 = tA1 + N * N;
@@ -219,11 +251,21 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
   double* tli4 = tl3 + N;
   double* tB = tli4 + N * N;
 
-  const PsiS T = stage_psi<DIM, N>(R, sm + L::o_ps);
   const int64_t e = A.elem_list ? A.elem_list[blockIdx.x] : (int64_t)blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* scr = smk2 + L::o_sc + warp * NC * 32;
   const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
-  // ---- stage tables, states and metrics in shared memory ----
+  const double* gv = A.geo_vol + (size_t)e * S::GVS;
+  // ---- stage states, metrics, traces and facet normals by bulk copies; tables by the threads ----
+  if (tid == 0) {
+    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8;
+    mbar_init(&mbar, 1);
+    mbar_expect_tx(&mbar, bP + bG + bF + bJ);
+    bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &mbar);
+    bulk_g2s(sG, gv, bG, &mbar);
+    bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &mbar);
+    bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &mbar);
+  }
   for (int k = tid; k < N * N; k += NT) {
     tQ1[k] = R.skQ1[k];
     tA1[k] = R.skA1[k];
@@ -243,22 +285,13 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
     if constexpr (DIM == 3) tl3[k] = R.l3L[k];
   }
   for (int k = tid; k < NF; k += NT) tB[k] = R.Bf[k];
-  const double* pe = A.prim + (size_t)e * NC * Nq;
-  for (int k = tid; k < NC * Nq; k += NT) sP[k] = pe[k];
-  const double* gv = A.geo_vol + (size_t)e * S::NGV * Nq;
-  for (int k = tid; k < S::NG * Nq; k += NT) sG[k] = gv[k];
-  for (int k = tid; k < NC * NF; k += NT) {
-    int v = k / NF, fz = k % NF;
-    fP[k] = A.trace[(((size_t)e * S::Nf + fz / Nqf) * NC + v) * Nqf + fz % Nqf];
-  }
-  const double* gf = A.geo_face + (size_t)e * S::Nf * DIM * Nqf;
-  for (int k = tid; k < DIM * NF; k += NT) {
-    int m = (k / Nqf) % DIM, z = k / (DIM * Nqf), f = k % Nqf;
-    fJ[m * NF + z * Nqf + f] = gf[k];
-  }
-  __syncthreads();
+  __syncthreads();  // mbarrier initialised before anyone waits
+  mbar_wait(&mbar, 0);
   for (int i = tid; i < Nq; i += NT) sP[(DIM + 2) * Nq + i] = sP[i] / sP[(DIM + 1) * Nq + i];
-  for (int fz = tid; fz < NF; fz += NT) fP[NC * NF + fz] = fP[fz] / fP[(DIM + 1) * NF + fz];
+  for (int fz = tid; fz < NF; fz += NT) {
+    const double* q = fP + (fz / Nqf) * NC * Nqf + fz % Nqf;
+    fB[fz] = q[0] / q[(DIM + 1) * Nqf];
+  }
   __syncthreads();
 
   auto state_at = [&](int i) {
@@ -268,15 +301,6 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
     for (int m = 0; m < DIM; ++m) s.v[m] = sP[(1 + m) * Nq + i];
     s.p = sP[(DIM + 1) * Nq + i];
     s.b = sP[(DIM + 2) * Nq + i];
-    return s;
-  };
-  auto fstate_at = [&](int fz) {
-    NodeState s;
-    s.r = fP[fz];
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) s.v[m] = fP[(1 + m) * NF + fz];
-    s.p = fP[(DIM + 1) * NF + fz];
-    s.b = fP[NC * NF + fz];
     return s;
   };
   auto Gat = [&](int l, int m, int i) { return sG[(l * DIM + m) * Nq + i]; };
@@ -309,13 +333,14 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
         cc = pos;
       }
       if constexpr (DIM == 2) cc = 0;
-      const int i = ca + N * cb + N * N * cc;
-      NodeState me = state_at(valid ? i : 0);
+      const int i = valid ? ca + N * cb + N * N * cc : 0;
+      const double vmask = valid ? 1.0 : 0.0;
+      NodeState me = state_at(i);
       double gl[3][3];  // own metric rows g^(l)
 #pragma unroll
       for (int l = 0; l < DIM; ++l)
 #pragma unroll
-        for (int m = 0; m < DIM; ++m) gl[l][m] = Gat(l, m, valid ? i : 0);
+        for (int m = 0; m < DIM; ++m) gl[l][m] = Gat(l, m, i);
       double acc[NC];
 #pragma unroll
       for (int v = 0; v < NC; ++v) acc[v] = 0.0;
@@ -333,32 +358,33 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
           const int ix = pos * N + pos2;
           Job<DIM>& jb = jv[t];
           jb.base = sP;
+          jb.bb = sP + (DIM + 2) * Nq;
           jb.stride = Nq;
           jb.idx = j;
           const bool half = (N % 2 == 0) && (s == NS);
-          jb.coef = (valid && s <= NS && !(half && pos >= N / 2)) ? 1.0 : 0.0;
+          const double mk = (s <= NS && !(half && pos >= N / 2)) ? vmask : 0.0;
           if constexpr (DIM == 2) {
             if (k == 0) {
-              const double cl = tw[cb], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
+              const double cl = mk * tw[cb], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
 #pragma unroll
               for (int m = 0; m < 2; ++m) jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * (gl[1][m] + Gat(1, m, j));
             } else {
-              const double a2 = tw[ca] * tA2[ix];
+              const double a2 = mk * tw[ca] * tA2[ix];
 #pragma unroll
               for (int m = 0; m < 2; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j));
             }
           } else {
             if (k == 0) {
-              const double cl = 0.5 * tw[cb] * tw3[cc], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
+              const double cl = mk * 0.5 * tw[cb] * tw3[cc], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
 #pragma unroll
               for (int m = 0; m < 3; ++m)
                 jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * ((gl[1][m] + gl[2][m]) + (Gat(1, m, j) + Gat(2, m, j)));
             } else if (k == 1) {
-              const double cl = 0.5 * tw[ca] * tw3[cc], a2 = cl * tA2[ix], a3 = cl * tA3[ix];
+              const double cl = mk * 0.5 * tw[ca] * tw3[cc], a2 = cl * tA2[ix], a3 = cl * tA3[ix];
 #pragma unroll
               for (int m = 0; m < 3; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j)) + a3 * (gl[2][m] + Gat(2, m, j));
             } else {
-              const double a4 = 0.125 * tw[ca] * tw[cb] * (1.0 - teta[cb]) * tA4[ix];
+              const double a4 = mk * 0.125 * tw[ca] * tw[cb] * (1.0 - teta[cb]) * tA4[ix];
 #pragma unroll
               for (int m = 0; m < 3; ++m) jb.n[m] = a4 * (gl[2][m] + Gat(2, m, j));
             }
@@ -370,42 +396,51 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
         for (int t = 0; t < W::VB; ++t) {
           const int s = s0 + t;
           if (s > NS) break;
-          const bool half = (N % 2 == 0) && (s == NS);
           int pos0 = pos - s;
           if (pos0 < 0) pos0 += N;
           const int src = grp * N + pos0;
-          const bool recv = valid && !(half && pos < N / 2);
 #pragma unroll
-          for (int v = 0; v < NC; ++v) {
-            double tt = __shfl_sync(0xffffffffu, Fs[t][v], src);
-            acc[v] -= Fs[t][v];
-            if (recv) acc[v] += tt;
-          }
+          for (int v = 0; v < NC; ++v) acc[v] += shfl_d(Fs[t][v], src) - Fs[t][v];  // masked jobs send 0
         }
       }
 
       // -- facet-correction pairs along the same lines --
-      // a facet job: state of facet node fz, normal (G_i^T nhat + J n_f)/2, coefficient (R^T B)_if
+      // a facet job: state of facet node (z, f), normal coef (G_i^T nhat + J n_f)/2 with coefficient
+      // coef = (R^T B)_if
       auto fjob = [&](Job<DIM>& jb, int z, int f, double coef, const double* gtn) {
-        const int fz = z * Nqf + f;
-        jb.base = fP;
-        jb.stride = NF;
-        jb.idx = fz;
-        jb.coef = valid ? coef : 0.0;
+        jb.base = fP + z * NC * Nqf;
+        jb.bb = fB + z * Nqf;
+        jb.stride = Nqf;
+        jb.idx = f;
+        const double c2 = 0.5 * coef * vmask;
 #pragma unroll
-        for (int m = 0; m < DIM; ++m) jb.n[m] = 0.5 * (gtn[m] + fJ[m * NF + fz]);
+        for (int m = 0; m < DIM; ++m) jb.n[m] = c2 * (gtn[m] + fJ[(z * DIM + m) * Nqf + f]);
       };
-      // facet-side sums over the line group; the first lane of the group writes C^T 1
-      auto line_sum = [&](const double* Fc, double* dst) {
+      // facet-side sums over each line group through the warp scratch, in lane order; dest(line, v)
+      // returns where the sum of line `gq` goes (nullptr: discard)
+      auto line_sums = [&](const double* Fc, auto dest) {
 #pragma unroll
         for (int v = 0; v < NC; ++v) {
           acc[v] -= Fc[v];
-          double sum = group_sum<N>(Fc[v], pos);
-          if (valid && pos == 0 && dst) dst[v] = sum;
+          scr[v * 32 + lane] = Fc[v];
         }
+        __syncwarp();
+        for (int sidx = lane; sidx < W::LPW * NC; sidx += 32) {
+          const int gq = sidx / NC, v = sidx - gq * NC;
+          const double* src = scr + v * 32 + gq * N;
+          double sum = 0.0;
+#pragma unroll
+          for (int a = 0; a < N; ++a) sum += src[a];
+          const int Lq = slot * W::LPW + gq;
+          if (Lq < W::NL) {
+            double* d = dest(Lq, v);
+            if (d) *d = sum;
+          }
+        }
+        __syncwarp();
       };
       if constexpr (DIM == 2) {
-        Job<DIM> jf[3];
+        Job<DIM> jf[2];
         if (k == 0) {  // eta1 = +1 (facet 2) and eta1 = -1 (facet 3): facet node b
           const double r2 = 0.70710678118654752440;
           double gtn[2] = {(gl[0][0] + gl[1][0]) * r2, (gl[0][1] + gl[1][1]) * r2};
@@ -414,28 +449,17 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
           fjob(jf[1], 2, cb, tlL[ca] * tB[2 * Nqf + cb], gtn3);
           double Fc[2][NC];
           flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
-          double d1[NC], d2[NC];
-          line_sum(Fc[0], d1);
-          line_sum(Fc[1], d2);
-          if (valid && pos == 0)
-#pragma unroll
-            for (int v = 0; v < NC; ++v) {
-              ct[v * NF + 1 * Nqf + cb] = d1[v];
-              ct[v * NF + 2 * Nqf + cb] = d2[v];
-            }
+          line_sums(Fc[0], [&](int Lq, int v) { return ct + v * NF + 1 * Nqf + Lq; });
+          line_sums(Fc[1], [&](int Lq, int v) { return ct + v * NF + 2 * Nqf + Lq; });
         } else {  // eta2 = -1 (facet 1): facet node a
           double gtn[2] = {-gl[1][0], -gl[1][1]};
           fjob(jf[0], 0, ca, tlL[cb] * tB[0 * Nqf + ca], gtn);
           double Fc[1][NC];
           flux_batch<DIM, 1>(me, jf, gm1inv, Fc);
-          double d1[NC];
-          line_sum(Fc[0], d1);
-          if (valid && pos == 0)
-#pragma unroll
-            for (int v = 0; v < NC; ++v) ct[v * NF + ca] = d1[v];
+          line_sums(Fc[0], [&](int Lq, int v) { return ct + v * NF + Lq; });
         }
       } else {
-        if (k == 0) {  // facets 2 and 3 (eta1 = +1 / -1): facet node (b, c)
+        if (k == 0) {  // facets 2 and 3 (eta1 = +1 / -1): facet node (b, c) = line index
           const double r3 = 0.57735026918962576451;
           const int f = cb + N * cc;
           double gtn[3], gtn3[3];
@@ -449,16 +473,9 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
           fjob(jf[1], 2, f, tlL[ca] * tB[2 * Nqf + f], gtn3);
           double Fc[2][NC];
           flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
-          double d1[NC], d2[NC];
-          line_sum(Fc[0], d1);
-          line_sum(Fc[1], d2);
-          if (valid && pos == 0)
-#pragma unroll
-            for (int v = 0; v < NC; ++v) {
-              ct[v * NF + 1 * Nqf + f] = d1[v];
-              ct[v * NF + 2 * Nqf + f] = d2[v];
-            }
-        } else if (k == 1) {  // facet 1 (eta2 = -1): node (a, c); facet 4 (eta3 = -1): nodes (a, j)
+          line_sums(Fc[0], [&](int Lq, int v) { return ct + v * NF + 1 * Nqf + Lq; });
+          line_sums(Fc[1], [&](int Lq, int v) { return ct + v * NF + 2 * Nqf + Lq; });
+        } else if (k == 1) {  // facet 1 (eta2 = -1): node (a, c) = line; facet 4 (eta3 = -1): nodes (a, j)
           const int f = ca + N * cc;
           double gtn[3] = {-gl[1][0], -gl[1][1], -gl[1][2]};
           double gt4[3] = {-gl[2][0], -gl[2][1], -gl[2][2]};
@@ -482,17 +499,13 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
 #pragma unroll
             for (int t = 0; t < JB; ++t) {
               const int jf = j0 + t;
-              double dd[NC];
-              line_sum(Fb[t], dd);  // sum over b on the (a, c) line
-              if (valid && pos == 0) {
-                if (jf < 0) {
-#pragma unroll
-                  for (int v = 0; v < NC; ++v) ct[v * NF + f] = dd[v];
-                } else if (jf < N) {
-#pragma unroll
-                  for (int v = 0; v < NC; ++v) pt[((v * N + jf) * N + ca) * N + cc] = dd[v];
-                }
-              }
+              // sum over b on the (a, c) line; line Lq = a + N c
+              line_sums(Fb[t], [&](int Lq, int v) -> double* {
+                if (jf < 0) return ct + v * NF + Lq;
+                if (jf >= N) return nullptr;
+                const int a = Lq % N, c = Lq / N;
+                return pt + ((v * N + jf) * N + a) * N + c;
+              });
             }
           }
         }
@@ -510,6 +523,8 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
     }
     __syncthreads();
   }
+  // the epilogue reuses the state / metric region: psi tables for the transforms
+  const PsiS T = stage_psi<DIM, N>(R, smk2 + L::o_ps);
   if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
     for (int it = tid; it < NC * N * N; it += NT) {
       const int v = it / (N * N), jf = (it / N) % N, a = it % N;
@@ -517,8 +532,8 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
       for (int c = 0; c < N; ++c) s += pt[((v * N + jf) * N + a) * N + c];
       ct[v * NF + 3 * Nqf + a + N * jf] = s;
     }
-    __syncthreads();
   }
+  __syncthreads();
 
   // ---- interface flux and s = B J_f f* - C^T 1 ----
   for (int fz = tid; fz < NF; fz += NT) {
@@ -531,7 +546,15 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
     else
       fo = rf ? (N - 1 - f % N) + N * (f / N) : f;
     const double* tp = A.trace + (size_t)slot * NC * Nqf;
-    NodeState up, um = fstate_at(fz);
+    NodeState up, um;
+    {
+      const double* q = fP + z * NC * Nqf + f;
+      um.r = q[0];
+#pragma unroll
+      for (int m = 0; m < DIM; ++m) um.v[m] = q[(1 + m) * Nqf];
+      um.p = q[(DIM + 1) * Nqf];
+      um.b = fB[fz];
+    }
     up.r = tp[fo];
 #pragma unroll
     for (int m = 0; m < DIM; ++m) up.v[m] = tp[(1 + m) * Nqf + fo];
@@ -540,7 +563,7 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
     double Jn[DIM], Jf = 0.0;
 #pragma unroll
     for (int m = 0; m < DIM; ++m) {
-      Jn[m] = fJ[m * NF + fz];
+      Jn[m] = fJ[(z * DIM + m) * Nqf + f];
       Jf += Jn[m] * Jn[m];
     }
     Jf = sqrt(Jf);
@@ -590,9 +613,10 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
   __syncthreads();
 
   // ---- d u~/dt = V^T W/J~ V (V^T r) ----
-  double* T1 = sm + L::o_pr;
-  double* T2 = T1 + t1_size<DIM, N>();
-  double* um = sm + L::o_pt;
+  double* T1 = smk2 + L::o_t1;
+  double* T2 = smk2 + L::o_t2;
+  double* um = smk2 + L::o_pt;  // facet partials, states and C^T 1 are dead: modal scratch
+  static_assert(S::NC * S::Np <= L::o_sc - L::o_pt, "modal scratch");
   nodal_to_modal<DIM, N, NC>(T, sR, um, T1, T2);
   if (A.mode == 5) {  // entropy production sum w~ . (V^T r) and conservation (V^T r)_0 / c0
     double loc = 0.0, la = 0.0;
