@@ -10,6 +10,8 @@
 // and facet normals arrive by bulk asynchronous copies (cp.async.bulk, TMA engine) completing on an
 // mbarrier.  Interface flux, lifting and the weight-adjusted inverse follow in the same CTA.
 #pragma once
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace esb {
@@ -23,7 +25,7 @@ struct Lw {  // line-group layout
   static constexpr int NW = SLOTS <= 12 ? SLOTS : (SLOTS % 9 == 0 ? 9 : (SLOTS % 8 == 0 ? 8 : 12));
   static constexpr int NT = NW * 32;
   static constexpr int NS = N / 2;                            // shifts
-  static constexpr int VB = 2;  // volume pair jobs per flux batch (ILP vs registers)
+  static constexpr int VB = 2;  // volume pair jobs per flux batch (ILP vs registers: 4 spills at N = 9)
 };
 
 __host__ __device__ constexpr int ev2(int x) { return (x + 1) & ~1; }
@@ -308,10 +310,10 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
   const int grp = lane / N, pos = lane - grp * N;
   const bool lane_ok = grp < W::LPW;
 
-  // ---- three direction passes ----
-#pragma unroll 1
-  for (int k = 0; k < DIM; ++k) {
-    const int stride = k == 0 ? 1 : (k == 1 ? N : N * N);
+  // ---- direction passes, one specialisation per direction k ----
+  auto pass = [&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    constexpr int stride = k == 0 ? 1 : (k == 1 ? N : N * N);
 #pragma unroll 1
     for (int slot = warp; slot < W::SLOTS; slot += W::NW) {
       const int Lidx = slot * W::LPW + grp;
@@ -522,7 +524,10 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
       }
     }
     __syncthreads();
-  }
+  };
+  pass(std::integral_constant<int, 0>{});
+  pass(std::integral_constant<int, 1>{});
+  if constexpr (DIM == 3) pass(std::integral_constant<int, 2>{});
   // the epilogue reuses the state / metric region: psi tables for the transforms
   const PsiS T = stage_psi<DIM, N>(R, smk2 + L::o_ps);
   if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
