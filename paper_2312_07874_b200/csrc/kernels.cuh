@@ -170,193 +170,149 @@ __device__ PsiS stage_psi(const DevRef& R, double* buf) {
   return PsiS{p1, p2, p3, pi, pi + NPAIR, pi + 2 * NPAIR};
 }
 
-template <int DIM, int N, int NV>
-__device__ void modal_to_nodal(const PsiS& T, const double* um, double* un, double* t1, double* t2) {
-  using S = Sz<DIM, N>;
-  constexpr int P = N - 1, NPAIR = S::NPAIR, Np = S::Np, Nq = S::Nq;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  if constexpr (DIM == 2) {
-    for (int it = tid; it < N * NV; it += nt) {  // t1[v][a1][b] = sum_a2 psi2[a1][a2][b] u[v][off(a1)+a2]
-      const int a1 = it / NV, v = it - a1 * NV;
-      const double* src = um + v * Np + T.poff[a1];
-      double x[N];
+// Two fibers per work item share every psi load (register blocking): y_f[o] = sum_{i < ni} A[i][o]
+// x_f[i] for o < no, f = 0, 1, with A[i][o] = ps[i N + o] (TR = false) or ps[o N + i] (TR = true);
+// inputs beyond ni are not read (the tables vanish there).  Optional per-input scales sc0 / sc1
+// multiply x (the diagonal W/J~ factor fused into the load).
+template <int N, bool TR>
+__device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const double* in0,
+                                       const double* in1, int sin, const double* sc0, const double* sc1,
+                                       double* out0, double* out1, int sout, bool has1) {
+  double x0[N], x1[N];
 #pragma unroll
-      for (int a2 = 0; a2 < N; ++a2) x[a2] = (a2 <= P - a1) ? src[a2] : 0.0;
-      const double* ps = T.p2 + a1 * N * N;
-      double* dst = t1 + (v * N + a1) * N;
-#pragma unroll
-      for (int b = 0; b < N; ++b) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a2 = 0; a2 < N; ++a2) acc = fma(ps[a2 * N + b], x[a2], acc);
-        dst[b] = acc;
-      }
+  for (int i = 0; i < N; ++i) {
+    const bool ok = i < ni;
+    x0[i] = ok ? in0[i * sin] : 0.0;
+    x1[i] = ok ? in1[i * sin] : 0.0;
+    if (sc0) {
+      x0[i] *= ok ? sc0[i * sin] : 0.0;
+      x1[i] *= ok ? sc1[i * sin] : 0.0;
     }
-    __syncthreads();
-    for (int it = tid; it < NV * N; it += nt) {  // u[v][a + N b] = sum_a1 psi1[a1][a] t1[v][a1][b]
-      const int v = it / N, b = it - v * N;
-      double x[N];
+  }
 #pragma unroll
-      for (int a1 = 0; a1 < N; ++a1) x[a1] = t1[(v * N + a1) * N + b];
-      double* dst = un + v * Nq + N * b;
+  for (int o = 0; o < N; ++o) {
+    if (o >= no) break;
+    double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-      for (int a = 0; a < N; ++a) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a1 = 0; a1 < N; ++a1) acc = fma(T.p1[a1 * N + a], x[a1], acc);
-        dst[a] = acc;
-      }
+    for (int i = 0; i < N; ++i) {
+      const double pv = TR ? ps[o * N + i] : ps[i * N + o];
+      a0 = fma(pv, x0[i], a0);
+      a1 = fma(pv, x1[i], a1);
     }
-    __syncthreads();
-  } else {
-    for (int it = tid; it < NPAIR * NV; it += nt) {  // t1[v][pr][c] = sum_a3 psi3[s][a3][c] u[v][off+a3]
-      const int pr = it / NV, v = it - pr * NV;
-      const int sdeg = T.pa1[pr] + T.pa2[pr];
-      const double* src = um + v * Np + T.poff[pr];
-      double x[N];
-#pragma unroll
-      for (int a3 = 0; a3 < N; ++a3) x[a3] = (a3 <= P - sdeg) ? src[a3] : 0.0;
-      const double* ps = T.p3 + sdeg * N * N;
-      double* dst = t1 + (v * NPAIR + pr) * N;
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a3 = 0; a3 < N; ++a3) acc = fma(ps[a3 * N + c], x[a3], acc);
-        dst[c] = acc;
-      }
-    }
-    __syncthreads();
-    for (int it = tid; it < N * NV * N; it += nt) {  // t2[v][a1][c][b] = sum_a2 psi2[a1][a2][b] t1[v][pr(a1,a2)][c]
-      const int a1 = it / (NV * N), r = it - a1 * NV * N, v = r / N, c = r - v * N;
-      const int prs = a1 * N - a1 * (a1 - 1) / 2;
-      const double* src = t1 + (v * NPAIR + prs) * N + c;
-      double x[N];
-#pragma unroll
-      for (int a2 = 0; a2 < N; ++a2) x[a2] = (a2 <= P - a1) ? src[a2 * N] : 0.0;
-      const double* ps = T.p2 + a1 * N * N;
-      double* dst = t2 + ((v * N + a1) * N + c) * N;
-#pragma unroll
-      for (int b = 0; b < N; ++b) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a2 = 0; a2 < N; ++a2) acc = fma(ps[a2 * N + b], x[a2], acc);
-        dst[b] = acc;
-      }
-    }
-    __syncthreads();
-    for (int it = tid; it < NV * N * N; it += nt) {  // u[v][a + N bc] = sum_a1 psi1[a1][a] t2[v][a1][bc]
-      const int v = it / (N * N), bc = it - v * N * N;
-      double x[N];
-#pragma unroll
-      for (int a1 = 0; a1 < N; ++a1) x[a1] = t2[(v * N + a1) * N * N + bc];
-      double* dst = un + v * Nq + N * bc;
-#pragma unroll
-      for (int a = 0; a < N; ++a) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a1 = 0; a1 < N; ++a1) acc = fma(T.p1[a1 * N + a], x[a1], acc);
-        dst[a] = acc;
-      }
-    }
-    __syncthreads();
+    out0[o * sout] = a0;
+    if (has1) out1[o * sout] = a1;
   }
 }
 
+// u = V u~ (modal [NV][Np] -> nodal [NV][Nq]); t1, t2 scratch (t1_size, t2_size)
 template <int DIM, int N, int NV>
-__device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, double* t1, double* t2) {
+__device__ void modal_to_nodal(const PsiS& T, const double* um, double* un, double* t1, double* t2) {
   using S = Sz<DIM, N>;
-  constexpr int P = N - 1, NPAIR = S::NPAIR, Np = S::Np, Nq = S::Nq;
+  constexpr int P = N - 1, NPAIR = S::NPAIR, Np = S::Np, Nq = S::Nq, NVP = (NV + 1) / 2;
   const int tid = threadIdx.x, nt = blockDim.x;
   if constexpr (DIM == 2) {
-    for (int it = tid; it < NV * N; it += nt) {  // s1[v][a1][b] = sum_a psi1[a1][a] y[v][a + N b]
-      const int v = it / N, b = it - v * N;
-      double x[N];
-      const double* src = y + v * Nq + N * b;
-#pragma unroll
-      for (int a = 0; a < N; ++a) x[a] = src[a];
-#pragma unroll
-      for (int a1 = 0; a1 < N; ++a1) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a = 0; a < N; ++a) acc = fma(T.p1[a1 * N + a], x[a], acc);
-        t1[(v * N + a1) * N + b] = acc;
-      }
+    // t1[v][a1][b] = sum_a2 psi2[a1][a2][b] u[v][off(a1)+a2]; items (a1, variable pair)
+    for (int it = tid; it < N * NVP; it += nt) {
+      const int a1 = it / NVP, v0 = 2 * (it - a1 * NVP), v1 = v0 + 1 < NV ? v0 + 1 : v0;
+      fiber2<N, false>(T.p2 + a1 * N * N, N - a1, N, um + v0 * Np + T.poff[a1], um + v1 * Np + T.poff[a1], 1, nullptr, nullptr,
+                t1 + (v0 * N + a1) * N, t1 + (v1 * N + a1) * N, 1, v1 != v0);
     }
     __syncthreads();
-    for (int it = tid; it < N * NV; it += nt) {  // u[v][off(a1)+a2] = sum_b psi2[a1][a2][b] s1[v][a1][b]
-      const int a1 = it / NV, v = it - a1 * NV;
-      double x[N];
-      const double* src = t1 + (v * N + a1) * N;
-#pragma unroll
-      for (int b = 0; b < N; ++b) x[b] = src[b];
-      const double* ps = T.p2 + a1 * N * N;
-      double* dst = um + v * Np + T.poff[a1];
-#pragma unroll
-      for (int a2 = 0; a2 < N; ++a2) {
-        if (a2 > P - a1) break;
-        double acc = 0.0;
-#pragma unroll
-        for (int b = 0; b < N; ++b) acc = fma(ps[a2 * N + b], x[b], acc);
-        dst[a2] = acc;
-      }
+    // u[v][a + N b] = sum_a1 psi1[a1][a] t1[v][a1][b]; items pairs of (v, b) fibers
+    constexpr int NFB = NV * N;
+    for (int it = tid; it < (NFB + 1) / 2; it += nt) {
+      const int q0 = 2 * it, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+      const int v0 = q0 / N, b0 = q0 - v0 * N, v1 = q1 / N, b1 = q1 - v1 * N;
+      fiber2<N, false>(T.p1, N, N, t1 + v0 * N * N + b0, t1 + v1 * N * N + b1, N, nullptr, nullptr, un + v0 * Nq + N * b0,
+                un + v1 * Nq + N * b1, 1, q1 != q0);
     }
     __syncthreads();
   } else {
-    for (int it = tid; it < NV * N * N; it += nt) {  // s2[v][a1][bc] = sum_a psi1[a1][a] y[v][a + N bc]
-      const int v = it / (N * N), bc = it - v * N * N;
-      double x[N];
-      const double* src = y + v * Nq + N * bc;
-#pragma unroll
-      for (int a = 0; a < N; ++a) x[a] = src[a];
-#pragma unroll
-      for (int a1 = 0; a1 < N; ++a1) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a = 0; a < N; ++a) acc = fma(T.p1[a1 * N + a], x[a], acc);
-        t2[(v * N + a1) * N * N + bc] = acc;
-      }
-    }
-    __syncthreads();
-    for (int it = tid; it < N * NV * N; it += nt) {  // s1[v][pr(a1,a2)][c] = sum_b psi2[a1][a2][b] s2[v][a1][c][b]
-      const int a1 = it / (NV * N), r = it - a1 * NV * N, v = r / N, c = r - v * N;
-      const int prs = a1 * N - a1 * (a1 - 1) / 2;
-      double x[N];
-      const double* src = t2 + ((v * N + a1) * N + c) * N;
-#pragma unroll
-      for (int b = 0; b < N; ++b) x[b] = src[b];
-      const double* ps = T.p2 + a1 * N * N;
-      double* dst = t1 + (v * NPAIR + prs) * N + c;
-#pragma unroll
-      for (int a2 = 0; a2 < N; ++a2) {
-        if (a2 > P - a1) break;
-        double acc = 0.0;
-#pragma unroll
-        for (int b = 0; b < N; ++b) acc = fma(ps[a2 * N + b], x[b], acc);
-        dst[a2 * N] = acc;
-      }
-    }
-    __syncthreads();
-    for (int it = tid; it < NPAIR * NV; it += nt) {  // u[v][off+a3] = sum_c psi3[s][a3][c] s1[v][pr][c]
-      const int pr = it / NV, v = it - pr * NV;
+    // t1[v][pr][c] = sum_a3 psi3[s][a3][c] u[v][off(pr)+a3]; items (pr, variable pair)
+    for (int it = tid; it < NPAIR * NVP; it += nt) {
+      const int pr = it / NVP, v0 = 2 * (it - pr * NVP), v1 = v0 + 1 < NV ? v0 + 1 : v0;
       const int sdeg = T.pa1[pr] + T.pa2[pr];
-      double x[N];
-      const double* src = t1 + (v * NPAIR + pr) * N;
-#pragma unroll
-      for (int c = 0; c < N; ++c) x[c] = src[c];
-      const double* ps = T.p3 + sdeg * N * N;
-      double* dst = um + v * Np + T.poff[pr];
-#pragma unroll
-      for (int a3 = 0; a3 < N; ++a3) {
-        if (a3 > P - sdeg) break;
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c < N; ++c) acc = fma(ps[a3 * N + c], x[c], acc);
-        dst[a3] = acc;
-      }
+      fiber2<N, false>(T.p3 + sdeg * N * N, N - sdeg, N, um + v0 * Np + T.poff[pr], um + v1 * Np + T.poff[pr], 1, nullptr,
+                nullptr, t1 + (v0 * NPAIR + pr) * N, t1 + (v1 * NPAIR + pr) * N, 1, v1 != v0);
+    }
+    __syncthreads();
+    // t2[v][a1][c][b] = sum_a2 psi2[a1][a2][b] t1[v][pr(a1,a2)][c]; items (a1, pair of (v, c) fibers)
+    constexpr int NFC = NV * N, NPC = (NFC + 1) / 2;
+    for (int it = tid; it < N * NPC; it += nt) {
+      const int a1 = it / NPC, w = it - a1 * NPC, q0 = 2 * w, q1 = q0 + 1 < NFC ? q0 + 1 : q0;
+      const int v0 = q0 / N, c0 = q0 - v0 * N, v1 = q1 / N, c1 = q1 - v1 * N;
+      const int prs = a1 * N - a1 * (a1 - 1) / 2;
+      fiber2<N, false>(T.p2 + a1 * N * N, N - a1, N, t1 + (v0 * NPAIR + prs) * N + c0, t1 + (v1 * NPAIR + prs) * N + c1, N,
+                nullptr, nullptr, t2 + ((v0 * N + a1) * N + c0) * N, t2 + ((v1 * N + a1) * N + c1) * N, 1, q1 != q0);
+    }
+    __syncthreads();
+    // u[v][a + N bc] = sum_a1 psi1[a1][a] t2[v][a1][bc]; items pairs of (v, bc) fibers
+    constexpr int NFB = NV * N * N;
+    for (int it = tid; it < (NFB + 1) / 2; it += nt) {
+      const int q0 = 2 * it, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+      const int v0 = q0 / (N * N), bc0 = q0 - v0 * N * N, v1 = q1 / (N * N), bc1 = q1 - v1 * N * N;
+      fiber2<N, false>(T.p1, N, N, t2 + v0 * Nq + bc0, t2 + v1 * Nq + bc1, N * N, nullptr, nullptr, un + v0 * Nq + N * bc0,
+                un + v1 * Nq + N * bc1, 1, q1 != q0);
     }
     __syncthreads();
   }
+  (void)P;
+}
+
+// u~ = V^T (scale o y) (nodal [NV][Nq] -> modal [NV][Np]); scale: optional per-node factor [Nq]
+template <int DIM, int N, int NV>
+__device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, double* t1, double* t2,
+                               const double* scale = nullptr) {
+  using S = Sz<DIM, N>;
+  constexpr int P = N - 1, NPAIR = S::NPAIR, Np = S::Np, Nq = S::Nq, NVP = (NV + 1) / 2;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if constexpr (DIM == 2) {
+    // s1[v][a1][b] = sum_a psi1[a1][a] y[v][a + N b]; items pairs of (v, b) fibers
+    constexpr int NFB = NV * N;
+    for (int it = tid; it < (NFB + 1) / 2; it += nt) {
+      const int q0 = 2 * it, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+      const int v0 = q0 / N, b0 = q0 - v0 * N, v1 = q1 / N, b1 = q1 - v1 * N;
+      fiber2<N, true>(T.p1, N, N, y + v0 * Nq + N * b0, y + v1 * Nq + N * b1, 1, scale ? scale + N * b0 : nullptr,
+                scale ? scale + N * b1 : nullptr, t1 + v0 * N * N + b0, t1 + v1 * N * N + b1, N, q1 != q0);
+    }
+    __syncthreads();
+    // u[v][off(a1)+a2] = sum_b psi2[a1][a2][b] s1[v][a1][b]; items (a1, variable pair)
+    for (int it = tid; it < N * NVP; it += nt) {
+      const int a1 = it / NVP, v0 = 2 * (it - a1 * NVP), v1 = v0 + 1 < NV ? v0 + 1 : v0;
+      fiber2<N, true>(T.p2 + a1 * N * N, N, N - a1, t1 + (v0 * N + a1) * N, t1 + (v1 * N + a1) * N, 1, nullptr,
+                nullptr, um + v0 * Np + T.poff[a1], um + v1 * Np + T.poff[a1], 1, v1 != v0);
+    }
+    __syncthreads();
+  } else {
+    // s2[v][a1][bc] = sum_a psi1[a1][a] y[v][a + N bc]; items pairs of (v, bc) fibers
+    constexpr int NFB = NV * N * N;
+    for (int it = tid; it < (NFB + 1) / 2; it += nt) {
+      const int q0 = 2 * it, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+      const int v0 = q0 / (N * N), bc0 = q0 - v0 * N * N, v1 = q1 / (N * N), bc1 = q1 - v1 * N * N;
+      fiber2<N, true>(T.p1, N, N, y + v0 * Nq + N * bc0, y + v1 * Nq + N * bc1, 1, scale ? scale + N * bc0 : nullptr,
+                      scale ? scale + N * bc1 : nullptr, t2 + v0 * Nq + bc0, t2 + v1 * Nq + bc1, N * N, q1 != q0);
+    }
+    __syncthreads();
+    // s1[v][pr(a1,a2)][c] = sum_b psi2[a1][a2][b] s2[v][a1][c][b]; items (a1, pair of (v, c) fibers)
+    constexpr int NFC = NV * N, NPC = (NFC + 1) / 2;
+    for (int it = tid; it < N * NPC; it += nt) {
+      const int a1 = it / NPC, w = it - a1 * NPC, q0 = 2 * w, q1 = q0 + 1 < NFC ? q0 + 1 : q0;
+      const int v0 = q0 / N, c0 = q0 - v0 * N, v1 = q1 / N, c1 = q1 - v1 * N;
+      const int prs = a1 * N - a1 * (a1 - 1) / 2;
+      fiber2<N, true>(T.p2 + a1 * N * N, N, N - a1, t2 + ((v0 * N + a1) * N + c0) * N, t2 + ((v1 * N + a1) * N + c1) * N, 1,
+                nullptr, nullptr, t1 + (v0 * NPAIR + prs) * N + c0, t1 + (v1 * NPAIR + prs) * N + c1, N, q1 != q0);
+    }
+    __syncthreads();
+    // u[v][off(pr)+a3] = sum_c psi3[s][a3][c] s1[v][pr][c]; items (pr, variable pair)
+    for (int it = tid; it < NPAIR * NVP; it += nt) {
+      const int pr = it / NVP, v0 = 2 * (it - pr * NVP), v1 = v0 + 1 < NV ? v0 + 1 : v0;
+      const int sdeg = T.pa1[pr] + T.pa2[pr];
+      fiber2<N, true>(T.p3 + sdeg * N * N, N, N - sdeg, t1 + (v0 * NPAIR + pr) * N, t1 + (v1 * NPAIR + pr) * N, 1, nullptr,
+                nullptr, um + v0 * Np + T.poff[pr], um + v1 * Np + T.poff[pr], 1, v1 != v0);
+    }
+    __syncthreads();
+  }
+  (void)P;
 }
 
 template <int DIM, int N>
@@ -381,7 +337,7 @@ __host__ __device__ constexpr size_t project_smem_doubles() {
 }
 
 template <int DIM, int N>
-__global__ void __launch_bounds__(Sz<DIM, N>::NT) project_kernel(DevRef R, ProjArgs A) {
+__global__ void __launch_bounds__(Sz<DIM, N>::NT, 2) project_kernel(DevRef R, ProjArgs A) {
   using S = Sz<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf;
   extern __shared__ double sm[];
@@ -423,9 +379,11 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT) project_kernel(DevRef R, ProjA
   __syncthreads();
   nodal_to_modal<DIM, N, NC>(T, X, um, T1, T2);
   modal_to_nodal<DIM, N, NC>(T, um, X, T1, T2);
-  for (int it = tid; it < NC * Nq; it += nt) X[it] *= gv[(S::NG + 1) * Nq + it % Nq];  // W / J~
+  // W / J~ staged in the (not yet used) facet buffer and fused into the transform's loads
+  static_assert(S::NC * S::NF >= Nq, "W/J~ staging");
+  for (int i = tid; i < Nq; i += nt) FW[i] = gv[(S::NG + 1) * Nq + i];
   __syncthreads();
-  nodal_to_modal<DIM, N, NC>(T, X, um, T1, T2);  // w~
+  nodal_to_modal<DIM, N, NC>(T, X, um, T1, T2, FW);  // w~
   if (A.wt)
     for (int k = tid; k < NC * Np; k += nt) A.wt[(size_t)e * NC * Np + k] = um[k];
   modal_to_nodal<DIM, N, NC>(T, um, X, T1, T2);  // w = V w~

@@ -52,7 +52,10 @@ struct Rhs2Smem {
   static constexpr int o_t1 = 0, o_t2 = o_t1 + t1_size<DIM, N>(), o_ps0 = ev2(o_t2 + t2_size<DIM, N>());
   static constexpr bool PS_IN = o_ps0 + psi_smem_doubles<DIM, N>() <= PR + GG;
   static constexpr int o_ps = PS_IN ? o_ps0 : o_end;
-  static constexpr int total = PS_IN ? o_end : o_end + psi_smem_doubles<DIM, N>();
+  static constexpr int o_end2 = PS_IN ? o_end : ev2(o_end + psi_smem_doubles<DIM, N>());
+  static constexpr bool WJ_IN = ev2(o_ps0 + (PS_IN ? psi_smem_doubles<DIM, N>() : 0)) + S::Nq <= PR + GG;
+  static constexpr int o_wj = WJ_IN ? ev2(o_ps0 + (PS_IN ? psi_smem_doubles<DIM, N>() : 0)) : o_end2;
+  static constexpr int total = WJ_IN ? o_end2 : o_end2 + S::Nq;
   static_assert(o_t2 + t2_size<DIM, N>() <= PR + GG, "epilogue scratch");
   static_assert(S::PRS <= PR, "prim copy");
 };
@@ -528,8 +531,10 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
   pass(std::integral_constant<int, 0>{});
   pass(std::integral_constant<int, 1>{});
   if constexpr (DIM == 3) pass(std::integral_constant<int, 2>{});
-  // the epilogue reuses the state / metric region: psi tables for the transforms
+  // the epilogue reuses the state / metric region: psi tables for the transforms and W / J~
   const PsiS T = stage_psi<DIM, N>(R, smk2 + L::o_ps);
+  double* sWJ = smk2 + L::o_wj;
+  for (int i = tid; i < Nq; i += NT) sWJ[i] = gv[(S::NG + 1) * Nq + i];
   if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
     for (int it = tid; it < NC * N * N; it += NT) {
       const int v = it / (N * N), jf = (it / N) % N, a = it % N;
@@ -653,9 +658,7 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
     }
   }
   modal_to_nodal<DIM, N, NC>(T, um, sR, T1, T2);
-  for (int it = tid; it < NC * Nq; it += NT) sR[it] *= gv[(S::NG + 1) * Nq + it % Nq];
-  __syncthreads();
-  nodal_to_modal<DIM, N, NC>(T, sR, um, T1, T2);
+  nodal_to_modal<DIM, N, NC>(T, sR, um, T1, T2, sWJ);  // W / J~ fused into the loads
   const size_t base = (size_t)e * NC * Np;
   const double dt = A.dt;
   for (int kk = tid; kk < NC * Np; kk += NT) {
