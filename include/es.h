@@ -143,10 +143,10 @@ void* es_stream(const es_context* ctx);
 int64_t es_launch_count(const es_context* ctx);
 void es_reset_launch_count(es_context* ctx);
 
-/* Per-launch timing of the flux-differencing kernel (CUDA events on the context stream):
- * es_timing_enable(ctx, 1) starts recording; es_timing_read returns the summed milliseconds and
- * the number of launches of each kernel class since enabling: 0 = trace/projection kernel,
- * 1 = flux-differencing + surface + inverse-mass kernel. */
+/* Per-launch timing of the kernels (CUDA events on the context stream): es_timing_enable(ctx, 1)
+ * starts recording; es_timing_read returns the summed milliseconds and the number of launches of
+ * each kernel class since enabling: 0 = entropy projection / trace kernel, 1 = flux-differencing
+ * + lifting + inverse-mass kernel, 2 = interface-flux kernel. */
 es_status es_timing_enable(es_context* ctx, int on);
 es_status es_timing_read(es_context* ctx, int kernel_class, double* total_ms, int64_t* launches);
 

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -20,6 +21,8 @@ cudaError_t launch_project_2d(int n, const DevRef& R, const ProjArgs& A, cudaStr
 cudaError_t launch_project_3d(int n, const DevRef& R, const ProjArgs& A, cudaStream_t st);
 cudaError_t launch_rhs_2d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
 cudaError_t launch_rhs_3d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
+cudaError_t launch_iface_2d(int n, const DevRef& R, const IfaceArgs& A, cudaStream_t st);
+cudaError_t launch_iface_3d(int n, const DevRef& R, const IfaceArgs& A, cudaStream_t st);
 cudaError_t launch_projnodal_2d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st);
 cudaError_t launch_projnodal_3d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st);
 }  // namespace esb
@@ -46,7 +49,8 @@ struct es_context {
   DevRef R{};
   void* d_tables = nullptr;
   double *geo_vol = nullptr, *geo_face = nullptr, *xq = nullptr, *jt = nullptr;
-  double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr;
+  double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr, *fstar = nullptr;
+  int num_sms = 148;
   int64_t *face_slot = nullptr, *d_interior = nullptr, *d_boundary = nullptr, *d_send = nullptr;
   int* face_reflect = nullptr;
   int* bad = nullptr;
@@ -54,6 +58,7 @@ struct es_context {
   ncclComm_t comm = nullptr;
   int64_t launches = 0;
   bool timing = false;
+  long long* dbg = nullptr;  // ES_PHASE_TIMING diagnostics
   std::vector<TimedEvent> tev;
   std::vector<cudaEvent_t> ev_pool;
 };
@@ -175,6 +180,23 @@ cudaError_t run_rhs(es_context* c, RhsArgs A, int64_t n, const int64_t* list) {
   return e;
 }
 
+cudaError_t run_iface(es_context* c, int64_t n, const int64_t* list) {
+  if (n <= 0) return cudaSuccess;
+  IfaceArgs I{n, list, c->trace, c->geo_face, c->face_slot, c->face_reflect, c->fstar, c->gamma, c->es};
+  TimedEvent te{};
+  if (c->timing) {
+    te = {get_event(c), get_event(c), 2};
+    cudaEventRecord(te.a, c->stream);
+  }
+  c->launches++;
+  cudaError_t e = c->d == 2 ? launch_iface_2d(c->n, c->R, I, c->stream) : launch_iface_3d(c->n, c->R, I, c->stream);
+  if (c->timing) {
+    cudaEventRecord(te.b, c->stream);
+    c->tev.push_back(te);
+  }
+  return e;
+}
+
 RhsArgs base_rhs_args(es_context* c) {
   RhsArgs A{};
   A.prim = c->prim;
@@ -186,6 +208,9 @@ RhsArgs base_rhs_args(es_context* c) {
   A.gamma = c->gamma;
   A.es = c->es;
   A.c0 = c->c0;
+  A.dbg = c->dbg;
+  A.fstar = c->fstar;
+  A.max_ctas = c->num_sms;
   return A;
 }
 
@@ -203,6 +228,7 @@ es_status rhs_pass(es_context* c, const double* u, RhsArgs A, double* wt) {
     c->tev.push_back(te);
   }
   if (c->world == 1) {
+    CK(run_iface(c, c->nloc, nullptr));
     CK(run_rhs(c, A, c->nloc, nullptr));
     return ES_OK;
   }
@@ -224,9 +250,11 @@ es_status rhs_pass(es_context* c, const double* u, RhsArgs A, double* wt) {
   }
   NK(ncclGroupEnd());
   CK(cudaEventRecord(c->ev_comm, c->comm_stream));
-  CK(run_rhs(c, A, (int64_t)c->plan.interior.size(), c->d_interior));
+  // interface fluxes of elements without remote neighbours overlap the exchange
+  CK(run_iface(c, (int64_t)c->plan.interior.size(), c->d_interior));
   CK(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
-  CK(run_rhs(c, A, (int64_t)c->plan.boundary.size(), c->d_boundary));
+  CK(run_iface(c, (int64_t)c->plan.boundary.size(), c->d_boundary));
+  CK(run_rhs(c, A, c->nloc, nullptr));
   return ES_OK;
 }
 
@@ -255,7 +283,7 @@ void es_destroy(es_context* c) {
                   (void*)c->prim, (void*)c->trace, (void*)c->wt, (void*)c->part, (void*)c->red,
                   (void*)c->face_slot, (void*)c->d_interior, (void*)c->d_boundary, (void*)c->d_send,
                   (void*)c->face_reflect, (void*)c->bad, (void*)c->U, (void*)c->ACC, (void*)c->US,
-                  (void*)c->hin, (void*)c->hout, (void*)c->send_buf})
+                  (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg, (void*)c->fstar})
     if (p) cudaFree(p);
   for (auto& t : c->tev) {
     cudaEventDestroy(t.a);
@@ -305,6 +333,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   c->nloc = c->plan.nloc;
   c->nslots = c->nloc * c->Nf + c->plan.n_halo;
   CK(cudaSetDevice(c->device));
+  CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   if (opt->cuda_stream) {
     c->stream = (cudaStream_t)opt->cuda_stream;
   } else {
@@ -394,6 +423,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   const size_t nmod = (size_t)c->nloc * c->NC * c->Np;
   CK(cudaMalloc((void**)&c->prim, (size_t)c->nloc * even_up(c->NC * c->Nq) * sizeof(double)));
   CK(cudaMalloc((void**)&c->trace, (size_t)c->nslots * c->NC * c->Nqf * sizeof(double)));
+  CK(cudaMalloc((void**)&c->fstar, (size_t)c->nloc * c->Nf * c->NC * c->Nqf * sizeof(double)));
   CK(cudaMalloc((void**)&c->wt, nmod * sizeof(double)));
   CK(cudaMalloc((void**)&c->part, (size_t)c->nloc * (2 + c->NC) * sizeof(double)));
   CK(cudaMalloc((void**)&c->red, 8 * sizeof(double)));
@@ -401,6 +431,10 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   CK(cudaMalloc((void**)&c->ACC, nmod * sizeof(double)));
   CK(cudaMalloc((void**)&c->US, nmod * sizeof(double)));
   CK(cudaMemset(c->U, 0, nmod * sizeof(double)));
+  if (std::getenv("ES_PHASE_TIMING")) {
+    CK(cudaMalloc((void**)&c->dbg, 4096 * 16 * sizeof(long long)));
+    CK(cudaMemset(c->dbg, 0, 4096 * 16 * sizeof(long long)));
+  }
   if (c->world > 1) {
     const size_t nsend = c->plan.send_slots.size();
     CK(cudaMalloc((void**)&c->send_buf, std::max<size_t>(nsend, 1) * c->NC * c->Nqf * sizeof(double)));
@@ -430,6 +464,19 @@ es_status es_rhs(es_context* c, const double* u, double* dudt) {
   A.out = dudt;
   es_status s = rhs_pass(c, u, A, nullptr);
   if (s != ES_OK) return s;
+  if (c->dbg) {  // ES_PHASE_TIMING: mean clock cycles per phase of the flux kernel over the first blocks
+    std::vector<long long> h(4096 * 16);
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(h.data(), c->dbg, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    int nb = (int)std::min<int64_t>(4096, c->nloc);
+    double acc[16] = {0};
+    for (int b = 0; b < nb; ++b)
+      for (int k = 1; k < 12; ++k)
+        if (h[b * 16 + k] && h[b * 16 + k - 1]) acc[k] += (double)(h[b * 16 + k] - h[b * 16 + k - 1]);
+    std::fprintf(stderr, "ES_PHASE_TIMING cycles/element:");
+    for (int k = 1; k < 12; ++k) std::fprintf(stderr, " %d:%.0f", k, acc[k] / nb);
+    std::fprintf(stderr, "\n");
+  }
   if (c->check_adm) return check_bad(c);
   return ES_OK;
 }

@@ -75,6 +75,21 @@ struct RhsArgs {
   const double* wt;           // entropy mode: w~
   double* part;               // entropy mode: [nloc][2 + NC]
   double c0;                  // value of the constant PKD mode (1/sqrt|ref|)
+  long long* dbg;             // optional [4096][16] phase clock stamps (diagnostics)
+  const double* fstar;        // [nloc][Nf][NC][Nqf] B J_f f* from the interface kernel
+  int max_ctas;               // persistent grid size (CTAs resident at once)
+};
+
+struct IfaceArgs {
+  int64_t n_elem;
+  const int64_t* elem_list;
+  const double* trace;        // [slots][NC][Nqf] entropy-projected primitive states at facet nodes
+  const double* geo_face;     // [nloc][Nf][DIM][Nqf] J n
+  const int64_t* face_slot;   // [nloc][Nf]
+  const int* face_reflect;    // [nloc][Nf]
+  double* fstar;              // [nloc][Nf][NC][Nqf]
+  double gamma;
+  int es;
 };
 
 // ------------------------------------------------------------------------------------------------
@@ -189,18 +204,29 @@ __device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const d
       x1[i] *= ok ? sc1[i * sin] : 0.0;
     }
   }
+  // outputs in chunks of OC, each accumulated over all inputs (independent FMA chains)
+  constexpr int OC = 3;
+#pragma unroll 1
+  for (int o0 = 0; o0 < no; o0 += OC) {
+    double a0[OC], a1[OC];
 #pragma unroll
-  for (int o = 0; o < N; ++o) {
-    if (o >= no) break;
-    double a0 = 0.0, a1 = 0.0;
+    for (int q = 0; q < OC; ++q) a0[q] = a1[q] = 0.0;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const double pv = TR ? ps[o * N + i] : ps[i * N + o];
-      a0 = fma(pv, x0[i], a0);
-      a1 = fma(pv, x1[i], a1);
+#pragma unroll
+      for (int q = 0; q < OC; ++q) {
+        const int o = o0 + q < N ? o0 + q : N - 1;
+        const double pv = TR ? ps[o * N + i] : ps[i * N + o];
+        a0[q] = fma(pv, x0[i], a0[q]);
+        a1[q] = fma(pv, x1[i], a1[q]);
+      }
     }
-    out0[o * sout] = a0;
-    if (has1) out1[o * sout] = a1;
+#pragma unroll
+    for (int q = 0; q < OC; ++q) {
+      if (o0 + q >= no) break;
+      out0[(o0 + q) * sout] = a0[q];
+      if (has1) out1[(o0 + q) * sout] = a1[q];
+    }
   }
 }
 
@@ -486,6 +512,7 @@ struct LaunchCfg {
 };
 cudaError_t launch_project(int dim, int n, const DevRef& R, const ProjArgs& A, cudaStream_t st);
 cudaError_t launch_rhs(int dim, int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
+cudaError_t launch_iface(int dim, int n, const DevRef& R, const IfaceArgs& A, cudaStream_t st);
 cudaError_t launch_project_nodal(int dim, int n, const DevRef& R, int64_t ne, const double* un, double* um,
                                  cudaStream_t st);
 

@@ -1,4 +1,4 @@
-// rhs2.cuh -- K2 (v4): warp-synchronous line-wise flux differencing (product code).
+// rhs2.cuh -- K2 (v5): persistent warp-synchronous line-wise flux differencing (product code).
 //
 // Each warp owns whole eta_k lines ("line groups" of N lanes, floor(32/N) lines per warp).  For one
 // direction k a lane keeps its node's entropy-projected state and metric rows in registers, pairs
@@ -6,9 +6,12 @@
 // P:572), subtracts F from its own accumulator and receives the partner's +F by a warp shuffle.
 // The facet-correction pairs whose extrapolation runs along the same lines are done in
 // the same pass; their facet-side sums C^T 1 go through a per-warp shared-memory scratch and are
-// summed in a fixed order (deterministic, no atomics).  The element's states, metric terms, traces
-// and facet normals arrive by bulk asynchronous copies (cp.async.bulk, TMA engine) completing on an
-// mbarrier.  Interface flux, lifting and the weight-adjusted inverse follow in the same CTA.
+// summed in a fixed order (deterministic, no atomics).  One persistent CTA per SM loops over
+// elements; the element's states, metric terms, traces, facet normals, interface fluxes and W/J~
+// arrive by bulk asynchronous copies (cp.async.bulk, TMA engine) on two mbarriers, issued for the
+// next element as soon as the current one is done with each buffer, so the copies overlap compute.
+// The facet correction is subtracted in place from the interface fluxes (computed beforehand by
+// iface_kernel), then lifting and the weight-adjusted inverse (in-place transforms) follow.
 #pragma once
 #include <type_traits>
 
@@ -34,30 +37,29 @@ template <int DIM, int N>
 struct Rhs2Smem {
   using S = Sz<DIM, N>;
   using W = Lw<DIM, N>;
+  // per-CTA constants (staged once by the persistent CTA)
+  static constexpr int TB = 5 * N * N + 6 * N + N * N + S::NF;  // line operators, weights, extrapolation, B
+  static constexpr int PS = psi_smem_doubles<DIM, N>();         // PKD sum-factorisation tables
+  // per element
   static constexpr int PR = ev2((DIM + 3) * S::Nq);  // rho, v, p, beta   (bulk copy of prim: PRS)
   static constexpr int GG = ev2(S::NG * S::Nq);      // G_lm              (bulk copy)
-  static constexpr int RR = S::NC * S::Nq;           // nodal residual r
+  static constexpr int RR = ev2(S::NC * S::Nq);      // nodal residual r; in-place transform buffer
   static constexpr int PT = DIM == 3 ? S::NC * N * N * N : 0;  // facet-4 partial sums [v][j][a][c]
+  static constexpr int UM = ev2(S::NC * S::Np + (DIM == 3 ? S::NC * N * N : 0));  // modal result, facet-4 lift
   static constexpr int FP = S::Nf * S::NC * S::Nqf;  // facet states [z][rho, v, p][f] (bulk copy)
-  static constexpr int FB = S::NF;                   // facet beta = rho / p
+  static constexpr int FB = ev2(S::NF);              // facet beta = rho / p
   static constexpr int FJ = S::Nf * DIM * S::Nqf;    // J n at facet nodes [z][m][f] (bulk copy)
-  static constexpr int CT = S::NC * S::NF;           // C^T 1, then s = B J_f f* - C^T 1
+  static constexpr int FS = S::Nf * S::NC * S::Nqf;  // B J_f f* (bulk copy), then s = B J_f f* - C^T 1
   static constexpr int SC = W::NW * S::NC * 32;      // per-warp reduction scratch
-  static constexpr int TB = 5 * N * N + 6 * N + N * N + S::NF;
-  static constexpr int o_pr = 0, o_g = o_pr + PR, o_r = ev2(o_g + GG), o_pt = ev2(o_r + RR), o_fp = ev2(o_pt + PT),
-                       o_fb = ev2(o_fp + FP), o_fj = ev2(o_fb + FB), o_ct = ev2(o_fj + FJ), o_sc = ev2(o_ct + CT),
-                       o_tb = ev2(o_sc + SC), o_end = ev2(o_tb + TB);
-  // epilogue: transform scratch reuses the state / metric region, and so do the psi tables when
-  // they fit there (3D); otherwise they get their own region
-  static constexpr int o_t1 = 0, o_t2 = o_t1 + t1_size<DIM, N>(), o_ps0 = ev2(o_t2 + t2_size<DIM, N>());
-  static constexpr bool PS_IN = o_ps0 + psi_smem_doubles<DIM, N>() <= PR + GG;
-  static constexpr int o_ps = PS_IN ? o_ps0 : o_end;
-  static constexpr int o_end2 = PS_IN ? o_end : ev2(o_end + psi_smem_doubles<DIM, N>());
-  static constexpr bool WJ_IN = ev2(o_ps0 + (PS_IN ? psi_smem_doubles<DIM, N>() : 0)) + S::Nq <= PR + GG;
-  static constexpr int o_wj = WJ_IN ? ev2(o_ps0 + (PS_IN ? psi_smem_doubles<DIM, N>() : 0)) : o_end2;
-  static constexpr int total = WJ_IN ? o_end2 : o_end2 + S::Nq;
-  static_assert(o_t2 + t2_size<DIM, N>() <= PR + GG, "epilogue scratch");
+  static constexpr int WJ0 = ((S::NG * S::Nq) % 2 == 0) ? S::NG * S::Nq : (S::NG + 1) * S::Nq;  // first even row
+  static constexpr int WJN = ((S::NG * S::Nq) % 2 == 0) ? 2 * S::Nq : ev2(S::Nq);                // doubles copied
+  static constexpr int WJOFF = ((S::NG * S::Nq) % 2 == 0) ? S::Nq : 0;  // W / J~ within the copied rows
+  static constexpr int o_tb = 0, o_ps = ev2(o_tb + TB), o_pr = ev2(o_ps + PS), o_g = o_pr + PR, o_r = ev2(o_g + GG),
+                       o_pt = ev2(o_r + RR), o_um = o_pt, o_fp = ev2(o_pt + (PT > UM ? PT : UM)), o_fb = ev2(o_fp + FP),
+                       o_fj = ev2(o_fb + FB), o_fs = ev2(o_fj + FJ), o_sc = ev2(o_fs + FS), o_wj = ev2(o_sc + SC),
+                       total = ev2(o_wj + WJN);
   static_assert(S::PRS <= PR, "prim copy");
+  static_assert(total * 8 <= 227 * 1024 - 256, "shared memory");
 };
 
 template <int DIM, int N>
@@ -225,6 +227,174 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
+// in-place sum-factorised transforms on one shared buffer B: every thread owns at
+// most one two-fiber item per step, loads its fibers into registers, the block synchronises, then
+// the item is contracted and stored over the (now dead) inputs.  Not inlined: the persistent
+// element loop would otherwise keep their loop-invariant addressing live through the flux passes.
+template <int N>
+struct Fib2 {
+  double x0[N], x1[N];
+};
+template <int N>
+__device__ __forceinline__ void fib_load(Fib2<N>& F, int ni, const double* in0, const double* in1, int sin,
+                                         const double* sc0, const double* sc1) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const bool ok = i < ni;
+    F.x0[i] = ok ? in0[i * sin] : 0.0;
+    F.x1[i] = ok ? in1[i * sin] : 0.0;
+    if (sc0) {
+      F.x0[i] *= ok ? sc0[i * sin] : 0.0;
+      F.x1[i] *= ok ? sc1[i * sin] : 0.0;
+    }
+  }
+}
+// all outputs are accumulated in registers first (independent FMA chains), then stored
+template <int N, bool TR>
+__device__ __forceinline__ void fib_store(const Fib2<N>& F, const double* ps, int no, double* out0, double* out1,
+                                          int sout, bool has1) {
+  double a0[N], a1[N];
+#pragma unroll
+  for (int o = 0; o < N; ++o) a0[o] = a1[o] = 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int o = 0; o < N; ++o) {
+      const double pv = TR ? ps[o * N + i] : ps[i * N + o];
+      a0[o] = fma(pv, F.x0[i], a0[o]);
+      a1[o] = fma(pv, F.x1[i], a1[o]);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < N; ++o) {
+    if (o >= no) break;
+    out0[o * sout] = a0[o];
+    if (has1) out1[o * sout] = a1[o];
+  }
+}
+
+// u~ = V^T (scale o y): y = B [NV][Nq] (destroyed) -> um [NV][Np] (separate buffer)
+template <int DIM, int N, int NV, int NT>
+__device__ __noinline__ void n2m_inplace(const PsiS& T, double* B, double* um, const double* scale) {
+  using S = Sz<DIM, N>;
+  constexpr int NPAIR = S::NPAIR, Np = S::Np, Nq = S::Nq, NVP = (NV + 1) / 2;
+  const int tid = threadIdx.x;
+  Fib2<N> F;
+  if constexpr (DIM == 2) {
+    constexpr int NFB = NV * N, I1 = (NFB + 1) / 2, I2 = N * NVP;
+    static_assert(I1 <= NT && I2 <= NT, "one item per thread");
+    // s1[v][a1][b] = sum_a psi1[a1][a] y[v][a + N b]
+    const int q0 = 2 * tid, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+    const int v0 = q0 / N, b0 = q0 - v0 * N, v1 = q1 / N, b1 = q1 - v1 * N;
+    if (tid < I1)
+      fib_load<N>(F, N, B + v0 * Nq + N * b0, B + v1 * Nq + N * b1, 1, scale ? scale + N * b0 : nullptr,
+                  scale ? scale + N * b1 : nullptr);
+    __syncthreads();
+    if (tid < I1) fib_store<N, true>(F, T.p1, N, B + v0 * Nq + b0, B + v1 * Nq + b1, N, q1 != q0);
+    __syncthreads();
+    // u[v][off(a1)+a2] = sum_b psi2[a1][a2][b] s1[v][a1][b]
+    if (tid < I2) {
+      const int a1 = tid / NVP, w0 = 2 * (tid - a1 * NVP), w1 = w0 + 1 < NV ? w0 + 1 : w0;
+      fib_load<N>(F, N, B + w0 * Nq + a1 * N, B + w1 * Nq + a1 * N, 1, nullptr, nullptr);
+      fib_store<N, true>(F, T.p2 + a1 * N * N, N - a1, um + w0 * Np + T.poff[a1], um + w1 * Np + T.poff[a1], 1,
+                         w1 != w0);
+    }
+    __syncthreads();
+  } else {
+    constexpr int NFB = NV * N * N, I1 = (NFB + 1) / 2, NFC = NV * N, NPC = (NFC + 1) / 2, I2 = N * NPC,
+                  I3 = NPAIR * NVP;
+    static_assert(I1 <= NT && I2 <= NT && I3 <= NT, "one item per thread");
+    {  // s2[v][a1][bc] = sum_a psi1[a1][a] y[v][a + N bc]
+      const int q0 = 2 * tid, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+      const int v0 = q0 / (N * N), bc0 = q0 - v0 * N * N, v1 = q1 / (N * N), bc1 = q1 - v1 * N * N;
+      if (tid < I1)
+        fib_load<N>(F, N, B + v0 * Nq + N * bc0, B + v1 * Nq + N * bc1, 1, scale ? scale + N * bc0 : nullptr,
+                    scale ? scale + N * bc1 : nullptr);
+      __syncthreads();
+      if (tid < I1) fib_store<N, true>(F, T.p1, N, B + v0 * Nq + bc0, B + v1 * Nq + bc1, N * N, q1 != q0);
+      __syncthreads();
+    }
+    {  // s1[v][pr(a1,a2)][c] = sum_b psi2[a1][a2][b] s2[v][a1][c][b]
+      const int a1 = tid / NPC, w = tid - a1 * NPC, q0 = 2 * w, q1 = q0 + 1 < NFC ? q0 + 1 : q0;
+      const int v0 = q0 / N, c0 = q0 - v0 * N, v1 = q1 / N, c1 = q1 - v1 * N;
+      const int prs = a1 * N - a1 * (a1 - 1) / 2;
+      if (tid < I2)
+        fib_load<N>(F, N, B + v0 * Nq + (a1 * N + c0) * N, B + v1 * Nq + (a1 * N + c1) * N, 1, nullptr, nullptr);
+      __syncthreads();
+      if (tid < I2)
+        fib_store<N, true>(F, T.p2 + a1 * N * N, N - a1, B + (v0 * NPAIR + prs) * N + c0,
+                           B + (v1 * NPAIR + prs) * N + c1, N, q1 != q0);
+      __syncthreads();
+    }
+    if (tid < I3) {  // u[v][off(pr)+a3] = sum_c psi3[s][a3][c] s1[v][pr][c]
+      const int pr = tid / NVP, w0 = 2 * (tid - pr * NVP), w1 = w0 + 1 < NV ? w0 + 1 : w0;
+      const int sdeg = T.pa1[pr] + T.pa2[pr];
+      fib_load<N>(F, N, B + (w0 * NPAIR + pr) * N, B + (w1 * NPAIR + pr) * N, 1, nullptr, nullptr);
+      fib_store<N, true>(F, T.p3 + sdeg * N * N, N - sdeg, um + w0 * Np + T.poff[pr], um + w1 * Np + T.poff[pr], 1,
+                         w1 != w0);
+    }
+    __syncthreads();
+  }
+}
+
+// u = V u~: um [NV][Np] -> B [NV][Nq]
+template <int DIM, int N, int NV, int NT>
+__device__ __noinline__ void m2n_inplace(const PsiS& T, const double* um, double* B) {
+  using S = Sz<DIM, N>;
+  constexpr int NPAIR = S::NPAIR, Np = S::Np, Nq = S::Nq, NVP = (NV + 1) / 2;
+  const int tid = threadIdx.x;
+  Fib2<N> F;
+  if constexpr (DIM == 2) {
+    constexpr int NFB = NV * N, I1 = N * NVP, I2 = (NFB + 1) / 2;
+    static_assert(I1 <= NT && I2 <= NT, "one item per thread");
+    if (tid < I1) {  // t1[v][a1][b] = sum_a2 psi2[a1][a2][b] u[v][off(a1)+a2]
+      const int a1 = tid / NVP, w0 = 2 * (tid - a1 * NVP), w1 = w0 + 1 < NV ? w0 + 1 : w0;
+      fib_load<N>(F, N - a1, um + w0 * Np + T.poff[a1], um + w1 * Np + T.poff[a1], 1, nullptr, nullptr);
+      fib_store<N, false>(F, T.p2 + a1 * N * N, N, B + w0 * Nq + a1 * N, B + w1 * Nq + a1 * N, 1, w1 != w0);
+    }
+    __syncthreads();
+    // u[v][a + N b] = sum_a1 psi1[a1][a] t1[v][a1][b]
+    const int q0 = 2 * tid, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+    const int v0 = q0 / N, b0 = q0 - v0 * N, v1 = q1 / N, b1 = q1 - v1 * N;
+    if (tid < I2) fib_load<N>(F, N, B + v0 * Nq + b0, B + v1 * Nq + b1, N, nullptr, nullptr);
+    __syncthreads();
+    if (tid < I2) fib_store<N, false>(F, T.p1, N, B + v0 * Nq + N * b0, B + v1 * Nq + N * b1, 1, q1 != q0);
+    __syncthreads();
+  } else {
+    constexpr int I1 = NPAIR * NVP, NFC = NV * N, NPC = (NFC + 1) / 2, I2 = N * NPC, NFB = NV * N * N,
+                  I3 = (NFB + 1) / 2;
+    static_assert(I1 <= NT && I2 <= NT && I3 <= NT, "one item per thread");
+    if (tid < I1) {  // t1[v][pr][c] = sum_a3 psi3[s][a3][c] u[v][off(pr)+a3]
+      const int pr = tid / NVP, w0 = 2 * (tid - pr * NVP), w1 = w0 + 1 < NV ? w0 + 1 : w0;
+      const int sdeg = T.pa1[pr] + T.pa2[pr];
+      fib_load<N>(F, N - sdeg, um + w0 * Np + T.poff[pr], um + w1 * Np + T.poff[pr], 1, nullptr, nullptr);
+      fib_store<N, false>(F, T.p3 + sdeg * N * N, N, B + (w0 * NPAIR + pr) * N, B + (w1 * NPAIR + pr) * N, 1,
+                          w1 != w0);
+    }
+    __syncthreads();
+    {  // t2[v][a1][c][b] = sum_a2 psi2[a1][a2][b] t1[v][pr(a1,a2)][c]
+      const int a1 = tid / NPC, w = tid - a1 * NPC, q0 = 2 * w, q1 = q0 + 1 < NFC ? q0 + 1 : q0;
+      const int v0 = q0 / N, c0 = q0 - v0 * N, v1 = q1 / N, c1 = q1 - v1 * N;
+      const int prs = a1 * N - a1 * (a1 - 1) / 2;
+      if (tid < I2)
+        fib_load<N>(F, N - a1, B + (v0 * NPAIR + prs) * N + c0, B + (v1 * NPAIR + prs) * N + c1, N, nullptr, nullptr);
+      __syncthreads();
+      if (tid < I2)
+        fib_store<N, false>(F, T.p2 + a1 * N * N, N, B + v0 * Nq + (a1 * N + c0) * N, B + v1 * Nq + (a1 * N + c1) * N,
+                            1, q1 != q0);
+      __syncthreads();
+    }
+    {  // u[v][a + N bc] = sum_a1 psi1[a1][a] t2[v][a1][bc]
+      const int q0 = 2 * tid, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+      const int v0 = q0 / (N * N), bc0 = q0 - v0 * N * N, v1 = q1 / (N * N), bc1 = q1 - v1 * N * N;
+      if (tid < I3) fib_load<N>(F, N, B + v0 * Nq + bc0, B + v1 * Nq + bc1, N * N, nullptr, nullptr);
+      __syncthreads();
+      if (tid < I3) fib_store<N, false>(F, T.p1, N, B + v0 * Nq + N * bc0, B + v1 * Nq + N * bc1, 1, q1 != q0);
+      __syncthreads();
+    }
+  }
+}
+
 template <int DIM, int N>
 __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsArgs A) {
   using S = Sz<DIM, N>;
@@ -232,15 +402,17 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
   using L = Rhs2Smem<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf, NT = W::NT, NS = W::NS;
   extern __shared__ __align__(16) double smk2[];
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t barA, barB;  // element data for the passes / for the epilogue
   double* sP = smk2 + L::o_pr;  // [DIM+3][Nq]: rho, v_1..v_d, p, beta
   double* sG = smk2 + L::o_g;   // [NG][Nq]: G_lm at (l*DIM+m)
   double* sR = smk2 + L::o_r;   // [NC][Nq] nodal residual
   double* pt = smk2 + L::o_pt;  // [NC][N(j)][N(a)][N(c)] facet-4 partials
+  double* sU = smk2 + L::o_um;  // [NC][Np] modal result, then [NC][N][N] facet-4 lifting (aliases pt)
   double* fP = smk2 + L::o_fp;  // [Nf][NC][Nqf] facet states rho, v, p
   double* fB = smk2 + L::o_fb;  // [Nf*Nqf] facet beta
   double* fJ = smk2 + L::o_fj;  // [Nf][DIM][Nqf] J n
-  double* ct = smk2 + L::o_ct;  // [NC][NF] C^T 1, then s = B J_f f* - C^T 1
+  double* fS = smk2 + L::o_fs;  // [Nf][NC][Nqf] B J_f f*, then s = B J_f f* - C^T 1
+  double* sWJ = smk2 + L::o_wj + L::WJOFF;  // [Nq] W / J~
   double* tb = smk2 + L::o_tb;
   double* tQ1 = tb;
   double* tA1 = tQ1 + N * N;
@@ -256,20 +428,35 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
   double* tli4 = tl3 + N;
   double* tB = tli4 + N * N;
 
-  const int64_t e = A.elem_list ? A.elem_list[blockIdx.x] : (int64_t)blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* scr = smk2 + L::o_sc + warp * NC * 32;
   const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
-  const double* gv = A.geo_vol + (size_t)e * S::GVS;
-  // ---- stage states, metrics, traces and facet normals by bulk copies; tables by the threads ----
-  if (tid == 0) {
+  auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
+  // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers
+  auto issue_A = [&](int64_t e) {
     constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8;
-    mbar_init(&mbar, 1);
-    mbar_expect_tx(&mbar, bP + bG + bF + bJ);
-    bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &mbar);
-    bulk_g2s(sG, gv, bG, &mbar);
-    bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &mbar);
-    bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &mbar);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&barA, bP + bG + bF + bJ);
+    bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &barA);
+    bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &barA);
+    bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &barA);
+    bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &barA);
+  };
+  auto issue_B = [&](int64_t e) {
+    constexpr unsigned bS = L::FS * 8, bW = L::WJN * 8;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&barB, bS + bW);
+    bulk_g2s(fS, A.fstar + (size_t)e * L::FS, bS, &barB);
+    bulk_g2s(smk2 + L::o_wj, A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &barB);
+  };
+  // ---- per-CTA: barriers, first element's copies, constant tables ----
+  if (tid == 0) {
+    mbar_init(&barA, 1);
+    mbar_init(&barB, 1);
+    if ((int64_t)blockIdx.x < A.n_elem) {
+      issue_A(elem_of(blockIdx.x));
+      issue_B(elem_of(blockIdx.x));
+    }
   }
   for (int k = tid; k < N * N; k += NT) {
     tQ1[k] = R.skQ1[k];
@@ -290,401 +477,464 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
     if constexpr (DIM == 3) tl3[k] = R.l3L[k];
   }
   for (int k = tid; k < NF; k += NT) tB[k] = R.Bf[k];
-  __syncthreads();  // mbarrier initialised before anyone waits
-  mbar_wait(&mbar, 0);
-  for (int i = tid; i < Nq; i += NT) sP[(DIM + 2) * Nq + i] = sP[i] / sP[(DIM + 1) * Nq + i];
-  for (int fz = tid; fz < NF; fz += NT) {
-    const double* q = fP + (fz / Nqf) * NC * Nqf + fz % Nqf;
-    fB[fz] = q[0] / q[(DIM + 1) * Nqf];
-  }
-  __syncthreads();
-
-  auto state_at = [&](int i) {
-    NodeState s;
-    s.r = sP[i];
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) s.v[m] = sP[(1 + m) * Nq + i];
-    s.p = sP[(DIM + 1) * Nq + i];
-    s.b = sP[(DIM + 2) * Nq + i];
-    return s;
-  };
-  auto Gat = [&](int l, int m, int i) { return sG[(l * DIM + m) * Nq + i]; };
+  const PsiS T = stage_psi<DIM, N>(R, smk2 + L::o_ps);
+  __syncthreads();  // mbarriers initialised and tables staged before anyone uses them
 
   const int grp = lane / N, pos = lane - grp * N;
   const bool lane_ok = grp < W::LPW;
-
-  // ---- direction passes, one specialisation per direction k ----
-  auto pass = [&](auto kc) {
-    constexpr int k = decltype(kc)::value;
-    constexpr int stride = k == 0 ? 1 : (k == 1 ? N : N * N);
+  unsigned it = 0;
 #pragma unroll 1
-    for (int slot = warp; slot < W::SLOTS; slot += W::NW) {
-      const int Lidx = slot * W::LPW + grp;
-      const bool valid = lane_ok && Lidx < W::NL;
-      const int l0 = valid ? Lidx % N : 0, l1 = valid ? Lidx / N : 0;
-      // node coordinates (a, b, c) and index
-      int ca, cb, cc;
-      if (k == 0) {
-        ca = pos;
-        cb = l0;
-        cc = l1;
-      } else if (k == 1) {
-        ca = l0;
-        cb = pos;
-        cc = l1;
-      } else {
-        ca = l0;
-        cb = l1;
-        cc = pos;
-      }
-      if constexpr (DIM == 2) cc = 0;
-      const int i = valid ? ca + N * cb + N * N * cc : 0;
-      const double vmask = valid ? 1.0 : 0.0;
-      NodeState me = state_at(i);
-      double gl[3][3];  // own metric rows g^(l)
-#pragma unroll
-      for (int l = 0; l < DIM; ++l)
-#pragma unroll
-        for (int m = 0; m < DIM; ++m) gl[l][m] = Gat(l, m, i);
-      double acc[NC];
-#pragma unroll
-      for (int v = 0; v < NC; ++v) acc[v] = 0.0;
+  for (int64_t idx = blockIdx.x; idx < A.n_elem; idx += gridDim.x, ++it) {
+    const int64_t e = elem_of(idx);
+    const int64_t nidx = idx + gridDim.x;
+    const bool has_next = nidx < A.n_elem;
+    const double* gv = A.geo_vol + (size_t)e * S::GVS;
+    // optional phase clock stamps (diagnostics, ES_PHASE_TIMING)
+    auto stamp = [&](int k) {
+      if (A.dbg && tid == 0 && idx < 4096) A.dbg[idx * 16 + k] = clock64();
+    };
+    stamp(0);
+    mbar_wait(&barA, it & 1);
+    for (int i = tid; i < Nq; i += NT) sP[(DIM + 2) * Nq + i] = sP[i] / sP[(DIM + 1) * Nq + i];
+    for (int fz = tid; fz < NF; fz += NT) {
+      const double* q = fP + (fz / Nqf) * NC * Nqf + fz % Nqf;
+      fB[fz] = q[0] / q[(DIM + 1) * Nqf];
+    }
+    mbar_wait(&barB, it & 1);  // f* is updated in place by the passes
+    __syncthreads();
+    stamp(1);
 
-      // -- volume pairs on this line: shifts in batches of VB (ILP), exchanged by shuffles --
+    auto state_at = [&](int i) {
+      NodeState s;
+      s.r = sP[i];
 #pragma unroll
-      for (int s0 = 1; s0 <= NS; s0 += W::VB) {
-        Job<DIM> jv[W::VB];
-#pragma unroll
-        for (int t = 0; t < W::VB; ++t) {
-          const int s = s0 + t;
-          int pos2 = pos + (s <= NS ? s : 0);
-          if (pos2 >= N) pos2 -= N;
-          const int j = valid ? i + (pos2 - pos) * stride : 0;
-          const int ix = pos * N + pos2;
-          Job<DIM>& jb = jv[t];
-          jb.base = sP;
-          jb.bb = sP + (DIM + 2) * Nq;
-          jb.stride = Nq;
-          jb.idx = j;
-          const bool half = (N % 2 == 0) && (s == NS);
-          const double mk = (s <= NS && !(half && pos >= N / 2)) ? vmask : 0.0;
-          if constexpr (DIM == 2) {
-            if (k == 0) {
-              const double cl = mk * tw[cb], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
-#pragma unroll
-              for (int m = 0; m < 2; ++m) jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * (gl[1][m] + Gat(1, m, j));
-            } else {
-              const double a2 = mk * tw[ca] * tA2[ix];
-#pragma unroll
-              for (int m = 0; m < 2; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j));
-            }
-          } else {
-            if (k == 0) {
-              const double cl = mk * 0.5 * tw[cb] * tw3[cc], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
-#pragma unroll
-              for (int m = 0; m < 3; ++m)
-                jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * ((gl[1][m] + gl[2][m]) + (Gat(1, m, j) + Gat(2, m, j)));
-            } else if (k == 1) {
-              const double cl = mk * 0.5 * tw[ca] * tw3[cc], a2 = cl * tA2[ix], a3 = cl * tA3[ix];
-#pragma unroll
-              for (int m = 0; m < 3; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j)) + a3 * (gl[2][m] + Gat(2, m, j));
-            } else {
-              const double a4 = mk * 0.125 * tw[ca] * tw[cb] * (1.0 - teta[cb]) * tA4[ix];
-#pragma unroll
-              for (int m = 0; m < 3; ++m) jb.n[m] = a4 * (gl[2][m] + Gat(2, m, j));
-            }
-          }
-        }
-        double Fs[W::VB][NC];
-        flux_batch<DIM, W::VB>(me, jv, gm1inv, Fs);
-#pragma unroll
-        for (int t = 0; t < W::VB; ++t) {
-          const int s = s0 + t;
-          if (s > NS) break;
-          int pos0 = pos - s;
-          if (pos0 < 0) pos0 += N;
-          const int src = grp * N + pos0;
-#pragma unroll
-          for (int v = 0; v < NC; ++v) acc[v] += shfl_d(Fs[t][v], src) - Fs[t][v];  // masked jobs send 0
-        }
-      }
+      for (int m = 0; m < DIM; ++m) s.v[m] = sP[(1 + m) * Nq + i];
+      s.p = sP[(DIM + 1) * Nq + i];
+      s.b = sP[(DIM + 2) * Nq + i];
+      return s;
+    };
+    auto Gat = [&](int l, int m, int i) { return sG[(l * DIM + m) * Nq + i]; };
 
-      // -- facet-correction pairs along the same lines --
-      // a facet job: state of facet node (z, f), normal coef (G_i^T nhat + J n_f)/2 with coefficient
-      // coef = (R^T B)_if
-      auto fjob = [&](Job<DIM>& jb, int z, int f, double coef, const double* gtn) {
-        jb.base = fP + z * NC * Nqf;
-        jb.bb = fB + z * Nqf;
-        jb.stride = Nqf;
-        jb.idx = f;
-        const double c2 = 0.5 * coef * vmask;
-#pragma unroll
-        for (int m = 0; m < DIM; ++m) jb.n[m] = c2 * (gtn[m] + fJ[(z * DIM + m) * Nqf + f]);
-      };
-      // facet-side sums over each line group through the warp scratch, in lane order; dest(line, v)
-      // returns where the sum of line `gq` goes (nullptr: discard)
-      auto line_sums = [&](const double* Fc, auto dest) {
-#pragma unroll
-        for (int v = 0; v < NC; ++v) {
-          acc[v] -= Fc[v];
-          scr[v * 32 + lane] = Fc[v];
+    // ---- direction passes, one specialisation per direction k ----
+    auto pass = [&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int stride = k == 0 ? 1 : (k == 1 ? N : N * N);
+  #pragma unroll 1
+      for (int slot = warp; slot < W::SLOTS; slot += W::NW) {
+        const int Lidx = slot * W::LPW + grp;
+        const bool valid = lane_ok && Lidx < W::NL;
+        const int l0 = valid ? Lidx % N : 0, l1 = valid ? Lidx / N : 0;
+        // node coordinates (a, b, c) and index
+        int ca, cb, cc;
+        if (k == 0) {
+          ca = pos;
+          cb = l0;
+          cc = l1;
+        } else if (k == 1) {
+          ca = l0;
+          cb = pos;
+          cc = l1;
+        } else {
+          ca = l0;
+          cb = l1;
+          cc = pos;
         }
-        __syncwarp();
-        for (int sidx = lane; sidx < W::LPW * NC; sidx += 32) {
-          const int gq = sidx / NC, v = sidx - gq * NC;
-          const double* src = scr + v * 32 + gq * N;
-          double sum = 0.0;
-#pragma unroll
-          for (int a = 0; a < N; ++a) sum += src[a];
-          const int Lq = slot * W::LPW + gq;
-          if (Lq < W::NL) {
-            double* d = dest(Lq, v);
-            if (d) *d = sum;
-          }
-        }
-        __syncwarp();
-      };
-      if constexpr (DIM == 2) {
-        Job<DIM> jf[2];
-        if (k == 0) {  // eta1 = +1 (facet 2) and eta1 = -1 (facet 3): facet node b
-          const double r2 = 0.70710678118654752440;
-          double gtn[2] = {(gl[0][0] + gl[1][0]) * r2, (gl[0][1] + gl[1][1]) * r2};
-          double gtn3[2] = {-gl[0][0], -gl[0][1]};
-          fjob(jf[0], 1, cb, tlR[ca] * tB[1 * Nqf + cb], gtn);
-          fjob(jf[1], 2, cb, tlL[ca] * tB[2 * Nqf + cb], gtn3);
-          double Fc[2][NC];
-          flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
-          line_sums(Fc[0], [&](int Lq, int v) { return ct + v * NF + 1 * Nqf + Lq; });
-          line_sums(Fc[1], [&](int Lq, int v) { return ct + v * NF + 2 * Nqf + Lq; });
-        } else {  // eta2 = -1 (facet 1): facet node a
-          double gtn[2] = {-gl[1][0], -gl[1][1]};
-          fjob(jf[0], 0, ca, tlL[cb] * tB[0 * Nqf + ca], gtn);
-          double Fc[1][NC];
-          flux_batch<DIM, 1>(me, jf, gm1inv, Fc);
-          line_sums(Fc[0], [&](int Lq, int v) { return ct + v * NF + Lq; });
-        }
-      } else {
-        if (k == 0) {  // facets 2 and 3 (eta1 = +1 / -1): facet node (b, c) = line index
-          const double r3 = 0.57735026918962576451;
-          const int f = cb + N * cc;
-          double gtn[3], gtn3[3];
-#pragma unroll
-          for (int m = 0; m < 3; ++m) {
-            gtn[m] = (gl[0][m] + gl[1][m] + gl[2][m]) * r3;
-            gtn3[m] = -gl[0][m];
-          }
-          Job<DIM> jf[2];
-          fjob(jf[0], 1, f, tlR[ca] * tB[1 * Nqf + f], gtn);
-          fjob(jf[1], 2, f, tlL[ca] * tB[2 * Nqf + f], gtn3);
-          double Fc[2][NC];
-          flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
-          line_sums(Fc[0], [&](int Lq, int v) { return ct + v * NF + 1 * Nqf + Lq; });
-          line_sums(Fc[1], [&](int Lq, int v) { return ct + v * NF + 2 * Nqf + Lq; });
-        } else if (k == 1) {  // facet 1 (eta2 = -1): node (a, c) = line; facet 4 (eta3 = -1): nodes (a, j)
-          const int f = ca + N * cc;
-          double gtn[3] = {-gl[1][0], -gl[1][1], -gl[1][2]};
-          double gt4[3] = {-gl[2][0], -gl[2][1], -gl[2][2]};
-          constexpr int JB = 2;  // jobs per batch: facet 1 and the N facet-4 nodes
-#pragma unroll 1
-          for (int j0 = -1; j0 < N; j0 += JB) {
-            Job<DIM> jq[JB];
-#pragma unroll
-            for (int t = 0; t < JB; ++t) {
-              const int jf = j0 + t;
-              if (jf < 0) {
-                fjob(jq[t], 0, f, tlL[cb] * tB[0 * Nqf + f], gtn);
+        if constexpr (DIM == 2) cc = 0;
+        const int i = valid ? ca + N * cb + N * N * cc : 0;
+        const double vmask = valid ? 1.0 : 0.0;
+        NodeState me = state_at(i);
+        double gl[3][3];  // own metric rows g^(l)
+  #pragma unroll
+        for (int l = 0; l < DIM; ++l)
+  #pragma unroll
+          for (int m = 0; m < DIM; ++m) gl[l][m] = Gat(l, m, i);
+        double acc[NC];
+  #pragma unroll
+        for (int v = 0; v < NC; ++v) acc[v] = 0.0;
+
+        // -- volume pairs on this line: shifts in batches of VB (ILP), exchanged by shuffles --
+  #pragma unroll
+        for (int s0 = 1; s0 <= NS; s0 += W::VB) {
+          Job<DIM> jv[W::VB];
+  #pragma unroll
+          for (int t = 0; t < W::VB; ++t) {
+            const int s = s0 + t;
+            int pos2 = pos + (s <= NS ? s : 0);
+            if (pos2 >= N) pos2 -= N;
+            const int j = valid ? i + (pos2 - pos) * stride : 0;
+            const int ix = pos * N + pos2;
+            Job<DIM>& jb = jv[t];
+            jb.base = sP;
+            jb.bb = sP + (DIM + 2) * Nq;
+            jb.stride = Nq;
+            jb.idx = j;
+            const bool half = (N % 2 == 0) && (s == NS);
+            const double mk = (s <= NS && !(half && pos >= N / 2)) ? vmask : 0.0;
+            if constexpr (DIM == 2) {
+              if (k == 0) {
+                const double cl = mk * tw[cb], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
+  #pragma unroll
+                for (int m = 0; m < 2; ++m) jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * (gl[1][m] + Gat(1, m, j));
               } else {
-                const int jj = jf < N ? jf : N - 1;
-                const int f4 = ca + N * jj;
-                fjob(jq[t], 3, f4, jf < N ? tli4[jj * N + cb] * tl3[cc] * tB[3 * Nqf + f4] : 0.0, gt4);
+                const double a2 = mk * tw[ca] * tA2[ix];
+  #pragma unroll
+                for (int m = 0; m < 2; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j));
+              }
+            } else {
+              if (k == 0) {
+                const double cl = mk * 0.5 * tw[cb] * tw3[cc], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
+  #pragma unroll
+                for (int m = 0; m < 3; ++m)
+                  jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * ((gl[1][m] + gl[2][m]) + (Gat(1, m, j) + Gat(2, m, j)));
+              } else if (k == 1) {
+                const double cl = mk * 0.5 * tw[ca] * tw3[cc], a2 = cl * tA2[ix], a3 = cl * tA3[ix];
+  #pragma unroll
+                for (int m = 0; m < 3; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j)) + a3 * (gl[2][m] + Gat(2, m, j));
+              } else {
+                const double a4 = mk * 0.125 * tw[ca] * tw[cb] * (1.0 - teta[cb]) * tA4[ix];
+  #pragma unroll
+                for (int m = 0; m < 3; ++m) jb.n[m] = a4 * (gl[2][m] + Gat(2, m, j));
               }
             }
-            double Fb[JB][NC];
-            flux_batch<DIM, JB>(me, jq, gm1inv, Fb);
-#pragma unroll
-            for (int t = 0; t < JB; ++t) {
-              const int jf = j0 + t;
-              // sum over b on the (a, c) line; line Lq = a + N c
-              line_sums(Fb[t], [&](int Lq, int v) -> double* {
-                if (jf < 0) return ct + v * NF + Lq;
-                if (jf >= N) return nullptr;
-                const int a = Lq % N, c = Lq / N;
-                return pt + ((v * N + jf) * N + a) * N + c;
-              });
+          }
+          double Fs[W::VB][NC];
+          flux_batch<DIM, W::VB>(me, jv, gm1inv, Fs);
+  #pragma unroll
+          for (int t = 0; t < W::VB; ++t) {
+            const int s = s0 + t;
+            if (s > NS) break;
+            int pos0 = pos - s;
+            if (pos0 < 0) pos0 += N;
+            const int src = grp * N + pos0;
+  #pragma unroll
+            for (int v = 0; v < NC; ++v) acc[v] += shfl_d(Fs[t][v], src) - Fs[t][v];  // masked jobs send 0
+          }
+        }
+
+        // -- facet-correction pairs along the same lines --
+        // a facet job: state of facet node (z, f), normal coef (G_i^T nhat + J n_f)/2 with coefficient
+        // coef = (R^T B)_if
+        auto fjob = [&](Job<DIM>& jb, int z, int f, double coef, const double* gtn) {
+          jb.base = fP + z * NC * Nqf;
+          jb.bb = fB + z * Nqf;
+          jb.stride = Nqf;
+          jb.idx = f;
+          const double c2 = 0.5 * coef * vmask;
+  #pragma unroll
+          for (int m = 0; m < DIM; ++m) jb.n[m] = c2 * (gtn[m] + fJ[(z * DIM + m) * Nqf + f]);
+        };
+        // facet-side sums over each line group through the warp scratch, in lane order; dest(line, v)
+        // returns where the sum of line `gq` goes (nullptr: discard)
+        auto line_sums = [&](const double* Fc, auto dest) {
+  #pragma unroll
+          for (int v = 0; v < NC; ++v) {
+            acc[v] -= Fc[v];
+            scr[v * 32 + lane] = Fc[v];
+          }
+          __syncwarp();
+          for (int sidx = lane; sidx < W::LPW * NC; sidx += 32) {
+            const int gq = sidx / NC, v = sidx - gq * NC;
+            const double* src = scr + v * 32 + gq * N;
+            double tv[N];  // pairwise tree sum, depth ceil(log2 N)
+  #pragma unroll
+            for (int a = 0; a < N; ++a) tv[a] = src[a];
+  #pragma unroll
+            for (int w = 1; w < N; w *= 2)
+  #pragma unroll
+              for (int a = 0; a + w < N; a += 2 * w) tv[a] += tv[a + w];
+            const double sum = tv[0];
+            const int Lq = slot * W::LPW + gq;
+            if (Lq < W::NL) {
+              double* d = dest(Lq, v);
+              if (d) *d -= sum;  // s = B J_f f* - C^T 1
             }
+          }
+          __syncwarp();
+        };
+        if constexpr (DIM == 2) {
+          Job<DIM> jf[2];
+          if (k == 0) {  // eta1 = +1 (facet 2) and eta1 = -1 (facet 3): facet node b
+            const double r2 = 0.70710678118654752440;
+            double gtn[2] = {(gl[0][0] + gl[1][0]) * r2, (gl[0][1] + gl[1][1]) * r2};
+            double gtn3[2] = {-gl[0][0], -gl[0][1]};
+            fjob(jf[0], 1, cb, tlR[ca] * tB[1 * Nqf + cb], gtn);
+            fjob(jf[1], 2, cb, tlL[ca] * tB[2 * Nqf + cb], gtn3);
+            double Fc[2][NC];
+            flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
+            line_sums(Fc[0], [&](int Lq, int v) { return fS + (1 * NC + v) * Nqf + Lq; });
+            line_sums(Fc[1], [&](int Lq, int v) { return fS + (2 * NC + v) * Nqf + Lq; });
+          } else {  // eta2 = -1 (facet 1): facet node a
+            double gtn[2] = {-gl[1][0], -gl[1][1]};
+            fjob(jf[0], 0, ca, tlL[cb] * tB[0 * Nqf + ca], gtn);
+            double Fc[1][NC];
+            flux_batch<DIM, 1>(me, jf, gm1inv, Fc);
+            line_sums(Fc[0], [&](int Lq, int v) { return fS + (0 * NC + v) * Nqf + Lq; });
+          }
+        } else {
+          if (k == 0) {  // facets 2 and 3 (eta1 = +1 / -1): facet node (b, c) = line index
+            const double r3 = 0.57735026918962576451;
+            const int f = cb + N * cc;
+            double gtn[3], gtn3[3];
+  #pragma unroll
+            for (int m = 0; m < 3; ++m) {
+              gtn[m] = (gl[0][m] + gl[1][m] + gl[2][m]) * r3;
+              gtn3[m] = -gl[0][m];
+            }
+            Job<DIM> jf[2];
+            fjob(jf[0], 1, f, tlR[ca] * tB[1 * Nqf + f], gtn);
+            fjob(jf[1], 2, f, tlL[ca] * tB[2 * Nqf + f], gtn3);
+            double Fc[2][NC];
+            flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
+            line_sums(Fc[0], [&](int Lq, int v) { return fS + (1 * NC + v) * Nqf + Lq; });
+            line_sums(Fc[1], [&](int Lq, int v) { return fS + (2 * NC + v) * Nqf + Lq; });
+          } else if (k == 1) {  // facet 1 (eta2 = -1): node (a, c) = line; facet 4 (eta3 = -1): nodes (a, j)
+            const int f = ca + N * cc;
+            double gtn[3] = {-gl[1][0], -gl[1][1], -gl[1][2]};
+            double gt4[3] = {-gl[2][0], -gl[2][1], -gl[2][2]};
+            {  // facet 1: one job per lane, summed over the line
+              Job<DIM> j1[1];
+              fjob(j1[0], 0, f, tlL[cb] * tB[0 * Nqf + f], gtn);
+              double F1[1][NC];
+              flux_batch<DIM, 1>(me, j1, gm1inv, F1);
+              line_sums(F1[0], [&](int Lq, int v) { return fS + (0 * NC + v) * Nqf + Lq; });
+            }
+            // facet 4, rotating schedule: at step t lane pos pairs its node (a, b = pos, c) with the
+            // facet node (a, j = (pos + t) mod N); the facet-side value travels by shuffle to lane j,
+            // which accumulates the sum over b of its facet node (no reduction tree, no scratch)
+            double facc[NC];
+  #pragma unroll
+            for (int v = 0; v < NC; ++v) facc[v] = 0.0;
+  #pragma unroll 1
+            for (int t0 = 0; t0 < N; t0 += 2) {
+              Job<DIM> jq[2];
+  #pragma unroll
+              for (int tt = 0; tt < 2; ++tt) {
+                const int t = t0 + tt;
+                int jf = pos + (t < N ? t : 0);
+                if (jf >= N) jf -= N;
+                const int f4 = ca + N * jf;
+                fjob(jq[tt], 3, f4, t < N ? tli4[jf * N + cb] * tl3[cc] * tB[3 * Nqf + f4] : 0.0, gt4);
+              }
+              double Fb[2][NC];
+              flux_batch<DIM, 2>(me, jq, gm1inv, Fb);
+  #pragma unroll
+              for (int tt = 0; tt < 2; ++tt) {
+                const int t = t0 + tt;
+                if (t >= N) break;
+                int p0 = pos - t;
+                if (p0 < 0) p0 += N;
+                const int src = grp * N + p0;
+  #pragma unroll
+                for (int v = 0; v < NC; ++v) {
+                  acc[v] -= Fb[tt][v];
+                  facc[v] += shfl_d(Fb[tt][v], src);
+                }
+              }
+            }
+            if (valid)  // partial over b of facet node (a, j = pos) on line c
+  #pragma unroll
+              for (int v = 0; v < NC; ++v) pt[((v * N + pos) * N + ca) * N + cc] = facc[v];
+          }
+        }
+        // -- residual of this pass (exclusive owner of node i within the pass) --
+        if (valid) {
+  #pragma unroll
+          for (int v = 0; v < NC; ++v) {
+            if (k == 0)
+              sR[v * Nq + i] = acc[v];
+            else
+              sR[v * Nq + i] += acc[v];
           }
         }
       }
-      // -- residual of this pass (exclusive owner of node i within the pass) --
-      if (valid) {
+      __syncthreads();
+      stamp(2 + k);
+    };
+    pass(std::integral_constant<int, 0>{});
+    pass(std::integral_constant<int, 1>{});
+    if constexpr (DIM == 3) pass(std::integral_constant<int, 2>{});
+    // states, metrics and facet inputs are dead: the next element's copies land during the epilogue
+    if (tid == 0 && has_next) issue_A(elem_of(nidx));
+    if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
+      for (int q = tid; q < NC * N * N; q += NT) {
+        const int v = q / (N * N), jf = (q / N) % N, a = q % N;
+        double s = 0.0;
 #pragma unroll
-        for (int v = 0; v < NC; ++v) {
-          if (k == 0)
-            sR[v * Nq + i] = acc[v];
-          else
-            sR[v * Nq + i] += acc[v];
+        for (int c = 0; c < N; ++c) s += pt[((v * N + jf) * N + a) * N + c];
+        fS[(3 * NC + v) * Nqf + a + N * jf] -= s;
+      }
+      __syncthreads();
+    }
+    stamp(5);
+    // ---- lifting r -= R^T s; facet 4 sum-factorised: t4[v][a][b] = sum_j l_b(eta3_j) s4[v][a + N j] ----
+    if constexpr (DIM == 3) {
+      double* t4 = sU + L::UM - NC * N * N;
+      for (int q = tid; q < NC * N * N; q += NT) {
+        const int v = q / (N * N), b = (q / N) % N, a = q % N;
+        const double* s4 = fS + (3 * NC + v) * Nqf + a;
+        double t = 0.0;
+#pragma unroll
+        for (int jf = 0; jf < N; ++jf) t = fma(tli4[jf * N + b], s4[N * jf], t);
+        t4[(v * N + b) * N + a] = t;
+      }
+      __syncthreads();
+    }
+    for (int i = tid; i < Nq; i += NT) {
+      const int a = i % N, b = (i / N) % N, c = DIM == 3 ? i / (N * N) : 0;
+#pragma unroll
+      for (int v = 0; v < NC; ++v) {
+        double t;
+        if constexpr (DIM == 2) {
+          t = tlL[b] * fS[(0 * NC + v) * Nqf + a] + tlR[a] * fS[(1 * NC + v) * Nqf + b] +
+              tlL[a] * fS[(2 * NC + v) * Nqf + b];
+        } else {
+          const double* t4 = sU + L::UM - NC * N * N;
+          t = tlL[b] * fS[(0 * NC + v) * Nqf + a + N * c] + tlR[a] * fS[(1 * NC + v) * Nqf + b + N * c] +
+              tlL[a] * fS[(2 * NC + v) * Nqf + b + N * c] + tl3[c] * t4[(v * N + b) * N + a];
         }
+        sR[v * Nq + i] -= t;
       }
     }
     __syncthreads();
-  };
-  pass(std::integral_constant<int, 0>{});
-  pass(std::integral_constant<int, 1>{});
-  if constexpr (DIM == 3) pass(std::integral_constant<int, 2>{});
-  // the epilogue reuses the state / metric region: psi tables for the transforms and W / J~
-  const PsiS T = stage_psi<DIM, N>(R, smk2 + L::o_ps);
-  double* sWJ = smk2 + L::o_wj;
-  for (int i = tid; i < Nq; i += NT) sWJ[i] = gv[(S::NG + 1) * Nq + i];
-  if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
-    for (int it = tid; it < NC * N * N; it += NT) {
-      const int v = it / (N * N), jf = (it / N) % N, a = it % N;
-      double s = 0.0;
-      for (int c = 0; c < N; ++c) s += pt[((v * N + jf) * N + a) * N + c];
-      ct[v * NF + 3 * Nqf + a + N * jf] = s;
-    }
-  }
-  __syncthreads();
+    stamp(7);
 
-  // ---- interface flux and s = B J_f f* - C^T 1 ----
-  for (int fz = tid; fz < NF; fz += NT) {
-    int z = fz / Nqf, f = fz % Nqf;
-    int64_t slot = A.face_slot[e * S::Nf + z];
-    int rf = A.face_reflect[e * S::Nf + z];
-    int fo;
-    if constexpr (DIM == 2)
-      fo = rf ? N - 1 - f : f;
-    else
-      fo = rf ? (N - 1 - f % N) + N * (f / N) : f;
-    const double* tp = A.trace + (size_t)slot * NC * Nqf;
-    NodeState up, um;
-    {
-      const double* q = fP + z * NC * Nqf + f;
-      um.r = q[0];
-#pragma unroll
-      for (int m = 0; m < DIM; ++m) um.v[m] = q[(1 + m) * Nqf];
-      um.p = q[(DIM + 1) * Nqf];
-      um.b = fB[fz];
+    // ---- d u~/dt = V^T W/J~ V (V^T r), transforms in place in sR ----
+    n2m_inplace<DIM, N, NC, NT>(T, sR, sU, nullptr);
+    stamp(8);
+    if (A.mode == 5) {  // entropy production sum w~ . (V^T r) and conservation (V^T r)_0 / c0
+      double loc = 0.0, la = 0.0;
+      for (int k = tid; k < NC * Np; k += NT) {
+        double t = A.wt[(size_t)e * NC * Np + k] * sU[k];
+        loc += t;
+        la += fabs(t);
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        loc += __shfl_down_sync(0xffffffffu, loc, o);
+        la += __shfl_down_sync(0xffffffffu, la, o);
+      }
+      __shared__ double red[2][W::NW];
+      if (lane == 0) {
+        red[0][warp] = loc;
+        red[1][warp] = la;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int wv = 0; wv < W::NW; ++wv) {
+          s0 += red[0][wv];
+          s1 += red[1][wv];
+        }
+        double* pe2 = A.part + (size_t)e * (2 + NC);
+        pe2[0] = s0;
+        pe2[1] = s1;
+        for (int v = 0; v < NC; ++v) pe2[2 + v] = sU[v * Np] / A.c0;
+      }
+      __syncthreads();
     }
-    up.r = tp[fo];
+    m2n_inplace<DIM, N, NC, NT>(T, sU, sR);
+    stamp(9);
+    n2m_inplace<DIM, N, NC, NT>(T, sR, sU, sWJ);  // W / J~ fused into the loads
+    stamp(10);
+    // f* and W / J~ are consumed: the next element's copies land during its passes
+    if (tid == 0 && has_next) issue_B(elem_of(nidx));
+    const size_t base = (size_t)e * NC * Np;
+    const double dt = A.dt;
+    for (int kk = tid; kk < NC * Np; kk += NT) {
+      double du = sU[kk];
+      switch (A.mode) {
+        case 0:
+        case 5:
+          A.out[base + kk] = du;
+          break;
+        case 1:  // classical RK4 stage 1 (R17)
+          A.acc[base + kk] = A.u0[base + kk] + (dt / 6.0) * du;
+          A.ustage[base + kk] = A.u0[base + kk] + (0.5 * dt) * du;
+          break;
+        case 2:
+          A.acc[base + kk] += (dt / 3.0) * du;
+          A.ustage[base + kk] = A.u0[base + kk] + (0.5 * dt) * du;
+          break;
+        case 3:
+          A.acc[base + kk] += (dt / 3.0) * du;
+          A.ustage[base + kk] = A.u0[base + kk] + dt * du;
+          break;
+        case 4:
+          A.out[base + kk] = A.acc[base + kk] + (dt / 6.0) * du;
+          break;
+      }
+    }
+    __syncthreads();  // sU / sR are reused by the next element
+    stamp(11);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// interface flux (Davis wave speed P:839): one thread per (element, facet node);
+// writes B J_f f*(u-, u+, n) with the element's own unit normal n = J n / J_f and the
+// neighbour's trace at the permuted node.  Both sides of a face evaluate it with their
+// own normals; the arithmetic per side does not depend on the partition.
+// ------------------------------------------------------------------------------------------------
+template <int DIM, int N>
+__global__ void __launch_bounds__(256) iface_kernel(DevRef R, IfaceArgs A) {
+  using S = Sz<DIM, N>;
+  constexpr int NC = S::NC, Nqf = S::Nqf, NF = S::NF, Nf = S::Nf;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= A.n_elem * NF) return;
+  const int64_t idx = t / NF;
+  const int fz = (int)(t - idx * NF), z = fz / Nqf, f = fz - z * Nqf;
+  const int64_t e = A.elem_list ? A.elem_list[idx] : idx;
+  const int64_t slot = A.face_slot[e * Nf + z];
+  const int rf = A.face_reflect[e * Nf + z];
+  int fo;
+  if constexpr (DIM == 2)
+    fo = rf ? N - 1 - f : f;
+  else
+    fo = rf ? (N - 1 - f % N) + N * (f / N) : f;
+  const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
+  const double* tm = A.trace + (size_t)(e * Nf + z) * NC * Nqf + f;
+  const double* tp = A.trace + (size_t)slot * NC * Nqf + fo;
+  NodeState um, up;
+  um.r = tm[0];
+  up.r = tp[0];
 #pragma unroll
-    for (int m = 0; m < DIM; ++m) up.v[m] = tp[(1 + m) * Nqf + fo];
-    up.p = tp[(DIM + 1) * Nqf + fo];
-    up.b = up.r / up.p;
-    double Jn[DIM], Jf = 0.0;
+  for (int m = 0; m < DIM; ++m) {
+    um.v[m] = tm[(1 + m) * Nqf];
+    up.v[m] = tp[(1 + m) * Nqf];
+  }
+  um.p = tm[(DIM + 1) * Nqf];
+  up.p = tp[(DIM + 1) * Nqf];
+  um.b = um.r / um.p;
+  up.b = up.r / up.p;
+  double Jn[DIM], Jf = 0.0;
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) {
+    Jn[m] = A.geo_face[((size_t)(e * Nf + z) * DIM + m) * Nqf + f];
+    Jf += Jn[m] * Jn[m];
+  }
+  Jf = sqrt(Jf);
+  double nu[DIM];
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) nu[m] = Jn[m] / Jf;
+  double F[NC];
+  ec_flux_v2<DIM>(um, up, nu, gm1inv, F);
+  if (A.es) {  // local Lax-Friedrichs with Davis's wave speed
+    double vnm = 0.0, vnp = 0.0;
 #pragma unroll
     for (int m = 0; m < DIM; ++m) {
-      Jn[m] = fJ[(z * DIM + m) * Nqf + f];
-      Jf += Jn[m] * Jn[m];
+      vnm += um.v[m] * nu[m];
+      vnp += up.v[m] * nu[m];
     }
-    Jf = sqrt(Jf);
-    double nu[DIM];
+    const double lam = fmax(fabs(vnm), fabs(vnp)) + fmax(sqrt(g * um.p / um.r), sqrt(g * up.p / up.r));
+    double Um[NC], Up[NC];
+    cons_of<DIM>(um.r, um.v, um.p, gm1inv, Um);
+    cons_of<DIM>(up.r, up.v, up.p, gm1inv, Up);
 #pragma unroll
-    for (int m = 0; m < DIM; ++m) nu[m] = Jn[m] / Jf;
-    double F[NC];
-    ec_flux_v2<DIM>(um, up, nu, gm1inv, F);
-    if (A.es) {  // local Lax-Friedrichs with Davis's wave speed
-      double vnm = 0.0, vnp = 0.0;
-#pragma unroll
-      for (int m = 0; m < DIM; ++m) {
-        vnm += um.v[m] * nu[m];
-        vnp += up.v[m] * nu[m];
-      }
-      double lam = fmax(fabs(vnm), fabs(vnp)) + fmax(sqrt(g * um.p / um.r), sqrt(g * up.p / up.r));
-      double Um[NC], Up[NC];
-      cons_of<DIM>(um.r, um.v, um.p, gm1inv, Um);
-      cons_of<DIM>(up.r, up.v, up.p, gm1inv, Up);
-#pragma unroll
-      for (int v = 0; v < NC; ++v) F[v] -= 0.5 * lam * (Up[v] - Um[v]);
-    }
-    double bj = tB[fz] * Jf;
-#pragma unroll
-    for (int v = 0; v < NC; ++v) ct[v * NF + fz] = bj * F[v] - ct[v * NF + fz];
+    for (int v = 0; v < NC; ++v) F[v] -= 0.5 * lam * (Up[v] - Um[v]);
   }
-  __syncthreads();
-
-  // ---- lifting r -= R^T s ----
-  for (int i = tid; i < Nq; i += NT) {
-    int a = i % N, b = (i / N) % N, c = DIM == 3 ? i / (N * N) : 0;
+  const double bj = __ldg(&R.Bf[fz]) * Jf;
+  double* out = A.fstar + (size_t)(e * Nf + z) * NC * Nqf + f;
 #pragma unroll
-    for (int v = 0; v < NC; ++v) {
-      const double* sv = ct + v * NF;
-      double t;
-      if constexpr (DIM == 2) {
-        t = tlL[b] * sv[a] + tlR[a] * sv[Nqf + b] + tlL[a] * sv[2 * Nqf + b];
-      } else {
-        t = tlL[b] * sv[a + N * c] + tlR[a] * sv[Nqf + b + N * c] + tlL[a] * sv[2 * Nqf + b + N * c];
-        double t4 = 0.0;
-        for (int jf = 0; jf < N; ++jf) t4 += tli4[jf * N + b] * sv[3 * Nqf + a + N * jf];
-        t += tl3[c] * t4;
-      }
-      sR[v * Nq + i] -= t;
-    }
-  }
-  __syncthreads();
-
-  // ---- d u~/dt = V^T W/J~ V (V^T r) ----
-  double* T1 = smk2 + L::o_t1;
-  double* T2 = smk2 + L::o_t2;
-  double* um = smk2 + L::o_pt;  // facet partials, states and C^T 1 are dead: modal scratch
-  static_assert(S::NC * S::Np <= L::o_sc - L::o_pt, "modal scratch");
-  nodal_to_modal<DIM, N, NC>(T, sR, um, T1, T2);
-  if (A.mode == 5) {  // entropy production sum w~ . (V^T r) and conservation (V^T r)_0 / c0
-    double loc = 0.0, la = 0.0;
-    for (int k = tid; k < NC * Np; k += NT) {
-      double t = A.wt[(size_t)e * NC * Np + k] * um[k];
-      loc += t;
-      la += fabs(t);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      loc += __shfl_down_sync(0xffffffffu, loc, o);
-      la += __shfl_down_sync(0xffffffffu, la, o);
-    }
-    __shared__ double red[2][W::NW];
-    if (lane == 0) {
-      red[0][warp] = loc;
-      red[1][warp] = la;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double s0 = 0.0, s1 = 0.0;
-      for (int wv = 0; wv < W::NW; ++wv) {
-        s0 += red[0][wv];
-        s1 += red[1][wv];
-      }
-      double* pe2 = A.part + (size_t)e * (2 + NC);
-      pe2[0] = s0;
-      pe2[1] = s1;
-      for (int v = 0; v < NC; ++v) pe2[2 + v] = um[v * Np] / A.c0;
-    }
-  }
-  modal_to_nodal<DIM, N, NC>(T, um, sR, T1, T2);
-  nodal_to_modal<DIM, N, NC>(T, sR, um, T1, T2, sWJ);  // W / J~ fused into the loads
-  const size_t base = (size_t)e * NC * Np;
-  const double dt = A.dt;
-  for (int kk = tid; kk < NC * Np; kk += NT) {
-    double du = um[kk];
-    switch (A.mode) {
-      case 0:
-      case 5:
-        A.out[base + kk] = du;
-        break;
-      case 1:  // classical RK4 stage 1 (R17)
-        A.acc[base + kk] = A.u0[base + kk] + (dt / 6.0) * du;
-        A.ustage[base + kk] = A.u0[base + kk] + (0.5 * dt) * du;
-        break;
-      case 2:
-        A.acc[base + kk] += (dt / 3.0) * du;
-        A.ustage[base + kk] = A.u0[base + kk] + (0.5 * dt) * du;
-        break;
-      case 3:
-        A.acc[base + kk] += (dt / 3.0) * du;
-        A.ustage[base + kk] = A.u0[base + kk] + dt * du;
-        break;
-      case 4:
-        A.out[base + kk] = A.acc[base + kk] + (dt / 6.0) * du;
-        break;
-    }
-  }
+  for (int v = 0; v < NC; ++v) out[v * Nqf] = bj * F[v];
 }
 
 }  // namespace esb
