@@ -19,6 +19,10 @@
 
 namespace esb {
 
+// the dynamic shared memory of the flux kernel, visible to its non-inlined helpers so that their
+// accesses compile to shared-memory loads and stores
+extern __shared__ __align__(16) double smk2[];
+
 template <int DIM, int N>
 struct Lw {  // line-group layout
   using S = Sz<DIM, N>;
@@ -249,34 +253,60 @@ __device__ __forceinline__ void fib_load(Fib2<N>& F, int ni, const double* in0, 
     }
   }
 }
-// all outputs are accumulated in registers first (independent FMA chains), then stored
+// outputs in chunks of OC, each accumulated over all inputs (independent FMA chains); the chunk
+// loop is not unrolled so that only one chunk's table entries are in flight (bounded registers)
 template <int N, bool TR>
 __device__ __forceinline__ void fib_store(const Fib2<N>& F, const double* ps, int no, double* out0, double* out1,
                                           int sout, bool has1) {
-  double a0[N], a1[N];
+  constexpr int OC = 3;
+#pragma unroll 1
+  for (int o0 = 0; o0 < no; o0 += OC) {
+    double a0[OC], a1[OC];
 #pragma unroll
-  for (int o = 0; o < N; ++o) a0[o] = a1[o] = 0.0;
+    for (int q = 0; q < OC; ++q) a0[q] = a1[q] = 0.0;
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
+    for (int i = 0; i < N; ++i) {
 #pragma unroll
-    for (int o = 0; o < N; ++o) {
-      const double pv = TR ? ps[o * N + i] : ps[i * N + o];
-      a0[o] = fma(pv, F.x0[i], a0[o]);
-      a1[o] = fma(pv, F.x1[i], a1[o]);
+      for (int q = 0; q < OC; ++q) {
+        const int o = o0 + q < N ? o0 + q : N - 1;
+        const double pv = TR ? ps[o * N + i] : ps[i * N + o];
+        a0[q] = fma(pv, F.x0[i], a0[q]);
+        a1[q] = fma(pv, F.x1[i], a1[q]);
+      }
     }
-  }
 #pragma unroll
-  for (int o = 0; o < N; ++o) {
-    if (o >= no) break;
-    out0[o * sout] = a0[o];
-    if (has1) out1[o * sout] = a1[o];
+    for (int q = 0; q < OC; ++q) {
+      if (o0 + q >= no) break;
+      out0[(o0 + q) * sout] = a0[q];
+      if (has1) out1[(o0 + q) * sout] = a1[q];
+    }
   }
 }
 
 // u~ = V^T (scale o y): y = B [NV][Nq] (destroyed) -> um [NV][Np] (separate buffer)
-template <int DIM, int N, int NV, int NT>
-__device__ __noinline__ void n2m_inplace(const PsiS& T, double* B, double* um, const double* scale) {
+template <int N>
+struct PsiL {  // psi tables at a shared-memory offset (layout of stage_psi)
+  const double *p1, *p2, *p3;
+  const int *pa1, *pa2, *poff;
+};
+template <int DIM, int N, int OPS>
+__device__ __forceinline__ PsiL<N> psi_at() {
+  constexpr int NPAIR = DIM == 2 ? N : N * (N + 1) / 2;
+  const double* p1 = smk2 + OPS;
+  const double* p2 = p1 + N * N;
+  const double* p3 = p2 + N * N * N;
+  const int* pi = (const int*)(p3 + (DIM == 3 ? N * N * N : 0));
+  return PsiL<N>{p1, p2, p3, pi, pi + NPAIR, pi + 2 * NPAIR};
+}
+
+// (shared-memory offsets in doubles; oSc < 0: no scale)
+template <int DIM, int N, int NV, int NT, int OPS>
+__device__ __noinline__ void n2m_inplace(int oB, int oU, int oSc) {
   using S = Sz<DIM, N>;
+  const PsiL<N> T = psi_at<DIM, N, OPS>();
+  double* B = smk2 + oB;
+  double* um = smk2 + oU;
+  const double* scale = oSc >= 0 ? smk2 + oSc : nullptr;
   constexpr int NPAIR = S::NPAIR, Np = S::Np, Nq = S::Nq, NVP = (NV + 1) / 2;
   const int tid = threadIdx.x;
   Fib2<N> F;
@@ -338,9 +368,12 @@ __device__ __noinline__ void n2m_inplace(const PsiS& T, double* B, double* um, c
 }
 
 // u = V u~: um [NV][Np] -> B [NV][Nq]
-template <int DIM, int N, int NV, int NT>
-__device__ __noinline__ void m2n_inplace(const PsiS& T, const double* um, double* B) {
+template <int DIM, int N, int NV, int NT, int OPS>
+__device__ __noinline__ void m2n_inplace(int oU, int oB) {
   using S = Sz<DIM, N>;
+  const PsiL<N> T = psi_at<DIM, N, OPS>();
+  const double* um = smk2 + oU;
+  double* B = smk2 + oB;
   constexpr int NPAIR = S::NPAIR, Np = S::Np, Nq = S::Nq, NVP = (NV + 1) / 2;
   const int tid = threadIdx.x;
   Fib2<N> F;
@@ -401,7 +434,6 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
   using W = Lw<DIM, N>;
   using L = Rhs2Smem<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf, NT = W::NT, NS = W::NS;
-  extern __shared__ __align__(16) double smk2[];
   __shared__ uint64_t barA, barB;  // element data for the passes / for the epilogue
   double* sP = smk2 + L::o_pr;  // [DIM+3][Nq]: rho, v_1..v_d, p, beta
   double* sG = smk2 + L::o_g;   // [NG][Nq]: G_lm at (l*DIM+m)
@@ -799,7 +831,7 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
     stamp(7);
 
     // ---- d u~/dt = V^T W/J~ V (V^T r), transforms in place in sR ----
-    n2m_inplace<DIM, N, NC, NT>(T, sR, sU, nullptr);
+    n2m_inplace<DIM, N, NC, NT, L::o_ps>(L::o_r, L::o_um, -1);
     stamp(8);
     if (A.mode == 5) {  // entropy production sum w~ . (V^T r) and conservation (V^T r)_0 / c0
       double loc = 0.0, la = 0.0;
@@ -831,9 +863,9 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
       }
       __syncthreads();
     }
-    m2n_inplace<DIM, N, NC, NT>(T, sU, sR);
+    m2n_inplace<DIM, N, NC, NT, L::o_ps>(L::o_um, L::o_r);
     stamp(9);
-    n2m_inplace<DIM, N, NC, NT>(T, sR, sU, sWJ);  // W / J~ fused into the loads
+    n2m_inplace<DIM, N, NC, NT, L::o_ps>(L::o_r, L::o_um, L::o_wj + L::WJOFF);  // W / J~ fused into the loads
     stamp(10);
     // f* and W / J~ are consumed: the next element's copies land during its passes
     if (tid == 0 && has_next) issue_B(elem_of(nidx));
