@@ -164,6 +164,17 @@ __host__ __device__ constexpr int psi_smem_doubles() {
   return N * N + N * N * N + (DIM == 3 ? N * N * N : 0) + (3 * (DIM == 2 ? N : N * (N + 1) / 2) + 1) / 2 + 1;
 }
 
+// the psi tables at `buf` (layout of stage_psi)
+template <int DIM, int N>
+__device__ __forceinline__ PsiS psi_tables(double* buf) {
+  constexpr int NPAIR = DIM == 2 ? N : N * (N + 1) / 2;
+  double* p1 = buf;
+  double* p2 = p1 + N * N;
+  double* p3 = p2 + N * N * N;
+  int* pi = (int*)(p3 + (DIM == 3 ? N * N * N : 0));
+  return PsiS{p1, p2, p3, pi, pi + NPAIR, pi + 2 * NPAIR};
+}
+
 // stage the tables of R into shared memory at `buf` (psi_smem_doubles<DIM,N>() doubles)
 template <int DIM, int N>
 __device__ PsiS stage_psi(const DevRef& R, double* buf) {

@@ -47,9 +47,9 @@ struct Rhs2Smem {
   // per element
   static constexpr int PR = ev2((DIM + 3) * S::Nq);  // rho, v, p, beta   (bulk copy of prim: PRS)
   static constexpr int GG = ev2(S::NG * S::Nq);      // G_lm              (bulk copy)
-  static constexpr int RR = ev2(S::NC * S::Nq);      // nodal residual r; in-place transform buffer
+  static constexpr int RR = ev2(S::NC * S::Nq);      // nodal residual r; first transform buffer
   static constexpr int PT = DIM == 3 ? S::NC * N * N * N : 0;  // facet-4 partial sums [v][j][a][c]
-  static constexpr int UM = ev2(S::NC * S::Np + (DIM == 3 ? S::NC * N * N : 0));  // modal result, facet-4 lift
+  static constexpr int UM = ev2(S::NC * S::Np) + (DIM == 3 ? S::NC * N * N : 0);  // modal result, facet-4 lift
   static constexpr int FP = S::Nf * S::NC * S::Nqf;  // facet states [z][rho, v, p][f] (bulk copy)
   static constexpr int FB = ev2(S::NF);              // facet beta = rho / p
   static constexpr int FJ = S::Nf * DIM * S::Nqf;    // J n at facet nodes [z][m][f] (bulk copy)
@@ -58,9 +58,11 @@ struct Rhs2Smem {
   static constexpr int WJ0 = ((S::NG * S::Nq) % 2 == 0) ? S::NG * S::Nq : (S::NG + 1) * S::Nq;  // first even row
   static constexpr int WJN = ((S::NG * S::Nq) % 2 == 0) ? 2 * S::Nq : ev2(S::Nq);                // doubles copied
   static constexpr int WJOFF = ((S::NG * S::Nq) % 2 == 0) ? S::Nq : 0;  // W / J~ within the copied rows
+  static constexpr int PB = PT > RR ? PT : RR;  // facet-4 partials, then the second transform buffer
+  static constexpr int SCU = SC > UM ? SC : UM;   // warp scratch, then modal result + facet-4 lifting
   static constexpr int o_tb = 0, o_ps = ev2(o_tb + TB), o_pr = ev2(o_ps + PS), o_g = o_pr + PR, o_r = ev2(o_g + GG),
-                       o_pt = ev2(o_r + RR), o_um = o_pt, o_fp = ev2(o_pt + (PT > UM ? PT : UM)), o_fb = ev2(o_fp + FP),
-                       o_fj = ev2(o_fb + FB), o_fs = ev2(o_fj + FJ), o_sc = ev2(o_fs + FS), o_wj = ev2(o_sc + SC),
+                       o_pt = ev2(o_r + RR), o_fp = ev2(o_pt + PB), o_fb = ev2(o_fp + FP),
+                       o_fj = ev2(o_fb + FB), o_fs = ev2(o_fj + FJ), o_sc = ev2(o_fs + FS), o_um = o_sc, o_wj = ev2(o_sc + SCU),
                        total = ev2(o_wj + WJN);
   static_assert(S::PRS <= PR, "prim copy");
   static_assert(total * 8 <= 227 * 1024 - 256, "shared memory");
@@ -231,215 +233,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
-// in-place sum-factorised transforms on one shared buffer B: every thread owns at
-// most one two-fiber item per step, loads its fibers into registers, the block synchronises, then
-// the item is contracted and stored over the (now dead) inputs.  Not inlined: the persistent
-// element loop would otherwise keep their loop-invariant addressing live through the flux passes.
-template <int N>
-struct Fib2 {
-  double x0[N], x1[N];
-};
-template <int N>
-__device__ __forceinline__ void fib_load(Fib2<N>& F, int ni, const double* in0, const double* in1, int sin,
-                                         const double* sc0, const double* sc1) {
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const bool ok = i < ni;
-    F.x0[i] = ok ? in0[i * sin] : 0.0;
-    F.x1[i] = ok ? in1[i * sin] : 0.0;
-    if (sc0) {
-      F.x0[i] *= ok ? sc0[i * sin] : 0.0;
-      F.x1[i] *= ok ? sc1[i * sin] : 0.0;
-    }
-  }
-}
-// outputs in chunks of OC, each accumulated over all inputs (independent FMA chains); the chunk
-// loop is not unrolled so that only one chunk's table entries are in flight (bounded registers)
-template <int N, bool TR>
-__device__ __forceinline__ void fib_store(const Fib2<N>& F, const double* ps, int no, double* out0, double* out1,
-                                          int sout, bool has1) {
-  constexpr int OC = 3;
-#pragma unroll 1
-  for (int o0 = 0; o0 < no; o0 += OC) {
-    double a0[OC], a1[OC];
-#pragma unroll
-    for (int q = 0; q < OC; ++q) a0[q] = a1[q] = 0.0;
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-#pragma unroll
-      for (int q = 0; q < OC; ++q) {
-        const int o = o0 + q < N ? o0 + q : N - 1;
-        const double pv = TR ? ps[o * N + i] : ps[i * N + o];
-        a0[q] = fma(pv, F.x0[i], a0[q]);
-        a1[q] = fma(pv, F.x1[i], a1[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < OC; ++q) {
-      if (o0 + q >= no) break;
-      out0[(o0 + q) * sout] = a0[q];
-      if (has1) out1[(o0 + q) * sout] = a1[q];
-    }
-  }
-}
+// mbarriers of the flux kernel: element data for the passes (A) / interface fluxes and W/J~ (B)
+__shared__ uint64_t k2_barA, k2_barB;
 
-// u~ = V^T (scale o y): y = B [NV][Nq] (destroyed) -> um [NV][Np] (separate buffer)
-template <int N>
-struct PsiL {  // psi tables at a shared-memory offset (layout of stage_psi)
-  const double *p1, *p2, *p3;
-  const int *pa1, *pa2, *poff;
-};
-template <int DIM, int N, int OPS>
-__device__ __forceinline__ PsiL<N> psi_at() {
-  constexpr int NPAIR = DIM == 2 ? N : N * (N + 1) / 2;
-  const double* p1 = smk2 + OPS;
-  const double* p2 = p1 + N * N;
-  const double* p3 = p2 + N * N * N;
-  const int* pi = (const int*)(p3 + (DIM == 3 ? N * N * N : 0));
-  return PsiL<N>{p1, p2, p3, pi, pi + NPAIR, pi + 2 * NPAIR};
-}
-
-// (shared-memory offsets in doubles; oSc < 0: no scale)
-template <int DIM, int N, int NV, int NT, int OPS>
-__device__ __noinline__ void n2m_inplace(int oB, int oU, int oSc) {
-  using S = Sz<DIM, N>;
-  const PsiL<N> T = psi_at<DIM, N, OPS>();
-  double* B = smk2 + oB;
-  double* um = smk2 + oU;
-  const double* scale = oSc >= 0 ? smk2 + oSc : nullptr;
-  constexpr int NPAIR = S::NPAIR, Np = S::Np, Nq = S::Nq, NVP = (NV + 1) / 2;
-  const int tid = threadIdx.x;
-  Fib2<N> F;
-  if constexpr (DIM == 2) {
-    constexpr int NFB = NV * N, I1 = (NFB + 1) / 2, I2 = N * NVP;
-    static_assert(I1 <= NT && I2 <= NT, "one item per thread");
-    // s1[v][a1][b] = sum_a psi1[a1][a] y[v][a + N b]
-    const int q0 = 2 * tid, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
-    const int v0 = q0 / N, b0 = q0 - v0 * N, v1 = q1 / N, b1 = q1 - v1 * N;
-    if (tid < I1)
-      fib_load<N>(F, N, B + v0 * Nq + N * b0, B + v1 * Nq + N * b1, 1, scale ? scale + N * b0 : nullptr,
-                  scale ? scale + N * b1 : nullptr);
-    __syncthreads();
-    if (tid < I1) fib_store<N, true>(F, T.p1, N, B + v0 * Nq + b0, B + v1 * Nq + b1, N, q1 != q0);
-    __syncthreads();
-    // u[v][off(a1)+a2] = sum_b psi2[a1][a2][b] s1[v][a1][b]
-    if (tid < I2) {
-      const int a1 = tid / NVP, w0 = 2 * (tid - a1 * NVP), w1 = w0 + 1 < NV ? w0 + 1 : w0;
-      fib_load<N>(F, N, B + w0 * Nq + a1 * N, B + w1 * Nq + a1 * N, 1, nullptr, nullptr);
-      fib_store<N, true>(F, T.p2 + a1 * N * N, N - a1, um + w0 * Np + T.poff[a1], um + w1 * Np + T.poff[a1], 1,
-                         w1 != w0);
-    }
-    __syncthreads();
-  } else {
-    constexpr int NFB = NV * N * N, I1 = (NFB + 1) / 2, NFC = NV * N, NPC = (NFC + 1) / 2, I2 = N * NPC,
-                  I3 = NPAIR * NVP;
-    static_assert(I1 <= NT && I2 <= NT && I3 <= NT, "one item per thread");
-    {  // s2[v][a1][bc] = sum_a psi1[a1][a] y[v][a + N bc]
-      const int q0 = 2 * tid, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
-      const int v0 = q0 / (N * N), bc0 = q0 - v0 * N * N, v1 = q1 / (N * N), bc1 = q1 - v1 * N * N;
-      if (tid < I1)
-        fib_load<N>(F, N, B + v0 * Nq + N * bc0, B + v1 * Nq + N * bc1, 1, scale ? scale + N * bc0 : nullptr,
-                    scale ? scale + N * bc1 : nullptr);
-      __syncthreads();
-      if (tid < I1) fib_store<N, true>(F, T.p1, N, B + v0 * Nq + bc0, B + v1 * Nq + bc1, N * N, q1 != q0);
-      __syncthreads();
-    }
-    {  // s1[v][pr(a1,a2)][c] = sum_b psi2[a1][a2][b] s2[v][a1][c][b]
-      const int a1 = tid / NPC, w = tid - a1 * NPC, q0 = 2 * w, q1 = q0 + 1 < NFC ? q0 + 1 : q0;
-      const int v0 = q0 / N, c0 = q0 - v0 * N, v1 = q1 / N, c1 = q1 - v1 * N;
-      const int prs = a1 * N - a1 * (a1 - 1) / 2;
-      if (tid < I2)
-        fib_load<N>(F, N, B + v0 * Nq + (a1 * N + c0) * N, B + v1 * Nq + (a1 * N + c1) * N, 1, nullptr, nullptr);
-      __syncthreads();
-      if (tid < I2)
-        fib_store<N, true>(F, T.p2 + a1 * N * N, N - a1, B + (v0 * NPAIR + prs) * N + c0,
-                           B + (v1 * NPAIR + prs) * N + c1, N, q1 != q0);
-      __syncthreads();
-    }
-    if (tid < I3) {  // u[v][off(pr)+a3] = sum_c psi3[s][a3][c] s1[v][pr][c]
-      const int pr = tid / NVP, w0 = 2 * (tid - pr * NVP), w1 = w0 + 1 < NV ? w0 + 1 : w0;
-      const int sdeg = T.pa1[pr] + T.pa2[pr];
-      fib_load<N>(F, N, B + (w0 * NPAIR + pr) * N, B + (w1 * NPAIR + pr) * N, 1, nullptr, nullptr);
-      fib_store<N, true>(F, T.p3 + sdeg * N * N, N - sdeg, um + w0 * Np + T.poff[pr], um + w1 * Np + T.poff[pr], 1,
-                         w1 != w0);
-    }
-    __syncthreads();
-  }
-}
-
-// u = V u~: um [NV][Np] -> B [NV][Nq]
-template <int DIM, int N, int NV, int NT, int OPS>
-__device__ __noinline__ void m2n_inplace(int oU, int oB) {
-  using S = Sz<DIM, N>;
-  const PsiL<N> T = psi_at<DIM, N, OPS>();
-  const double* um = smk2 + oU;
-  double* B = smk2 + oB;
-  constexpr int NPAIR = S::NPAIR, Np = S::Np, Nq = S::Nq, NVP = (NV + 1) / 2;
-  const int tid = threadIdx.x;
-  Fib2<N> F;
-  if constexpr (DIM == 2) {
-    constexpr int NFB = NV * N, I1 = N * NVP, I2 = (NFB + 1) / 2;
-    static_assert(I1 <= NT && I2 <= NT, "one item per thread");
-    if (tid < I1) {  // t1[v][a1][b] = sum_a2 psi2[a1][a2][b] u[v][off(a1)+a2]
-      const int a1 = tid / NVP, w0 = 2 * (tid - a1 * NVP), w1 = w0 + 1 < NV ? w0 + 1 : w0;
-      fib_load<N>(F, N - a1, um + w0 * Np + T.poff[a1], um + w1 * Np + T.poff[a1], 1, nullptr, nullptr);
-      fib_store<N, false>(F, T.p2 + a1 * N * N, N, B + w0 * Nq + a1 * N, B + w1 * Nq + a1 * N, 1, w1 != w0);
-    }
-    __syncthreads();
-    // u[v][a + N b] = sum_a1 psi1[a1][a] t1[v][a1][b]
-    const int q0 = 2 * tid, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
-    const int v0 = q0 / N, b0 = q0 - v0 * N, v1 = q1 / N, b1 = q1 - v1 * N;
-    if (tid < I2) fib_load<N>(F, N, B + v0 * Nq + b0, B + v1 * Nq + b1, N, nullptr, nullptr);
-    __syncthreads();
-    if (tid < I2) fib_store<N, false>(F, T.p1, N, B + v0 * Nq + N * b0, B + v1 * Nq + N * b1, 1, q1 != q0);
-    __syncthreads();
-  } else {
-    constexpr int I1 = NPAIR * NVP, NFC = NV * N, NPC = (NFC + 1) / 2, I2 = N * NPC, NFB = NV * N * N,
-                  I3 = (NFB + 1) / 2;
-    static_assert(I1 <= NT && I2 <= NT && I3 <= NT, "one item per thread");
-    if (tid < I1) {  // t1[v][pr][c] = sum_a3 psi3[s][a3][c] u[v][off(pr)+a3]
-      const int pr = tid / NVP, w0 = 2 * (tid - pr * NVP), w1 = w0 + 1 < NV ? w0 + 1 : w0;
-      const int sdeg = T.pa1[pr] + T.pa2[pr];
-      fib_load<N>(F, N - sdeg, um + w0 * Np + T.poff[pr], um + w1 * Np + T.poff[pr], 1, nullptr, nullptr);
-      fib_store<N, false>(F, T.p3 + sdeg * N * N, N, B + (w0 * NPAIR + pr) * N, B + (w1 * NPAIR + pr) * N, 1,
-                          w1 != w0);
-    }
-    __syncthreads();
-    {  // t2[v][a1][c][b] = sum_a2 psi2[a1][a2][b] t1[v][pr(a1,a2)][c]
-      const int a1 = tid / NPC, w = tid - a1 * NPC, q0 = 2 * w, q1 = q0 + 1 < NFC ? q0 + 1 : q0;
-      const int v0 = q0 / N, c0 = q0 - v0 * N, v1 = q1 / N, c1 = q1 - v1 * N;
-      const int prs = a1 * N - a1 * (a1 - 1) / 2;
-      if (tid < I2)
-        fib_load<N>(F, N - a1, B + (v0 * NPAIR + prs) * N + c0, B + (v1 * NPAIR + prs) * N + c1, N, nullptr, nullptr);
-      __syncthreads();
-      if (tid < I2)
-        fib_store<N, false>(F, T.p2 + a1 * N * N, N, B + v0 * Nq + (a1 * N + c0) * N, B + v1 * Nq + (a1 * N + c1) * N,
-                            1, q1 != q0);
-      __syncthreads();
-    }
-    {  // u[v][a + N bc] = sum_a1 psi1[a1][a] t2[v][a1][bc]
-      const int q0 = 2 * tid, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
-      const int v0 = q0 / (N * N), bc0 = q0 - v0 * N * N, v1 = q1 / (N * N), bc1 = q1 - v1 * N * N;
-      if (tid < I3) fib_load<N>(F, N, B + v0 * Nq + bc0, B + v1 * Nq + bc1, N * N, nullptr, nullptr);
-      __syncthreads();
-      if (tid < I3) fib_store<N, false>(F, T.p1, N, B + v0 * Nq + N * bc0, B + v1 * Nq + N * bc1, 1, q1 != q0);
-      __syncthreads();
-    }
-  }
-}
-
+// one element of the flux kernel (the body of the persistent loop)
 template <int DIM, int N>
-__global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsArgs A) {
+__device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsigned it) {
   using S = Sz<DIM, N>;
   using W = Lw<DIM, N>;
   using L = Rhs2Smem<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf, NT = W::NT, NS = W::NS;
-  __shared__ uint64_t barA, barB;  // element data for the passes / for the epilogue
   double* sP = smk2 + L::o_pr;  // [DIM+3][Nq]: rho, v_1..v_d, p, beta
   double* sG = smk2 + L::o_g;   // [NG][Nq]: G_lm at (l*DIM+m)
   double* sR = smk2 + L::o_r;   // [NC][Nq] nodal residual
   double* pt = smk2 + L::o_pt;  // [NC][N(j)][N(a)][N(c)] facet-4 partials
-  double* sU = smk2 + L::o_um;  // [NC][Np] modal result, then [NC][N][N] facet-4 lifting (aliases pt)
+  double* sU = smk2 + L::o_um;  // [NC][Np] modal result + [NC][N][N] facet-4 lifting (aliases the scratch)
   double* fP = smk2 + L::o_fp;  // [Nf][NC][Nqf] facet states rho, v, p
   double* fB = smk2 + L::o_fb;  // [Nf*Nqf] facet beta
   double* fJ = smk2 + L::o_fj;  // [Nf][DIM][Nqf] J n
@@ -468,23 +276,471 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
   auto issue_A = [&](int64_t e) {
     constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&barA, bP + bG + bF + bJ);
-    bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &barA);
-    bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &barA);
-    bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &barA);
-    bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &barA);
+    mbar_expect_tx(&k2_barA, bP + bG + bF + bJ);
+    bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &k2_barA);
+    bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &k2_barA);
+    bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &k2_barA);
+    bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &k2_barA);
   };
   auto issue_B = [&](int64_t e) {
     constexpr unsigned bS = L::FS * 8, bW = L::WJN * 8;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&barB, bS + bW);
-    bulk_g2s(fS, A.fstar + (size_t)e * L::FS, bS, &barB);
-    bulk_g2s(smk2 + L::o_wj, A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &barB);
+    mbar_expect_tx(&k2_barB, bS + bW);
+    bulk_g2s(fS, A.fstar + (size_t)e * L::FS, bS, &k2_barB);
+    bulk_g2s(smk2 + L::o_wj, A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barB);
+  };
+  const int grp = lane / N, pos = lane - grp * N;
+  const bool lane_ok = grp < W::LPW;
+  const int64_t e = elem_of(idx);
+  const int64_t nidx = idx + gridDim.x;
+  const bool has_next = nidx < A.n_elem;
+  const double* gv = A.geo_vol + (size_t)e * S::GVS;
+  // optional phase clock stamps (diagnostics, ES_PHASE_TIMING)
+  auto stamp = [&](int k) {
+    if (A.dbg && tid == 0 && idx < 4096) A.dbg[idx * 16 + k] = clock64();
+  };
+  stamp(0);
+  mbar_wait(&k2_barA, it & 1);
+  for (int i = tid; i < Nq; i += NT) sP[(DIM + 2) * Nq + i] = sP[i] / sP[(DIM + 1) * Nq + i];
+  for (int fz = tid; fz < NF; fz += NT) {
+    const double* q = fP + (fz / Nqf) * NC * Nqf + fz % Nqf;
+    fB[fz] = q[0] / q[(DIM + 1) * Nqf];
+  }
+  mbar_wait(&k2_barB, it & 1);  // f* is updated in place by the passes
+  __syncthreads();
+  stamp(1);
+
+  auto state_at = [&](int i) {
+    NodeState s;
+    s.r = sP[i];
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) s.v[m] = sP[(1 + m) * Nq + i];
+    s.p = sP[(DIM + 1) * Nq + i];
+    s.b = sP[(DIM + 2) * Nq + i];
+    return s;
+  };
+  auto Gat = [&](int l, int m, int i) { return sG[(l * DIM + m) * Nq + i]; };
+
+  // ---- direction passes, one specialisation per direction k ----
+  auto pass = [&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    constexpr int stride = k == 0 ? 1 : (k == 1 ? N : N * N);
+#pragma unroll 1
+    for (int slot = warp; slot < W::SLOTS; slot += W::NW) {
+      const int Lidx = slot * W::LPW + grp;
+      const bool valid = lane_ok && Lidx < W::NL;
+      const int l0 = valid ? Lidx % N : 0, l1 = valid ? Lidx / N : 0;
+      // node coordinates (a, b, c) and index
+      int ca, cb, cc;
+      if (k == 0) {
+        ca = pos;
+        cb = l0;
+        cc = l1;
+      } else if (k == 1) {
+        ca = l0;
+        cb = pos;
+        cc = l1;
+      } else {
+        ca = l0;
+        cb = l1;
+        cc = pos;
+      }
+      if constexpr (DIM == 2) cc = 0;
+      const int i = valid ? ca + N * cb + N * N * cc : 0;
+      const double vmask = valid ? 1.0 : 0.0;
+      NodeState me = state_at(i);
+      double gl[3][3];  // own metric rows g^(l)
+#pragma unroll
+      for (int l = 0; l < DIM; ++l)
+#pragma unroll
+        for (int m = 0; m < DIM; ++m) gl[l][m] = Gat(l, m, i);
+      double acc[NC];
+#pragma unroll
+      for (int v = 0; v < NC; ++v) acc[v] = 0.0;
+
+      // -- volume pairs on this line: shifts in batches of VB (ILP), exchanged by shuffles --
+#pragma unroll
+      for (int s0 = 1; s0 <= NS; s0 += W::VB) {
+        Job<DIM> jv[W::VB];
+#pragma unroll
+        for (int t = 0; t < W::VB; ++t) {
+          const int s = s0 + t;
+          int pos2 = pos + (s <= NS ? s : 0);
+          if (pos2 >= N) pos2 -= N;
+          const int j = valid ? i + (pos2 - pos) * stride : 0;
+          const int ix = pos * N + pos2;
+          Job<DIM>& jb = jv[t];
+          jb.base = sP;
+          jb.bb = sP + (DIM + 2) * Nq;
+          jb.stride = Nq;
+          jb.idx = j;
+          const bool half = (N % 2 == 0) && (s == NS);
+          const double mk = (s <= NS && !(half && pos >= N / 2)) ? vmask : 0.0;
+          if constexpr (DIM == 2) {
+            if (k == 0) {
+              const double cl = mk * tw[cb], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
+#pragma unroll
+              for (int m = 0; m < 2; ++m) jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * (gl[1][m] + Gat(1, m, j));
+            } else {
+              const double a2 = mk * tw[ca] * tA2[ix];
+#pragma unroll
+              for (int m = 0; m < 2; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j));
+            }
+          } else {
+            if (k == 0) {
+              const double cl = mk * 0.5 * tw[cb] * tw3[cc], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
+#pragma unroll
+              for (int m = 0; m < 3; ++m)
+                jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * ((gl[1][m] + gl[2][m]) + (Gat(1, m, j) + Gat(2, m, j)));
+            } else if (k == 1) {
+              const double cl = mk * 0.5 * tw[ca] * tw3[cc], a2 = cl * tA2[ix], a3 = cl * tA3[ix];
+#pragma unroll
+              for (int m = 0; m < 3; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j)) + a3 * (gl[2][m] + Gat(2, m, j));
+            } else {
+              const double a4 = mk * 0.125 * tw[ca] * tw[cb] * (1.0 - teta[cb]) * tA4[ix];
+#pragma unroll
+              for (int m = 0; m < 3; ++m) jb.n[m] = a4 * (gl[2][m] + Gat(2, m, j));
+            }
+          }
+        }
+        double Fs[W::VB][NC];
+        flux_batch<DIM, W::VB>(me, jv, gm1inv, Fs);
+#pragma unroll
+        for (int t = 0; t < W::VB; ++t) {
+          const int s = s0 + t;
+          if (s > NS) break;
+          int pos0 = pos - s;
+          if (pos0 < 0) pos0 += N;
+          const int src = grp * N + pos0;
+#pragma unroll
+          for (int v = 0; v < NC; ++v) acc[v] += shfl_d(Fs[t][v], src) - Fs[t][v];  // masked jobs send 0
+        }
+      }
+
+      // -- facet-correction pairs along the same lines --
+      // a facet job: state of facet node (z, f), normal coef (G_i^T nhat + J n_f)/2 with coefficient
+      // coef = (R^T B)_if
+      auto fjob = [&](Job<DIM>& jb, int z, int f, double coef, const double* gtn) {
+        jb.base = fP + z * NC * Nqf;
+        jb.bb = fB + z * Nqf;
+        jb.stride = Nqf;
+        jb.idx = f;
+        const double c2 = 0.5 * coef * vmask;
+#pragma unroll
+        for (int m = 0; m < DIM; ++m) jb.n[m] = c2 * (gtn[m] + fJ[(z * DIM + m) * Nqf + f]);
+      };
+      // facet-side sums over each line group through the warp scratch, in lane order; dest(line, v)
+      // returns where the sum of line `gq` goes (nullptr: discard)
+      auto line_sums = [&](const double* Fc, auto dest) {
+#pragma unroll
+        for (int v = 0; v < NC; ++v) {
+          acc[v] -= Fc[v];
+          scr[v * 32 + lane] = Fc[v];
+        }
+        __syncwarp();
+        for (int sidx = lane; sidx < W::LPW * NC; sidx += 32) {
+          const int gq = sidx / NC, v = sidx - gq * NC;
+          const double* src = scr + v * 32 + gq * N;
+          double tv[N];  // pairwise tree sum, depth ceil(log2 N)
+#pragma unroll
+          for (int a = 0; a < N; ++a) tv[a] = src[a];
+#pragma unroll
+          for (int w = 1; w < N; w *= 2)
+#pragma unroll
+            for (int a = 0; a + w < N; a += 2 * w) tv[a] += tv[a + w];
+          const double sum = tv[0];
+          const int Lq = slot * W::LPW + gq;
+          if (Lq < W::NL) {
+            double* d = dest(Lq, v);
+            if (d) *d -= sum;  // s = B J_f f* - C^T 1
+          }
+        }
+        __syncwarp();
+      };
+      if constexpr (DIM == 2) {
+        Job<DIM> jf[2];
+        if (k == 0) {  // eta1 = +1 (facet 2) and eta1 = -1 (facet 3): facet node b
+          const double r2 = 0.70710678118654752440;
+          double gtn[2] = {(gl[0][0] + gl[1][0]) * r2, (gl[0][1] + gl[1][1]) * r2};
+          double gtn3[2] = {-gl[0][0], -gl[0][1]};
+          fjob(jf[0], 1, cb, tlR[ca] * tB[1 * Nqf + cb], gtn);
+          fjob(jf[1], 2, cb, tlL[ca] * tB[2 * Nqf + cb], gtn3);
+          double Fc[2][NC];
+          flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
+          line_sums(Fc[0], [&](int Lq, int v) { return fS + (1 * NC + v) * Nqf + Lq; });
+          line_sums(Fc[1], [&](int Lq, int v) { return fS + (2 * NC + v) * Nqf + Lq; });
+        } else {  // eta2 = -1 (facet 1): facet node a
+          double gtn[2] = {-gl[1][0], -gl[1][1]};
+          fjob(jf[0], 0, ca, tlL[cb] * tB[0 * Nqf + ca], gtn);
+          double Fc[1][NC];
+          flux_batch<DIM, 1>(me, jf, gm1inv, Fc);
+          line_sums(Fc[0], [&](int Lq, int v) { return fS + (0 * NC + v) * Nqf + Lq; });
+        }
+      } else {
+        if (k == 0) {  // facets 2 and 3 (eta1 = +1 / -1): facet node (b, c) = line index
+          const double r3 = 0.57735026918962576451;
+          const int f = cb + N * cc;
+          double gtn[3], gtn3[3];
+#pragma unroll
+          for (int m = 0; m < 3; ++m) {
+            gtn[m] = (gl[0][m] + gl[1][m] + gl[2][m]) * r3;
+            gtn3[m] = -gl[0][m];
+          }
+          Job<DIM> jf[2];
+          fjob(jf[0], 1, f, tlR[ca] * tB[1 * Nqf + f], gtn);
+          fjob(jf[1], 2, f, tlL[ca] * tB[2 * Nqf + f], gtn3);
+          double Fc[2][NC];
+          flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
+          line_sums(Fc[0], [&](int Lq, int v) { return fS + (1 * NC + v) * Nqf + Lq; });
+          line_sums(Fc[1], [&](int Lq, int v) { return fS + (2 * NC + v) * Nqf + Lq; });
+        } else if (k == 1) {  // facet 1 (eta2 = -1): node (a, c) = line; facet 4 (eta3 = -1): nodes (a, j)
+          const int f = ca + N * cc;
+          double gtn[3] = {-gl[1][0], -gl[1][1], -gl[1][2]};
+          double gt4[3] = {-gl[2][0], -gl[2][1], -gl[2][2]};
+          {  // facet 1: one job per lane, summed over the line
+            Job<DIM> j1[1];
+            fjob(j1[0], 0, f, tlL[cb] * tB[0 * Nqf + f], gtn);
+            double F1[1][NC];
+            flux_batch<DIM, 1>(me, j1, gm1inv, F1);
+            line_sums(F1[0], [&](int Lq, int v) { return fS + (0 * NC + v) * Nqf + Lq; });
+          }
+          // facet 4, rotating schedule: at step t lane pos pairs its node (a, b = pos, c) with the
+          // facet node (a, j = (pos + t) mod N); the facet-side value travels by shuffle to lane j,
+          // which accumulates the sum over b of its facet node (no reduction tree, no scratch)
+          double facc[NC];
+#pragma unroll
+          for (int v = 0; v < NC; ++v) facc[v] = 0.0;
+#pragma unroll 1
+          for (int t0 = 0; t0 < N; t0 += 2) {
+            Job<DIM> jq[2];
+#pragma unroll
+            for (int tt = 0; tt < 2; ++tt) {
+              const int t = t0 + tt;
+              int jf = pos + (t < N ? t : 0);
+              if (jf >= N) jf -= N;
+              const int f4 = ca + N * jf;
+              fjob(jq[tt], 3, f4, t < N ? tli4[jf * N + cb] * tl3[cc] * tB[3 * Nqf + f4] : 0.0, gt4);
+            }
+            double Fb[2][NC];
+            flux_batch<DIM, 2>(me, jq, gm1inv, Fb);
+#pragma unroll
+            for (int tt = 0; tt < 2; ++tt) {
+              const int t = t0 + tt;
+              if (t >= N) break;
+              int p0 = pos - t;
+              if (p0 < 0) p0 += N;
+              const int src = grp * N + p0;
+#pragma unroll
+              for (int v = 0; v < NC; ++v) {
+                acc[v] -= Fb[tt][v];
+                facc[v] += shfl_d(Fb[tt][v], src);
+              }
+            }
+          }
+          if (valid)  // partial over b of facet node (a, j = pos) on line c
+#pragma unroll
+            for (int v = 0; v < NC; ++v) pt[((v * N + pos) * N + ca) * N + cc] = facc[v];
+        }
+      }
+      // -- residual of this pass (exclusive owner of node i within the pass) --
+      if (valid) {
+#pragma unroll
+        for (int v = 0; v < NC; ++v) {
+          if (k == 0)
+            sR[v * Nq + i] = acc[v];
+          else
+            sR[v * Nq + i] += acc[v];
+        }
+      }
+    }
+    __syncthreads();
+    stamp(2 + k);
+  };
+  pass(std::integral_constant<int, 0>{});
+  pass(std::integral_constant<int, 1>{});
+  if constexpr (DIM == 3) pass(std::integral_constant<int, 2>{});
+  // states, metrics and facet inputs are dead: the next element's copies land during the epilogue
+  if (tid == 0 && has_next) issue_A(elem_of(nidx));
+  if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
+    for (int q = tid; q < NC * N * N; q += NT) {
+      const int v = q / (N * N), jf = (q / N) % N, a = q % N;
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < N; ++c) s += pt[((v * N + jf) * N + a) * N + c];
+      fS[(3 * NC + v) * Nqf + a + N * jf] -= s;
+    }
+    __syncthreads();
+  }
+  stamp(5);
+  // ---- lifting r -= R^T s; facet 4 sum-factorised: t4[v][a][b] = sum_j l_b(eta3_j) s4[v][a + N j] ----
+  if constexpr (DIM == 3) {
+    double* t4 = sU + L::UM - NC * N * N;
+    for (int q = tid; q < NC * N * N; q += NT) {
+      const int v = q / (N * N), b = (q / N) % N, a = q % N;
+      const double* s4 = fS + (3 * NC + v) * Nqf + a;
+      double t = 0.0;
+#pragma unroll
+      for (int jf = 0; jf < N; ++jf) t = fma(tli4[jf * N + b], s4[N * jf], t);
+      t4[(v * N + b) * N + a] = t;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < Nq; i += NT) {
+    const int a = i % N, b = (i / N) % N, c = DIM == 3 ? i / (N * N) : 0;
+#pragma unroll
+    for (int v = 0; v < NC; ++v) {
+      double t;
+      if constexpr (DIM == 2) {
+        t = tlL[b] * fS[(0 * NC + v) * Nqf + a] + tlR[a] * fS[(1 * NC + v) * Nqf + b] +
+            tlL[a] * fS[(2 * NC + v) * Nqf + b];
+      } else {
+        const double* t4 = sU + ev2(NC * Np);
+        t = tlL[b] * fS[(0 * NC + v) * Nqf + a + N * c] + tlR[a] * fS[(1 * NC + v) * Nqf + b + N * c] +
+            tlL[a] * fS[(2 * NC + v) * Nqf + b + N * c] + tl3[c] * t4[(v * N + b) * N + a];
+      }
+      sR[v * Nq + i] -= t;
+    }
+  }
+  __syncthreads();
+  stamp(7);
+
+  // ---- d u~/dt = V^T W/J~ V (V^T r), transforms in place in sR ----
+  // ping-pong between sR and the dead facet-4 partial buffer pt (both [NC][Nq]); 3D steps may
+  // write their second scratch over the already consumed input
+  const PsiS T = psi_tables<DIM, N>(smk2 + L::o_ps);
+  if constexpr (DIM == 3)
+    nodal_to_modal<DIM, N, NC>(T, sR, sU, sR, pt);
+  else
+    nodal_to_modal<DIM, N, NC>(T, sR, sU, pt, nullptr);
+  stamp(8);
+  if (A.mode == 5) {  // entropy production sum w~ . (V^T r) and conservation (V^T r)_0 / c0
+    double loc = 0.0, la = 0.0;
+    for (int k = tid; k < NC * Np; k += NT) {
+      double t = A.wt[(size_t)e * NC * Np + k] * sU[k];
+      loc += t;
+      la += fabs(t);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      loc += __shfl_down_sync(0xffffffffu, loc, o);
+      la += __shfl_down_sync(0xffffffffu, la, o);
+    }
+    __shared__ double red[2][W::NW];
+    if (lane == 0) {
+      red[0][warp] = loc;
+      red[1][warp] = la;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int wv = 0; wv < W::NW; ++wv) {
+        s0 += red[0][wv];
+        s1 += red[1][wv];
+      }
+      double* pe2 = A.part + (size_t)e * (2 + NC);
+      pe2[0] = s0;
+      pe2[1] = s1;
+      for (int v = 0; v < NC; ++v) pe2[2 + v] = sU[v * Np] / A.c0;
+    }
+    __syncthreads();
+  }
+  if constexpr (DIM == 3)
+    modal_to_nodal<DIM, N, NC>(T, sU, pt, pt, sR);
+  else
+    modal_to_nodal<DIM, N, NC>(T, sU, pt, sR, nullptr);
+  stamp(9);
+  if constexpr (DIM == 3)
+    nodal_to_modal<DIM, N, NC>(T, pt, sU, pt, sR, sWJ);  // W / J~ fused into the loads
+  else
+    nodal_to_modal<DIM, N, NC>(T, pt, sU, sR, nullptr, sWJ);
+  stamp(10);
+  // f* and W / J~ are consumed: the next element's copies land during its passes
+  if (tid == 0 && has_next) issue_B(elem_of(nidx));
+  const size_t base = (size_t)e * NC * Np;
+  const double dt = A.dt;
+  for (int kk = tid; kk < NC * Np; kk += NT) {
+    double du = sU[kk];
+    switch (A.mode) {
+      case 0:
+      case 5:
+        A.out[base + kk] = du;
+        break;
+      case 1:  // classical RK4 stage 1 (R17)
+        A.acc[base + kk] = A.u0[base + kk] + (dt / 6.0) * du;
+        A.ustage[base + kk] = A.u0[base + kk] + (0.5 * dt) * du;
+        break;
+      case 2:
+        A.acc[base + kk] += (dt / 3.0) * du;
+        A.ustage[base + kk] = A.u0[base + kk] + (0.5 * dt) * du;
+        break;
+      case 3:
+        A.acc[base + kk] += (dt / 3.0) * du;
+        A.ustage[base + kk] = A.u0[base + kk] + dt * du;
+        break;
+      case 4:
+        A.out[base + kk] = A.acc[base + kk] + (dt / 6.0) * du;
+        break;
+    }
+  }
+  __syncthreads();  // sU / sR are reused by the next element
+  stamp(11);
+}
+
+template <int DIM, int N>
+__global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
+  using S = Sz<DIM, N>;
+  using W = Lw<DIM, N>;
+  using L = Rhs2Smem<DIM, N>;
+  constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf, NT = W::NT, NS = W::NS;
+  double* sP = smk2 + L::o_pr;  // [DIM+3][Nq]: rho, v_1..v_d, p, beta
+  double* sG = smk2 + L::o_g;   // [NG][Nq]: G_lm at (l*DIM+m)
+  double* sR = smk2 + L::o_r;   // [NC][Nq] nodal residual
+  double* pt = smk2 + L::o_pt;  // [NC][N(j)][N(a)][N(c)] facet-4 partials
+  double* sU = smk2 + L::o_um;  // [NC][Np] modal result + [NC][N][N] facet-4 lifting (aliases the scratch)
+  double* fP = smk2 + L::o_fp;  // [Nf][NC][Nqf] facet states rho, v, p
+  double* fB = smk2 + L::o_fb;  // [Nf*Nqf] facet beta
+  double* fJ = smk2 + L::o_fj;  // [Nf][DIM][Nqf] J n
+  double* fS = smk2 + L::o_fs;  // [Nf][NC][Nqf] B J_f f*, then s = B J_f f* - C^T 1
+  double* sWJ = smk2 + L::o_wj + L::WJOFF;  // [Nq] W / J~
+  double* tb = smk2 + L::o_tb;
+  double* tQ1 = tb;
+  double* tA1 = tQ1 + N * N;
+  double* tA2 = tA1 + N * N;
+  double* tA3 = tA2 + N * N;
+  double* tA4 = tA3 + N * N;
+  double* tw = tA4 + N * N;
+  double* tw3 = tw + N;
+  double* teta = tw3 + N;
+  double* tlL = teta + N;
+  double* tlR = tlL + N;
+  double* tl3 = tlR + N;
+  double* tli4 = tl3 + N;
+  double* tB = tli4 + N * N;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* scr = smk2 + L::o_sc + warp * NC * 32;
+  const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
+  auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
+  // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers
+  auto issue_A = [&](int64_t e) {
+    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&k2_barA, bP + bG + bF + bJ);
+    bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &k2_barA);
+    bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &k2_barA);
+    bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &k2_barA);
+    bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &k2_barA);
+  };
+  auto issue_B = [&](int64_t e) {
+    constexpr unsigned bS = L::FS * 8, bW = L::WJN * 8;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&k2_barB, bS + bW);
+    bulk_g2s(fS, A.fstar + (size_t)e * L::FS, bS, &k2_barB);
+    bulk_g2s(smk2 + L::o_wj, A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barB);
   };
   // ---- per-CTA: barriers, first element's copies, constant tables ----
   if (tid == 0) {
-    mbar_init(&barA, 1);
-    mbar_init(&barB, 1);
+    mbar_init(&k2_barA, 1);
+    mbar_init(&k2_barB, 1);
     if ((int64_t)blockIdx.x < A.n_elem) {
       issue_A(elem_of(blockIdx.x));
       issue_B(elem_of(blockIdx.x));
@@ -512,392 +768,8 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, RhsAr
   const PsiS T = stage_psi<DIM, N>(R, smk2 + L::o_ps);
   __syncthreads();  // mbarriers initialised and tables staged before anyone uses them
 
-  const int grp = lane / N, pos = lane - grp * N;
-  const bool lane_ok = grp < W::LPW;
-  unsigned it = 0;
 #pragma unroll 1
-  for (int64_t idx = blockIdx.x; idx < A.n_elem; idx += gridDim.x, ++it) {
-    const int64_t e = elem_of(idx);
-    const int64_t nidx = idx + gridDim.x;
-    const bool has_next = nidx < A.n_elem;
-    const double* gv = A.geo_vol + (size_t)e * S::GVS;
-    // optional phase clock stamps (diagnostics, ES_PHASE_TIMING)
-    auto stamp = [&](int k) {
-      if (A.dbg && tid == 0 && idx < 4096) A.dbg[idx * 16 + k] = clock64();
-    };
-    stamp(0);
-    mbar_wait(&barA, it & 1);
-    for (int i = tid; i < Nq; i += NT) sP[(DIM + 2) * Nq + i] = sP[i] / sP[(DIM + 1) * Nq + i];
-    for (int fz = tid; fz < NF; fz += NT) {
-      const double* q = fP + (fz / Nqf) * NC * Nqf + fz % Nqf;
-      fB[fz] = q[0] / q[(DIM + 1) * Nqf];
-    }
-    mbar_wait(&barB, it & 1);  // f* is updated in place by the passes
-    __syncthreads();
-    stamp(1);
-
-    auto state_at = [&](int i) {
-      NodeState s;
-      s.r = sP[i];
-#pragma unroll
-      for (int m = 0; m < DIM; ++m) s.v[m] = sP[(1 + m) * Nq + i];
-      s.p = sP[(DIM + 1) * Nq + i];
-      s.b = sP[(DIM + 2) * Nq + i];
-      return s;
-    };
-    auto Gat = [&](int l, int m, int i) { return sG[(l * DIM + m) * Nq + i]; };
-
-    // ---- direction passes, one specialisation per direction k ----
-    auto pass = [&](auto kc) {
-      constexpr int k = decltype(kc)::value;
-      constexpr int stride = k == 0 ? 1 : (k == 1 ? N : N * N);
-  #pragma unroll 1
-      for (int slot = warp; slot < W::SLOTS; slot += W::NW) {
-        const int Lidx = slot * W::LPW + grp;
-        const bool valid = lane_ok && Lidx < W::NL;
-        const int l0 = valid ? Lidx % N : 0, l1 = valid ? Lidx / N : 0;
-        // node coordinates (a, b, c) and index
-        int ca, cb, cc;
-        if (k == 0) {
-          ca = pos;
-          cb = l0;
-          cc = l1;
-        } else if (k == 1) {
-          ca = l0;
-          cb = pos;
-          cc = l1;
-        } else {
-          ca = l0;
-          cb = l1;
-          cc = pos;
-        }
-        if constexpr (DIM == 2) cc = 0;
-        const int i = valid ? ca + N * cb + N * N * cc : 0;
-        const double vmask = valid ? 1.0 : 0.0;
-        NodeState me = state_at(i);
-        double gl[3][3];  // own metric rows g^(l)
-  #pragma unroll
-        for (int l = 0; l < DIM; ++l)
-  #pragma unroll
-          for (int m = 0; m < DIM; ++m) gl[l][m] = Gat(l, m, i);
-        double acc[NC];
-  #pragma unroll
-        for (int v = 0; v < NC; ++v) acc[v] = 0.0;
-
-        // -- volume pairs on this line: shifts in batches of VB (ILP), exchanged by shuffles --
-  #pragma unroll
-        for (int s0 = 1; s0 <= NS; s0 += W::VB) {
-          Job<DIM> jv[W::VB];
-  #pragma unroll
-          for (int t = 0; t < W::VB; ++t) {
-            const int s = s0 + t;
-            int pos2 = pos + (s <= NS ? s : 0);
-            if (pos2 >= N) pos2 -= N;
-            const int j = valid ? i + (pos2 - pos) * stride : 0;
-            const int ix = pos * N + pos2;
-            Job<DIM>& jb = jv[t];
-            jb.base = sP;
-            jb.bb = sP + (DIM + 2) * Nq;
-            jb.stride = Nq;
-            jb.idx = j;
-            const bool half = (N % 2 == 0) && (s == NS);
-            const double mk = (s <= NS && !(half && pos >= N / 2)) ? vmask : 0.0;
-            if constexpr (DIM == 2) {
-              if (k == 0) {
-                const double cl = mk * tw[cb], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
-  #pragma unroll
-                for (int m = 0; m < 2; ++m) jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * (gl[1][m] + Gat(1, m, j));
-              } else {
-                const double a2 = mk * tw[ca] * tA2[ix];
-  #pragma unroll
-                for (int m = 0; m < 2; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j));
-              }
-            } else {
-              if (k == 0) {
-                const double cl = mk * 0.5 * tw[cb] * tw3[cc], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
-  #pragma unroll
-                for (int m = 0; m < 3; ++m)
-                  jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * ((gl[1][m] + gl[2][m]) + (Gat(1, m, j) + Gat(2, m, j)));
-              } else if (k == 1) {
-                const double cl = mk * 0.5 * tw[ca] * tw3[cc], a2 = cl * tA2[ix], a3 = cl * tA3[ix];
-  #pragma unroll
-                for (int m = 0; m < 3; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j)) + a3 * (gl[2][m] + Gat(2, m, j));
-              } else {
-                const double a4 = mk * 0.125 * tw[ca] * tw[cb] * (1.0 - teta[cb]) * tA4[ix];
-  #pragma unroll
-                for (int m = 0; m < 3; ++m) jb.n[m] = a4 * (gl[2][m] + Gat(2, m, j));
-              }
-            }
-          }
-          double Fs[W::VB][NC];
-          flux_batch<DIM, W::VB>(me, jv, gm1inv, Fs);
-  #pragma unroll
-          for (int t = 0; t < W::VB; ++t) {
-            const int s = s0 + t;
-            if (s > NS) break;
-            int pos0 = pos - s;
-            if (pos0 < 0) pos0 += N;
-            const int src = grp * N + pos0;
-  #pragma unroll
-            for (int v = 0; v < NC; ++v) acc[v] += shfl_d(Fs[t][v], src) - Fs[t][v];  // masked jobs send 0
-          }
-        }
-
-        // -- facet-correction pairs along the same lines --
-        // a facet job: state of facet node (z, f), normal coef (G_i^T nhat + J n_f)/2 with coefficient
-        // coef = (R^T B)_if
-        auto fjob = [&](Job<DIM>& jb, int z, int f, double coef, const double* gtn) {
-          jb.base = fP + z * NC * Nqf;
-          jb.bb = fB + z * Nqf;
-          jb.stride = Nqf;
-          jb.idx = f;
-          const double c2 = 0.5 * coef * vmask;
-  #pragma unroll
-          for (int m = 0; m < DIM; ++m) jb.n[m] = c2 * (gtn[m] + fJ[(z * DIM + m) * Nqf + f]);
-        };
-        // facet-side sums over each line group through the warp scratch, in lane order; dest(line, v)
-        // returns where the sum of line `gq` goes (nullptr: discard)
-        auto line_sums = [&](const double* Fc, auto dest) {
-  #pragma unroll
-          for (int v = 0; v < NC; ++v) {
-            acc[v] -= Fc[v];
-            scr[v * 32 + lane] = Fc[v];
-          }
-          __syncwarp();
-          for (int sidx = lane; sidx < W::LPW * NC; sidx += 32) {
-            const int gq = sidx / NC, v = sidx - gq * NC;
-            const double* src = scr + v * 32 + gq * N;
-            double tv[N];  // pairwise tree sum, depth ceil(log2 N)
-  #pragma unroll
-            for (int a = 0; a < N; ++a) tv[a] = src[a];
-  #pragma unroll
-            for (int w = 1; w < N; w *= 2)
-  #pragma unroll
-              for (int a = 0; a + w < N; a += 2 * w) tv[a] += tv[a + w];
-            const double sum = tv[0];
-            const int Lq = slot * W::LPW + gq;
-            if (Lq < W::NL) {
-              double* d = dest(Lq, v);
-              if (d) *d -= sum;  // s = B J_f f* - C^T 1
-            }
-          }
-          __syncwarp();
-        };
-        if constexpr (DIM == 2) {
-          Job<DIM> jf[2];
-          if (k == 0) {  // eta1 = +1 (facet 2) and eta1 = -1 (facet 3): facet node b
-            const double r2 = 0.70710678118654752440;
-            double gtn[2] = {(gl[0][0] + gl[1][0]) * r2, (gl[0][1] + gl[1][1]) * r2};
-            double gtn3[2] = {-gl[0][0], -gl[0][1]};
-            fjob(jf[0], 1, cb, tlR[ca] * tB[1 * Nqf + cb], gtn);
-            fjob(jf[1], 2, cb, tlL[ca] * tB[2 * Nqf + cb], gtn3);
-            double Fc[2][NC];
-            flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
-            line_sums(Fc[0], [&](int Lq, int v) { return fS + (1 * NC + v) * Nqf + Lq; });
-            line_sums(Fc[1], [&](int Lq, int v) { return fS + (2 * NC + v) * Nqf + Lq; });
-          } else {  // eta2 = -1 (facet 1): facet node a
-            double gtn[2] = {-gl[1][0], -gl[1][1]};
-            fjob(jf[0], 0, ca, tlL[cb] * tB[0 * Nqf + ca], gtn);
-            double Fc[1][NC];
-            flux_batch<DIM, 1>(me, jf, gm1inv, Fc);
-            line_sums(Fc[0], [&](int Lq, int v) { return fS + (0 * NC + v) * Nqf + Lq; });
-          }
-        } else {
-          if (k == 0) {  // facets 2 and 3 (eta1 = +1 / -1): facet node (b, c) = line index
-            const double r3 = 0.57735026918962576451;
-            const int f = cb + N * cc;
-            double gtn[3], gtn3[3];
-  #pragma unroll
-            for (int m = 0; m < 3; ++m) {
-              gtn[m] = (gl[0][m] + gl[1][m] + gl[2][m]) * r3;
-              gtn3[m] = -gl[0][m];
-            }
-            Job<DIM> jf[2];
-            fjob(jf[0], 1, f, tlR[ca] * tB[1 * Nqf + f], gtn);
-            fjob(jf[1], 2, f, tlL[ca] * tB[2 * Nqf + f], gtn3);
-            double Fc[2][NC];
-            flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
-            line_sums(Fc[0], [&](int Lq, int v) { return fS + (1 * NC + v) * Nqf + Lq; });
-            line_sums(Fc[1], [&](int Lq, int v) { return fS + (2 * NC + v) * Nqf + Lq; });
-          } else if (k == 1) {  // facet 1 (eta2 = -1): node (a, c) = line; facet 4 (eta3 = -1): nodes (a, j)
-            const int f = ca + N * cc;
-            double gtn[3] = {-gl[1][0], -gl[1][1], -gl[1][2]};
-            double gt4[3] = {-gl[2][0], -gl[2][1], -gl[2][2]};
-            {  // facet 1: one job per lane, summed over the line
-              Job<DIM> j1[1];
-              fjob(j1[0], 0, f, tlL[cb] * tB[0 * Nqf + f], gtn);
-              double F1[1][NC];
-              flux_batch<DIM, 1>(me, j1, gm1inv, F1);
-              line_sums(F1[0], [&](int Lq, int v) { return fS + (0 * NC + v) * Nqf + Lq; });
-            }
-            // facet 4, rotating schedule: at step t lane pos pairs its node (a, b = pos, c) with the
-            // facet node (a, j = (pos + t) mod N); the facet-side value travels by shuffle to lane j,
-            // which accumulates the sum over b of its facet node (no reduction tree, no scratch)
-            double facc[NC];
-  #pragma unroll
-            for (int v = 0; v < NC; ++v) facc[v] = 0.0;
-  #pragma unroll 1
-            for (int t0 = 0; t0 < N; t0 += 2) {
-              Job<DIM> jq[2];
-  #pragma unroll
-              for (int tt = 0; tt < 2; ++tt) {
-                const int t = t0 + tt;
-                int jf = pos + (t < N ? t : 0);
-                if (jf >= N) jf -= N;
-                const int f4 = ca + N * jf;
-                fjob(jq[tt], 3, f4, t < N ? tli4[jf * N + cb] * tl3[cc] * tB[3 * Nqf + f4] : 0.0, gt4);
-              }
-              double Fb[2][NC];
-              flux_batch<DIM, 2>(me, jq, gm1inv, Fb);
-  #pragma unroll
-              for (int tt = 0; tt < 2; ++tt) {
-                const int t = t0 + tt;
-                if (t >= N) break;
-                int p0 = pos - t;
-                if (p0 < 0) p0 += N;
-                const int src = grp * N + p0;
-  #pragma unroll
-                for (int v = 0; v < NC; ++v) {
-                  acc[v] -= Fb[tt][v];
-                  facc[v] += shfl_d(Fb[tt][v], src);
-                }
-              }
-            }
-            if (valid)  // partial over b of facet node (a, j = pos) on line c
-  #pragma unroll
-              for (int v = 0; v < NC; ++v) pt[((v * N + pos) * N + ca) * N + cc] = facc[v];
-          }
-        }
-        // -- residual of this pass (exclusive owner of node i within the pass) --
-        if (valid) {
-  #pragma unroll
-          for (int v = 0; v < NC; ++v) {
-            if (k == 0)
-              sR[v * Nq + i] = acc[v];
-            else
-              sR[v * Nq + i] += acc[v];
-          }
-        }
-      }
-      __syncthreads();
-      stamp(2 + k);
-    };
-    pass(std::integral_constant<int, 0>{});
-    pass(std::integral_constant<int, 1>{});
-    if constexpr (DIM == 3) pass(std::integral_constant<int, 2>{});
-    // states, metrics and facet inputs are dead: the next element's copies land during the epilogue
-    if (tid == 0 && has_next) issue_A(elem_of(nidx));
-    if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
-      for (int q = tid; q < NC * N * N; q += NT) {
-        const int v = q / (N * N), jf = (q / N) % N, a = q % N;
-        double s = 0.0;
-#pragma unroll
-        for (int c = 0; c < N; ++c) s += pt[((v * N + jf) * N + a) * N + c];
-        fS[(3 * NC + v) * Nqf + a + N * jf] -= s;
-      }
-      __syncthreads();
-    }
-    stamp(5);
-    // ---- lifting r -= R^T s; facet 4 sum-factorised: t4[v][a][b] = sum_j l_b(eta3_j) s4[v][a + N j] ----
-    if constexpr (DIM == 3) {
-      double* t4 = sU + L::UM - NC * N * N;
-      for (int q = tid; q < NC * N * N; q += NT) {
-        const int v = q / (N * N), b = (q / N) % N, a = q % N;
-        const double* s4 = fS + (3 * NC + v) * Nqf + a;
-        double t = 0.0;
-#pragma unroll
-        for (int jf = 0; jf < N; ++jf) t = fma(tli4[jf * N + b], s4[N * jf], t);
-        t4[(v * N + b) * N + a] = t;
-      }
-      __syncthreads();
-    }
-    for (int i = tid; i < Nq; i += NT) {
-      const int a = i % N, b = (i / N) % N, c = DIM == 3 ? i / (N * N) : 0;
-#pragma unroll
-      for (int v = 0; v < NC; ++v) {
-        double t;
-        if constexpr (DIM == 2) {
-          t = tlL[b] * fS[(0 * NC + v) * Nqf + a] + tlR[a] * fS[(1 * NC + v) * Nqf + b] +
-              tlL[a] * fS[(2 * NC + v) * Nqf + b];
-        } else {
-          const double* t4 = sU + L::UM - NC * N * N;
-          t = tlL[b] * fS[(0 * NC + v) * Nqf + a + N * c] + tlR[a] * fS[(1 * NC + v) * Nqf + b + N * c] +
-              tlL[a] * fS[(2 * NC + v) * Nqf + b + N * c] + tl3[c] * t4[(v * N + b) * N + a];
-        }
-        sR[v * Nq + i] -= t;
-      }
-    }
-    __syncthreads();
-    stamp(7);
-
-    // ---- d u~/dt = V^T W/J~ V (V^T r), transforms in place in sR ----
-    n2m_inplace<DIM, N, NC, NT, L::o_ps>(L::o_r, L::o_um, -1);
-    stamp(8);
-    if (A.mode == 5) {  // entropy production sum w~ . (V^T r) and conservation (V^T r)_0 / c0
-      double loc = 0.0, la = 0.0;
-      for (int k = tid; k < NC * Np; k += NT) {
-        double t = A.wt[(size_t)e * NC * Np + k] * sU[k];
-        loc += t;
-        la += fabs(t);
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        loc += __shfl_down_sync(0xffffffffu, loc, o);
-        la += __shfl_down_sync(0xffffffffu, la, o);
-      }
-      __shared__ double red[2][W::NW];
-      if (lane == 0) {
-        red[0][warp] = loc;
-        red[1][warp] = la;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        double s0 = 0.0, s1 = 0.0;
-        for (int wv = 0; wv < W::NW; ++wv) {
-          s0 += red[0][wv];
-          s1 += red[1][wv];
-        }
-        double* pe2 = A.part + (size_t)e * (2 + NC);
-        pe2[0] = s0;
-        pe2[1] = s1;
-        for (int v = 0; v < NC; ++v) pe2[2 + v] = sU[v * Np] / A.c0;
-      }
-      __syncthreads();
-    }
-    m2n_inplace<DIM, N, NC, NT, L::o_ps>(L::o_um, L::o_r);
-    stamp(9);
-    n2m_inplace<DIM, N, NC, NT, L::o_ps>(L::o_r, L::o_um, L::o_wj + L::WJOFF);  // W / J~ fused into the loads
-    stamp(10);
-    // f* and W / J~ are consumed: the next element's copies land during its passes
-    if (tid == 0 && has_next) issue_B(elem_of(nidx));
-    const size_t base = (size_t)e * NC * Np;
-    const double dt = A.dt;
-    for (int kk = tid; kk < NC * Np; kk += NT) {
-      double du = sU[kk];
-      switch (A.mode) {
-        case 0:
-        case 5:
-          A.out[base + kk] = du;
-          break;
-        case 1:  // classical RK4 stage 1 (R17)
-          A.acc[base + kk] = A.u0[base + kk] + (dt / 6.0) * du;
-          A.ustage[base + kk] = A.u0[base + kk] + (0.5 * dt) * du;
-          break;
-        case 2:
-          A.acc[base + kk] += (dt / 3.0) * du;
-          A.ustage[base + kk] = A.u0[base + kk] + (0.5 * dt) * du;
-          break;
-        case 3:
-          A.acc[base + kk] += (dt / 3.0) * du;
-          A.ustage[base + kk] = A.u0[base + kk] + dt * du;
-          break;
-        case 4:
-          A.out[base + kk] = A.acc[base + kk] + (dt / 6.0) * du;
-          break;
-      }
-    }
-    __syncthreads();  // sU / sR are reused by the next element
-    stamp(11);
-  }
+  for (int64_t idx = blockIdx.x, it = 0; idx < A.n_elem; idx += gridDim.x, ++it) k2_element<DIM, N>(A, idx, (unsigned)it);
 }
 
 // ------------------------------------------------------------------------------------------------
