@@ -50,7 +50,7 @@ struct es_context {
   void* d_tables = nullptr;
   double *geo_vol = nullptr, *geo_face = nullptr, *xq = nullptr, *jt = nullptr;
   double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr, *fstar = nullptr;
-  int num_sms = 148;
+  int num_sms = 148, proj_ctas = 296;
   int64_t *face_slot = nullptr, *d_interior = nullptr, *d_boundary = nullptr, *d_send = nullptr;
   int* face_reflect = nullptr;
   int* bad = nullptr;
@@ -157,7 +157,8 @@ es_status upload_tables(es_context* c) {
 }
 
 cudaError_t run_project(es_context* c, const double* u, int64_t n, const int64_t* list, double* wt) {
-  ProjArgs A{n, list, u, c->geo_vol, c->prim, c->trace, wt, c->bad, c->gamma};
+  ProjArgs A{n, list, u, c->geo_vol, c->prim, c->trace, wt, c->bad, c->gamma, c->dbg ? c->dbg + 4096 * 16 : nullptr,
+             c->proj_ctas};
   c->launches++;
   return c->d == 2 ? launch_project_2d(c->n, c->R, A, c->stream) : launch_project_3d(c->n, c->R, A, c->stream);
 }
@@ -334,6 +335,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   c->nslots = c->nloc * c->Nf + c->plan.n_halo;
   CK(cudaSetDevice(c->device));
   CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  c->proj_ctas = c->num_sms;  // persistent kernels: SM count x resident CTAs per SM (launcher)
   if (opt->cuda_stream) {
     c->stream = (cudaStream_t)opt->cuda_stream;
   } else {
@@ -432,8 +434,8 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   CK(cudaMalloc((void**)&c->US, nmod * sizeof(double)));
   CK(cudaMemset(c->U, 0, nmod * sizeof(double)));
   if (std::getenv("ES_PHASE_TIMING")) {
-    CK(cudaMalloc((void**)&c->dbg, 4096 * 16 * sizeof(long long)));
-    CK(cudaMemset(c->dbg, 0, 4096 * 16 * sizeof(long long)));
+    CK(cudaMalloc((void**)&c->dbg, 2 * 4096 * 16 * sizeof(long long)));
+    CK(cudaMemset(c->dbg, 0, 2 * 4096 * 16 * sizeof(long long)));
   }
   if (c->world > 1) {
     const size_t nsend = c->plan.send_slots.size();
@@ -464,18 +466,22 @@ es_status es_rhs(es_context* c, const double* u, double* dudt) {
   A.out = dudt;
   es_status s = rhs_pass(c, u, A, nullptr);
   if (s != ES_OK) return s;
-  if (c->dbg) {  // ES_PHASE_TIMING: mean clock cycles per phase of the flux kernel over the first blocks
-    std::vector<long long> h(4096 * 16);
+  if (c->dbg) {  // ES_PHASE_TIMING: mean clock cycles per phase over the first blocks of each kernel
+    std::vector<long long> h(2 * 4096 * 16);
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaMemcpy(h.data(), c->dbg, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     int nb = (int)std::min<int64_t>(4096, c->nloc);
-    double acc[16] = {0};
-    for (int b = 0; b < nb; ++b)
-      for (int k = 1; k < 12; ++k)
-        if (h[b * 16 + k] && h[b * 16 + k - 1]) acc[k] += (double)(h[b * 16 + k] - h[b * 16 + k - 1]);
-    std::fprintf(stderr, "ES_PHASE_TIMING cycles/element:");
-    for (int k = 1; k < 12; ++k) std::fprintf(stderr, " %d:%.0f", k, acc[k] / nb);
-    std::fprintf(stderr, "\n");
+    for (int kk = 0; kk < 2; ++kk) {
+      double acc[16] = {0};
+      for (int b = 0; b < nb; ++b)
+        for (int k = 1; k < 16; ++k) {
+          long long t1 = h[(kk * 4096 + b) * 16 + k], t0 = h[(kk * 4096 + b) * 16 + k - 1];
+          if (t1 && t0) acc[k] += (double)(t1 - t0);
+        }
+      std::fprintf(stderr, "ES_PHASE_TIMING %s cycles/element:", kk ? "project" : "flux");
+      for (int k = 1; k < 12; ++k) std::fprintf(stderr, " %d:%.0f", k, acc[k] / nb);
+      std::fprintf(stderr, "\n");
+    }
   }
   if (c->check_adm) return check_bad(c);
   return ES_OK;

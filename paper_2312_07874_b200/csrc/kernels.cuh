@@ -53,6 +53,8 @@ struct ProjArgs {
   double* wt;                // optional [nloc][NC][Np] projected entropy variables w~
   int* bad;                  // admissibility flag
   double gamma;
+  long long* dbg;            // optional [4096][16] phase clock stamps (diagnostics)
+  int max_ctas;              // number of SMs (the launcher multiplies by resident CTAs per SM)
 };
 
 struct RhsArgs {
@@ -77,7 +79,7 @@ struct RhsArgs {
   double c0;                  // value of the constant PKD mode (1/sqrt|ref|)
   long long* dbg;             // optional [4096][16] phase clock stamps (diagnostics)
   const double* fstar;        // [nloc][Nf][NC][Nqf] B J_f f* from the interface kernel
-  int max_ctas;               // persistent grid size (CTAs resident at once)
+  int max_ctas;               // number of SMs (the launcher multiplies by resident CTAs per SM)
 };
 
 struct IfaceArgs {
@@ -364,124 +366,217 @@ __host__ __device__ constexpr int t2_size() {
 }
 
 // ------------------------------------------------------------------------------------------------
-// K1: entropy projection and traces
+// K1: entropy projection and traces (persistent: two CTAs per SM loop over elements)
 // ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int DIM, int N>
+struct ProjSmem {
+  using S = Sz<DIM, N>;
+  static constexpr int ev(int x) { return (x + 1) & ~1; }
+  static constexpr int XB = S::NC * S::Nq;            // nodal buffer
+  static constexpr int T2B = S::NC * S::Nq;           // second transform buffer
+  static constexpr int FWB = S::NC * S::NF;           // facet values
+  static constexpr int UMB = S::NC * S::Np;           // modal work buffer
+  static constexpr int INB = S::NC * S::Np + 2 * S::Nq;  // prefetched input: u~, W J~, W / J~
+  static constexpr int TBB = 3 * N + N * N;           // lL, lR, l3L, lint4
+  static constexpr int o_x = 0, o_t2 = ev(o_x + XB), o_fw = ev(o_t2 + T2B), o_um = ev(o_fw + FWB),
+                       o_in = ev(o_um + UMB), o_tb = ev(o_in + INB), o_ps = ev(o_tb + TBB),
+                       total = o_ps + psi_smem_doubles<DIM, N>();
+  static_assert(S::NC * N * N <= T2B, "facet-4 scratch");
+};
+
 template <int DIM, int N>
 __host__ __device__ constexpr size_t project_smem_doubles() {
-  using S = Sz<DIM, N>;
-  return (size_t)S::NC * S::Np + (size_t)S::NC * S::Nq + t1_size<DIM, N>() + t2_size<DIM, N>() +
-         (size_t)S::NC * S::NF + psi_smem_doubles<DIM, N>();
+  return ProjSmem<DIM, N>::total;
 }
 
 template <int DIM, int N>
 __global__ void __launch_bounds__(Sz<DIM, N>::NT, 2) project_kernel(DevRef R, ProjArgs A) {
   using S = Sz<DIM, N>;
+  using L = ProjSmem<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf;
   extern __shared__ double sm[];
-  double* um = sm;
-  double* X = um + NC * Np;
-  double* T1 = X + NC * Nq;
-  double* T2 = T1 + t1_size<DIM, N>();
-  double* FW = T2 + t2_size<DIM, N>();
-  const PsiS T = stage_psi<DIM, N>(R, FW + NC * NF);
-  const int64_t e = A.elem_list ? A.elem_list[blockIdx.x] : (int64_t)blockIdx.x;
+  double* X = sm + L::o_x;    // [NC][Nq]
+  double* T2 = sm + L::o_t2;  // [NC][Nq]
+  double* FW = sm + L::o_fw;  // [NC][NF]
+  double* um = sm + L::o_um;  // [NC][Np]
+  double* uin = sm + L::o_in;  // [NC][Np] u~, then W J~ [Nq], W / J~ [Nq]
+  double* wj = uin + NC * Np;
+  double* wjinv = wj + Nq;
+  double* tlL = sm + L::o_tb;
+  double* tlR = tlL + N;
+  double* tl3 = tlR + N;
+  double* tli4 = tl3 + N;
   const int tid = threadIdx.x, nt = blockDim.x;
   const double g = A.gamma, gm1 = g - 1.0, gm1inv = 1.0 / gm1;
-  const double* gv = A.geo_vol + (size_t)e * S::GVS;
-  for (int k = tid; k < NC * Np; k += nt) um[k] = A.u[(size_t)e * NC * Np + k];
-  __syncthreads();
-  modal_to_nodal<DIM, N, NC>(T, um, X, T1, T2);  // u = V u~
-  int bad = 0;
-  for (int i = tid; i < Nq; i += nt) {  // W J~ W(u)   (App. B formulas, R7)
-    double U[NC];
-#pragma unroll
-    for (int v = 0; v < NC; ++v) U[v] = X[v * Nq + i];
-    double r = U[0], ke = 0.0, vel[DIM];
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) {
-      vel[m] = U[1 + m] / r;
-      ke += vel[m] * U[1 + m];
-    }
-    double p = gm1 * (U[DIM + 1] - 0.5 * ke);
-    if (!(r > 0.0) || !(p > 0.0)) bad = 1;
-    double s = log(p) - g * log(r), beta = r / p, v2 = 0.0;
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) v2 += vel[m] * vel[m];
-    double wj = gv[S::NG * Nq + i];
-    X[0 * Nq + i] = wj * ((g - s) * gm1inv - 0.5 * beta * v2);
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) X[(1 + m) * Nq + i] = wj * beta * vel[m];
-    X[(DIM + 1) * Nq + i] = -wj * beta;
-  }
-  __syncthreads();
-  nodal_to_modal<DIM, N, NC>(T, X, um, T1, T2);
-  modal_to_nodal<DIM, N, NC>(T, um, X, T1, T2);
-  // W / J~ staged in the (not yet used) facet buffer and fused into the transform's loads
-  static_assert(S::NC * S::NF >= Nq, "W/J~ staging");
-  for (int i = tid; i < Nq; i += nt) FW[i] = gv[(S::NG + 1) * Nq + i];
-  __syncthreads();
-  nodal_to_modal<DIM, N, NC>(T, X, um, T1, T2, FW);  // w~
-  if (A.wt)
-    for (int k = tid; k < NC * Np; k += nt) A.wt[(size_t)e * NC * Np + k] = um[k];
-  modal_to_nodal<DIM, N, NC>(T, um, X, T1, T2);  // w = V w~
-  // w_f = R^(z) w along lines
-  for (int it = tid; it < NC * NF; it += nt) {
-    int v = it / NF, fz = it % NF, z = fz / Nqf, f = fz % Nqf;
-    const double* x = X + v * Nq;
-    double s = 0.0;
-    if constexpr (DIM == 2) {
-      if (z == 0)
-        for (int b = 0; b < N; ++b) s += __ldg(&R.lL[b]) * x[f + N * b];
-      else
-        for (int a = 0; a < N; ++a) s += __ldg(z == 1 ? &R.lR[a] : &R.lL[a]) * x[a + N * f];
-    } else {
-      int f1 = f % N, f2 = f / N;
-      if (z == 0)
-        for (int b = 0; b < N; ++b) s += __ldg(&R.lL[b]) * x[f1 + N * b + N * N * f2];
-      else if (z < 3)
-        for (int a = 0; a < N; ++a) s += __ldg(z == 1 ? &R.lR[a] : &R.lL[a]) * x[a + N * f1 + N * N * f2];
-      else
-        for (int c = 0; c < N; ++c) {
-          double t = 0.0;
-          for (int b = 0; b < N; ++b) t += __ldg(&R.lint4[f2 * N + b]) * x[f1 + N * b + N * N * c];
-          s += __ldg(&R.l3L[c]) * t;
-        }
-    }
-    FW[it] = s;
-  }
-  __syncthreads();
-  // entropy-projected conservative variables U(w) -> stored as primitive (rho, v, p)
-  auto Uofw = [&](const double* w, double* out) -> int {
-    double b = -w[DIM + 1], vel[DIM], v2 = 0.0;
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) {
-      vel[m] = w[1 + m] / b;
-      v2 += vel[m] * vel[m];
-    }
-    double s = g - gm1 * (w[0] + 0.5 * b * v2);
-    double r = exp((s + log(b)) / (1.0 - g));
-    out[0] = r;
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) out[1 + m] = vel[m];
-    out[DIM + 1] = r / b;
-    return (b > 0.0 && r > 0.0) ? 0 : 1;
+  auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
+  // asynchronous copies (cp.async) of one element's inputs into uin / wj / wjinv
+  auto prefetch = [&](int64_t e) {
+    const double* src = A.u + (size_t)e * NC * Np;
+    for (int k = tid; k < NC * Np; k += nt) cp_async8(uin + k, src + k);
+    const double* gv = A.geo_vol + (size_t)e * S::GVS + S::NG * Nq;
+    for (int k = tid; k < 2 * Nq; k += nt) cp_async8(wj + k, gv + k);
+    cp_async_commit();
   };
-  for (int i = tid; i < Nq; i += nt) {
-    double w[NC], o[NC];
-#pragma unroll
-    for (int v = 0; v < NC; ++v) w[v] = X[v * Nq + i];
-    bad |= Uofw(w, o);
-#pragma unroll
-    for (int v = 0; v < NC; ++v) A.prim[(size_t)e * S::PRS + v * Nq + i] = o[v];
+  if ((int64_t)blockIdx.x < A.n_elem) prefetch(elem_of(blockIdx.x));
+  const PsiS T = stage_psi<DIM, N>(R, sm + L::o_ps);
+  for (int k = tid; k < N; k += nt) {
+    tlL[k] = R.lL[k];
+    tlR[k] = R.lR[k];
+    if constexpr (DIM == 3) tl3[k] = R.l3L[k];
   }
-  for (int fz = tid; fz < NF; fz += nt) {
-    double w[NC], o[NC];
+  if constexpr (DIM == 3)
+    for (int k = tid; k < N * N; k += nt) tli4[k] = R.lint4[k];
+  int bad = 0;
+#pragma unroll 1
+  for (int64_t idx = blockIdx.x; idx < A.n_elem; idx += gridDim.x) {
+    const int64_t e = elem_of(idx);
+    auto stamp = [&](int q) {
+      if (A.dbg && tid == 0 && idx < 4096) A.dbg[idx * 16 + q] = clock64();
+    };
+    stamp(0);
+    cp_async_wait_all();
+    __syncthreads();
+    stamp(1);
+    // u = V u~ (ping-pong X / T2; 3D writes its first scratch into the output buffer)
+    if constexpr (DIM == 3)
+      modal_to_nodal<DIM, N, NC>(T, uin, X, X, T2);
+    else
+      modal_to_nodal<DIM, N, NC>(T, uin, X, T2, nullptr);
+    stamp(2);
+    for (int i = tid; i < Nq; i += nt) {  // W J~ W(u)   (App. B formulas, R7)
+      double U[NC];
 #pragma unroll
-    for (int v = 0; v < NC; ++v) w[v] = FW[v * NF + fz];
-    bad |= Uofw(w, o);
-    int z = fz / Nqf, f = fz % Nqf;
+      for (int v = 0; v < NC; ++v) U[v] = X[v * Nq + i];
+      double r = U[0], ke = 0.0, vel[DIM];
+      const double ir = 1.0 / r;
 #pragma unroll
-    for (int v = 0; v < NC; ++v) A.trace[(((size_t)e * S::Nf + z) * NC + v) * Nqf + f] = o[v];
+      for (int m = 0; m < DIM; ++m) {
+        vel[m] = U[1 + m] * ir;
+        ke += vel[m] * U[1 + m];
+      }
+      double p = gm1 * (U[DIM + 1] - 0.5 * ke);
+      if (!(r > 0.0) || !(p > 0.0)) bad = 1;
+      double s = log(p) - g * log(r), beta = r / p, v2 = 0.0;
+#pragma unroll
+      for (int m = 0; m < DIM; ++m) v2 += vel[m] * vel[m];
+      const double w = wj[i];
+      X[0 * Nq + i] = w * ((g - s) * gm1inv - 0.5 * beta * v2);
+#pragma unroll
+      for (int m = 0; m < DIM; ++m) X[(1 + m) * Nq + i] = w * beta * vel[m];
+      X[(DIM + 1) * Nq + i] = -w * beta;
+    }
+    __syncthreads();
+    stamp(3);
+    if constexpr (DIM == 3) {
+      nodal_to_modal<DIM, N, NC>(T, X, um, X, T2);
+      stamp(4);
+      modal_to_nodal<DIM, N, NC>(T, um, X, X, T2);
+      stamp(5);
+      nodal_to_modal<DIM, N, NC>(T, X, um, X, T2, wjinv);  // w~, W / J~ fused into the loads
+    } else {
+      nodal_to_modal<DIM, N, NC>(T, X, um, T2, nullptr);
+      stamp(4);
+      modal_to_nodal<DIM, N, NC>(T, um, X, T2, nullptr);
+      stamp(5);
+      nodal_to_modal<DIM, N, NC>(T, X, um, T2, nullptr, wjinv);
+    }
+    stamp(7);
+    // the prefetched inputs are consumed: the next element's copies overlap the rest
+    if (idx + gridDim.x < A.n_elem) prefetch(elem_of(idx + gridDim.x));
+    if (A.wt)
+      for (int k = tid; k < NC * Np; k += nt) A.wt[(size_t)e * NC * Np + k] = um[k];
+    if constexpr (DIM == 3)  // w = V w~
+      modal_to_nodal<DIM, N, NC>(T, um, X, X, T2);
+    else
+      modal_to_nodal<DIM, N, NC>(T, um, X, T2, nullptr);
+    stamp(8);
+    // w_f = R^(z) w along lines; facet 4 (3D) contracts eta3 first: y[a][b] = sum_c l3(c) w
+    if constexpr (DIM == 3) {
+      double* y = T2;  // [NC][N(b)][N(a)]
+      for (int it = tid; it < NC * N * N; it += nt) {
+        const int v = it / (N * N), ab = it - v * N * N;
+        const double* x = X + v * Nq + ab;
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) s = fma(tl3[c], x[N * N * c], s);
+        y[it] = s;
+      }
+      __syncthreads();
+    }
+    for (int it = tid; it < NC * NF; it += nt) {
+      const int v = it / NF, fz = it - v * NF, z = fz / Nqf, f = fz - z * Nqf;
+      const double* x = X + v * Nq;
+      double s = 0.0;
+      if constexpr (DIM == 2) {
+        if (z == 0) {
+#pragma unroll
+          for (int b = 0; b < N; ++b) s = fma(tlL[b], x[f + N * b], s);
+        } else {
+          const double* l = z == 1 ? tlR : tlL;
+#pragma unroll
+          for (int a = 0; a < N; ++a) s = fma(l[a], x[a + N * f], s);
+        }
+      } else {
+        const int f1 = f % N, f2 = f / N;
+        if (z == 0) {
+#pragma unroll
+          for (int b = 0; b < N; ++b) s = fma(tlL[b], x[f1 + N * b + N * N * f2], s);
+        } else if (z < 3) {
+          const double* l = z == 1 ? tlR : tlL;
+#pragma unroll
+          for (int a = 0; a < N; ++a) s = fma(l[a], x[a + N * f1 + N * N * f2], s);
+        } else {
+          const double* y = T2 + v * N * N + f1;
+#pragma unroll
+          for (int b = 0; b < N; ++b) s = fma(tli4[f2 * N + b], y[N * b], s);
+        }
+      }
+      FW[it] = s;
+    }
+    __syncthreads();
+    stamp(9);
+    // entropy-projected conservative variables U(w) -> stored as primitive (rho, v, p)
+    auto Uofw = [&](const double* w, double* out) -> int {
+      const double b = -w[DIM + 1], ib = 1.0 / b;
+      double vel[DIM], v2 = 0.0;
+#pragma unroll
+      for (int m = 0; m < DIM; ++m) {
+        vel[m] = w[1 + m] * ib;
+        v2 += vel[m] * vel[m];
+      }
+      const double s = g - gm1 * (w[0] + 0.5 * b * v2);
+      const double r = exp((s + log(b)) / (1.0 - g));
+      out[0] = r;
+#pragma unroll
+      for (int m = 0; m < DIM; ++m) out[1 + m] = vel[m];
+      out[DIM + 1] = r * ib;
+      return (b > 0.0 && r > 0.0) ? 0 : 1;
+    };
+    for (int i = tid; i < Nq + NF; i += nt) {
+      double w[NC], o[NC];
+      if (i < Nq) {
+#pragma unroll
+        for (int v = 0; v < NC; ++v) w[v] = X[v * Nq + i];
+        bad |= Uofw(w, o);
+#pragma unroll
+        for (int v = 0; v < NC; ++v) A.prim[(size_t)e * S::PRS + v * Nq + i] = o[v];
+      } else {
+        const int fz = i - Nq, z = fz / Nqf, f = fz - z * Nqf;
+#pragma unroll
+        for (int v = 0; v < NC; ++v) w[v] = FW[v * NF + fz];
+        bad |= Uofw(w, o);
+#pragma unroll
+        for (int v = 0; v < NC; ++v) A.trace[(((size_t)e * S::Nf + z) * NC + v) * Nqf + f] = o[v];
+      }
+    }
+    stamp(10);
   }
   if (bad) atomicOr(A.bad, 1);
 }
