@@ -46,7 +46,7 @@ FLUX_FLOPS = {2: 67, 3: 81}            # Ranocha EC flux, Taylor branch of both 
 VOL_NORMAL_FLOPS = {2: 12, 3: 24}      # n_ij from the line operators and averaged metrics
 FAC_NORMAL_FLOPS = {2: 10, 3: 21}      # <J n> of the facet correction
 ACC_FLOPS = {2: 8, 3: 10}              # -F to node i, +F to node j (or C^T 1)
-IFACE_FLOPS = {2: 110, 3: 140}         # EC flux + Davis wave speed + LF jump + B J_f scaling
+IFACE_FLOPS = {2: 110, 3: 140}         # EC flux + Davis wave speed + LF jump + B J_f scaling (iface kernel)
 
 
 def counts(dim, p):
@@ -65,15 +65,26 @@ def counts(dim, p):
 
 
 def rhs_kernel_flops(dim, p):
-    """algorithmic flops of the flux-differencing kernel (K2) per element and RHS"""
+    """algorithmic flops of the flux-differencing kernel (K2) per element and RHS: volume and
+    facet-correction pairs, C^T 1 subtraction, lifting and the weight-adjusted inverse (the
+    interface flux runs in its own kernel)"""
     c = counts(dim, p)
     nc = dim + 2
     f = c["vol"] * (FLUX_FLOPS[dim] + VOL_NORMAL_FLOPS[dim] + ACC_FLOPS[dim])
     f += c["fac"] * (FLUX_FLOPS[dim] + FAC_NORMAL_FLOPS[dim] + ACC_FLOPS[dim])
-    f += c["iface"] * IFACE_FLOPS[dim]
     f += 2 * 3 * nc * c["sf"]  # V^T, V, V^T of the weight-adjusted inverse (P:593)
     f += nc * c["Nq"] * (2 * (dim + 1) + 1)  # lifting R^T s and W/J~ scaling
     return f
+
+
+def ncu_traffic_per_element():
+    """DRAM bytes per element of K2 from the committed ncu --set full capture (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)
+        return d["rhs2_kernel"]["dram_bytes_per_element"], d["source"]
+    except Exception:
+        return None, None
 
 
 def measured_peaks():
@@ -294,6 +305,7 @@ def run(args):
     ms = e0.elapsed_time(e1)
     k2_ms, k2_n = ctx.timing_read(1)
     k1_ms, k1_n = ctx.timing_read(0)
+    kf_ms, kf_n = ctx.timing_read(2)
     launches = ctx.launch_count()
     ctx.timing_enable(False)
     if world > 1:
@@ -335,9 +347,10 @@ def run(args):
     nbytes = host_in.numel() * 8
     # ---- roofline of the dominant kernel (K2) ----
     k2_avg_ms = k2_ms / max(k2_n, 1)
-    elems_per_launch = ne / world if world == 1 else ne / world / 2  # interior/boundary split
     k2_flops = rhs_kernel_flops(dim, p) * (ne / world) / (k2_n / max(1, args.steps * 4))
     achieved = k2_flops / (k2_avg_ms * 1e-3) / 1e12
+    tpe, traffic_src = ncu_traffic_per_element()
+    traffic = tpe * (ne / world) / (k2_n / max(1, args.steps * 4)) if tpe else None
     peak = fp64_peak_tflops()
     line = {
         "metric": "EC two-point flux evals/s", "value": value, "unit": "flux_evals/s", "n_gpus": world,
@@ -352,9 +365,14 @@ def run(args):
         "rhs_per_s": rhs_per_step / (ms_step * 1e-3),
         "eq56_equivalent_evals_per_s": rhs_per_step * ne * c["eq56"] / (ms_step * 1e-3),
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "rhs_kernel (K2)",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "rhs2_kernel (K2, flux differencing)",
                      "kernel_ms_avg": k2_avg_ms, "kernel_share_of_step": k2_ms / args.steps / ms_step,
+                     "traffic_source": traffic_src,
+                     "algorithmic_flops_per_element": rhs_kernel_flops(dim, p),
                      "projection_kernel_ms_avg": k1_ms / max(k1_n, 1),
+                     "projection_share_of_step": k1_ms / args.steps / ms_step,
+                     "iface_kernel_ms_avg": kf_ms / max(kf_n, 1),
+                     "iface_share_of_step": kf_ms / args.steps / ms_step,
                      "peak_basis": "148 SM x 64 DFMA/clk x 2 x sm_max_mhz (DESIGN.md 6)"},
         "e2e": {"value": e2e_value, "unit": "flux_evals/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                 "api": "cudaMemcpyAsync(pinned->device) + es_set_state + es_step + es_get_state + copy back"},

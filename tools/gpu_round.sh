@@ -16,6 +16,6 @@ timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_launch.log 2>&1
 timeout 300 python tools/profile_run.py 3 12 8 2 > gpurun_out/${TAG}_prof_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"rhs2_kernel|project_kernel" -s 2 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"rhs2_kernel|project_kernel|iface_kernel" -s 3 -c 3 \
   -o gpurun_out/${TAG}_prof python tools/profile_run.py 3 12 8 2 > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo done
