@@ -40,7 +40,7 @@ __device__ __forceinline__ dd dd_neg(dd a) { return {-a.hi, -a.lo}; }
 __device__ __forceinline__ dd dd_sub(dd a, dd b) { return dd_add(a, dd_neg(b)); }
 
 __global__ void geometry_kernel(GeoArgs g) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   const int d = g.dim, Npg = g.Npg, Ncl = g.Ncl, Nq = g.Nq, NF = g.NF, Nqf = g.Nqf;
   const int NG = d * d;
   double* xs = sm;               // [Npg][d] local mapping-node coordinates (exact inputs)

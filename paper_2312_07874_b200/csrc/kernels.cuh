@@ -161,51 +161,68 @@ struct PsiS {
   const int* poff;   // pair -> first modal index
 };
 
+// psi tables in shared memory with rows padded to an even length NP (16-byte aligned pairs for
+// LDS.128): p1 [N][NP], p2 [N][N][NP], p3 [N][N][NP], then the int pair tables; PSPAD trailing
+// doubles keep the over-reads of the last output chunk inside the allocation
+template <int N>
+__host__ __device__ constexpr int psi_np() { return (N + 1) & ~1; }
+constexpr int PSPAD = 4 * 12;
 template <int DIM, int N>
 __host__ __device__ constexpr int psi_smem_doubles() {
-  return N * N + N * N * N + (DIM == 3 ? N * N * N : 0) + (3 * (DIM == 2 ? N : N * (N + 1) / 2) + 1) / 2 + 1;
+  return N * psi_np<N>() + N * N * psi_np<N>() + (DIM == 3 ? N * N * psi_np<N>() : 0) + PSPAD +
+         (3 * (DIM == 2 ? N : N * (N + 1) / 2) + 1) / 2 + 1;
 }
 
 // the psi tables at `buf` (layout of stage_psi)
 template <int DIM, int N>
 __device__ __forceinline__ PsiS psi_tables(double* buf) {
-  constexpr int NPAIR = DIM == 2 ? N : N * (N + 1) / 2;
+  constexpr int NPAIR = DIM == 2 ? N : N * (N + 1) / 2, NP = psi_np<N>();
   double* p1 = buf;
-  double* p2 = p1 + N * N;
-  double* p3 = p2 + N * N * N;
-  int* pi = (int*)(p3 + (DIM == 3 ? N * N * N : 0));
+  double* p2 = p1 + N * NP;
+  double* p3 = p2 + N * N * NP;
+  int* pi = (int*)(p3 + (DIM == 3 ? N * N * NP : 0) + PSPAD);
   return PsiS{p1, p2, p3, pi, pi + NPAIR, pi + 2 * NPAIR};
 }
 
 // stage the tables of R into shared memory at `buf` (psi_smem_doubles<DIM,N>() doubles)
 template <int DIM, int N>
 __device__ PsiS stage_psi(const DevRef& R, double* buf) {
-  constexpr int NPAIR = DIM == 2 ? N : N * (N + 1) / 2;
-  double* p1 = buf;
-  double* p2 = p1 + N * N;
-  double* p3 = p2 + N * N * N;
-  int* pi = (int*)(p3 + (DIM == 3 ? N * N * N : 0));
-  for (int k = threadIdx.x; k < N * N; k += blockDim.x) p1[k] = R.psi1[k];
-  for (int k = threadIdx.x; k < N * N * N; k += blockDim.x) {
-    p2[k] = R.psi2[k];
-    if constexpr (DIM == 3) p3[k] = R.psi3[k];
+  constexpr int NPAIR = DIM == 2 ? N : N * (N + 1) / 2, NP = psi_np<N>();
+  const PsiS T = psi_tables<DIM, N>(buf);
+  double* p1 = (double*)T.p1;
+  double* p2 = (double*)T.p2;
+  double* p3 = (double*)T.p3;
+  for (int k = threadIdx.x; k < N * NP; k += blockDim.x) {
+    const int r = k / NP, c = k - r * NP;
+    p1[k] = c < N ? R.psi1[r * N + c] : 0.0;
   }
+  for (int k = threadIdx.x; k < N * N * NP; k += blockDim.x) {
+    const int r = k / NP, c = k - r * NP;
+    p2[k] = c < N ? R.psi2[r * N + c] : 0.0;
+    if constexpr (DIM == 3) p3[k] = c < N ? R.psi3[r * N + c] : 0.0;
+  }
+  for (int k = threadIdx.x; k < PSPAD; k += blockDim.x) p1[(N + N * N + (DIM == 3 ? N * N : 0)) * NP + k] = 0.0;
+  int* pi = (int*)T.pa1;
   for (int k = threadIdx.x; k < NPAIR; k += blockDim.x) {
     pi[k] = R.pair_a1[k];
     pi[NPAIR + k] = R.pair_a2[k];
     pi[2 * NPAIR + k] = R.pair_off[k];
   }
-  return PsiS{p1, p2, p3, pi, pi + NPAIR, pi + 2 * NPAIR};
+  return T;
 }
 
 // Two fibers per work item share every psi load (register blocking): y_f[o] = sum_{i < ni} A[i][o]
-// x_f[i] for o < no, f = 0, 1, with A[i][o] = ps[i N + o] (TR = false) or ps[o N + i] (TR = true);
-// inputs beyond ni are not read (the tables vanish there).  Optional per-input scales sc0 / sc1
-// multiply x (the diagonal W/J~ factor fused into the load).
+// (the two fibers of an item are half a step apart, so that consecutive lanes own consecutive
+// fibers: odd strides between lanes, no shared-memory bank conflicts)
+// x_f[i] for o < no, f = 0, 1, with A[i][o] = ps[i NP + o] (TR = false) or ps[o NP + i] (TR = true);
+// psi pairs are read as 16-byte vectors (padded rows).  Inputs beyond ni are not read (the tables
+// vanish there).  Optional per-input scales sc0 / sc1 multiply x (the diagonal W/J~ factor fused
+// into the load).  Outputs in chunks of OC, each accumulated over all inputs (independent chains).
 template <int N, bool TR>
 __device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const double* in0,
                                        const double* in1, int sin, const double* sc0, const double* sc1,
                                        double* out0, double* out1, int sout, bool has1) {
+  constexpr int NP = psi_np<N>(), OC = 4;
   double x0[N], x1[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) {
@@ -217,21 +234,37 @@ __device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const d
       x1[i] *= ok ? sc1[i * sin] : 0.0;
     }
   }
-  // outputs in chunks of OC, each accumulated over all inputs (independent FMA chains)
-  constexpr int OC = 3;
 #pragma unroll 1
   for (int o0 = 0; o0 < no; o0 += OC) {
     double a0[OC], a1[OC];
 #pragma unroll
     for (int q = 0; q < OC; ++q) a0[q] = a1[q] = 0.0;
+    if constexpr (!TR) {
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int q2 = 0; q2 < OC / 2; ++q2) {
+          const double2 pv = *reinterpret_cast<const double2*>(ps + i * NP + o0 + 2 * q2);
+          a0[2 * q2] = fma(pv.x, x0[i], a0[2 * q2]);
+          a1[2 * q2] = fma(pv.x, x1[i], a1[2 * q2]);
+          a0[2 * q2 + 1] = fma(pv.y, x0[i], a0[2 * q2 + 1]);
+          a1[2 * q2 + 1] = fma(pv.y, x1[i], a1[2 * q2 + 1]);
+        }
+      }
+    } else {
 #pragma unroll
       for (int q = 0; q < OC; ++q) {
-        const int o = o0 + q < N ? o0 + q : N - 1;
-        const double pv = TR ? ps[o * N + i] : ps[i * N + o];
-        a0[q] = fma(pv, x0[i], a0[q]);
-        a1[q] = fma(pv, x1[i], a1[q]);
+        const double* row = ps + (o0 + q) * NP;
+#pragma unroll
+        for (int i2 = 0; i2 < NP / 2; ++i2) {
+          const double2 pv = *reinterpret_cast<const double2*>(row + 2 * i2);
+          a0[q] = fma(pv.x, x0[2 * i2], a0[q]);
+          a1[q] = fma(pv.x, x1[2 * i2], a1[q]);
+          if (2 * i2 + 1 < N) {
+            a0[q] = fma(pv.y, x0[2 * i2 + 1], a0[q]);
+            a1[q] = fma(pv.y, x1[2 * i2 + 1], a1[q]);
+          }
+        }
       }
     }
 #pragma unroll
@@ -253,14 +286,14 @@ __device__ void modal_to_nodal(const PsiS& T, const double* um, double* un, doub
     // t1[v][a1][b] = sum_a2 psi2[a1][a2][b] u[v][off(a1)+a2]; items (a1, variable pair)
     for (int it = tid; it < N * NVP; it += nt) {
       const int a1 = it / NVP, v0 = 2 * (it - a1 * NVP), v1 = v0 + 1 < NV ? v0 + 1 : v0;
-      fiber2<N, false>(T.p2 + a1 * N * N, N - a1, N, um + v0 * Np + T.poff[a1], um + v1 * Np + T.poff[a1], 1, nullptr, nullptr,
+      fiber2<N, false>(T.p2 + a1 * N * psi_np<N>(), N - a1, N, um + v0 * Np + T.poff[a1], um + v1 * Np + T.poff[a1], 1, nullptr, nullptr,
                 t1 + (v0 * N + a1) * N, t1 + (v1 * N + a1) * N, 1, v1 != v0);
     }
     __syncthreads();
     // u[v][a + N b] = sum_a1 psi1[a1][a] t1[v][a1][b]; items pairs of (v, b) fibers
     constexpr int NFB = NV * N;
     for (int it = tid; it < (NFB + 1) / 2; it += nt) {
-      const int q0 = 2 * it, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+      const int q0 = it, q1 = it + (NFB + 1) / 2 < NFB ? it + (NFB + 1) / 2 : it;
       const int v0 = q0 / N, b0 = q0 - v0 * N, v1 = q1 / N, b1 = q1 - v1 * N;
       fiber2<N, false>(T.p1, N, N, t1 + v0 * N * N + b0, t1 + v1 * N * N + b1, N, nullptr, nullptr, un + v0 * Nq + N * b0,
                 un + v1 * Nq + N * b1, 1, q1 != q0);
@@ -271,24 +304,24 @@ __device__ void modal_to_nodal(const PsiS& T, const double* um, double* un, doub
     for (int it = tid; it < NPAIR * NVP; it += nt) {
       const int pr = it / NVP, v0 = 2 * (it - pr * NVP), v1 = v0 + 1 < NV ? v0 + 1 : v0;
       const int sdeg = T.pa1[pr] + T.pa2[pr];
-      fiber2<N, false>(T.p3 + sdeg * N * N, N - sdeg, N, um + v0 * Np + T.poff[pr], um + v1 * Np + T.poff[pr], 1, nullptr,
+      fiber2<N, false>(T.p3 + sdeg * N * psi_np<N>(), N - sdeg, N, um + v0 * Np + T.poff[pr], um + v1 * Np + T.poff[pr], 1, nullptr,
                 nullptr, t1 + (v0 * NPAIR + pr) * N, t1 + (v1 * NPAIR + pr) * N, 1, v1 != v0);
     }
     __syncthreads();
     // t2[v][a1][c][b] = sum_a2 psi2[a1][a2][b] t1[v][pr(a1,a2)][c]; items (a1, pair of (v, c) fibers)
     constexpr int NFC = NV * N, NPC = (NFC + 1) / 2;
     for (int it = tid; it < N * NPC; it += nt) {
-      const int a1 = it / NPC, w = it - a1 * NPC, q0 = 2 * w, q1 = q0 + 1 < NFC ? q0 + 1 : q0;
+      const int a1 = it / NPC, w = it - a1 * NPC, q0 = w, q1 = w + NPC < NFC ? w + NPC : w;
       const int v0 = q0 / N, c0 = q0 - v0 * N, v1 = q1 / N, c1 = q1 - v1 * N;
       const int prs = a1 * N - a1 * (a1 - 1) / 2;
-      fiber2<N, false>(T.p2 + a1 * N * N, N - a1, N, t1 + (v0 * NPAIR + prs) * N + c0, t1 + (v1 * NPAIR + prs) * N + c1, N,
+      fiber2<N, false>(T.p2 + a1 * N * psi_np<N>(), N - a1, N, t1 + (v0 * NPAIR + prs) * N + c0, t1 + (v1 * NPAIR + prs) * N + c1, N,
                 nullptr, nullptr, t2 + ((v0 * N + a1) * N + c0) * N, t2 + ((v1 * N + a1) * N + c1) * N, 1, q1 != q0);
     }
     __syncthreads();
     // u[v][a + N bc] = sum_a1 psi1[a1][a] t2[v][a1][bc]; items pairs of (v, bc) fibers
     constexpr int NFB = NV * N * N;
     for (int it = tid; it < (NFB + 1) / 2; it += nt) {
-      const int q0 = 2 * it, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+      const int q0 = it, q1 = it + (NFB + 1) / 2 < NFB ? it + (NFB + 1) / 2 : it;
       const int v0 = q0 / (N * N), bc0 = q0 - v0 * N * N, v1 = q1 / (N * N), bc1 = q1 - v1 * N * N;
       fiber2<N, false>(T.p1, N, N, t2 + v0 * Nq + bc0, t2 + v1 * Nq + bc1, N * N, nullptr, nullptr, un + v0 * Nq + N * bc0,
                 un + v1 * Nq + N * bc1, 1, q1 != q0);
@@ -309,7 +342,7 @@ __device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, doubl
     // s1[v][a1][b] = sum_a psi1[a1][a] y[v][a + N b]; items pairs of (v, b) fibers
     constexpr int NFB = NV * N;
     for (int it = tid; it < (NFB + 1) / 2; it += nt) {
-      const int q0 = 2 * it, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+      const int q0 = it, q1 = it + (NFB + 1) / 2 < NFB ? it + (NFB + 1) / 2 : it;
       const int v0 = q0 / N, b0 = q0 - v0 * N, v1 = q1 / N, b1 = q1 - v1 * N;
       fiber2<N, true>(T.p1, N, N, y + v0 * Nq + N * b0, y + v1 * Nq + N * b1, 1, scale ? scale + N * b0 : nullptr,
                 scale ? scale + N * b1 : nullptr, t1 + v0 * N * N + b0, t1 + v1 * N * N + b1, N, q1 != q0);
@@ -318,7 +351,7 @@ __device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, doubl
     // u[v][off(a1)+a2] = sum_b psi2[a1][a2][b] s1[v][a1][b]; items (a1, variable pair)
     for (int it = tid; it < N * NVP; it += nt) {
       const int a1 = it / NVP, v0 = 2 * (it - a1 * NVP), v1 = v0 + 1 < NV ? v0 + 1 : v0;
-      fiber2<N, true>(T.p2 + a1 * N * N, N, N - a1, t1 + (v0 * N + a1) * N, t1 + (v1 * N + a1) * N, 1, nullptr,
+      fiber2<N, true>(T.p2 + a1 * N * psi_np<N>(), N, N - a1, t1 + (v0 * N + a1) * N, t1 + (v1 * N + a1) * N, 1, nullptr,
                 nullptr, um + v0 * Np + T.poff[a1], um + v1 * Np + T.poff[a1], 1, v1 != v0);
     }
     __syncthreads();
@@ -326,7 +359,7 @@ __device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, doubl
     // s2[v][a1][bc] = sum_a psi1[a1][a] y[v][a + N bc]; items pairs of (v, bc) fibers
     constexpr int NFB = NV * N * N;
     for (int it = tid; it < (NFB + 1) / 2; it += nt) {
-      const int q0 = 2 * it, q1 = q0 + 1 < NFB ? q0 + 1 : q0;
+      const int q0 = it, q1 = it + (NFB + 1) / 2 < NFB ? it + (NFB + 1) / 2 : it;
       const int v0 = q0 / (N * N), bc0 = q0 - v0 * N * N, v1 = q1 / (N * N), bc1 = q1 - v1 * N * N;
       fiber2<N, true>(T.p1, N, N, y + v0 * Nq + N * bc0, y + v1 * Nq + N * bc1, 1, scale ? scale + N * bc0 : nullptr,
                       scale ? scale + N * bc1 : nullptr, t2 + v0 * Nq + bc0, t2 + v1 * Nq + bc1, N * N, q1 != q0);
@@ -335,10 +368,10 @@ __device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, doubl
     // s1[v][pr(a1,a2)][c] = sum_b psi2[a1][a2][b] s2[v][a1][c][b]; items (a1, pair of (v, c) fibers)
     constexpr int NFC = NV * N, NPC = (NFC + 1) / 2;
     for (int it = tid; it < N * NPC; it += nt) {
-      const int a1 = it / NPC, w = it - a1 * NPC, q0 = 2 * w, q1 = q0 + 1 < NFC ? q0 + 1 : q0;
+      const int a1 = it / NPC, w = it - a1 * NPC, q0 = w, q1 = w + NPC < NFC ? w + NPC : w;
       const int v0 = q0 / N, c0 = q0 - v0 * N, v1 = q1 / N, c1 = q1 - v1 * N;
       const int prs = a1 * N - a1 * (a1 - 1) / 2;
-      fiber2<N, true>(T.p2 + a1 * N * N, N, N - a1, t2 + ((v0 * N + a1) * N + c0) * N, t2 + ((v1 * N + a1) * N + c1) * N, 1,
+      fiber2<N, true>(T.p2 + a1 * N * psi_np<N>(), N, N - a1, t2 + ((v0 * N + a1) * N + c0) * N, t2 + ((v1 * N + a1) * N + c1) * N, 1,
                 nullptr, nullptr, t1 + (v0 * NPAIR + prs) * N + c0, t1 + (v1 * NPAIR + prs) * N + c1, N, q1 != q0);
     }
     __syncthreads();
@@ -346,7 +379,7 @@ __device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, doubl
     for (int it = tid; it < NPAIR * NVP; it += nt) {
       const int pr = it / NVP, v0 = 2 * (it - pr * NVP), v1 = v0 + 1 < NV ? v0 + 1 : v0;
       const int sdeg = T.pa1[pr] + T.pa2[pr];
-      fiber2<N, true>(T.p3 + sdeg * N * N, N, N - sdeg, t1 + (v0 * NPAIR + pr) * N, t1 + (v1 * NPAIR + pr) * N, 1, nullptr,
+      fiber2<N, true>(T.p3 + sdeg * N * psi_np<N>(), N, N - sdeg, t1 + (v0 * NPAIR + pr) * N, t1 + (v1 * NPAIR + pr) * N, 1, nullptr,
                 nullptr, um + v0 * Np + T.poff[pr], um + v1 * Np + T.poff[pr], 1, v1 != v0);
     }
     __syncthreads();
@@ -401,7 +434,7 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT, 2) project_kernel(DevRef R, Pr
   using S = Sz<DIM, N>;
   using L = ProjSmem<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   double* X = sm + L::o_x;    // [NC][Nq]
   double* T2 = sm + L::o_t2;  // [NC][Nq]
   double* FW = sm + L::o_fw;  // [NC][NF]
@@ -589,12 +622,14 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT) project_nodal_kernel(DevRef R,
                                                                     double* um_out) {
   using S = Sz<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
+  constexpr int o_um = (NC * Nq + 1) & ~1, o_t1 = (o_um + NC * Np + 1) & ~1, o_t2 = (o_t1 + t1_size<DIM, N>() + 1) & ~1,
+                o_ps = (o_t2 + t2_size<DIM, N>() + 1) & ~1;
   double* X = sm;
-  double* um = X + NC * Nq;
-  double* T1 = um + NC * Np;
-  double* T2 = T1 + t1_size<DIM, N>();
-  const PsiS T = stage_psi<DIM, N>(R, T2 + t2_size<DIM, N>());
+  double* um = sm + o_um;
+  double* T1 = sm + o_t1;
+  double* T2 = sm + o_t2;
+  const PsiS T = stage_psi<DIM, N>(R, sm + o_ps);
   int64_t e = blockIdx.x;
   for (int it = threadIdx.x; it < NC * Nq; it += blockDim.x) {
     int v = it / Nq, i = it % Nq;
@@ -608,7 +643,7 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT) project_nodal_kernel(DevRef R,
 template <int DIM, int N>
 __host__ __device__ constexpr size_t projnodal_smem_doubles() {
   using S = Sz<DIM, N>;
-  return (size_t)S::NC * S::Nq + (size_t)S::NC * S::Np + t1_size<DIM, N>() + t2_size<DIM, N>() +
+  return (size_t)S::NC * S::Nq + (size_t)S::NC * S::Np + t1_size<DIM, N>() + t2_size<DIM, N>() + 4 +
          psi_smem_doubles<DIM, N>();
 }
 
