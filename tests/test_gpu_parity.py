@@ -90,6 +90,13 @@ CASES = [
     (3, 3, 4, "paper", "tgv3", 1),
     (3, 3, 6, "paper", "tgv3", 1),
     (3, 3, 8, "bj", "tgv", 1),         # C5 degree
+    (3, 3, 5, "paper", "tgv3", 1),     # even line length, 3D
+    (3, 3, 7, "paper", "tgv3", 0),     # even line length, 3D, EC
+    (3, 3, 1, "paper", "tgv3", 1),     # p = 1: two nodes per line
+    (2, 3, 1, "paper", "wave", 1),
+    (2, 3, 8, "paper", "wave", 1),
+    (2, 3, 9, "bj", "vortex", 0),
+    (3, 4, 8, "paper", "tgv3", 0),     # C5 degree on the hardest geometry, EC
 ]
 
 
@@ -222,3 +229,20 @@ def test_full_size_sampled_parity(es, name, d, M, p, warp, kind, fm):
     ref, st = om.rhs(u, flux_mode=fm, variant=1, elems=sample)
     err = _relerr(got[sample], ref[sample])
     assert (err <= TOL).all(), (name, err)
+
+
+def test_full_size_c4_entropy_conservation(es):
+    # BASELINE C4 (EC volume and interface fluxes): sum_k w~^T M~ du~/dt = 0 to roundoff
+    # (reading R21), and discrete conservation, on the full 24 576-element mesh
+    d, M, p = 3, 16, 4
+    L = _L(d)
+    mesh = I.split_cartesian(d, M, L)
+    u = I.modal_state_from_centroids(mesh, p, "tgv", seed=5, amp=1e-2)
+    ctx = es.Context(mesh, p, warp=I.bj_warp(d, L, M), interface_flux=0)
+    rate, scale, cons = ctx.entropy_production(torch.from_numpy(u).cuda())
+    assert abs(rate) <= 1e-12 * scale, (rate, scale)
+    du = _gpu_rhs(ctx, u)
+    assert np.abs(cons).max() <= 1e-12 * len(mesh["elem_vertices"]) * np.abs(du).max(), cons
+    ctx2 = es.Context(mesh, p, warp=I.bj_warp(d, L, M), interface_flux=1)
+    rate2, scale2, _ = ctx2.entropy_production(torch.from_numpy(u).cuda())
+    assert rate2 < -1e-8 * scale2, (rate2, scale2)  # LLF dissipates
