@@ -164,7 +164,10 @@ struct Job {
 // B Ranocha fluxes (R3) of `me` with the job states, straight-line in the common case: both
 // log means take the Taylor branch; a warp-uniform fallback recomputes the members that need the
 // log branch (R5).  F[b][v] = f#(me, other_b, n_b).
-template <int DIM, int B>
+// CHK = false: the caller guarantees that every pair of the element takes the Taylor branch of
+// both logarithmic means (element-wide bound on the spread of rho and beta), so the branch test
+// is dropped -- the arithmetic is identical to the checked path for such pairs.
+template <int DIM, int B, bool CHK = true>
 __device__ __forceinline__ void flux_batch(const NodeState& me, const Job<DIM>* jb, double gm1inv,
                                            double (*F)[DIM + 2]) {
   NodeState o[B];
@@ -189,9 +192,9 @@ __device__ __forceinline__ void flux_batch(const NodeState& me, const Job<DIM>* 
     const double sb = me.b + o[t].b, isb = rcp_nr(sb), ub = (me.b - o[t].b) * isb;
     f2b[t] = ub * ub;
     ib[t] = (2.0 + f2b[t] * (2.0 / 3.0 + f2b[t] * (2.0 / 5.0 + f2b[t] * (2.0 / 7.0)))) * isb;
-    need |= (f2r[t] >= 1e-4) | (f2b[t] >= 1e-4);
+    if constexpr (CHK) need |= (f2r[t] >= 1e-4) | (f2b[t] >= 1e-4);
   }
-  if (__any_sync(0xffffffffu, need)) {
+  if (CHK && __any_sync(0xffffffffu, need)) {
 #pragma unroll
     for (int t = 0; t < B; ++t) {
       if (f2r[t] >= 1e-4) rl[t] = (o[t].r - me.r) / log(o[t].r / me.r);
@@ -310,13 +313,39 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   };
   stamp(0);
   mbar_wait(&k2_barA, it & 1);
-  for (int i = tid; i < Nq; i += NT) sP[(DIM + 2) * Nq + i] = sP[i] / sP[(DIM + 1) * Nq + i];
+  // beta = rho / p, and the element-wide spread of rho and beta: when (max - min) < 0.0099 (max +
+  // min) for both, every pair has f2 = ((x - y) / (x + y))^2 < 1e-4, i.e. takes the Taylor branch
+  double mm[4] = {1e300, -1e300, 1e300, -1e300};  // rho min, max, beta min, max
+  for (int i = tid; i < Nq; i += NT) {
+    const double r = sP[i], b = r / sP[(DIM + 1) * Nq + i];
+    sP[(DIM + 2) * Nq + i] = b;
+    mm[0] = fmin(mm[0], r), mm[1] = fmax(mm[1], r), mm[2] = fmin(mm[2], b), mm[3] = fmax(mm[3], b);
+  }
   for (int fz = tid; fz < NF; fz += NT) {
     const double* q = fP + (fz / Nqf) * NC * Nqf + fz % Nqf;
-    fB[fz] = q[0] / q[(DIM + 1) * Nqf];
+    const double r = q[0], b = r / q[(DIM + 1) * Nqf];
+    fB[fz] = b;
+    mm[0] = fmin(mm[0], r), mm[1] = fmax(mm[1], r), mm[2] = fmin(mm[2], b), mm[3] = fmax(mm[3], b);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mm[0] = fmin(mm[0], __shfl_xor_sync(0xffffffffu, mm[0], o));
+    mm[1] = fmax(mm[1], __shfl_xor_sync(0xffffffffu, mm[1], o));
+    mm[2] = fmin(mm[2], __shfl_xor_sync(0xffffffffu, mm[2], o));
+    mm[3] = fmax(mm[3], __shfl_xor_sync(0xffffffffu, mm[3], o));
+  }
+  __shared__ double red_mm[W::NW][4];
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red_mm[warp][q] = mm[q];
   mbar_wait(&k2_barB, it & 1);  // f* is updated in place by the passes
   __syncthreads();
+#pragma unroll 1
+  for (int w = 0; w < W::NW; ++w) {
+    mm[0] = fmin(mm[0], red_mm[w][0]), mm[1] = fmax(mm[1], red_mm[w][1]);
+    mm[2] = fmin(mm[2], red_mm[w][2]), mm[3] = fmax(mm[3], red_mm[w][3]);
+  }
+  const bool all_taylor = (mm[1] - mm[0]) < 0.0099 * (mm[1] + mm[0]) && (mm[3] - mm[2]) < 0.0099 * (mm[3] + mm[2]);
   stamp(1);
 
   auto state_at = [&](int i) {
@@ -331,8 +360,9 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   auto Gat = [&](int l, int m, int i) { return sG[(l * DIM + m) * Nq + i]; };
 
   // ---- direction passes, one specialisation per direction k ----
-  auto pass = [&](auto kc) {
+  auto pass = [&](auto kc, auto tc) {
     constexpr int k = decltype(kc)::value;
+    constexpr bool CHK = !decltype(tc)::value;
     constexpr int stride = k == 0 ? 1 : (k == 1 ? N : N * N);
 #pragma unroll 1
     for (int slot = warp; slot < W::SLOTS; slot += W::NW) {
@@ -413,7 +443,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           }
         }
         double Fs[W::VB][NC];
-        flux_batch<DIM, W::VB>(me, jv, gm1inv, Fs);
+        flux_batch<DIM, W::VB, CHK>(me, jv, gm1inv, Fs);
 #pragma unroll
         for (int t = 0; t < W::VB; ++t) {
           const int s = s0 + t;
@@ -475,14 +505,14 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           fjob(jf[0], 1, cb, tlR[ca] * tB[1 * Nqf + cb], gtn);
           fjob(jf[1], 2, cb, tlL[ca] * tB[2 * Nqf + cb], gtn3);
           double Fc[2][NC];
-          flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
+          flux_batch<DIM, 2, CHK>(me, jf, gm1inv, Fc);
           line_sums(Fc[0], [&](int Lq, int v) { return fS + (1 * NC + v) * Nqf + Lq; });
           line_sums(Fc[1], [&](int Lq, int v) { return fS + (2 * NC + v) * Nqf + Lq; });
         } else {  // eta2 = -1 (facet 1): facet node a
           double gtn[2] = {-gl[1][0], -gl[1][1]};
           fjob(jf[0], 0, ca, tlL[cb] * tB[0 * Nqf + ca], gtn);
           double Fc[1][NC];
-          flux_batch<DIM, 1>(me, jf, gm1inv, Fc);
+          flux_batch<DIM, 1, CHK>(me, jf, gm1inv, Fc);
           line_sums(Fc[0], [&](int Lq, int v) { return fS + (0 * NC + v) * Nqf + Lq; });
         }
       } else {
@@ -499,7 +529,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           fjob(jf[0], 1, f, tlR[ca] * tB[1 * Nqf + f], gtn);
           fjob(jf[1], 2, f, tlL[ca] * tB[2 * Nqf + f], gtn3);
           double Fc[2][NC];
-          flux_batch<DIM, 2>(me, jf, gm1inv, Fc);
+          flux_batch<DIM, 2, CHK>(me, jf, gm1inv, Fc);
           line_sums(Fc[0], [&](int Lq, int v) { return fS + (1 * NC + v) * Nqf + Lq; });
           line_sums(Fc[1], [&](int Lq, int v) { return fS + (2 * NC + v) * Nqf + Lq; });
         } else if (k == 1) {  // facet 1 (eta2 = -1): node (a, c) = line; facet 4 (eta3 = -1): nodes (a, j)
@@ -510,7 +540,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
             Job<DIM> j1[1];
             fjob(j1[0], 0, f, tlL[cb] * tB[0 * Nqf + f], gtn);
             double F1[1][NC];
-            flux_batch<DIM, 1>(me, j1, gm1inv, F1);
+            flux_batch<DIM, 1, CHK>(me, j1, gm1inv, F1);
             line_sums(F1[0], [&](int Lq, int v) { return fS + (0 * NC + v) * Nqf + Lq; });
           }
           // facet 4, rotating schedule: at step t lane pos pairs its node (a, b = pos, c) with the
@@ -531,7 +561,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
               fjob(jq[tt], 3, f4, t < N ? tli4[jf * N + cb] * tl3[cc] * tB[3 * Nqf + f4] : 0.0, gt4);
             }
             double Fb[2][NC];
-            flux_batch<DIM, 2>(me, jq, gm1inv, Fb);
+            flux_batch<DIM, 2, CHK>(me, jq, gm1inv, Fb);
 #pragma unroll
             for (int tt = 0; tt < 2; ++tt) {
               const int t = t0 + tt;
@@ -565,9 +595,15 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     __syncthreads();
     stamp(2 + k);
   };
-  pass(std::integral_constant<int, 0>{});
-  pass(std::integral_constant<int, 1>{});
-  if constexpr (DIM == 3) pass(std::integral_constant<int, 2>{});
+  auto passes = [&](auto tc) {
+    pass(std::integral_constant<int, 0>{}, tc);
+    pass(std::integral_constant<int, 1>{}, tc);
+    if constexpr (DIM == 3) pass(std::integral_constant<int, 2>{}, tc);
+  };
+  if (all_taylor)  // uniform over the CTA
+    passes(std::true_type{});
+  else
+    passes(std::false_type{});
   // states, metrics and facet inputs are dead: the next element's copies land during the epilogue
   if (tid == 0 && has_next) issue_A(elem_of(nidx));
   if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
