@@ -63,7 +63,7 @@ struct Rhs2Smem {
   static constexpr int o_tb = 0, o_ps = ev2(o_tb + TB), o_pr = ev2(o_ps + PS), o_g = o_pr + PR, o_r = ev2(o_g + GG),
                        o_pt = ev2(o_r + RR), o_fp = ev2(o_pt + PB), o_fb = ev2(o_fp + FP),
                        o_fj = ev2(o_fb + FB), o_fs = ev2(o_fj + FJ), o_sc = ev2(o_fs + FS), o_um = o_sc, o_wj = ev2(o_sc + SCU),
-                       total = ev2(o_wj + WJN);
+                       total = ev2(o_wj + 2 * ev2(WJN));  // W/J~ double-buffered by element parity
   static_assert(S::PRS <= PR, "prim copy");
   static_assert(total * 8 <= 227 * 1024 - 256, "shared memory");
 };
@@ -264,7 +264,6 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   double* fB = smk2 + L::o_fb;  // [Nf*Nqf] facet beta
   double* fJ = smk2 + L::o_fj;  // [Nf][DIM][Nqf] J n
   double* fS = smk2 + L::o_fs;  // [Nf][NC][Nqf] B J_f f*, then s = B J_f f* - C^T 1
-  double* sWJ = smk2 + L::o_wj + L::WJOFF;  // [Nq] W / J~
   double* tb = smk2 + L::o_tb;
   double* tQ1 = tb;
   double* tA1 = tQ1 + N * N;
@@ -285,21 +284,21 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
   auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
   // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers
-  auto issue_A = [&](int64_t e) {
-    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8;
+  auto issue_A = [&](int64_t e, unsigned buf) {
+    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8, bW = L::WJN * 8;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&k2_barA, bP + bG + bF + bJ);
+    mbar_expect_tx(&k2_barA, bP + bG + bF + bJ + bW);
     bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &k2_barA);
     bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &k2_barA);
     bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &k2_barA);
     bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &k2_barA);
+    bulk_g2s(smk2 + L::o_wj + buf * ev2(L::WJN), A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barA);
   };
   auto issue_B = [&](int64_t e) {
-    constexpr unsigned bS = L::FS * 8, bW = L::WJN * 8;
+    constexpr unsigned bS = L::FS * 8;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&k2_barB, bS + bW);
+    mbar_expect_tx(&k2_barB, bS);
     bulk_g2s(fS, A.fstar + (size_t)e * L::FS, bS, &k2_barB);
-    bulk_g2s(smk2 + L::o_wj, A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barB);
   };
   const int grp = lane / N, pos = lane - grp * N;
   const bool lane_ok = grp < W::LPW;
@@ -316,23 +315,32 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   // beta = rho / p, and the element-wide spread of rho and beta: when (max - min) < 0.0099 (max +
   // min) for both, every pair has f2 = ((x - y) / (x + y))^2 < 1e-4, i.e. takes the Taylor branch
   double mm[4] = {1e300, -1e300, 1e300, -1e300};  // rho min, max, beta min, max
+  auto upd = [&](double r, double b) {
+    mm[0] = r < mm[0] ? r : mm[0];
+    mm[1] = r > mm[1] ? r : mm[1];
+    mm[2] = b < mm[2] ? b : mm[2];
+    mm[3] = b > mm[3] ? b : mm[3];
+  };
   for (int i = tid; i < Nq; i += NT) {
     const double r = sP[i], b = r / sP[(DIM + 1) * Nq + i];
     sP[(DIM + 2) * Nq + i] = b;
-    mm[0] = fmin(mm[0], r), mm[1] = fmax(mm[1], r), mm[2] = fmin(mm[2], b), mm[3] = fmax(mm[3], b);
+    upd(r, b);
   }
   for (int fz = tid; fz < NF; fz += NT) {
     const double* q = fP + (fz / Nqf) * NC * Nqf + fz % Nqf;
     const double r = q[0], b = r / q[(DIM + 1) * Nqf];
     fB[fz] = b;
-    mm[0] = fmin(mm[0], r), mm[1] = fmax(mm[1], r), mm[2] = fmin(mm[2], b), mm[3] = fmax(mm[3], b);
+    upd(r, b);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    mm[0] = fmin(mm[0], __shfl_xor_sync(0xffffffffu, mm[0], o));
-    mm[1] = fmax(mm[1], __shfl_xor_sync(0xffffffffu, mm[1], o));
-    mm[2] = fmin(mm[2], __shfl_xor_sync(0xffffffffu, mm[2], o));
-    mm[3] = fmax(mm[3], __shfl_xor_sync(0xffffffffu, mm[3], o));
+    double t[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] = shfl_d(mm[q], lane ^ o);
+    mm[0] = t[0] < mm[0] ? t[0] : mm[0];
+    mm[1] = t[1] > mm[1] ? t[1] : mm[1];
+    mm[2] = t[2] < mm[2] ? t[2] : mm[2];
+    mm[3] = t[3] > mm[3] ? t[3] : mm[3];
   }
   __shared__ double red_mm[W::NW][4];
   if (lane == 0)
@@ -340,10 +348,12 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     for (int q = 0; q < 4; ++q) red_mm[warp][q] = mm[q];
   mbar_wait(&k2_barB, it & 1);  // f* is updated in place by the passes
   __syncthreads();
-#pragma unroll 1
+#pragma unroll
   for (int w = 0; w < W::NW; ++w) {
-    mm[0] = fmin(mm[0], red_mm[w][0]), mm[1] = fmax(mm[1], red_mm[w][1]);
-    mm[2] = fmin(mm[2], red_mm[w][2]), mm[3] = fmax(mm[3], red_mm[w][3]);
+    mm[0] = red_mm[w][0] < mm[0] ? red_mm[w][0] : mm[0];
+    mm[1] = red_mm[w][1] > mm[1] ? red_mm[w][1] : mm[1];
+    mm[2] = red_mm[w][2] < mm[2] ? red_mm[w][2] : mm[2];
+    mm[3] = red_mm[w][3] > mm[3] ? red_mm[w][3] : mm[3];
   }
   const bool all_taylor = (mm[1] - mm[0]) < 0.0099 * (mm[1] + mm[0]) && (mm[3] - mm[2]) < 0.0099 * (mm[3] + mm[2]);
   stamp(1);
@@ -605,7 +615,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   else
     passes(std::false_type{});
   // states, metrics and facet inputs are dead: the next element's copies land during the epilogue
-  if (tid == 0 && has_next) issue_A(elem_of(nidx));
+  if (tid == 0 && has_next) issue_A(elem_of(nidx), (it + 1) & 1);
   if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
     for (int q = tid; q < NC * N * N; q += NT) {
       const int v = q / (N * N), jf = (q / N) % N, a = q % N;
@@ -648,6 +658,9 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   }
   __syncthreads();
   stamp(7);
+  // the interface fluxes are consumed: the next element's copy lands during the transforms
+  if (tid == 0 && has_next) issue_B(elem_of(nidx));
+  const double* sWJ = smk2 + L::o_wj + (it & 1) * ev2(L::WJN) + L::WJOFF;  // [Nq] W / J~
 
   // ---- d u~/dt = V^T W/J~ V (V^T r), transforms in place in sR ----
   // ping-pong between sR and the dead facet-4 partial buffer pt (both [NC][Nq]); 3D steps may
@@ -698,8 +711,6 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   else
     nodal_to_modal<DIM, N, NC>(T, pt, sU, sR, nullptr, sWJ);
   stamp(10);
-  // f* and W / J~ are consumed: the next element's copies land during its passes
-  if (tid == 0 && has_next) issue_B(elem_of(nidx));
   const size_t base = (size_t)e * NC * Np;
   const double dt = A.dt;
   for (int kk = tid; kk < NC * Np; kk += NT) {
@@ -745,7 +756,6 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, const
   double* fB = smk2 + L::o_fb;  // [Nf*Nqf] facet beta
   double* fJ = smk2 + L::o_fj;  // [Nf][DIM][Nqf] J n
   double* fS = smk2 + L::o_fs;  // [Nf][NC][Nqf] B J_f f*, then s = B J_f f* - C^T 1
-  double* sWJ = smk2 + L::o_wj + L::WJOFF;  // [Nq] W / J~
   double* tb = smk2 + L::o_tb;
   double* tQ1 = tb;
   double* tA1 = tQ1 + N * N;
@@ -766,28 +776,28 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, const
   const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
   auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
   // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers
-  auto issue_A = [&](int64_t e) {
-    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8;
+  auto issue_A = [&](int64_t e, unsigned buf) {
+    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8, bW = L::WJN * 8;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&k2_barA, bP + bG + bF + bJ);
+    mbar_expect_tx(&k2_barA, bP + bG + bF + bJ + bW);
     bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &k2_barA);
     bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &k2_barA);
     bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &k2_barA);
     bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &k2_barA);
+    bulk_g2s(smk2 + L::o_wj + buf * ev2(L::WJN), A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barA);
   };
   auto issue_B = [&](int64_t e) {
-    constexpr unsigned bS = L::FS * 8, bW = L::WJN * 8;
+    constexpr unsigned bS = L::FS * 8;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&k2_barB, bS + bW);
+    mbar_expect_tx(&k2_barB, bS);
     bulk_g2s(fS, A.fstar + (size_t)e * L::FS, bS, &k2_barB);
-    bulk_g2s(smk2 + L::o_wj, A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barB);
   };
   // ---- per-CTA: barriers, first element's copies, constant tables ----
   if (tid == 0) {
     mbar_init(&k2_barA, 1);
     mbar_init(&k2_barB, 1);
     if ((int64_t)blockIdx.x < A.n_elem) {
-      issue_A(elem_of(blockIdx.x));
+      issue_A(elem_of(blockIdx.x), 0);
       issue_B(elem_of(blockIdx.x));
     }
   }
