@@ -234,8 +234,11 @@ __device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const d
       x1[i] *= ok ? sc1[i * sin] : 0.0;
     }
   }
-#pragma unroll 1
-  for (int o0 = 0; o0 < no; o0 += OC) {
+  // all output chunks in flight (independent chains); for N a multiple of OC ptxas hoists every
+  // table load of every chunk (register blow-up), so the chunks stay sequential there
+#pragma unroll(N % OC ? N : 1)
+  for (int o0 = 0; o0 < N; o0 += OC) {
+    if (o0 >= no) break;
     double a0[OC], a1[OC];
 #pragma unroll
     for (int q = 0; q < OC; ++q) a0[q] = a1[q] = 0.0;
@@ -276,8 +279,66 @@ __device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const d
   }
 }
 
+// K fibers per work item (the flattened steps): x_k = in[k][i sin] (* sc[k][i sin]), outputs
+// out[k][o sout] for k < nk; same arithmetic as fiber2 (K = 2) with the table loads shared K ways.
+template <int N, bool TR, int K>
+__device__ __forceinline__ void fiberK(const double* ps, const double* const* in, int sin, const double* const* sc,
+                                       double* const* out, int sout, int nk) {
+  constexpr int NP = psi_np<N>(), OC = 4;
+  double x[K][N];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      x[k][i] = in[k][i * sin];
+      if (sc) x[k][i] *= sc[k][i * sin];
+    }
+#pragma unroll(N % OC ? N : 1)
+  for (int o0 = 0; o0 < N; o0 += OC) {  // output chunks in flight (see fiber2)
+    double a[K][OC];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int q = 0; q < OC; ++q) a[k][q] = 0.0;
+    if constexpr (!TR) {
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int q2 = 0; q2 < OC / 2; ++q2) {
+          const double2 pv = *reinterpret_cast<const double2*>(ps + i * NP + o0 + 2 * q2);
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            a[k][2 * q2] = fma(pv.x, x[k][i], a[k][2 * q2]);
+            a[k][2 * q2 + 1] = fma(pv.y, x[k][i], a[k][2 * q2 + 1]);
+          }
+        }
+    } else {
+#pragma unroll
+      for (int q = 0; q < OC; ++q) {
+        const double* row = ps + (o0 + q) * NP;
+#pragma unroll
+        for (int i2 = 0; i2 < NP / 2; ++i2) {
+          const double2 pv = *reinterpret_cast<const double2*>(row + 2 * i2);
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            a[k][q] = fma(pv.x, x[k][2 * i2], a[k][q]);
+            if (2 * i2 + 1 < N) a[k][q] = fma(pv.y, x[k][2 * i2 + 1], a[k][q]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < OC; ++q) {
+      if (o0 + q >= N) break;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (k < nk) out[k][(o0 + q) * sout] = a[k][q];
+    }
+  }
+}
+
 // u = V u~ (modal [NV][Np] -> nodal [NV][Nq]); t1, t2 scratch (t1_size, t2_size)
-template <int DIM, int N, int NV>
+template <int DIM, int N, int NV, int FB = 2>
 __device__ void modal_to_nodal(const PsiS& T, const double* um, double* un, double* t1, double* t2) {
   using S = Sz<DIM, N>;
   constexpr int P = N - 1, NPAIR = S::NPAIR, Np = S::Np, Nq = S::Nq, NVP = (NV + 1) / 2;
@@ -318,13 +379,21 @@ __device__ void modal_to_nodal(const PsiS& T, const double* um, double* un, doub
                 nullptr, nullptr, t2 + ((v0 * N + a1) * N + c0) * N, t2 + ((v1 * N + a1) * N + c1) * N, 1, q1 != q0);
     }
     __syncthreads();
-    // u[v][a + N bc] = sum_a1 psi1[a1][a] t2[v][a1][bc]; items pairs of (v, bc) fibers
-    constexpr int NFB = NV * N * N;
-    for (int it = tid; it < (NFB + 1) / 2; it += nt) {
-      const int q0 = it, q1 = it + (NFB + 1) / 2 < NFB ? it + (NFB + 1) / 2 : it;
-      const int v0 = q0 / (N * N), bc0 = q0 - v0 * N * N, v1 = q1 / (N * N), bc1 = q1 - v1 * N * N;
-      fiber2<N, false>(T.p1, N, N, t2 + v0 * Nq + bc0, t2 + v1 * Nq + bc1, N * N, nullptr, nullptr, un + v0 * Nq + N * bc0,
-                un + v1 * Nq + N * bc1, 1, q1 != q0);
+    // u[v][a + N bc] = sum_a1 psi1[a1][a] t2[v][a1][bc]; items of FB (v, bc) fibers H apart
+    constexpr int NFB = NV * N * N, H = (NFB + FB - 1) / FB;
+    for (int it = tid; it < H; it += nt) {
+      const double* in[FB];
+      double* out[FB];
+      int nk = 0;
+#pragma unroll
+      for (int k = 0; k < FB; ++k) {
+        const int q = it + k * H < NFB ? it + k * H : it;
+        nk += it + k * H < NFB;
+        const int v = q / (N * N), bc = q - v * N * N;
+        in[k] = t2 + v * Nq + bc;
+        out[k] = un + v * Nq + N * bc;
+      }
+      fiberK<N, false, FB>(T.p1, in, N * N, nullptr, out, 1, nk);
     }
     __syncthreads();
   }
@@ -332,7 +401,7 @@ __device__ void modal_to_nodal(const PsiS& T, const double* um, double* un, doub
 }
 
 // u~ = V^T (scale o y) (nodal [NV][Nq] -> modal [NV][Np]); scale: optional per-node factor [Nq]
-template <int DIM, int N, int NV>
+template <int DIM, int N, int NV, int FB = 2>
 __device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, double* t1, double* t2,
                                const double* scale = nullptr) {
   using S = Sz<DIM, N>;
@@ -356,13 +425,23 @@ __device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, doubl
     }
     __syncthreads();
   } else {
-    // s2[v][a1][bc] = sum_a psi1[a1][a] y[v][a + N bc]; items pairs of (v, bc) fibers
-    constexpr int NFB = NV * N * N;
-    for (int it = tid; it < (NFB + 1) / 2; it += nt) {
-      const int q0 = it, q1 = it + (NFB + 1) / 2 < NFB ? it + (NFB + 1) / 2 : it;
-      const int v0 = q0 / (N * N), bc0 = q0 - v0 * N * N, v1 = q1 / (N * N), bc1 = q1 - v1 * N * N;
-      fiber2<N, true>(T.p1, N, N, y + v0 * Nq + N * bc0, y + v1 * Nq + N * bc1, 1, scale ? scale + N * bc0 : nullptr,
-                      scale ? scale + N * bc1 : nullptr, t2 + v0 * Nq + bc0, t2 + v1 * Nq + bc1, N * N, q1 != q0);
+    // s2[v][a1][bc] = sum_a psi1[a1][a] y[v][a + N bc]; items of FB (v, bc) fibers H apart
+    constexpr int NFB = NV * N * N, H = (NFB + FB - 1) / FB;
+    for (int it = tid; it < H; it += nt) {
+      const double* in[FB];
+      const double* sc[FB];
+      double* out[FB];
+      int nk = 0;
+#pragma unroll
+      for (int k = 0; k < FB; ++k) {
+        const int q = it + k * H < NFB ? it + k * H : it;
+        nk += it + k * H < NFB;
+        const int v = q / (N * N), bc = q - v * N * N;
+        in[k] = y + v * Nq + N * bc;
+        sc[k] = scale ? scale + N * bc : nullptr;
+        out[k] = t2 + v * Nq + bc;
+      }
+      fiberK<N, true, FB>(T.p1, in, 1, scale ? sc : nullptr, out, N * N, nk);
     }
     __syncthreads();
     // s1[v][pr(a1,a2)][c] = sum_b psi2[a1][a2][b] s2[v][a1][c][b]; items (a1, pair of (v, c) fibers)

@@ -667,7 +667,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   // write their second scratch over the already consumed input
   const PsiS T = psi_tables<DIM, N>(smk2 + L::o_ps);
   if constexpr (DIM == 3)
-    nodal_to_modal<DIM, N, NC>(T, sR, sU, sR, pt);
+    nodal_to_modal<DIM, N, NC, 2>(T, sR, sU, sR, pt);
   else
     nodal_to_modal<DIM, N, NC>(T, sR, sU, pt, nullptr);
   stamp(8);
@@ -702,12 +702,12 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     __syncthreads();
   }
   if constexpr (DIM == 3)
-    modal_to_nodal<DIM, N, NC>(T, sU, pt, pt, sR);
+    modal_to_nodal<DIM, N, NC, 2>(T, sU, pt, pt, sR);
   else
     modal_to_nodal<DIM, N, NC>(T, sU, pt, sR, nullptr);
   stamp(9);
   if constexpr (DIM == 3)
-    nodal_to_modal<DIM, N, NC>(T, pt, sU, pt, sR, sWJ);  // W / J~ fused into the loads
+    nodal_to_modal<DIM, N, NC, 2>(T, pt, sU, pt, sR, sWJ);  // W / J~ fused into the loads
   else
     nodal_to_modal<DIM, N, NC>(T, pt, sU, sR, nullptr, sWJ);
   stamp(10);
