@@ -247,6 +247,9 @@ def run(args):
     import es_inputs as I
     import paper_2312_07874_b200 as es
     dim, M, p, L, warp, kind, fm, desc = CONFIGS[args.config]
+    if args.p:
+        p = args.p  # degree sweep on the same mesh (BASELINE C3: p = 2, 4, 6, 8, 10)
+        desc = f"{desc} [degree override p={p}]"
     mesh = I.split_cartesian(dim, M, L)
     w = {"bj": I.bj_warp(dim, L, M), "none": None}.get(warp)
     nccl_id = None
@@ -401,6 +404,7 @@ def main():
     ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--p", type=int, default=0, help="override the configuration's polynomial degree")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
