@@ -95,43 +95,8 @@ struct IfaceArgs {
 };
 
 // ------------------------------------------------------------------------------------------------
-// physics (reading R3 for the energy component, R5 for the log mean)
+// physics: the two-point flux and the logarithmic mean live in rhs2.cuh
 // ------------------------------------------------------------------------------------------------
-__device__ __forceinline__ double ln_mean(double x, double y) {
-  double f2 = (x * (x - 2.0 * y) + y * y) / (x * (x + 2.0 * y) + y * y);
-  if (f2 < 1e-4) return (x + y) / (2.0 + f2 * (2.0 / 3.0 + f2 * (2.0 / 5.0 + f2 * (2.0 / 7.0))));
-  return (y - x) / log(y / x);
-}
-__device__ __forceinline__ double inv_ln_mean(double x, double y) {
-  double f2 = (x * (x - 2.0 * y) + y * y) / (x * (x + 2.0 * y) + y * y);
-  if (f2 < 1e-4) return (2.0 + f2 * (2.0 / 3.0 + f2 * (2.0 / 5.0 + f2 * (2.0 / 7.0)))) / (x + y);
-  return log(y / x) / (y - x);
-}
-
-// Ranocha EC flux in direction n: F = sum_m n_m f#_m(a, b)   (P:834 + R3)
-template <int DIM>
-__device__ __forceinline__ void ec_flux(double ra, const double* va, double pa, double ba, double rb,
-                                        const double* vb, double pb, double bb, const double* n,
-                                        double gm1inv, double* F) {
-  double rho_ln = ln_mean(ra, rb);
-  double ib_ln = inv_ln_mean(ba, bb);
-  double vn = 0.0, van = 0.0, vbn = 0.0, vdot = 0.0, vav[DIM];
-#pragma unroll
-  for (int m = 0; m < DIM; ++m) {
-    vav[m] = 0.5 * (va[m] + vb[m]);
-    vn += vav[m] * n[m];
-    van += va[m] * n[m];
-    vbn += vb[m] * n[m];
-    vdot += va[m] * vb[m];
-  }
-  double pav = 0.5 * (pa + pb);
-  double fr = rho_ln * vn;
-  F[0] = fr;
-#pragma unroll
-  for (int m = 0; m < DIM; ++m) F[1 + m] = fr * vav[m] + pav * n[m];
-  F[DIM + 1] = fr * (0.5 * vdot + ib_ln * gm1inv) + 0.5 * (pa * vbn + pb * van);
-}
-
 // conservative variables from primitive (for the Lax-Friedrichs jump)
 template <int DIM>
 __device__ __forceinline__ void cons_of(double r, const double* v, double p, double gm1inv, double* U) {
@@ -725,15 +690,5 @@ __host__ __device__ constexpr size_t projnodal_smem_doubles() {
   return (size_t)S::NC * S::Nq + (size_t)S::NC * S::Np + t1_size<DIM, N>() + t2_size<DIM, N>() + 4 +
          psi_smem_doubles<DIM, N>();
 }
-
-// host-side launchers (defined in kernels_2d.cu / kernels_3d.cu)
-struct LaunchCfg {
-  cudaStream_t stream;
-};
-cudaError_t launch_project(int dim, int n, const DevRef& R, const ProjArgs& A, cudaStream_t st);
-cudaError_t launch_rhs(int dim, int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
-cudaError_t launch_iface(int dim, int n, const DevRef& R, const IfaceArgs& A, cudaStream_t st);
-cudaError_t launch_project_nodal(int dim, int n, const DevRef& R, int64_t ne, const double* un, double* um,
-                                 cudaStream_t st);
 
 }  // namespace esb
