@@ -65,7 +65,9 @@ typedef struct {
   double gamma;                         /* ratio of specific heats (1.4) */
   int interface_flux;                   /* 0 = entropy conservative, 1 = entropy stable */
   int rank, world;                      /* local elements [rank*N_e/world, (rank+1)*N_e/world) */
-  const unsigned char* nccl_unique_id;  /* 128-byte ncclUniqueId (world > 1), broadcast by caller */
+  const unsigned char* nccl_unique_id;  /* 128-byte ncclUniqueId (world > 1), broadcast by caller;
+                                           NULL with world > 1: the caller moves the halo itself
+                                           (es_rhs_stage1 / es_halo_buffer / es_rhs_stage2) */
   void* cuda_stream;                    /* cudaStream_t to launch on; NULL = a library stream */
   int device;                           /* CUDA device ordinal */
   int check_admissibility;              /* 1: es_rhs synchronises and returns ES_ERR_INADMISSIBLE */
@@ -88,6 +90,18 @@ es_status es_sizes(const es_context* ctx, int* Np, int* Nq, int* Nqf, int64_t* n
 es_status es_rhs(es_context* ctx, const double* u_modal, double* dudt_modal);
 /* Same, with HOST buffers: host->device copy, es_rhs, device->host copy, synchronised. */
 es_status es_rhs_host(es_context* ctx, const double* u_modal_host, double* dudt_modal_host);
+
+/* Two-stage RHS for callers that move the face-trace halo themselves (world > 1 without NCCL, e.g.
+ * several ranks in one process).  Stage 1: entropy projection of u_modal
+ * (device) and packing of the boundary traces; *send_buf receives the device send buffer: faces
+ * ordered by destination rank, then by (element, face) id, N_c*N_qf doubles each (counts from
+ * es_plan).  es_halo_buffer: device buffer where the caller places the received faces, ordered by
+ * source rank, then by the sender's (element, face) id.  Stage 2 (after the halo is in place and
+ * the caller has ordered it before the context stream): interface fluxes and the flux kernel ->
+ * dudt_modal (device).  All asynchronous on the context stream. */
+es_status es_rhs_stage1(es_context* ctx, const double* u_modal, double** send_buf);
+es_status es_halo_buffer(es_context* ctx, double** recv_buf);
+es_status es_rhs_stage2(es_context* ctx, double* dudt_modal);
 
 /* Library-owned RK state: copy in/out (device pointers, [n_local][N_c][N_p*]). */
 es_status es_set_state(es_context* ctx, const double* u_modal);

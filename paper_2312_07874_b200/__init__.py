@@ -68,6 +68,9 @@ es_node_coords = _sig("es_node_coords", _i, _vp, _vp)
 es_project_nodal = _sig("es_project_nodal", _i, _vp, _vp, _vp)
 es_element_geometry = _sig("es_element_geometry", _i, _vp, ctypes.c_int64, _dp, _dp, _dp)
 es_synchronize = _sig("es_synchronize", _i, _vp)
+es_rhs_stage1 = _sig("es_rhs_stage1", _i, _vp, _vp, ctypes.POINTER(_vp))
+es_halo_buffer = _sig("es_halo_buffer", _i, _vp, ctypes.POINTER(_vp))
+es_rhs_stage2 = _sig("es_rhs_stage2", _i, _vp, _vp)
 es_stream = _sig("es_stream", _vp, _vp)
 es_launch_count = _sig("es_launch_count", ctypes.c_int64, _vp)
 es_reset_launch_count = _sig("es_reset_launch_count", None, _vp)
@@ -196,6 +199,20 @@ class Context:
     # -- device-pointer API (torch CUDA tensors) --
     def rhs(self, u, dudt):
         self._check(es_rhs(self.h, _ptr(u), _ptr(dudt)))
+
+    def rhs_stage1(self, u):
+        """entropy projection + packed boundary traces; returns the device send-buffer address"""
+        b = _vp()
+        self._check(es_rhs_stage1(self.h, _ptr(u), ctypes.byref(b)))
+        return b.value
+
+    def halo_buffer(self):
+        b = _vp()
+        self._check(es_halo_buffer(self.h, ctypes.byref(b)))
+        return b.value
+
+    def rhs_stage2(self, dudt):
+        self._check(es_rhs_stage2(self.h, _ptr(dudt)))
 
     def rhs_host(self, u_host, dudt_host):
         self._check(es_rhs_host(self.h, _ptr(u_host), _ptr(dudt_host)))

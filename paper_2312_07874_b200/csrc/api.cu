@@ -51,6 +51,7 @@ struct es_context {
   double *geo_vol = nullptr, *geo_face = nullptr, *xq = nullptr, *jt = nullptr;
   double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr, *fstar = nullptr;
   int num_sms = 148, proj_ctas = 296;
+  bool external = false;  // world > 1 without NCCL: the caller moves the halo (es_rhs_stage1/2)
   int64_t *face_slot = nullptr, *d_interior = nullptr, *d_boundary = nullptr, *d_send = nullptr;
   int* face_reflect = nullptr;
   int* bad = nullptr;
@@ -215,9 +216,9 @@ RhsArgs base_rhs_args(es_context* c) {
   return A;
 }
 
-// one right-hand side: projection, halo exchange overlapped with interior elements, then the
-// boundary elements
-es_status rhs_pass(es_context* c, const double* u, RhsArgs A, double* wt) {
+// first half of a right-hand side: entropy projection and, with remote neighbours, the packed
+// boundary traces (send buffer ordered by destination rank)
+es_status rhs_first(es_context* c, const double* u, double* wt) {
   TimedEvent te{};
   if (c->timing) {
     te = {get_event(c), get_event(c), 0};
@@ -228,15 +229,30 @@ es_status rhs_pass(es_context* c, const double* u, RhsArgs A, double* wt) {
     cudaEventRecord(te.b, c->stream);
     c->tev.push_back(te);
   }
-  if (c->world == 1) {
-    CK(run_iface(c, c->nloc, nullptr));
-    CK(run_rhs(c, A, c->nloc, nullptr));
-    return ES_OK;
+  if (c->world > 1) {
+    const int per_face = c->NC * c->Nqf;
+    const int64_t nsend = (int64_t)c->plan.send_slots.size();
+    CK(launch_pack(c->trace, c->d_send, nsend, per_face, c->send_buf, c->stream));
+    c->launches++;
   }
+  return ES_OK;
+}
+
+// second half: interface fluxes (halo slots filled) and the flux-differencing kernel
+es_status rhs_second(es_context* c, RhsArgs A) {
+  CK(run_iface(c, c->nloc, nullptr));
+  CK(run_rhs(c, A, c->nloc, nullptr));
+  return ES_OK;
+}
+
+// one right-hand side: projection, halo exchange overlapped with the interface fluxes of interior
+// elements, then the boundary elements' interface fluxes and the flux kernel
+es_status rhs_pass(es_context* c, const double* u, RhsArgs A, double* wt) {
+  if (c->external) return fail(c, ES_ERR_CONFIG, "world > 1 without NCCL: use es_rhs_stage1 / es_rhs_stage2");
+  es_status s0 = rhs_first(c, u, wt);
+  if (s0 != ES_OK) return s0;
+  if (c->world == 1) return rhs_second(c, A);
   const int per_face = c->NC * c->Nqf;
-  const int64_t nsend = (int64_t)c->plan.send_slots.size();
-  CK(launch_pack(c->trace, c->d_send, nsend, per_face, c->send_buf, c->stream));
-  c->launches++;
   CK(cudaEventRecord(c->ev_packed, c->stream));
   CK(cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
   NK(ncclGroupStart());
@@ -316,7 +332,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   if (c->d != 2 && c->d != 3) return fail(c, ES_ERR_CONFIG, "dim must be 2 or 3");
   if (!(c->gamma > 1.0)) return fail(c, ES_ERR_CONFIG, "gamma must exceed 1");
   if (c->rank < 0 || c->rank >= c->world) return fail(c, ES_ERR_ARG, "rank out of range");
-  if (c->world > 1 && !opt->nccl_unique_id) return fail(c, ES_ERR_ARG, "world > 1 needs nccl_unique_id");
+  c->external = c->world > 1 && !opt->nccl_unique_id;
   std::string err;
   if (!build_ref_tables(c->d, p, c->T, err)) return fail(c, ES_ERR_CONFIG, err);
   c->n = c->T.n;
@@ -440,9 +456,11 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   if (c->world > 1) {
     const size_t nsend = c->plan.send_slots.size();
     CK(cudaMalloc((void**)&c->send_buf, std::max<size_t>(nsend, 1) * c->NC * c->Nqf * sizeof(double)));
-    ncclUniqueId id;
-    std::memcpy(&id, opt->nccl_unique_id, sizeof(id));
-    NK(ncclCommInitRank(&c->comm, c->world, id, c->rank));
+    if (!c->external) {
+      ncclUniqueId id;
+      std::memcpy(&id, opt->nccl_unique_id, sizeof(id));
+      NK(ncclCommInitRank(&c->comm, c->world, id, c->rank));
+    }
   }
   return ES_OK;
 }
@@ -554,7 +572,7 @@ es_status es_entropy_production(es_context* c, const double* u, double* rate, do
   const int w = 2 + c->NC;
   CK(launch_reduce_parts(c->part, c->nloc, w, c->red, c->stream));
   c->launches++;
-  if (c->world > 1) NK(ncclAllReduce(c->red, c->red, w, ncclDouble, ncclSum, c->comm, c->stream));
+  if (c->world > 1 && c->comm) NK(ncclAllReduce(c->red, c->red, w, ncclDouble, ncclSum, c->comm, c->stream));
   double h[8] = {0};
   CK(cudaMemcpyAsync(h, c->red, w * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -670,6 +688,35 @@ es_status es_plan(int dim, int64_t ne, const int64_t* ev, int rank, int world, i
   if (recv_count) std::memcpy(recv_count, plan.recv_count.data(), plan.recv_count.size() * sizeof(int64_t));
   if (n_send) *n_send = (int64_t)plan.send_slots.size();
   if (n_halo) *n_halo = plan.n_halo;
+  return ES_OK;
+}
+
+es_status es_rhs_stage1(es_context* c, const double* u, double** send_buf) {
+  POISON_CHECK();
+  if (!u) return fail(c, ES_ERR_ARG, "null buffer");
+  CK(cudaSetDevice(c->device));
+  es_status s = rhs_first(c, u, nullptr);
+  if (s != ES_OK) return s;
+  if (send_buf) *send_buf = c->send_buf;
+  return ES_OK;
+}
+
+es_status es_halo_buffer(es_context* c, double** recv_buf) {
+  POISON_CHECK();
+  if (recv_buf) *recv_buf = c->trace + (size_t)c->nloc * c->Nf * c->NC * c->Nqf;
+  return ES_OK;
+}
+
+es_status es_rhs_stage2(es_context* c, double* dudt) {
+  POISON_CHECK();
+  if (!dudt) return fail(c, ES_ERR_ARG, "null buffer");
+  CK(cudaSetDevice(c->device));
+  RhsArgs A = base_rhs_args(c);
+  A.mode = 0;
+  A.out = dudt;
+  es_status s = rhs_second(c, A);
+  if (s != ES_OK) return s;
+  if (c->check_adm) return check_bad(c);
   return ES_OK;
 }
 
