@@ -187,8 +187,9 @@ __device__ __forceinline__ void flux_batch(const NodeState& me, const Job<DIM>* 
   for (int t = 0; t < B; ++t) {
     const double sr = me.r + o[t].r, isr = rcp_nr1(sr), ur = (me.r - o[t].r) * isr;
     f2r[t] = ur * ur;
-    const double g = f2r[t] * (1.0 / 3.0 + f2r[t] * (1.0 / 5.0 + f2r[t] * (1.0 / 7.0)));
-    rl[t] = sr * (0.5 * (1.0 + g * (-1.0 + g * (1.0 - g))));
+    // (x + y) / (2 P(f2)), P = 1 + f2/3 + f2^2/5 + f2^3/7, with 1/P = 1 - f2/3 - 4 f2^2/45
+    // - 44 f2^3/945 + O(f2^4) (the O(f2^4) term is below 3e-18 for f2 < 1e-4, R5)
+    rl[t] = sr * (0.5 + f2r[t] * (-1.0 / 6.0 + f2r[t] * (-2.0 / 45.0 + f2r[t] * (-22.0 / 945.0))));
     const double sb = me.b + o[t].b, isb = rcp_nr(sb), ub = (me.b - o[t].b) * isb;
     f2b[t] = ub * ub;
     ib[t] = (2.0 + f2b[t] * (2.0 / 3.0 + f2b[t] * (2.0 / 5.0 + f2b[t] * (2.0 / 7.0)))) * isb;
@@ -204,20 +205,20 @@ __device__ __forceinline__ void flux_batch(const NodeState& me, const Job<DIM>* 
 #pragma unroll
   for (int t = 0; t < B; ++t) {
     const double* n = jb[t].n;
-    double vn = 0.0, van = 0.0, vbn = 0.0, vdot = 0.0, vav[DIM];
+    // <v>.n = (v_a.n + v_b.n) / 2; <v_m> f = (v_a,m + v_b,m) f / 2
+    double van = 0.0, vbn = 0.0, vdot = 0.0;
 #pragma unroll
     for (int m = 0; m < DIM; ++m) {
-      vav[m] = 0.5 * (me.v[m] + o[t].v[m]);
-      vn += vav[m] * n[m];
       van += me.v[m] * n[m];
       vbn += o[t].v[m] * n[m];
       vdot += me.v[m] * o[t].v[m];
     }
     const double pav = 0.5 * (me.p + o[t].p);
-    const double fr = rl[t] * vn;
+    const double fr = rl[t] * (0.5 * (van + vbn));
+    const double hfr = 0.5 * fr;
     F[t][0] = fr;
 #pragma unroll
-    for (int m = 0; m < DIM; ++m) F[t][1 + m] = fr * vav[m] + pav * n[m];
+    for (int m = 0; m < DIM; ++m) F[t][1 + m] = hfr * (me.v[m] + o[t].v[m]) + pav * n[m];
     F[t][DIM + 1] = fr * (0.5 * vdot + ib[t] * gm1inv) + 0.5 * (me.p * vbn + o[t].p * van);
   }
 }
