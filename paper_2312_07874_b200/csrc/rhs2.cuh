@@ -29,7 +29,7 @@ struct Lw {  // line-group layout
   static constexpr int LPW = 32 / N;                         // lines per warp slot
   static constexpr int NL = DIM == 2 ? N : N * N;            // lines per direction
   static constexpr int SLOTS = (NL + LPW - 1) / LPW;         // warp slots per direction
-  static constexpr int NW = SLOTS <= 12 ? SLOTS : (SLOTS % 9 == 0 ? 9 : (SLOTS % 8 == 0 ? 8 : 12));
+  static constexpr int NW = SLOTS <= 12 ? SLOTS : 12;
   static constexpr int NT = NW * 32;
   static constexpr int NS = N / 2;                            // shifts
   static constexpr int VB = 2;  // volume pair jobs per flux batch (ILP vs registers: 4 spills at N = 9)
