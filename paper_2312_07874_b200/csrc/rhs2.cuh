@@ -440,8 +440,8 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
             if (k == 0) {
               const double cl = mk * 0.5 * tw[cb] * tw3[cc], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
 #pragma unroll
-              for (int m = 0; m < 3; ++m)
-                jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * ((gl[1][m] + gl[2][m]) + (Gat(1, m, j) + Gat(2, m, j)));
+              for (int m = 0; m < 3; ++m)  // metric row 1 holds g1 + g2 in this (last) pass
+                jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * (gl[1][m] + Gat(1, m, j));
             } else if (k == 1) {
               const double cl = mk * 0.5 * tw[ca] * tw3[cc], a2 = cl * tA2[ix], a3 = cl * tA3[ix];
 #pragma unroll
@@ -470,14 +470,16 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
       // -- facet-correction pairs along the same lines --
       // a facet job: state of facet node (z, f), normal coef (G_i^T nhat + J n_f)/2 with coefficient
       // coef = (R^T B)_if
-      auto fjob = [&](Job<DIM>& jb, int z, int f, double coef, const double* gtn) {
+      auto fjob_h = [&](Job<DIM>& jb, int z, int f, double c2, const double* gtn) {  // c2 = coef / 2, masked
         jb.base = fP + z * NC * Nqf;
         jb.bb = fB + z * Nqf;
         jb.stride = Nqf;
         jb.idx = f;
-        const double c2 = 0.5 * coef * vmask;
 #pragma unroll
         for (int m = 0; m < DIM; ++m) jb.n[m] = c2 * (gtn[m] + fJ[(z * DIM + m) * Nqf + f]);
+      };
+      auto fjob = [&](Job<DIM>& jb, int z, int f, double coef, const double* gtn) {
+        fjob_h(jb, z, f, 0.5 * coef * vmask, gtn);
       };
       // facet-side sums over each line group through the warp scratch, in lane order; dest(line, v)
       // returns where the sum of line `gq` goes (nullptr: discard)
@@ -533,7 +535,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           double gtn[3], gtn3[3];
 #pragma unroll
           for (int m = 0; m < 3; ++m) {
-            gtn[m] = (gl[0][m] + gl[1][m] + gl[2][m]) * r3;
+            gtn[m] = (gl[0][m] + gl[1][m]) * r3;  // row 1 = g1 + g2
             gtn3[m] = -gl[0][m];
           }
           Job<DIM> jf[2];
@@ -560,6 +562,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           double facc[NC];
 #pragma unroll
           for (int v = 0; v < NC; ++v) facc[v] = 0.0;
+          const double h3 = 0.5 * tl3[cc] * vmask;  // job-independent part of (R^T B)_if / 2
 #pragma unroll 1
           for (int t0 = 0; t0 < N; t0 += 2) {
             Job<DIM> jq[2];
@@ -569,7 +572,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
               int jf = pos + (t < N ? t : 0);
               if (jf >= N) jf -= N;
               const int f4 = ca + N * jf;
-              fjob(jq[tt], 3, f4, t < N ? tli4[jf * N + cb] * tl3[cc] * tB[3 * Nqf + f4] : 0.0, gt4);
+              fjob_h(jq[tt], 3, f4, t < N ? (h3 * tli4[jf * N + cb]) * tB[3 * Nqf + f4] : 0.0, gt4);
             }
             double Fb[2][NC];
             flux_batch<DIM, 2, CHK>(me, jq, gm1inv, Fb);
@@ -596,7 +599,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
       if (valid) {
 #pragma unroll
         for (int v = 0; v < NC; ++v) {
-          if (k == 0)
+          if (k == (DIM == 3 ? 1 : 0))  // the first pass executed
             sR[v * Nq + i] = acc[v];
           else
             sR[v * Nq + i] += acc[v];
@@ -606,10 +609,18 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     __syncthreads();
     stamp(2 + k);
   };
+  // 3D order 1, 2, 0: the eta1 pass only needs g0 and g1 + g2, summed in place once before it
   auto passes = [&](auto tc) {
-    pass(std::integral_constant<int, 0>{}, tc);
-    pass(std::integral_constant<int, 1>{}, tc);
-    if constexpr (DIM == 3) pass(std::integral_constant<int, 2>{}, tc);
+    if constexpr (DIM == 3) {
+      pass(std::integral_constant<int, 1>{}, tc);
+      pass(std::integral_constant<int, 2>{}, tc);
+      for (int q = tid; q < DIM * Nq; q += NT) sG[DIM * Nq + q] += sG[2 * DIM * Nq + q];
+      __syncthreads();
+      pass(std::integral_constant<int, 0>{}, tc);
+    } else {
+      pass(std::integral_constant<int, 0>{}, tc);
+      pass(std::integral_constant<int, 1>{}, tc);
+    }
   };
   if (all_taylor)  // uniform over the CTA
     passes(std::true_type{});
