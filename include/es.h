@@ -128,6 +128,13 @@ es_status es_node_coords(es_context* ctx, double* x_dev);
  * u_modal device [n_local][N_c][N_p*].  (Initial data; R18.) */
 es_status es_project_nodal(es_context* ctx, const double* u_nodal, double* u_modal);
 
+/* Evaluation at the volume quadrature nodes u = V u~: u_modal device [n_local][N_c][N_p*]
+ * -> u_nodal device [n_local][N_q][N_c].  (Error norms, output.) */
+es_status es_eval_nodal(es_context* ctx, const double* u_modal, double* u_nodal);
+/* Quadrature weights of the volume nodes in physical space, W J~: device [n_local][N_q];
+ * sum_k sum_i wj f(x_i) integrates f over the local elements (exact for the L2 norm of P_p data). */
+es_status es_node_weights(es_context* ctx, double* wj);
+
 /* Geometry of one local element copied to HOST buffers (tests): G [N_q][dim][dim] (G_lm),
  * Jn [N_f][N_qf][dim] = G^T nhat at facet nodes, Jt [N_q] = J~.  NULL = skip. */
 es_status es_element_geometry(es_context* ctx, int64_t local_element, double* G, double* Jn,

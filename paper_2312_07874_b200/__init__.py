@@ -66,6 +66,8 @@ es_entropy_production = _sig("es_entropy_production", _i, _vp, _vp, _dp, _dp, _d
 es_flux_counts = _sig("es_flux_counts", _i, _vp, _lp, _lp, _lp, _dp)
 es_node_coords = _sig("es_node_coords", _i, _vp, _vp)
 es_project_nodal = _sig("es_project_nodal", _i, _vp, _vp, _vp)
+es_eval_nodal = _sig("es_eval_nodal", _i, _vp, _vp, _vp)
+es_node_weights = _sig("es_node_weights", _i, _vp, _vp)
 es_element_geometry = _sig("es_element_geometry", _i, _vp, ctypes.c_int64, _dp, _dp, _dp)
 es_synchronize = _sig("es_synchronize", _i, _vp)
 es_rhs_stage1 = _sig("es_rhs_stage1", _i, _vp, _vp, ctypes.POINTER(_vp))
@@ -244,6 +246,12 @@ class Context:
 
     def project_nodal(self, un, um):
         self._check(es_project_nodal(self.h, _ptr(un), _ptr(um)))
+
+    def eval_nodal(self, um, un):
+        self._check(es_eval_nodal(self.h, _ptr(um), _ptr(un)))
+
+    def node_weights(self, wj):
+        self._check(es_node_weights(self.h, _ptr(wj)))
 
     def element_geometry(self, k):
         d = self.d

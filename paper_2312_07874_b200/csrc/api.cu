@@ -25,6 +25,8 @@ cudaError_t launch_iface_2d(int n, const DevRef& R, const IfaceArgs& A, cudaStre
 cudaError_t launch_iface_3d(int n, const DevRef& R, const IfaceArgs& A, cudaStream_t st);
 cudaError_t launch_projnodal_2d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st);
 cudaError_t launch_projnodal_3d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st);
+cudaError_t launch_evalnodal_2d(int n, const DevRef& R, int64_t ne, const double* um, double* un, cudaStream_t st);
+cudaError_t launch_evalnodal_3d(int n, const DevRef& R, int64_t ne, const double* um, double* un, cudaStream_t st);
 }  // namespace esb
 
 using namespace esb;
@@ -613,6 +615,26 @@ es_status es_project_nodal(es_context* c, const double* un, double* um) {
   c->launches++;
   CK(c->d == 2 ? launch_projnodal_2d(c->n, c->R, c->nloc, un, um, c->stream)
                : launch_projnodal_3d(c->n, c->R, c->nloc, un, um, c->stream));
+  return ES_OK;
+}
+
+es_status es_eval_nodal(es_context* c, const double* um, double* un) {
+  POISON_CHECK();
+  if (!um || !un) return fail(c, ES_ERR_ARG, "null buffer");
+  CK(cudaSetDevice(c->device));
+  c->launches++;
+  CK(c->d == 2 ? launch_evalnodal_2d(c->n, c->R, c->nloc, um, un, c->stream)
+               : launch_evalnodal_3d(c->n, c->R, c->nloc, um, un, c->stream));
+  return ES_OK;
+}
+
+es_status es_node_weights(es_context* c, double* wj) {
+  POISON_CHECK();
+  if (!wj) return fail(c, ES_ERR_ARG, "null buffer");
+  CK(cudaSetDevice(c->device));
+  const int NG = c->d * c->d, gvs = even_up((NG + 2) * c->Nq);
+  CK(cudaMemcpy2DAsync(wj, (size_t)c->Nq * sizeof(double), c->geo_vol + (size_t)NG * c->Nq, (size_t)gvs * sizeof(double),
+                       (size_t)c->Nq * sizeof(double), (size_t)c->nloc, cudaMemcpyDeviceToDevice, c->stream));
   return ES_OK;
 }
 

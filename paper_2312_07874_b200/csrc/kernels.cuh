@@ -684,6 +684,30 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT) project_nodal_kernel(DevRef R,
   for (int k = threadIdx.x; k < NC * Np; k += blockDim.x) um_out[(size_t)e * NC * Np + k] = um[k];
 }
 
+// modal -> nodal evaluation u = V u~ at the volume nodes, [ne][NC][Np] -> [ne][Nq][NC] (output)
+template <int DIM, int N>
+__global__ void __launch_bounds__(Sz<DIM, N>::NT) eval_nodal_kernel(DevRef R, int64_t ne, const double* um_in,
+                                                                 double* un) {
+  using S = Sz<DIM, N>;
+  constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np;
+  extern __shared__ __align__(16) double sm[];
+  constexpr int o_um = (NC * Nq + 1) & ~1, o_t1 = (o_um + NC * Np + 1) & ~1, o_t2 = (o_t1 + t1_size<DIM, N>() + 1) & ~1,
+                o_ps = (o_t2 + t2_size<DIM, N>() + 1) & ~1;
+  double* X = sm;
+  double* um = sm + o_um;
+  double* T1 = sm + o_t1;
+  double* T2 = sm + o_t2;
+  const PsiS T = stage_psi<DIM, N>(R, sm + o_ps);
+  const int64_t e = blockIdx.x;
+  for (int k = threadIdx.x; k < NC * Np; k += blockDim.x) um[k] = um_in[(size_t)e * NC * Np + k];
+  __syncthreads();
+  modal_to_nodal<DIM, N, NC>(T, um, X, T1, T2);
+  for (int it = threadIdx.x; it < NC * Nq; it += blockDim.x) {
+    const int v = it / Nq, i = it - v * Nq;
+    un[((size_t)e * Nq + i) * NC + v] = X[it];
+  }
+}
+
 template <int DIM, int N>
 __host__ __device__ constexpr size_t projnodal_smem_doubles() {
   using S = Sz<DIM, N>;

@@ -26,4 +26,7 @@ cudaError_t launch_iface_2d(int n, const DevRef& R, const IfaceArgs& A, cudaStre
 cudaError_t launch_projnodal_2d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st) {
   ES_CASES(do_projnodal, R, ne, un, um, st)
 }
+cudaError_t launch_evalnodal_2d(int n, const DevRef& R, int64_t ne, const double* um, double* un, cudaStream_t st) {
+  ES_CASES(do_evalnodal, R, ne, um, un, st)
+}
 }  // namespace esb

@@ -24,4 +24,7 @@ cudaError_t launch_iface_3d(int n, const DevRef& R, const IfaceArgs& A, cudaStre
 cudaError_t launch_projnodal_3d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st) {
   ES_CASES(do_projnodal, R, ne, un, um, st)
 }
+cudaError_t launch_evalnodal_3d(int n, const DevRef& R, int64_t ne, const double* um, double* un, cudaStream_t st) {
+  ES_CASES(do_evalnodal, R, ne, um, un, st)
+}
 }  // namespace esb

@@ -1,0 +1,58 @@
+"""The paper's accuracy experiment on the GPU path (Fig. 8): the
+density wave translates exactly with v = (1, ..., 1); the entropy-stable scheme converges
+at order ~p+1 in h.  Also: es_eval_nodal against the oracle's dense V, and es_node_weights
+integrating a constant to the domain measure.
+"""
+import math
+import os
+import sys
+
+import numpy as np
+import pytest
+
+import es_inputs as I
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+
+@pytest.fixture(scope="module")
+def es():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2312_07874_b200 as es
+    return es
+
+
+@pytest.mark.parametrize("d,p", [(2, 3), (3, 2)])
+def test_eval_nodal_and_weights(es, d, p):
+    L = 2.0
+    mesh = I.split_cartesian(d, 3, L)
+    w = I.paper_warp(d, L)
+    om = O.Mesh(mesh, p, warp=w)
+    u = I.perturb_modal(om.project(I.density_wave(om.node_coords(), L)), d, p, seed=4, amp=1e-2)
+    ctx = es.Context(mesh, p, warp=w)
+    ut = torch.from_numpy(u).cuda()
+    un = torch.empty((ctx.nloc, ctx.Nq, d + 2), dtype=torch.float64, device="cuda")
+    ctx.eval_nodal(ut, un)
+    wj = torch.empty((ctx.nloc, ctx.Nq), dtype=torch.float64, device="cuda")
+    ctx.node_weights(wj)
+    ctx.synchronize()
+    V = O.ref_get(d, p, "V")
+    ref = np.einsum("qk,evk->eqv", V, u)
+    assert np.abs(un.cpu().numpy() - ref).max() < 1e-13 * np.abs(ref).max()
+    # sum W J~ = |Omega| = L^d (the map is a bijection of the periodic box)
+    assert abs(float(wj.sum()) - L ** d) < 1e-12 * L ** d
+    for e in (0, 5):
+        assert np.allclose(wj[e].cpu().numpy(), O.ref_get(d, p, "W") * om.geometry(e)["Jt"], rtol=1e-13, atol=0)
+
+
+def test_density_wave_order(es):
+    import convergence as C
+    errs = [C.run_case(es, I, torch, 2, 2, M, 0.1, "paper")[0] for M in (4, 8, 16)]
+    orders = [math.log2(errs[k] / errs[k + 1]) for k in range(2)]
+    assert orders[-1] > 2.4, (errs, orders)  # p + 1 = 3 expected
