@@ -71,6 +71,10 @@ typedef struct {
   void* cuda_stream;                    /* cudaStream_t to launch on; NULL = a library stream */
   int device;                           /* CUDA device ordinal */
   int check_admissibility;              /* 1: es_rhs synchronises and returns ES_ERR_INADMISSIBLE */
+  int volume_mode;                      /* 0: line-wise flux differencing (the default);
+                                           1: ablation -- one flux per operator S^(l) with a
+                                           nonzero on the line, the paper's Eq. num_fluxes
+                                           iteration; same result up to rounding */
 } es_options;
 
 /* Builds tables, geometry (exact metrics in 2D, conservative curl metrics in 3D, P:345-364;
@@ -116,8 +120,9 @@ es_status es_step(es_context* ctx, double dt, int nsteps);
 es_status es_entropy_production(es_context* ctx, const double* u_modal, double* rate,
                                 double* abs_scale, double* conservation);
 
-/* Two-point flux evaluations per element and RHS (integers, exact): line-wise volume pairs,
- * facet-correction pairs, the Eq. num_fluxes count, interface evaluations per element. */
+/* Two-point flux evaluations per element and RHS (integers, exact): volume evaluations (line-wise
+ * pairs, or per-operator evaluations with volume_mode 1), facet-correction pairs, the Eq.
+ * num_fluxes count, interface evaluations per element. */
 es_status es_flux_counts(const es_context* ctx, int64_t* volume_pairs_per_el,
                          int64_t* facet_pairs_per_el, int64_t* eq56_per_el,
                          double* interface_per_el);

@@ -53,7 +53,8 @@ struct es_context {
   double *geo_vol = nullptr, *geo_face = nullptr, *xq = nullptr, *jt = nullptr;
   double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr, *fstar = nullptr;
   int num_sms = 148, proj_ctas = 296;
-  bool external = false;  // world > 1 without NCCL: the caller moves the halo (es_rhs_stage1/2)
+  bool external = false;
+  int eq56 = 0;  // volume_mode 1  // world > 1 without NCCL: the caller moves the halo (es_rhs_stage1/2)
   int64_t *face_slot = nullptr, *d_interior = nullptr, *d_boundary = nullptr, *d_send = nullptr;
   int* face_reflect = nullptr;
   int* bad = nullptr;
@@ -215,6 +216,7 @@ RhsArgs base_rhs_args(es_context* c) {
   A.dbg = c->dbg;
   A.fstar = c->fstar;
   A.max_ctas = c->num_sms;
+  A.eq56 = c->eq56;
   return A;
 }
 
@@ -328,6 +330,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   c->gamma = opt->gamma;
   c->es = opt->interface_flux ? 1 : 0;
   c->check_adm = opt->check_admissibility;
+  c->eq56 = opt->volume_mode == 1;
   c->rank = opt->rank;
   c->world = opt->world < 1 ? 1 : opt->world;
   c->device = opt->device;
@@ -589,12 +592,14 @@ es_status es_flux_counts(const es_context* c, int64_t* vol, int64_t* fac, int64_
   if (!c) return ES_ERR_ARG;
   int64_t n = c->n, q = c->p;
   if (c->d == 2) {
-    if (vol) *vol = q * n * n;                 // two eta-line directions, n(n-1)/2 pairs per line
+    // line-wise: one flux per pair on each eta line, n(n-1)/2 pairs per line, n lines per direction;
+    // Eq. num_fluxes mode: one per operator with a nonzero on the line (2 on eta1, 1 on eta2 lines)
+    if (vol) *vol = c->eq56 ? 3 * q * n * n / 2 : q * n * n;
     if (fac) *fac = 3 * n * n;                 // n volume nodes per facet node, 3 facets
     if (eq56) *eq56 = 3 * n * n * (q + 2) / 2; // sum_l nnz(S^(l))/2 + sum nnz(R^T B)
     if (iface) *iface = 3.0 * n;               // per element side
   } else {
-    if (vol) *vol = 3 * q * n * n * n / 2;
+    if (vol) *vol = c->eq56 ? 3 * q * n * n * n : 3 * q * n * n * n / 2;  // (3 + 2 + 1) vs 3 line directions
     if (fac) *fac = 3 * n * n * n + n * n * n * n;
     if (eq56) *eq56 = 4 * n * n * n * n;
     if (iface) *iface = 4.0 * n * n;

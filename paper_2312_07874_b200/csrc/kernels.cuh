@@ -80,6 +80,7 @@ struct RhsArgs {
   long long* dbg;             // optional [4096][16] phase clock stamps (diagnostics)
   const double* fstar;        // [nloc][Nf][NC][Nqf] B J_f f* from the interface kernel
   int max_ctas;               // number of SMs (the launcher multiplies by resident CTAs per SM)
+  int eq56;                   // 1: per-operator fluxes (Eq. num_fluxes ablation), 0: line-wise
 };
 
 struct IfaceArgs {

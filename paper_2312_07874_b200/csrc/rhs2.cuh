@@ -250,7 +250,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 __shared__ uint64_t k2_barA, k2_barB;
 
 // one element of the flux kernel (the body of the persistent loop)
-template <int DIM, int N>
+template <int DIM, int N, bool EQ>
 __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsigned it) {
   using S = Sz<DIM, N>;
   using W = Lw<DIM, N>;
@@ -371,9 +371,13 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   auto Gat = [&](int l, int m, int i) { return sG[(l * DIM + m) * Nq + i]; };
 
   // ---- direction passes, one specialisation per direction k ----
-  auto pass = [&](auto kc, auto tc) {
+  auto pass = [&](auto kc, auto tc, auto ec) {
     constexpr int k = decltype(kc)::value;
     constexpr bool CHK = !decltype(tc)::value;
+    // EQ56: ablation of the paper's per-operator nonzero iteration: one flux per
+    // operator S^(l) with a nonzero on this line instead of one flux with the summed normal
+    constexpr bool EQ56 = decltype(ec)::value;
+    constexpr int NLOP = EQ56 ? (DIM == 3 ? 3 - k : 2 - k) : 1;  // operators evaluated per pair
     constexpr int stride = k == 0 ? 1 : (k == 1 ? N : N * N);
 #pragma unroll 1
     for (int slot = warp; slot < W::SLOTS; slot += W::NW) {
@@ -412,6 +416,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
 #pragma unroll
       for (int s0 = 1; s0 <= NS; s0 += W::VB) {
         Job<DIM> jv[W::VB];
+        double nl[W::VB][NLOP][DIM];  // per-operator normals (summed unless EQ56)
 #pragma unroll
         for (int t = 0; t < W::VB; ++t) {
           const int s = s0 + t;
@@ -426,35 +431,69 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           jb.idx = j;
           const bool half = (N % 2 == 0) && (s == NS);
           const double mk = (s <= NS && !(half && pos >= N / 2)) ? vmask : 0.0;
+          // term l of n_ij = sum_l c A (g_i^(l) + g_j^(l)) goes to slot min(l', NLOP - 1)
+          auto put = [&](int slot, int m, double val) {
+            if (EQ56)
+              nl[t][slot][m] = val;
+            else if (slot == 0)
+              nl[t][0][m] = val;
+            else
+              nl[t][0][m] += val;
+          };
           if constexpr (DIM == 2) {
             if (k == 0) {
               const double cl = mk * tw[cb], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
 #pragma unroll
-              for (int m = 0; m < 2; ++m) jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * (gl[1][m] + Gat(1, m, j));
+              for (int m = 0; m < 2; ++m) {
+                put(0, m, q1 * (gl[0][m] + Gat(0, m, j)));
+                put(1, m, a1 * (gl[1][m] + Gat(1, m, j)));
+              }
             } else {
               const double a2 = mk * tw[ca] * tA2[ix];
 #pragma unroll
-              for (int m = 0; m < 2; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j));
+              for (int m = 0; m < 2; ++m) put(0, m, a2 * (gl[1][m] + Gat(1, m, j)));
             }
           } else {
             if (k == 0) {
               const double cl = mk * 0.5 * tw[cb] * tw3[cc], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
 #pragma unroll
-              for (int m = 0; m < 3; ++m)  // metric row 1 holds g1 + g2 in this (last) pass
-                jb.n[m] = q1 * (gl[0][m] + Gat(0, m, j)) + a1 * (gl[1][m] + Gat(1, m, j));
+              for (int m = 0; m < 3; ++m) {
+                if constexpr (EQ56) {
+                  put(0, m, q1 * (gl[0][m] + Gat(0, m, j)));
+                  put(1, m, a1 * (gl[1][m] + Gat(1, m, j)));
+                  put(2, m, a1 * (gl[2][m] + Gat(2, m, j)));
+                } else {  // metric row 1 holds g1 + g2 in this (last) pass
+                  put(0, m, q1 * (gl[0][m] + Gat(0, m, j)) + a1 * (gl[1][m] + Gat(1, m, j)));
+                }
+              }
             } else if (k == 1) {
               const double cl = mk * 0.5 * tw[ca] * tw3[cc], a2 = cl * tA2[ix], a3 = cl * tA3[ix];
 #pragma unroll
-              for (int m = 0; m < 3; ++m) jb.n[m] = a2 * (gl[1][m] + Gat(1, m, j)) + a3 * (gl[2][m] + Gat(2, m, j));
+              for (int m = 0; m < 3; ++m) {
+                put(0, m, a2 * (gl[1][m] + Gat(1, m, j)));
+                put(1, m, a3 * (gl[2][m] + Gat(2, m, j)));
+              }
             } else {
               const double a4 = mk * 0.125 * tw[ca] * tw[cb] * (1.0 - teta[cb]) * tA4[ix];
 #pragma unroll
-              for (int m = 0; m < 3; ++m) jb.n[m] = a4 * (gl[2][m] + Gat(2, m, j));
+              for (int m = 0; m < 3; ++m) put(0, m, a4 * (gl[2][m] + Gat(2, m, j)));
             }
           }
         }
         double Fs[W::VB][NC];
-        flux_batch<DIM, W::VB, CHK>(me, jv, gm1inv, Fs);
+#pragma unroll
+        for (int op = 0; op < NLOP; ++op) {
+#pragma unroll
+          for (int t = 0; t < W::VB; ++t)
+#pragma unroll
+            for (int m = 0; m < DIM; ++m) jv[t].n[m] = nl[t][op][m];
+          double Fo[W::VB][NC];
+          flux_batch<DIM, W::VB, CHK>(me, jv, gm1inv, Fo);
+#pragma unroll
+          for (int t = 0; t < W::VB; ++t)
+#pragma unroll
+            for (int v = 0; v < NC; ++v) Fs[t][v] = op == 0 ? Fo[t][v] : Fs[t][v] + Fo[t][v];
+        }
 #pragma unroll
         for (int t = 0; t < W::VB; ++t) {
           const int s = s0 + t;
@@ -535,7 +574,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           double gtn[3], gtn3[3];
 #pragma unroll
           for (int m = 0; m < 3; ++m) {
-            gtn[m] = (gl[0][m] + gl[1][m]) * r3;  // row 1 = g1 + g2
+            gtn[m] = (EQ56 ? gl[0][m] + gl[1][m] + gl[2][m] : gl[0][m] + gl[1][m]) * r3;  // row 1 = g1 + g2 unless EQ56
             gtn3[m] = -gl[0][m];
           }
           Job<DIM> jf[2];
@@ -610,22 +649,25 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     stamp(2 + k);
   };
   // 3D order 1, 2, 0: the eta1 pass only needs g0 and g1 + g2, summed in place once before it
-  auto passes = [&](auto tc) {
+  auto passes = [&](auto tc, auto ec) {
     if constexpr (DIM == 3) {
-      pass(std::integral_constant<int, 1>{}, tc);
-      pass(std::integral_constant<int, 2>{}, tc);
-      for (int q = tid; q < DIM * Nq; q += NT) sG[DIM * Nq + q] += sG[2 * DIM * Nq + q];
-      __syncthreads();
-      pass(std::integral_constant<int, 0>{}, tc);
+      pass(std::integral_constant<int, 1>{}, tc, ec);
+      pass(std::integral_constant<int, 2>{}, tc, ec);
+      if constexpr (!decltype(ec)::value) {
+        for (int q = tid; q < DIM * Nq; q += NT) sG[DIM * Nq + q] += sG[2 * DIM * Nq + q];
+        __syncthreads();
+      }
+      pass(std::integral_constant<int, 0>{}, tc, ec);
     } else {
-      pass(std::integral_constant<int, 0>{}, tc);
-      pass(std::integral_constant<int, 1>{}, tc);
+      pass(std::integral_constant<int, 0>{}, tc, ec);
+      pass(std::integral_constant<int, 1>{}, tc, ec);
     }
   };
+  // the ablation (EQ) is its own kernel instantiation: the production path keeps its registers
   if (all_taylor)  // uniform over the CTA
-    passes(std::true_type{});
+    passes(std::true_type{}, std::integral_constant<bool, EQ>{});
   else
-    passes(std::false_type{});
+    passes(std::false_type{}, std::integral_constant<bool, EQ>{});
   // states, metrics and facet inputs are dead: the next element's copies land during the epilogue
   if (tid == 0 && has_next) issue_A(elem_of(nidx), (it + 1) & 1);
   if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
@@ -753,8 +795,8 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   stamp(11);
 }
 
-template <int DIM, int N>
-__global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
+template <int DIM, int N, bool EQ>
+__device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   using S = Sz<DIM, N>;
   using W = Lw<DIM, N>;
   using L = Rhs2Smem<DIM, N>;
@@ -836,7 +878,17 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, const
   __syncthreads();  // mbarriers initialised and tables staged before anyone uses them
 
 #pragma unroll 1
-  for (int64_t idx = blockIdx.x, it = 0; idx < A.n_elem; idx += gridDim.x, ++it) k2_element<DIM, N>(A, idx, (unsigned)it);
+  for (int64_t idx = blockIdx.x, it = 0; idx < A.n_elem; idx += gridDim.x, ++it) k2_element<DIM, N, EQ>(A, idx, (unsigned)it);
+}
+
+template <int DIM, int N>
+__global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
+  rhs2_body<DIM, N, false>(R, A);
+}
+// ablation: the paper's Eq. num_fluxes per-operator fluxes (es_options.volume_mode = 1)
+template <int DIM, int N>
+__global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_eq56_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
+  rhs2_body<DIM, N, true>(R, A);
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -246,3 +246,22 @@ def test_full_size_c4_entropy_conservation(es):
     ctx2 = es.Context(mesh, p, warp=I.bj_warp(d, L, M), interface_flux=1)
     rate2, scale2, _ = ctx2.entropy_production(torch.from_numpy(u).cuda())
     assert rate2 < -1e-8 * scale2, (rate2, scale2)  # LLF dissipates
+
+
+@pytest.mark.parametrize("d,M,p,warp,ic,fm", [(2, 3, 4, "paper", "wave", 1), (3, 3, 3, "paper", "tgv3", 1),
+                                              (3, 3, 8, "bj", "tgv", 1)])
+def test_eq56_ablation_parity(es, d, M, p, warp, ic, fm):
+    # volume_mode 1: one flux per operator S^(l) (Eq. num_fluxes) -- same RHS as the
+    # oracle's Eq. 56 path (variant 0) and as the line-wise kernel, with the Eq. 56 evaluation count
+    L = _L(d)
+    mesh = I.split_cartesian(d, M, L)
+    w = _warp(warp, d, L, M)
+    om = O.Mesh(mesh, p, warp=w)
+    u = I.perturb_modal(om.project(_ic(ic, om.node_coords(), d, L)), d, p, seed=1, amp=1e-2)
+    ref, st = om.rhs(u, flux_mode=fm, variant=0)
+    ctx = es.Context(mesh, p, warp=w, interface_flux=fm, volume_mode=1)
+    got = _gpu_rhs(ctx, u)
+    assert (_relerr(got, ref) <= TOL).all()
+    c = ctx.flux_counts()
+    assert (c["volume"] + c["facet"]) * om.ne == st.volume_pairs + st.facet_pairs  # Eq. 56 count
+    assert c["volume"] + c["facet"] == c["eq56"]
