@@ -516,7 +516,11 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT, 2) project_kernel(DevRef R, Pr
   for (int64_t idx = blockIdx.x; idx < A.n_elem; idx += gridDim.x) {
     const int64_t e = elem_of(idx);
     auto stamp = [&](int q) {
-      if (A.dbg && tid == 0 && idx < 4096) A.dbg[idx * 16 + q] = clock64();
+      #ifdef ES_STAMPS  // diagnostics build only (tools/build.py with ES_STAMPS=1)
+    if (A.dbg && tid == 0 && idx < 4096) A.dbg[idx * 16 + q] = clock64();
+#else
+    (void)q;
+#endif
     };
     stamp(0);
     cp_async_wait_all();

@@ -309,7 +309,11 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   const double* gv = A.geo_vol + (size_t)e * S::GVS;
   // optional phase clock stamps (diagnostics, ES_PHASE_TIMING)
   auto stamp = [&](int k) {
+    #ifdef ES_STAMPS  // diagnostics build only (tools/build.py with ES_STAMPS=1)
     if (A.dbg && tid == 0 && idx < 4096) A.dbg[idx * 16 + k] = clock64();
+#else
+    (void)k;
+#endif
   };
   stamp(0);
   mbar_wait(&k2_barA, it & 1);

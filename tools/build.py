@@ -63,6 +63,8 @@ def build_lib(force=False, jobs=8):
     objs = []
     procs = []
     inc = ["-I", os.path.join(ROOT, "include"), "-I", c]
+    if os.environ.get("ES_STAMPS"):  # per-element clock stamps (ES_PHASE_TIMING diagnostics)
+        inc = ["-DES_STAMPS"] + inc
     nd = nccl_dir()
     if nd:
         inc = ["-I", os.path.join(nd, "include")] + inc
