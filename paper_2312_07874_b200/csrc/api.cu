@@ -444,7 +444,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
     return fail(c, ES_ERR_VERIFY, "face normals / weights do not match across faces (rel " + std::to_string(mism) + ")");
   // ---- work buffers ----
   const size_t nmod = (size_t)c->nloc * c->NC * c->Np;
-  CK(cudaMalloc((void**)&c->prim, (size_t)c->nloc * even_up(c->NC * c->Nq) * sizeof(double)));
+  CK(cudaMalloc((void**)&c->prim, (size_t)c->nloc * even_up((c->NC + 1) * c->Nq + 1) * sizeof(double)));
   CK(cudaMalloc((void**)&c->trace, (size_t)c->nslots * c->NC * c->Nqf * sizeof(double)));
   CK(cudaMalloc((void**)&c->fstar, (size_t)c->nloc * c->Nf * c->NC * c->Nqf * sizeof(double)));
   CK(cudaMalloc((void**)&c->wt, nmod * sizeof(double)));

@@ -28,7 +28,7 @@ struct Sz {
   static constexpr int NG = DIM * DIM;
   static constexpr int NGV = NG + 2;  // G_lm, W J~, W / J~
   static constexpr int GVS = (NGV * Nq + 1) & ~1;  // geo_vol element stride (even, 16-B aligned)
-  static constexpr int PRS = (NC * Nq + 1) & ~1;   // prim element stride
+  static constexpr int PRS = ((NC + 1) * Nq + 2) & ~1;  // prim element stride: rho, v, p, beta rows + flag
   static constexpr int KPT = (Nq + 383) / 384;
   static constexpr int NT = ((Nq + KPT - 1) / KPT + 31) / 32 * 32;
 };
@@ -48,7 +48,9 @@ struct ProjArgs {
   const int64_t* elem_list;  // optional element subset
   const double* u;           // [nloc][NC][Np] modal stage input
   const double* geo_vol;     // [nloc][GVS]: [NGV][Nq] + pad
-  double* prim;              // [nloc][PRS]: [NC][Nq] + pad, entropy-projected primitive (rho, v, p)
+  double* prim;              // [nloc][PRS]: [NC+1][Nq] entropy-projected (rho, v, p, beta = rho/p),
+                             // then the element's all-Taylor flag (1.0: every pair takes the Taylor
+                             // branch of both logarithmic means, see rhs2.cuh) + pad
   double* trace;             // [slots][NC][Nqf] entropy-projected primitive at facet nodes
   double* wt;                // optional [nloc][NC][Np] projected entropy variables w~
   int* bad;                  // admissibility flag
@@ -624,7 +626,10 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT, 2) project_kernel(DevRef R, Pr
     }
     __syncthreads();
     stamp(9);
-    // entropy-projected conservative variables U(w) -> stored as primitive (rho, v, p)
+    // entropy-projected conservative variables U(w) -> stored as primitive (rho, v, p) and
+    // beta = rho / p = -w_last (App. B); the spread of rho and beta over the element's volume and
+    // facet nodes decides the all-Taylor flag ((max - min) < 0.0099 (max + min) for both implies
+    // f2 = ((x - y)/(x + y))^2 < 1e-4 for every pair, reading R5)
     auto Uofw = [&](const double* w, double* out) -> int {
       const double b = -w[DIM + 1], ib = 1.0 / b;
       double vel[DIM], v2 = 0.0;
@@ -639,16 +644,18 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT, 2) project_kernel(DevRef R, Pr
 #pragma unroll
       for (int m = 0; m < DIM; ++m) out[1 + m] = vel[m];
       out[DIM + 1] = r * ib;
+      out[DIM + 2] = b;
       return (b > 0.0 && r > 0.0) ? 0 : 1;
     };
+    double mm[4] = {1e300, -1e300, 1e300, -1e300};  // rho min, max, beta min, max
     for (int i = tid; i < Nq + NF; i += nt) {
-      double w[NC], o[NC];
+      double w[NC], o[NC + 1];
       if (i < Nq) {
 #pragma unroll
         for (int v = 0; v < NC; ++v) w[v] = X[v * Nq + i];
         bad |= Uofw(w, o);
 #pragma unroll
-        for (int v = 0; v < NC; ++v) A.prim[(size_t)e * S::PRS + v * Nq + i] = o[v];
+        for (int v = 0; v <= NC; ++v) A.prim[(size_t)e * S::PRS + v * Nq + i] = o[v];
       } else {
         const int fz = i - Nq, z = fz / Nqf, f = fz - z * Nqf;
 #pragma unroll
@@ -657,6 +664,34 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT, 2) project_kernel(DevRef R, Pr
 #pragma unroll
         for (int v = 0; v < NC; ++v) A.trace[(((size_t)e * S::Nf + z) * NC + v) * Nqf + f] = o[v];
       }
+      mm[0] = o[0] < mm[0] ? o[0] : mm[0];
+      mm[1] = o[0] > mm[1] ? o[0] : mm[1];
+      mm[2] = o[NC] < mm[2] ? o[NC] : mm[2];
+      mm[3] = o[NC] > mm[3] ? o[NC] : mm[3];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double t0 = __shfl_xor_sync(0xffffffffu, mm[0], o), t1 = __shfl_xor_sync(0xffffffffu, mm[1], o);
+      const double t2 = __shfl_xor_sync(0xffffffffu, mm[2], o), t3 = __shfl_xor_sync(0xffffffffu, mm[3], o);
+      mm[0] = t0 < mm[0] ? t0 : mm[0];
+      mm[1] = t1 > mm[1] ? t1 : mm[1];
+      mm[2] = t2 < mm[2] ? t2 : mm[2];
+      mm[3] = t3 > mm[3] ? t3 : mm[3];
+    }
+    __shared__ double red_mm[16][4];  // NT <= 512
+    if ((tid & 31) == 0)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red_mm[tid >> 5][q] = mm[q];
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < nt / 32; ++w) {
+        mm[0] = red_mm[w][0] < mm[0] ? red_mm[w][0] : mm[0];
+        mm[1] = red_mm[w][1] > mm[1] ? red_mm[w][1] : mm[1];
+        mm[2] = red_mm[w][2] < mm[2] ? red_mm[w][2] : mm[2];
+        mm[3] = red_mm[w][3] > mm[3] ? red_mm[w][3] : mm[3];
+      }
+      const bool taylor = (mm[1] - mm[0]) < 0.0099 * (mm[1] + mm[0]) && (mm[3] - mm[2]) < 0.0099 * (mm[3] + mm[2]);
+      A.prim[(size_t)e * S::PRS + (NC + 1) * Nq] = taylor ? 1.0 : 0.0;
     }
     stamp(10);
   }

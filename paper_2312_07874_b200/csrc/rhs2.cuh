@@ -45,7 +45,7 @@ struct Rhs2Smem {
   static constexpr int TB = 5 * N * N + 6 * N + N * N + S::NF;  // line operators, weights, extrapolation, B
   static constexpr int PS = psi_smem_doubles<DIM, N>();         // PKD sum-factorisation tables
   // per element
-  static constexpr int PR = ev2((DIM + 3) * S::Nq);  // rho, v, p, beta   (bulk copy of prim: PRS)
+  static constexpr int PR = S::PRS;                  // rho, v, p, beta, flag (bulk copy of prim)
   static constexpr int GG = ev2(S::NG * S::Nq);      // G_lm              (bulk copy)
   static constexpr int RR = ev2(S::NC * S::Nq);      // nodal residual r; first transform buffer
   static constexpr int PT = DIM == 3 ? S::NC * N * N * N : 0;  // facet-4 partial sums [v][j][a][c]
@@ -317,50 +317,14 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   };
   stamp(0);
   mbar_wait(&k2_barA, it & 1);
-  // beta = rho / p, and the element-wide spread of rho and beta: when (max - min) < 0.0099 (max +
-  // min) for both, every pair has f2 = ((x - y) / (x + y))^2 < 1e-4, i.e. takes the Taylor branch
-  double mm[4] = {1e300, -1e300, 1e300, -1e300};  // rho min, max, beta min, max
-  auto upd = [&](double r, double b) {
-    mm[0] = r < mm[0] ? r : mm[0];
-    mm[1] = r > mm[1] ? r : mm[1];
-    mm[2] = b < mm[2] ? b : mm[2];
-    mm[3] = b > mm[3] ? b : mm[3];
-  };
-  for (int i = tid; i < Nq; i += NT) {
-    const double r = sP[i], b = r / sP[(DIM + 1) * Nq + i];
-    sP[(DIM + 2) * Nq + i] = b;
-    upd(r, b);
-  }
+  // facet beta = rho / p (the volume beta rows and the element's all-Taylor flag come from K1)
   for (int fz = tid; fz < NF; fz += NT) {
     const double* q = fP + (fz / Nqf) * NC * Nqf + fz % Nqf;
-    const double r = q[0], b = r / q[(DIM + 1) * Nqf];
-    fB[fz] = b;
-    upd(r, b);
+    fB[fz] = q[0] / q[(DIM + 1) * Nqf];
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double t[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) t[q] = shfl_d(mm[q], lane ^ o);
-    mm[0] = t[0] < mm[0] ? t[0] : mm[0];
-    mm[1] = t[1] > mm[1] ? t[1] : mm[1];
-    mm[2] = t[2] < mm[2] ? t[2] : mm[2];
-    mm[3] = t[3] > mm[3] ? t[3] : mm[3];
-  }
-  __shared__ double red_mm[W::NW][4];
-  if (lane == 0)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) red_mm[warp][q] = mm[q];
   mbar_wait(&k2_barB, it & 1);  // f* is updated in place by the passes
   __syncthreads();
-#pragma unroll
-  for (int w = 0; w < W::NW; ++w) {
-    mm[0] = red_mm[w][0] < mm[0] ? red_mm[w][0] : mm[0];
-    mm[1] = red_mm[w][1] > mm[1] ? red_mm[w][1] : mm[1];
-    mm[2] = red_mm[w][2] < mm[2] ? red_mm[w][2] : mm[2];
-    mm[3] = red_mm[w][3] > mm[3] ? red_mm[w][3] : mm[3];
-  }
-  const bool all_taylor = (mm[1] - mm[0]) < 0.0099 * (mm[1] + mm[0]) && (mm[3] - mm[2]) < 0.0099 * (mm[3] + mm[2]);
+  const bool all_taylor = sP[(DIM + 3) * Nq] != 0.0;
   stamp(1);
 
   auto state_at = [&](int i) {
