@@ -235,6 +235,19 @@ def run_reference(args):
     return 0
 
 
+def nccl_unique_id(dist, torch, rank, device):
+    """rank 0 creates the 128-byte ncclUniqueId the library's communicator is built from
+    (es_options.nccl_unique_id) and broadcasts it over the torch process group"""
+    import ctypes
+    lib = ctypes.CDLL("libnccl.so.2")
+    uid = (ctypes.c_ubyte * 128)()  # opaque bytes, zeros included
+    if rank == 0:
+        assert lib.ncclGetUniqueId(ctypes.byref(uid)) == 0
+    t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=device)
+    dist.broadcast(t, 0)
+    return bytes(t.cpu().numpy().tobytes())
+
+
 def run(args):
     import torch
     import torch.distributed as dist
@@ -252,25 +265,13 @@ def run(args):
         desc = f"{desc} [degree override p={p}]"
     mesh = I.split_cartesian(dim, M, L)
     w = {"bj": I.bj_warp(dim, L, M), "none": None}.get(warp)
-    nccl_id = None
-    if world > 1:
-        import ctypes
-        lib = ctypes.CDLL("libnccl.so.2")
-
-        class Uid(ctypes.Structure):
-            _fields_ = [("internal", ctypes.c_char * 128)]
-        uid = Uid()
-        if rank == 0:
-            lib.ncclGetUniqueId(ctypes.byref(uid))
-        t = torch.frombuffer(bytearray(uid.internal if rank == 0 else bytes(128)), dtype=torch.uint8).cuda()
-        dist.broadcast(t, 0)
-        nccl_id = bytes(t.cpu().numpy().tobytes())
+    nccl_id = nccl_unique_id(dist, torch, rank, "cuda") if world > 1 else None
     stream = torch.cuda.Stream()
     t_setup = time.perf_counter()
     ctx = es.Context(mesh, p, warp=w, interface_flux=fm, rank=rank, world=world, nccl_id=nccl_id,
                      stream=stream.cuda_stream, device=local, volume_mode=args.volume_mode)
     if args.volume_mode:
-        desc = f"{desc} [ablation: Eq. num_fluxes per-operator fluxes]" 
+        desc = f"{desc} [ablation: Eq. num_fluxes per-operator fluxes]"
     t_setup = time.perf_counter() - t_setup
     um, xn, un = initial_state(ctx, torch, kind, dim, L)
     dt = cfl_dt(xn, un, dim, L, M, p)

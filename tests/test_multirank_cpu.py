@@ -113,3 +113,30 @@ def test_plan_partition_is_exhaustive():
             assert pl["send_count"][r] == 0 and pl["recv_count"][r] == 0
         assert tot == ne
         assert np.array_equal(sends, recvs.T)  # what r sends to s is what s expects from r
+
+
+def _uid_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        uid = bench.nccl_unique_id(dist, torch, rank, "cpu")
+        q.put((rank, uid))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_nccl_unique_id_broadcast():
+    # the id bytes (with zeros) reach every rank intact (bench.py multi-GPU setup path)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_uid_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+    assert len(got[0]) == 128 and got[0] == got[1]
+    assert got[0].count(0) > 0  # the id contains zero bytes that a C-string path would truncate
