@@ -179,6 +179,10 @@ __device__ PsiS stage_psi(const DevRef& R, double* buf) {
   return T;
 }
 
+// outputs per chunk: a divisor of N when there is one (no wasted FMAs), else 4
+template <int N>
+__host__ __device__ constexpr int fib_oc() { return N % 3 == 0 ? 3 : (N % 4 == 0 ? 4 : (N % 5 == 0 ? 5 : 4)); }
+
 // Two fibers per work item share every psi load (register blocking): y_f[o] = sum_{i < ni} A[i][o]
 // (the two fibers of an item are half a step apart, so that consecutive lanes own consecutive
 // fibers: odd strides between lanes, no shared-memory bank conflicts)
@@ -190,7 +194,7 @@ template <int N, bool TR>
 __device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const double* in0,
                                        const double* in1, int sin, const double* sc0, const double* sc1,
                                        double* out0, double* out1, int sout, bool has1) {
-  constexpr int NP = psi_np<N>(), OC = 4;
+  constexpr int NP = psi_np<N>(), OC = fib_oc<N>();
   double x0[N], x1[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) {
@@ -204,7 +208,7 @@ __device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const d
   }
   // all output chunks in flight (independent chains); for N a multiple of OC ptxas hoists every
   // table load of every chunk (register blow-up), so the chunks stay sequential there
-#pragma unroll(N % OC ? N : 1)
+#pragma unroll(N == 8 ? 1 : N)
   for (int o0 = 0; o0 < N; o0 += OC) {
     if (o0 >= no) break;
     double a0[OC], a1[OC];
@@ -213,13 +217,22 @@ __device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const d
     if constexpr (!TR) {
 #pragma unroll
       for (int i = 0; i < N; ++i) {
+        if constexpr (OC % 2 == 0) {
 #pragma unroll
-        for (int q2 = 0; q2 < OC / 2; ++q2) {
-          const double2 pv = *reinterpret_cast<const double2*>(ps + i * NP + o0 + 2 * q2);
-          a0[2 * q2] = fma(pv.x, x0[i], a0[2 * q2]);
-          a1[2 * q2] = fma(pv.x, x1[i], a1[2 * q2]);
-          a0[2 * q2 + 1] = fma(pv.y, x0[i], a0[2 * q2 + 1]);
-          a1[2 * q2 + 1] = fma(pv.y, x1[i], a1[2 * q2 + 1]);
+          for (int q2 = 0; q2 < OC / 2; ++q2) {
+            const double2 pv = *reinterpret_cast<const double2*>(ps + i * NP + o0 + 2 * q2);
+            a0[2 * q2] = fma(pv.x, x0[i], a0[2 * q2]);
+            a1[2 * q2] = fma(pv.x, x1[i], a1[2 * q2]);
+            a0[2 * q2 + 1] = fma(pv.y, x0[i], a0[2 * q2 + 1]);
+            a1[2 * q2 + 1] = fma(pv.y, x1[i], a1[2 * q2 + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < OC; ++q) {
+            const double pv = ps[i * NP + o0 + q];
+            a0[q] = fma(pv, x0[i], a0[q]);
+            a1[q] = fma(pv, x1[i], a1[q]);
+          }
         }
       }
     } else {
@@ -252,7 +265,7 @@ __device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const d
 template <int N, bool TR, int K>
 __device__ __forceinline__ void fiberK(const double* ps, const double* const* in, int sin, const double* const* sc,
                                        double* const* out, int sout, int nk) {
-  constexpr int NP = psi_np<N>(), OC = 4;
+  constexpr int NP = psi_np<N>(), OC = fib_oc<N>();
   double x[K][N];
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -261,7 +274,7 @@ __device__ __forceinline__ void fiberK(const double* ps, const double* const* in
       x[k][i] = in[k][i * sin];
       if (sc) x[k][i] *= sc[k][i * sin];
     }
-#pragma unroll(N % OC ? N : 1)
+#pragma unroll(N == 8 ? 1 : N)
   for (int o0 = 0; o0 < N; o0 += OC) {  // output chunks in flight (see fiber2)
     double a[K][OC];
 #pragma unroll
@@ -270,16 +283,26 @@ __device__ __forceinline__ void fiberK(const double* ps, const double* const* in
       for (int q = 0; q < OC; ++q) a[k][q] = 0.0;
     if constexpr (!TR) {
 #pragma unroll
-      for (int i = 0; i < N; ++i)
+      for (int i = 0; i < N; ++i) {
+        if constexpr (OC % 2 == 0) {
 #pragma unroll
-        for (int q2 = 0; q2 < OC / 2; ++q2) {
-          const double2 pv = *reinterpret_cast<const double2*>(ps + i * NP + o0 + 2 * q2);
+          for (int q2 = 0; q2 < OC / 2; ++q2) {
+            const double2 pv = *reinterpret_cast<const double2*>(ps + i * NP + o0 + 2 * q2);
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            a[k][2 * q2] = fma(pv.x, x[k][i], a[k][2 * q2]);
-            a[k][2 * q2 + 1] = fma(pv.y, x[k][i], a[k][2 * q2 + 1]);
+            for (int k = 0; k < K; ++k) {
+              a[k][2 * q2] = fma(pv.x, x[k][i], a[k][2 * q2]);
+              a[k][2 * q2 + 1] = fma(pv.y, x[k][i], a[k][2 * q2 + 1]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < OC; ++q) {
+            const double pv = ps[i * NP + o0 + q];
+#pragma unroll
+            for (int k = 0; k < K; ++k) a[k][q] = fma(pv, x[k][i], a[k][q]);
           }
         }
+      }
     } else {
 #pragma unroll
       for (int q = 0; q < OC; ++q) {
