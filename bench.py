@@ -11,7 +11,7 @@ entropy-stable interface flux.  Multi-GPU (torchrun): elements are partitioned i
 slabs, face-trace halos go over NCCL; the timing is the max over ranks (CUDA events).
 
 value = EC two-point flux evaluations per second, whole job (line-wise volume + facet-correction
-pairs actually evaluated; DESIGN.md section 6).  DOF.RHS/s and the Eq.-num_fluxes-equivalent rate
+pairs actually evaluated; DESIGN.md section 5.4).  DOF.RHS/s and the Eq.-num_fluxes-equivalent rate
 are reported alongside.  Inputs are synthetic (analytic initial data projected by the library).
 """
 from __future__ import annotations
@@ -41,7 +41,7 @@ CONFIGS = {
            "3D Euler p=8 curved tetrahedra, 196608 elements, TGV Ma0.1, ES, RK4 step"),
 }
 
-# ---- algorithmic FP64 operation counts (DESIGN.md section 6): +,-,*,/,sqrt,log,exp = 1 flop ----
+# ---- algorithmic FP64 operation counts (DESIGN.md section 5.4): +,-,*,/,sqrt,log,exp = 1 flop ----
 FLUX_FLOPS = {2: 67, 3: 81}            # Ranocha EC flux, Taylor branch of both log means
 VOL_NORMAL_FLOPS = {2: 12, 3: 24}      # n_ij from the line operators and averaged metrics
 FAC_NORMAL_FLOPS = {2: 10, 3: 21}      # <J n> of the facet correction
@@ -97,7 +97,7 @@ def measured_peaks():
 
 def fp64_peak_tflops(sm_mhz=None):
     """FP64 CUDA-core peak from the unit counts: 148 SMs x 64 DFMA/clk x 2 flop x clock
-    (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz; DESIGN.md section 6)."""
+    (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz; DESIGN.md section 5.4)."""
     mhz = sm_mhz or measured_peaks().get("sm_max_mhz", 1965.0)
     return 148 * 64 * 2 * mhz * 1e6 / 1e12
 
@@ -382,7 +382,7 @@ def run(args):
                      "projection_share_of_step": k1_ms / args.steps / ms_step,
                      "iface_kernel_ms_avg": kf_ms / max(kf_n, 1),
                      "iface_share_of_step": kf_ms / args.steps / ms_step,
-                     "peak_basis": "148 SM x 64 DFMA/clk x 2 x sm_max_mhz (DESIGN.md 6)"},
+                     "peak_basis": "148 SM x 64 DFMA/clk x 2 x sm_max_mhz (DESIGN.md 5.4)"},
         "e2e": {"value": e2e_value, "unit": "flux_evals/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                 "api": "cudaMemcpyAsync(pinned->device) + es_set_state + es_step + es_get_state + copy back"},
         "gpu_launches": int(launches),

@@ -11,7 +11,7 @@ namespace esb {
 // Host-built reference tables for one (dim, p), q = p.  Everything the kernels need about
 // the reference element is here; it is re-derived for the line structure of the operators:
 //   S^(l) = (Q^(l) - Q^(l)^T)/2 restricted to an eta_k line = c_k(line) * skew(X_{k,l}),
-// with X one of the 1D matrices below (DESIGN.md section 5.2).
+// with X one of the 1D matrices below (DESIGN.md section 5.3).
 // ----------------------------------------------------------------------------------------------
 struct RefTables {
   int d = 0, p = 0, n = 0, Nq = 0, Nf = 0, Nqf = 0, Np = 0;

@@ -352,7 +352,7 @@ bool build_ref_tables(int d, int p, RefTables& t, std::string& err) {
   t.w = rnd(w);
   t.eta3 = rnd(e3);
   t.w3 = rnd(w3);
-  // 1D line operators (DESIGN.md 5.2): X = diag(weight) D, S-line = skew(X)
+  // 1D line operators (DESIGN.md 5.3): X = diag(weight) D, S-line = skew(X)
   std::vector<Q> D = diff_matrix(e), D3 = diff_matrix(e3);
   std::vector<Q> Q1(n * n), A1(n * n), A2(n * n), A3(n * n), A4(n * n);
   for (int i = 0; i < n; ++i)

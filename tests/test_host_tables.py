@@ -1,6 +1,6 @@
 """CPU checks of the product's host setup (no GPU): the reference tables the kernels use, compared
 against the oracle's dense operators.  This pins the line factorisation the kernels rely on
-(DESIGN.md 5.2): on an eta_k line, S^(l)_ij = c_k,l(line) * skew(X_k,l)[a_i, a_j]."""
+(DESIGN.md 5.3): on an eta_k line, S^(l)_ij = c_k,l(line) * skew(X_k,l)[a_i, a_j]."""
 import numpy as np
 import pytest
 

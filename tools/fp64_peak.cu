@@ -1,4 +1,4 @@
-// fp64_peak.cu -- DFMA throughput microbenchmark (FP64 CUDA-core roofline denominator, DESIGN.md 6)
+// fp64_peak.cu -- DFMA throughput microbenchmark (FP64 CUDA-core roofline denominator, DESIGN.md 5.4)
 #include <cstdio>
 #include <cuda_runtime.h>
 __global__ void dfma_kernel(double* out, int iters, double a, double b) {
