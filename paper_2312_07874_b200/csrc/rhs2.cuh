@@ -339,8 +339,12 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   auto Gat = [&](int l, int m, int i) { return sG[(l * DIM + m) * Nq + i]; };
 
   // ---- direction passes, one specialisation per direction k ----
-  auto pass = [&](auto kc, auto tc, auto ec) {
+  // DST: 0 = sR = acc (first pass), 1 = sR += acc, 2 = pt = acc (the pt buffer holds a second
+  // residual so that two passes can run without a barrier between them); SYNC: end with a barrier
+  auto pass = [&](auto kc, auto tc, auto ec, auto dc, auto sc) {
     constexpr int k = decltype(kc)::value;
+    constexpr int DST = decltype(dc)::value;
+    constexpr bool SYNC = decltype(sc)::value;
     constexpr bool CHK = !decltype(tc)::value;
     // EQ56: ablation of the paper's per-operator nonzero iteration: one flux per
     // operator S^(l) with a nonzero on this line instead of one flux with the summed normal
@@ -606,29 +610,49 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
       if (valid) {
 #pragma unroll
         for (int v = 0; v < NC; ++v) {
-          if (k == (DIM == 3 ? 1 : 0))  // the first pass executed
+          if constexpr (DST == 0)
             sR[v * Nq + i] = acc[v];
-          else
+          else if constexpr (DST == 1)
             sR[v * Nq + i] += acc[v];
+          else
+            pt[v * Nq + i] = acc[v];
         }
       }
     }
-    __syncthreads();
-    stamp(2 + k);
+    if constexpr (SYNC) {
+      __syncthreads();
+      stamp(2 + k);
+    }
   };
-  // 3D order 1, 2, 0: the eta1 pass only needs g0 and g1 + g2, summed in place once before it
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  using I2 = std::integral_constant<int, 2>;
+  using Yes = std::true_type;
+  using No = std::false_type;
+  // 3D: pass 1 (eta2 lines, with the facet-1 and facet-4 corrections); then the facet-4 sums over
+  // c, and g1 + g2 summed in place (the eta1 pass only needs g0 and g1 + g2); then passes 2 and 0
+  // back to back without a barrier -- pass 2 accumulates into the freed facet-4 buffer -- and the
+  // two residuals are added
   auto passes = [&](auto tc, auto ec) {
     if constexpr (DIM == 3) {
-      pass(std::integral_constant<int, 1>{}, tc, ec);
-      pass(std::integral_constant<int, 2>{}, tc, ec);
-      if constexpr (!decltype(ec)::value) {
-        for (int q = tid; q < DIM * Nq; q += NT) sG[DIM * Nq + q] += sG[2 * DIM * Nq + q];
-        __syncthreads();
+      pass(I1{}, tc, ec, I0{}, Yes{});
+      for (int q = tid; q < NC * N * N; q += NT) {  // facet 4: C^T 1 at (a, j) = sum over c of partials
+        const int v = q / (N * N), jf = (q / N) % N, a = q % N;
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) s += pt[((v * N + jf) * N + a) * N + c];
+        fS[(3 * NC + v) * Nqf + a + N * jf] -= s;
       }
-      pass(std::integral_constant<int, 0>{}, tc, ec);
+      if constexpr (!decltype(ec)::value)
+        for (int q = tid; q < DIM * Nq; q += NT) sG[DIM * Nq + q] += sG[2 * DIM * Nq + q];
+      __syncthreads();
+      pass(I2{}, tc, ec, I2{}, No{});
+      pass(I0{}, tc, ec, I1{}, Yes{});
+      for (int q = tid; q < NC * Nq; q += NT) sR[q] += pt[q];
+      __syncthreads();
     } else {
-      pass(std::integral_constant<int, 0>{}, tc, ec);
-      pass(std::integral_constant<int, 1>{}, tc, ec);
+      pass(I0{}, tc, ec, I0{}, Yes{});
+      pass(I1{}, tc, ec, I1{}, Yes{});
     }
   };
   // the ablation (EQ) is its own kernel instantiation: the production path keeps its registers
@@ -638,16 +662,6 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     passes(std::false_type{}, std::integral_constant<bool, EQ>{});
   // states, metrics and facet inputs are dead: the next element's copies land during the epilogue
   if (tid == 0 && has_next) issue_A(elem_of(nidx), (it + 1) & 1);
-  if constexpr (DIM == 3) {  // facet 4: C^T 1 at (a, j) = sum over c of the (a, c)-line partials
-    for (int q = tid; q < NC * N * N; q += NT) {
-      const int v = q / (N * N), jf = (q / N) % N, a = q % N;
-      double s = 0.0;
-#pragma unroll
-      for (int c = 0; c < N; ++c) s += pt[((v * N + jf) * N + a) * N + c];
-      fS[(3 * NC + v) * Nqf + a + N * jf] -= s;
-    }
-    __syncthreads();
-  }
   stamp(5);
   // ---- lifting r -= R^T s; facet 4 sum-factorised: t4[v][a][b] = sum_j l_b(eta3_j) s4[v][a + N j] ----
   if constexpr (DIM == 3) {
