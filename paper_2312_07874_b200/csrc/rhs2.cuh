@@ -341,7 +341,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   // ---- direction passes, one specialisation per direction k ----
   // DST: 0 = sR = acc (first pass), 1 = sR += acc, 2 = pt = acc (the pt buffer holds a second
   // residual so that two passes can run without a barrier between them); SYNC: end with a barrier
-  auto pass = [&](auto kc, auto tc, auto ec, auto dc, auto sc) {
+  auto pass = [&](auto kc, auto tc, auto ec, auto dc, auto sc, int woff) {
     constexpr int k = decltype(kc)::value;
     constexpr int DST = decltype(dc)::value;
     constexpr bool SYNC = decltype(sc)::value;
@@ -352,7 +352,9 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     constexpr int NLOP = EQ56 ? (DIM == 3 ? 3 - k : 2 - k) : 1;  // operators evaluated per pair
     constexpr int stride = k == 0 ? 1 : (k == 1 ? N : N * N);
 #pragma unroll 1
-    for (int slot = warp; slot < W::SLOTS; slot += W::NW) {
+    // warp w takes the slots s = w - woff (mod NW): the warps with an extra slot rotate between
+    // passes that run back to back
+    for (int slot = (warp + W::NW - woff) % W::NW; slot < W::SLOTS; slot += W::NW) {
       const int Lidx = slot * W::LPW + grp;
       const bool valid = lane_ok && Lidx < W::NL;
       const int l0 = valid ? Lidx % N : 0, l1 = valid ? Lidx / N : 0;
@@ -635,7 +637,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   // two residuals are added
   auto passes = [&](auto tc, auto ec) {
     if constexpr (DIM == 3) {
-      pass(I1{}, tc, ec, I0{}, Yes{});
+      pass(I1{}, tc, ec, I0{}, Yes{}, 0);
       for (int q = tid; q < NC * N * N; q += NT) {  // facet 4: C^T 1 at (a, j) = sum over c of partials
         const int v = q / (N * N), jf = (q / N) % N, a = q % N;
         double s = 0.0;
@@ -646,13 +648,13 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
       if constexpr (!decltype(ec)::value)
         for (int q = tid; q < DIM * Nq; q += NT) sG[DIM * Nq + q] += sG[2 * DIM * Nq + q];
       __syncthreads();
-      pass(I2{}, tc, ec, I2{}, No{});
-      pass(I0{}, tc, ec, I1{}, Yes{});
+      pass(I2{}, tc, ec, I2{}, No{}, 0);
+      pass(I0{}, tc, ec, I1{}, Yes{}, W::SLOTS % W::NW);
       for (int q = tid; q < NC * Nq; q += NT) sR[q] += pt[q];
       __syncthreads();
     } else {
-      pass(I0{}, tc, ec, I0{}, Yes{});
-      pass(I1{}, tc, ec, I1{}, Yes{});
+      pass(I0{}, tc, ec, I0{}, Yes{}, 0);
+      pass(I1{}, tc, ec, I1{}, Yes{}, 0);
     }
   };
   // the ablation (EQ) is its own kernel instantiation: the production path keeps its registers
