@@ -23,13 +23,16 @@ namespace esb {
 // accesses compile to shared-memory loads and stores
 extern __shared__ __align__(16) double smk2[];
 
+#ifndef ES_K2_NWMAX
+#define ES_K2_NWMAX 16  // warps per flux-kernel CTA (4 per SM sub-partition at <= 128 registers)
+#endif
 template <int DIM, int N>
 struct Lw {  // line-group layout
   using S = Sz<DIM, N>;
   static constexpr int LPW = 32 / N;                         // lines per warp slot
   static constexpr int NL = DIM == 2 ? N : N * N;            // lines per direction
   static constexpr int SLOTS = (NL + LPW - 1) / LPW;         // warp slots per direction
-  static constexpr int NW = SLOTS <= 12 ? SLOTS : 12;
+  static constexpr int NW = SLOTS <= ES_K2_NWMAX ? SLOTS : ES_K2_NWMAX;
   static constexpr int NT = NW * 32;
   static constexpr int NS = N / 2;                            // shifts
   static constexpr int VB = 2;  // volume pair jobs per flux batch (ILP vs registers: 4 spills at N = 9)
@@ -54,7 +57,10 @@ struct Rhs2Smem {
   static constexpr int FB = ev2(S::NF);              // facet beta = rho / p
   static constexpr int FJ = S::Nf * DIM * S::Nqf;    // J n at facet nodes [z][m][f] (bulk copy)
   static constexpr int FS = S::Nf * S::NC * S::Nqf;  // B J_f f* (bulk copy), then s = B J_f f* - C^T 1
-  static constexpr int SC = W::NW * S::NC * 32;      // per-warp reduction scratch
+  // per-warp reduction scratch of the line sums: SCV variables per round, sized to fit the region
+  // it shares with the modal result (all NC at once when there is room)
+  static constexpr int SCV = W::NW * S::NC * 32 <= UM ? S::NC : (UM / (W::NW * 32) >= 1 ? UM / (W::NW * 32) : 1);
+  static constexpr int SC = W::NW * SCV * 32;
   static constexpr int WJ0 = ((S::NG * S::Nq) % 2 == 0) ? S::NG * S::Nq : (S::NG + 1) * S::Nq;  // first even row
   static constexpr int WJN = ((S::NG * S::Nq) % 2 == 0) ? 2 * S::Nq : ev2(S::Nq);                // doubles copied
   static constexpr int WJOFF = ((S::NG * S::Nq) % 2 == 0) ? S::Nq : 0;  // W / J~ within the copied rows
@@ -281,7 +287,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   double* tB = tli4 + N * N;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* scr = smk2 + L::o_sc + warp * NC * 32;
+  double* scr = smk2 + L::o_sc + warp * L::SCV * 32;
   const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
   auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
   // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers
@@ -497,30 +503,34 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
       // facet-side sums over each line group through the warp scratch, in lane order; dest(line, v)
       // returns where the sum of line `gq` goes (nullptr: discard)
       auto line_sums = [&](const double* Fc, auto dest) {
+        constexpr int SCV = L::SCV;
 #pragma unroll
-        for (int v = 0; v < NC; ++v) {
-          acc[v] -= Fc[v];
-          scr[v * 32 + lane] = Fc[v];
-        }
-        __syncwarp();
-        for (int sidx = lane; sidx < W::LPW * NC; sidx += 32) {
-          const int gq = sidx / NC, v = sidx - gq * NC;
-          const double* src = scr + v * 32 + gq * N;
-          double tv[N];  // pairwise tree sum, depth ceil(log2 N)
+        for (int v = 0; v < NC; ++v) acc[v] -= Fc[v];
 #pragma unroll
-          for (int a = 0; a < N; ++a) tv[a] = src[a];
+        for (int v0 = 0; v0 < NC; v0 += SCV) {
 #pragma unroll
-          for (int w = 1; w < N; w *= 2)
+          for (int u = 0; u < SCV; ++u)
+            if (v0 + u < NC) scr[u * 32 + lane] = Fc[v0 + u];
+          __syncwarp();
+          for (int sidx = lane; sidx < W::LPW * SCV; sidx += 32) {
+            const int gq = sidx / SCV, u = sidx - gq * SCV, v = v0 + u;
+            const double* src = scr + u * 32 + gq * N;
+            double tv[N];  // pairwise tree sum, depth ceil(log2 N)
 #pragma unroll
-            for (int a = 0; a + w < N; a += 2 * w) tv[a] += tv[a + w];
-          const double sum = tv[0];
-          const int Lq = slot * W::LPW + gq;
-          if (Lq < W::NL) {
-            double* d = dest(Lq, v);
-            if (d) *d -= sum;  // s = B J_f f* - C^T 1
+            for (int a = 0; a < N; ++a) tv[a] = src[a];
+#pragma unroll
+            for (int w = 1; w < N; w *= 2)
+#pragma unroll
+              for (int a = 0; a + w < N; a += 2 * w) tv[a] += tv[a + w];
+            const double sum = tv[0];
+            const int Lq = slot * W::LPW + gq;
+            if (Lq < W::NL && v < NC) {
+              double* d = dest(Lq, v);
+              if (d) *d -= sum;  // s = B J_f f* - C^T 1
+            }
           }
+          __syncwarp();
         }
-        __syncwarp();
       };
       if constexpr (DIM == 2) {
         Job<DIM> jf[2];
@@ -810,7 +820,7 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   double* tB = tli4 + N * N;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* scr = smk2 + L::o_sc + warp * NC * 32;
+  double* scr = smk2 + L::o_sc + warp * L::SCV * 32;
   const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
   auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
   // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers
