@@ -51,6 +51,8 @@ def lib():
         L.ora_euler_flux.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, _dp, _dp, _dp]
         L.ora_ec_flux.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, _dp, _dp, _dp, _dp]
         L.ora_es_flux.argtypes = L.ora_ec_flux.argtypes
+        L.ora_ej_flux.argtypes = L.ora_ec_flux.argtypes
+        L.ora_dudw.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, _dp, _dp]
         L.ora_wave_speed.restype = ctypes.c_double
         L.ora_wave_speed.argtypes = [ctypes.c_int, ctypes.c_double, _dp, _dp, _dp]
         L.ora_ln_mean.restype = ctypes.c_double
@@ -177,6 +179,25 @@ def es_flux(Ua, Ub, nunit, gamma=1.4):
     F = np.zeros_like(Ua)
     lib().ora_es_flux(Ua.shape[1] - 2, gamma, len(Ua), _d(Ua), _d(Ub), _d(nunit), _d(F))
     return F
+
+
+def ej_flux(Ua, Ub, nunit, gamma=1.4):
+    """entropy-jump scalar dissipation interface flux (flux_mode 2, reading R27)"""
+    Ua = _c(np.atleast_2d(Ua))
+    Ub = _c(np.atleast_2d(Ub))
+    nunit = _c(np.broadcast_to(nunit, (len(Ua), Ua.shape[1] - 2)))
+    F = np.zeros_like(Ua)
+    lib().ora_ej_flux(Ua.shape[1] - 2, gamma, len(Ua), _d(Ua), _d(Ub), _d(nunit), _d(F))
+    return F
+
+
+def dudw(U, gamma=1.4):
+    """du/dw at each state [n][d+2][d+2] (reading R27)"""
+    U = _c(np.atleast_2d(U))
+    n = U.shape[1]
+    A = np.zeros((len(U), n, n))
+    lib().ora_dudw(n - 2, gamma, len(U), _d(U), _d(A))
+    return A
 
 
 def wave_speed(Ua, Ub, nunit, gamma=1.4):

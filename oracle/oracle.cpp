@@ -600,6 +600,56 @@ void es_flux(int d, double g, const double* Ua, const double* Ub, const double* 
   for (int e = 0; e < d + 2; ++e) F[e] -= 0.5 * lam * (Ub[e] - Ua[e]);
 }
 
+// du/dw at the state U: the inverse of the Hessian of S = -rho s/(g-1), symmetric positive
+// definite for rho, p > 0 (Harten / Barth form; reading R27):
+//   [ rho      rho v^T                E            ]
+//   [ rho v    rho v v^T + p I        rho h v      ]     h = (E + p)/rho, a^2 = g p / rho
+//   [ E        rho h v^T              rho h^2 - a^2 p/(g-1) ]
+void dudw(int d, double g, const double* U, double* A /*[(d+2)^2] row-major*/) {
+  Prim s = prim(d, g, U);
+  int n = d + 2;
+  double E = U[d + 1], h = (E + s.p) / s.rho, a2 = g * s.p / s.rho;
+  A[0] = s.rho;
+  for (int k = 0; k < d; ++k) A[1 + k] = A[(1 + k) * n] = s.rho * s.v[k];
+  A[d + 1] = A[(d + 1) * n] = E;
+  for (int k = 0; k < d; ++k) {
+    for (int l = 0; l < d; ++l) A[(1 + k) * n + 1 + l] = s.rho * s.v[k] * s.v[l] + (k == l ? s.p : 0.0);
+    A[(1 + k) * n + d + 1] = A[(d + 1) * n + 1 + k] = s.rho * h * s.v[k];
+  }
+  A[(d + 1) * n + d + 1] = s.rho * h * h - a2 * s.p / (g - 1.0);
+}
+// entropy-stable interface flux with scalar dissipation on the jump of the entropy variables
+// (the alternative named at P:497, after Chandrashekar; reading R27):
+//   f* = f#(Ua, Ub, n) - lambda/2 (du/dw)(U(wbar)) (w(Ub) - w(Ua)),  wbar = (w(Ua) + w(Ub))/2,
+// lambda = Davis's wave speed.  du/dw is symmetric positive definite, so the dissipation
+// removes entropy: [w]^T (f* - f#) = -lambda/2 [w]^T (du/dw) [w] <= 0.
+void ej_flux(int d, double g, const double* Ua, const double* Ub, const double* nu, double* F) {
+  ec_flux(d, g, Ua, Ub, nu, F);
+  double lam = wave_speed(d, g, Ua, Ub, nu);
+  int n = d + 2;
+  double wa[5], wb[5], wm[5], Um[5], A[25];
+  entropy_vars(d, g, Ua, wa);
+  entropy_vars(d, g, Ub, wb);
+  for (int e = 0; e < n; ++e) wm[e] = 0.5 * (wa[e] + wb[e]);
+  cons_from_entropy(d, g, wm, Um);
+  dudw(d, g, Um, A);
+  for (int e = 0; e < n; ++e) {
+    double t = 0.0;
+    for (int k = 0; k < n; ++k) t += A[e * n + k] * (wb[k] - wa[k]);
+    F[e] -= 0.5 * lam * t;
+  }
+}
+// interface flux by mode: 0 = entropy conservative, 1 = local Lax-Friedrichs,
+// 2 = entropy-jump scalar dissipation (R27)
+void iface_flux(int mode, int d, double g, const double* Ua, const double* Ub, const double* nu, double* F) {
+  if (mode == 1)
+    es_flux(d, g, Ua, Ub, nu, F);
+  else if (mode == 2)
+    ej_flux(d, g, Ua, Ub, nu, F);
+  else
+    ec_flux(d, g, Ua, Ub, nu, F);
+}
+
 // ------------------------------------------------------------------------------------------------
 // small dense linear algebra: Gaussian elimination with partial pivoting, A X = B (in place)
 // ------------------------------------------------------------------------------------------------
@@ -960,6 +1010,13 @@ void ora_ec_flux(int d, double g, int n, const double* Ua, const double* Ub, con
 void ora_es_flux(int d, double g, int n, const double* Ua, const double* Ub, const double* nu, double* F) {
   for (int i = 0; i < n; ++i)
     es_flux(d, g, Ua + (size_t)i * (d + 2), Ub + (size_t)i * (d + 2), nu + (size_t)i * d, F + (size_t)i * (d + 2));
+}
+void ora_dudw(int d, double g, int n, const double* U, double* A) {
+  for (int i = 0; i < n; ++i) dudw(d, g, U + (size_t)i * (d + 2), A + (size_t)i * (d + 2) * (d + 2));
+}
+void ora_ej_flux(int d, double g, int n, const double* Ua, const double* Ub, const double* nu, double* F) {
+  for (int i = 0; i < n; ++i)
+    ej_flux(d, g, Ua + (size_t)i * (d + 2), Ub + (size_t)i * (d + 2), nu + (size_t)i * d, F + (size_t)i * (d + 2));
 }
 double ora_wave_speed(int d, double g, const double* Ua, const double* Ub, const double* nu) {
   return wave_speed(d, g, Ua, Ub, nu);
@@ -1365,8 +1422,7 @@ void element_rhs(const ora_mesh& m, int64_t e, const vector<Proj>& PJ, const vec
         double nu[3];
         for (int k = 0; k < d; ++k) nu[k] = Jn[k] / Jf;
         double fs[5], fphys[5];
-        if (flux_mode == 1) es_flux(d, g, um, up, nu, fs);
-        else ec_flux(d, g, um, up, nu, fs);
+        iface_flux(flux_mode, d, g, um, up, nu, fs);
         out.ie++;
         euler_flux(d, g, um, nu, fphys);
         double bf = r.B[z * Nqf + f];
@@ -1482,8 +1538,7 @@ void element_rhs(const ora_mesh& m, int64_t e, const vector<Proj>& PJ, const vec
         double nu[3];
         for (int k = 0; k < d; ++k) nu[k] = Jn[k] / Jf;
         double fs[5];
-        if (flux_mode == 1) es_flux(d, g, um, up, nu, fs);  // P:491 (ES), P:841 (EC)
-        else ec_flux(d, g, um, up, nu, fs);
+        iface_flux(flux_mode, d, g, um, up, nu, fs);  // P:491 (ES), P:841 (EC), P:497 (R27)
         out.ie++;
         double bf = r.B[z * Nqf + f];
         for (int c = 0; c < Nc; ++c) {

@@ -88,6 +88,61 @@ def test_ec_flux_consistency_symmetry_tadmor(d):
 
 
 @pytest.mark.parametrize("d", [2, 3])
+def test_dudw_is_the_inverse_entropy_hessian(d):
+    # R27: du/dw in closed form against central differences of the paper's map u(w) (R7)
+    # and of w(u); symmetric positive definite
+    U = I.random_states(40, d, seed=11, spread=0.6)
+    A = O.dudw(U)
+    W = O.entropy_vars(U)
+    h = 1e-6
+    for i in range(0, 40, 8):
+        Jw = np.zeros((d + 2, d + 2))
+        Ju = np.zeros((d + 2, d + 2))
+        for k in range(d + 2):
+            e = np.zeros(d + 2)
+            e[k] = h * max(1.0, abs(W[i, k]))
+            Jw[:, k] = (O.cons_from_entropy(W[i] + e)[0] - O.cons_from_entropy(W[i] - e)[0]) / (2 * e[k])
+            e = np.zeros(d + 2)
+            e[k] = h * max(1.0, abs(U[i, k]))
+            Ju[:, k] = (O.entropy_vars(U[i] + e)[0] - O.entropy_vars(U[i] - e)[0]) / (2 * e[k])
+        assert np.abs(A[i] - Jw).max() < 1e-7 * np.abs(A[i]).max()
+        assert np.abs(A[i] @ Ju - np.eye(d + 2)).max() < 1e-6
+        np.testing.assert_allclose(A[i], A[i].T, rtol=1e-15, atol=1e-15)
+        assert np.linalg.eigvalsh(A[i]).min() > 0
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_entropy_jump_flux(d):
+    # interface flux mode 2 (R27): consistent, conservative, entropy stable with the exact
+    # dissipation -lambda/2 [w]^T (du/dw) [w], and equal to local Lax-Friedrichs to O(|[u]|^2)
+    Ua = I.random_states(300, d, seed=12, spread=0.6)
+    Ub = I.random_states(300, d, seed=13, spread=0.6)
+    rng = np.random.default_rng(14)
+    n = rng.standard_normal((300, d))
+    n /= np.linalg.norm(n, axis=1)[:, None]
+    F = O.ej_flux(Ua, Ub, n)
+    np.testing.assert_allclose(O.ej_flux(Ua, Ua, n), O.euler_flux(Ua, n), rtol=1e-14, atol=1e-13)
+    np.testing.assert_allclose(F, -O.ej_flux(Ub, Ua, -n), rtol=1e-13, atol=1e-13)
+    Wa, Wb = O.entropy_vars(Ua), O.entropy_vars(Ub)
+    dw = Wb - Wa
+    lhs = np.sum(dw * F, 1)
+    rhs = np.sum(Ub[:, 1:1 + d] * n, 1) - np.sum(Ua[:, 1:1 + d] * n, 1)
+    assert (lhs - rhs < 0).all()  # P:488, strictly for distinct states
+    # the dissipation as stated, with du/dw at u(wbar) and Davis's speed
+    Um = O.cons_from_entropy(0.5 * (Wa + Wb))
+    A = O.dudw(Um)
+    lam = np.array([O.wave_speed(Ua[i], Ub[i], n[i]) for i in range(300)])
+    Dexp = -0.5 * lam[:, None] * np.einsum("nij,nj->ni", A, dw)
+    np.testing.assert_allclose(F - O.ec_flux(Ua, Ub, n), Dexp, rtol=1e-12, atol=1e-12)
+    # small jumps: (du/dw)[w] = [u] + O(|[u]|^2), so the flux approaches local Lax-Friedrichs
+    errs = []
+    for eps in (1e-2, 5e-3):
+        Uc = Ua[:20] * (1.0 + eps * rng.standard_normal((20, d + 2)) * 0.1)
+        errs.append(np.abs(O.ej_flux(Ua[:20], Uc, n[:20]) - O.es_flux(Ua[:20], Uc, n[:20])).max())
+    assert errs[0] < 1e-3 and errs[1] < errs[0] / 2.5
+
+
+@pytest.mark.parametrize("d", [2, 3])
 def test_es_flux_conservation_and_entropy_condition(d):
     Ua = I.random_states(300, d, seed=5, spread=0.6)
     Ub = I.random_states(300, d, seed=6, spread=0.6)
