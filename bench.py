@@ -285,6 +285,9 @@ def run(args):
     if args.p:
         p = args.p  # degree sweep on the same mesh (BASELINE C3: p = 2, 4, 6, 8, 10)
         desc = f"{desc} [degree override p={p}]"
+    if args.interface_flux >= 0 and args.interface_flux != fm:
+        fm = args.interface_flux
+        desc = f"{desc} [interface flux {('EC', 'ES-LLF', 'ES-entropy-jump')[fm]}]"
     mesh = I.split_cartesian(dim, M, L)
     w = {"bj": I.bj_warp(dim, L, M), "none": None}.get(warp)
     nccl_id = nccl_unique_id(dist, torch, rank, "cuda") if world > 1 else None
@@ -433,6 +436,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--p", type=int, default=0, help="override the configuration's polynomial degree")
+    ap.add_argument("--interface-flux", type=int, default=-1,
+                    help="override the configuration's interface flux: 0 EC, 1 LLF, 2 entropy jump (R27)")
     ap.add_argument("--volume-mode", type=int, default=0,
                     help="1: ablation, one flux per operator S^(l) (the paper's Eq. num_fluxes iteration)")
     args = ap.parse_args()

@@ -885,6 +885,54 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_eq56_kernel(DevRef R, 
   rhs2_body<DIM, N, true>(R, A);
 }
 
+// entropy variables of a primitive state (App. B, R7): w = ((g - s)/(g - 1) - b|v|^2/2, b v, -b),
+// s = ln p - g ln rho, b = rho / p
+template <int DIM>
+__device__ __forceinline__ void wvars(const NodeState& a, double g, double* w) {
+  double v2 = 0.0;
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) v2 += a.v[m] * a.v[m];
+  const double s = log(a.p) - g * log(a.r);
+  w[0] = (g - s) / (g - 1.0) - 0.5 * a.b * v2;
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) w[1 + m] = a.b * a.v[m];
+  w[DIM + 1] = -a.b;
+}
+// D = (du/dw)(u(wbar)) (w+ - w-), wbar the mean of the two sides' entropy variables (reading R27).
+// du/dw in primitive form, applied without forming the matrix:
+//   D_0   = rho (dw_0 + v.dw_v) + E dw_E
+//   D_v   = rho v (dw_0 + v.dw_v) + p dw_v + rho h v dw_E
+//   D_E   = E dw_0 + rho h v.dw_v + (rho h^2 - g p^2 / (rho (g - 1))) dw_E,  h = (E + p) / rho
+template <int DIM>
+__device__ __forceinline__ void entropy_jump(const NodeState& um, const NodeState& up, double g, double* D) {
+  double wm[DIM + 2], wp[DIM + 2], wb[DIM + 2], dw[DIM + 2];
+  wvars<DIM>(um, g, wm);
+  wvars<DIM>(up, g, wp);
+#pragma unroll
+  for (int k = 0; k < DIM + 2; ++k) {
+    wb[k] = 0.5 * (wm[k] + wp[k]);
+    dw[k] = wp[k] - wm[k];
+  }
+  // u(wbar): b = -w_last, v = w_v / b, s = g - (g - 1)(w_0 + b|v|^2/2), rho = (b e^s)^(1/(1-g))
+  const double b = -wb[DIM + 1];
+  double v[DIM], v2 = 0.0, vdw = 0.0;
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) {
+    v[m] = wb[1 + m] / b;
+    v2 += v[m] * v[m];
+  }
+  const double s = g - (g - 1.0) * (wb[0] + 0.5 * b * v2);
+  const double r = exp((s + log(b)) / (1.0 - g)), p = r / b;
+  const double E = p / (g - 1.0) + 0.5 * r * v2, rh = E + p;
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) vdw += v[m] * dw[1 + m];
+  const double c0 = r * (dw[0] + vdw);
+  D[0] = c0 + E * dw[DIM + 1];
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) D[1 + m] = v[m] * (c0 + rh * dw[DIM + 1]) + p * dw[1 + m];
+  D[DIM + 1] = E * dw[0] + rh * vdw + (rh * rh / r - g * p * p / (r * (g - 1.0))) * dw[DIM + 1];
+}
+
 // ------------------------------------------------------------------------------------------------
 // interface flux (Davis wave speed P:839): one thread per (element, facet node);
 // writes B J_f f*(u-, u+, n) with the element's own unit normal n = J n / J_f and the
@@ -934,7 +982,7 @@ __global__ void __launch_bounds__(256) iface_kernel(DevRef R, IfaceArgs A) {
   for (int m = 0; m < DIM; ++m) nu[m] = Jn[m] / Jf;
   double F[NC];
   ec_flux_v2<DIM>(um, up, nu, gm1inv, F);
-  if (A.es) {  // local Lax-Friedrichs with Davis's wave speed
+  if (A.es) {  // dissipation with Davis's wave speed
     double vnm = 0.0, vnp = 0.0;
 #pragma unroll
     for (int m = 0; m < DIM; ++m) {
@@ -942,11 +990,18 @@ __global__ void __launch_bounds__(256) iface_kernel(DevRef R, IfaceArgs A) {
       vnp += up.v[m] * nu[m];
     }
     const double lam = fmax(fabs(vnm), fabs(vnp)) + fmax(sqrt(g * um.p / um.r), sqrt(g * up.p / up.r));
-    double Um[NC], Up[NC];
-    cons_of<DIM>(um.r, um.v, um.p, gm1inv, Um);
-    cons_of<DIM>(up.r, up.v, up.p, gm1inv, Up);
+    double D[NC];
+    if (A.es == 1) {  // local Lax-Friedrichs on the conservative jump
+      double Um[NC], Up[NC];
+      cons_of<DIM>(um.r, um.v, um.p, gm1inv, Um);
+      cons_of<DIM>(up.r, up.v, up.p, gm1inv, Up);
 #pragma unroll
-    for (int v = 0; v < NC; ++v) F[v] -= 0.5 * lam * (Up[v] - Um[v]);
+      for (int v = 0; v < NC; ++v) D[v] = Up[v] - Um[v];
+    } else {  // entropy-jump scalar dissipation (reading R27): (du/dw)(u(wbar)) [w]
+      entropy_jump<DIM>(um, up, g, D);
+    }
+#pragma unroll
+    for (int v = 0; v < NC; ++v) F[v] -= 0.5 * lam * D[v];
   }
   const double bj = __ldg(&R.Bf[fz]) * Jf;
   double* out = A.fstar + (size_t)(e * Nf + z) * NC * Nqf + f;
