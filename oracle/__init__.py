@@ -52,6 +52,7 @@ def lib():
         L.ora_ec_flux.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, _dp, _dp, _dp, _dp]
         L.ora_es_flux.argtypes = L.ora_ec_flux.argtypes
         L.ora_ej_flux.argtypes = L.ora_ec_flux.argtypes
+        L.ora_md_flux.argtypes = L.ora_ec_flux.argtypes
         L.ora_dudw.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, _dp, _dp]
         L.ora_wave_speed.restype = ctypes.c_double
         L.ora_wave_speed.argtypes = [ctypes.c_int, ctypes.c_double, _dp, _dp, _dp]
@@ -188,6 +189,16 @@ def ej_flux(Ua, Ub, nunit, gamma=1.4):
     nunit = _c(np.broadcast_to(nunit, (len(Ua), Ua.shape[1] - 2)))
     F = np.zeros_like(Ua)
     lib().ora_ej_flux(Ua.shape[1] - 2, gamma, len(Ua), _d(Ua), _d(Ub), _d(nunit), _d(F))
+    return F
+
+
+def md_flux(Ua, Ub, nunit, gamma=1.4):
+    """matrix-dissipation interface flux (flux_mode 3, reading R28)"""
+    Ua = _c(np.atleast_2d(Ua))
+    Ub = _c(np.atleast_2d(Ub))
+    nunit = _c(np.broadcast_to(nunit, (len(Ua), Ua.shape[1] - 2)))
+    F = np.zeros_like(Ua)
+    lib().ora_md_flux(Ua.shape[1] - 2, gamma, len(Ua), _d(Ua), _d(Ub), _d(nunit), _d(F))
     return F
 
 

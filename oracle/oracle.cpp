@@ -639,13 +639,56 @@ void ej_flux(int d, double g, const double* Ua, const double* Ub, const double* 
     F[e] -= 0.5 * lam * t;
   }
 }
+// entropy-stable matrix dissipation (the alternative named at P:497, after Ismail-Roe / Winters et
+// al.; reading R28): f* = f#(Ua, Ub, n) - 1/2 |A_n| (du/dw) [w], the normal flux Jacobian A_n and du/dw
+// both at U(wbar).  With the eigenvectors of A_n scaled so that R T R^T = du/dw (Barth),
+//   |A_n| du/dw = |v.n| du/dw + sum_{+,-} (|v.n +- a| - |v.n|) rho/(2g) r_+- r_+-^T,
+//   r_+- = (1, v +- a n, h +- a v.n),  a^2 = g p / rho,  h = (E + p)/rho.
+void md_flux(int d, double g, const double* Ua, const double* Ub, const double* nu, double* F) {
+  ec_flux(d, g, Ua, Ub, nu, F);
+  int n = d + 2;
+  double wa[5], wb[5], wm[5], Um[5], A[25], dw[5];
+  entropy_vars(d, g, Ua, wa);
+  entropy_vars(d, g, Ub, wb);
+  for (int e = 0; e < n; ++e) {
+    wm[e] = 0.5 * (wa[e] + wb[e]);
+    dw[e] = wb[e] - wa[e];
+  }
+  cons_from_entropy(d, g, wm, Um);
+  dudw(d, g, Um, A);
+  Prim s = prim(d, g, Um);
+  double a = std::sqrt(g * s.p / s.rho), h = (Um[d + 1] + s.p) / s.rho, vn = 0.0;
+  for (int k = 0; k < d; ++k) vn += s.v[k] * nu[k];
+  double rm[5], rp[5];
+  rm[0] = rp[0] = 1.0;
+  for (int k = 0; k < d; ++k) {
+    rm[1 + k] = s.v[k] - a * nu[k];
+    rp[1 + k] = s.v[k] + a * nu[k];
+  }
+  rm[d + 1] = h - a * vn;
+  rp[d + 1] = h + a * vn;
+  double cm = (std::fabs(vn - a) - std::fabs(vn)) * s.rho / (2.0 * g);
+  double cp = (std::fabs(vn + a) - std::fabs(vn)) * s.rho / (2.0 * g);
+  double pm = 0.0, pp = 0.0;
+  for (int e = 0; e < n; ++e) {
+    pm += rm[e] * dw[e];
+    pp += rp[e] * dw[e];
+  }
+  for (int e = 0; e < n; ++e) {
+    double t = 0.0;
+    for (int k = 0; k < n; ++k) t += A[e * n + k] * dw[k];
+    F[e] -= 0.5 * (std::fabs(vn) * t + cm * pm * rm[e] + cp * pp * rp[e]);
+  }
+}
 // interface flux by mode: 0 = entropy conservative, 1 = local Lax-Friedrichs,
-// 2 = entropy-jump scalar dissipation (R27)
+// 2 = entropy-jump scalar dissipation (R27), 3 = matrix dissipation (R28)
 void iface_flux(int mode, int d, double g, const double* Ua, const double* Ub, const double* nu, double* F) {
   if (mode == 1)
     es_flux(d, g, Ua, Ub, nu, F);
   else if (mode == 2)
     ej_flux(d, g, Ua, Ub, nu, F);
+  else if (mode == 3)
+    md_flux(d, g, Ua, Ub, nu, F);
   else
     ec_flux(d, g, Ua, Ub, nu, F);
 }
@@ -1017,6 +1060,10 @@ void ora_dudw(int d, double g, int n, const double* U, double* A) {
 void ora_ej_flux(int d, double g, int n, const double* Ua, const double* Ub, const double* nu, double* F) {
   for (int i = 0; i < n; ++i)
     ej_flux(d, g, Ua + (size_t)i * (d + 2), Ub + (size_t)i * (d + 2), nu + (size_t)i * d, F + (size_t)i * (d + 2));
+}
+void ora_md_flux(int d, double g, int n, const double* Ua, const double* Ub, const double* nu, double* F) {
+  for (int i = 0; i < n; ++i)
+    md_flux(d, g, Ua + (size_t)i * (d + 2), Ub + (size_t)i * (d + 2), nu + (size_t)i * d, F + (size_t)i * (d + 2));
 }
 double ora_wave_speed(int d, double g, const double* Ua, const double* Ub, const double* nu) {
   return wave_speed(d, g, Ua, Ub, nu);

@@ -56,6 +56,9 @@ double ora_wave_speed(int d, double gamma, const double* Ua, const double* Ub, c
 void ora_dudw(int d, double gamma, int n, const double* U, double* A);
 void ora_ej_flux(int d, double gamma, int n, const double* Ua, const double* Ub, const double* nunit,
                  double* F);
+/* matrix-dissipation interface flux (R28) */
+void ora_md_flux(int d, double gamma, int n, const double* Ua, const double* Ub, const double* nunit,
+                 double* F);
 double ora_ln_mean(double x, double y);
 double ora_inv_ln_mean(double x, double y);
 void ora_entropy(int d, double gamma, int n, const double* U, double* S, double* Fent /*[n][d]*/);
@@ -96,7 +99,8 @@ void ora_mesh_conn(const ora_mesh* m, int64_t* nbr, int* nbr_face, int* reflect)
 void ora_project(const ora_mesh* m, int64_t n_el, const int64_t* elems, const double* u_nodal,
                  double* u_modal);
 /* RHS: dudt [ne][Nc][Np] for the listed elements (NULL list = all).  flux_mode 0 = EC, 1 = ES
- * (EC + LLF/Davis), 2 = EC + entropy-jump scalar dissipation (R27).  variant 0 = Eq. num_fluxes nonzero loops, 1 = line-wise pairing
+ * (EC + LLF/Davis), 2 = EC + entropy-jump scalar dissipation (R27), 3 = EC + matrix
+ * dissipation (R28).  variant 0 = Eq. num_fluxes nonzero loops, 1 = line-wise pairing
  * (P:572), 2 = dense brute force (all i,j), 3 = hybridised SBP (Chan-Wilcox eq. 35).
  * nthreads <= 0 -> OpenMP default.  Returns 0, or 3 if an inadmissible state was met. */
 int ora_rhs(const ora_mesh* m, const double* u_modal, double* dudt, int flux_mode, int variant,

@@ -143,6 +143,36 @@ def test_entropy_jump_flux(d):
 
 
 @pytest.mark.parametrize("d", [2, 3])
+def test_matrix_dissipation_flux(d):
+    # interface flux mode 3 (R28): f* - f# = -1/2 |A_n| (du/dw) [w] at U(wbar), with |A_n| from
+    # numpy's eigendecomposition of a finite-difference Jacobian of the normal Euler flux
+    Ua = I.random_states(60, d, seed=15, spread=0.6)
+    Ub = I.random_states(60, d, seed=16, spread=0.6)
+    rng = np.random.default_rng(17)
+    n = rng.standard_normal((60, d))
+    n /= np.linalg.norm(n, axis=1)[:, None]
+    F = O.md_flux(Ua, Ub, n)
+    Wa, Wb = O.entropy_vars(Ua), O.entropy_vars(Ub)
+    Um = O.cons_from_entropy(0.5 * (Wa + Wb))
+    A0 = O.dudw(Um)
+    for i in range(0, 60, 6):
+        J = np.zeros((d + 2, d + 2))
+        for k in range(d + 2):
+            e = np.zeros(d + 2)
+            e[k] = 1e-6 * max(1.0, abs(Um[i, k]))
+            J[:, k] = (O.euler_flux(Um[i] + e, n[i])[0] - O.euler_flux(Um[i] - e, n[i])[0]) / (2 * e[k])
+        lam, R = np.linalg.eig(J)
+        absA = (R @ np.diag(np.abs(lam)) @ np.linalg.inv(R)).real
+        D = -0.5 * absA @ A0[i] @ (Wb[i] - Wa[i])
+        np.testing.assert_allclose(F[i] - O.ec_flux(Ua[i], Ub[i], n[i])[0], D, rtol=1e-7, atol=1e-8 * np.abs(F[i]).max())
+    np.testing.assert_allclose(O.md_flux(Ua, Ua, n), O.euler_flux(Ua, n), rtol=1e-14, atol=1e-13)
+    np.testing.assert_allclose(F, -O.md_flux(Ub, Ua, -n), rtol=1e-13, atol=1e-13)
+    lhs = np.sum((Wb - Wa) * F, 1)
+    rhs = np.sum(Ub[:, 1:1 + d] * n, 1) - np.sum(Ua[:, 1:1 + d] * n, 1)
+    assert (lhs - rhs < 0).all()  # |A_n| du/dw is symmetric positive semi-definite
+
+
+@pytest.mark.parametrize("d", [2, 3])
 def test_es_flux_conservation_and_entropy_condition(d):
     Ua = I.random_states(300, d, seed=5, spread=0.6)
     Ub = I.random_states(300, d, seed=6, spread=0.6)

@@ -64,7 +64,7 @@ def test_conservation_entropy_and_variant_agreement(d, p):
     u0 = I.density_wave(xq, L) if d == 2 else I.taylor_green(xq, Ma=0.3)
     u = I.perturb_modal(om.project(u0), d, p, seed=1, amp=2e-2)
     n = p + 1
-    for fm in (0, 1, 2):  # EC, LLF, entropy-jump dissipation (R27)
+    for fm in (0, 1, 2, 3):  # EC, LLF, entropy-jump (R27) and matrix (R28) dissipation
         ref, st = om.rhs(u, flux_mode=fm, variant=0)
         # conservation and entropy balance, periodic
         cons_scale = np.abs(ref).max() * om.ne
