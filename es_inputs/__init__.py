@@ -167,6 +167,16 @@ def taylor_green(x, Ma=0.1, gamma=GAMMA):
     return prim_to_cons(np.ones_like(x1), v, p, gamma)
 
 
+def kelvin_helmholtz(x, gamma=GAMMA):
+    """P:931-936 (robustness test): B = tanh(15(x2 - 1/2)) - tanh(15(x2 - 3/2)),
+    rho = 1/2 + 3/4 B, v = ((B - 1)/2, sin(2 pi x1)/10), p = 1 on (0, 2)^2."""
+    x = np.asarray(x)
+    x1, x2 = x[..., 0], x[..., 1]
+    B = np.tanh(15.0 * (x2 - 0.5)) - np.tanh(15.0 * (x2 - 1.5))
+    v = np.stack([0.5 * (B - 1.0), 0.1 * np.sin(2.0 * math.pi * x1)], axis=-1)
+    return prim_to_cons(0.5 + 0.75 * B, v, np.ones_like(x1), gamma)
+
+
 def isentropic_vortex(x, L, gamma=GAMMA, beta=1.0):
     """R14: exact translating isentropic vortex, centre (L/2, L/2), radius L/10, Mach-0.5 background."""
     x = np.asarray(x)

@@ -66,7 +66,8 @@ typedef struct {
   int interface_flux;                   /* 0 = entropy conservative, 1 = entropy stable with local
                                            Lax-Friedrichs dissipation, 2 = entropy stable
                                            with scalar dissipation on the entropy-variable jump (P:497,
-                                           DESIGN.md R27); other values: ES_ERR_CONFIG */
+                                           DESIGN.md R27), 3 = entropy stable with matrix dissipation
+                                           (R28); other values: ES_ERR_CONFIG */
   int rank, world;                      /* local elements [rank*N_e/world, (rank+1)*N_e/world) */
   const unsigned char* nccl_unique_id;  /* 128-byte ncclUniqueId (world > 1), broadcast by caller;
                                            NULL with world > 1: the caller moves the halo itself

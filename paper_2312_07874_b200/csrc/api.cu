@@ -336,7 +336,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   c->device = opt->device;
   if (c->d != 2 && c->d != 3) return fail(c, ES_ERR_CONFIG, "dim must be 2 or 3");
   if (!(c->gamma > 1.0)) return fail(c, ES_ERR_CONFIG, "gamma must exceed 1");
-  if (c->es < 0 || c->es > 2) return fail(c, ES_ERR_CONFIG, "interface_flux must be 0, 1 or 2");
+  if (c->es < 0 || c->es > 3) return fail(c, ES_ERR_CONFIG, "interface_flux must be 0, 1, 2 or 3");
   if (c->rank < 0 || c->rank >= c->world) return fail(c, ES_ERR_ARG, "rank out of range");
   c->external = c->world > 1 && !opt->nccl_unique_id;
   std::string err;

@@ -69,7 +69,7 @@ struct RhsArgs {
   const int64_t* face_slot;   // [nloc][Nf]
   const int* face_reflect;    // [nloc][Nf]
   double gamma;
-  int es;                     // interface dissipation: 0 none (EC), 1 LLF, 2 entropy jump (R27)
+  int es;                     // interface dissipation: 0 none (EC), 1 LLF, 2 entropy jump (R27), 3 matrix (R28)
   int mode;                   // 0 dudt, 1..4 RK stage 0..3, 5 dudt + entropy partials
   double* out;                // dudt [nloc][NC][Np]
   const double* u0;           // RK state

@@ -903,8 +903,12 @@ __device__ __forceinline__ void wvars(const NodeState& a, double g, double* w) {
 //   D_0   = rho (dw_0 + v.dw_v) + E dw_E
 //   D_v   = rho v (dw_0 + v.dw_v) + p dw_v + rho h v dw_E
 //   D_E   = E dw_0 + rho h v.dw_v + (rho h^2 - g p^2 / (rho (g - 1))) dw_E,  h = (E + p) / rho
-template <int DIM>
-__device__ __forceinline__ void entropy_jump(const NodeState& um, const NodeState& up, double g, double* D) {
+// MAT (reading R28): D = |A_n| (du/dw) [w] at the same state, with the Barth-scaled eigenvectors:
+//   |v.n| (du/dw)[w] + sum_{+,-} (|v.n +- a| - |v.n|) rho/(2g) (r_+- . [w]) r_+-,
+//   r_+- = (1, v +- a n, h +- a v.n), a^2 = g p / rho; lam is unused then
+template <int DIM, bool MAT = false>
+__device__ __forceinline__ void entropy_jump(const NodeState& um, const NodeState& up, double g, double* D,
+                                             const double* nu = nullptr) {
   double wm[DIM + 2], wp[DIM + 2], wb[DIM + 2], dw[DIM + 2];
   wvars<DIM>(um, g, wm);
   wvars<DIM>(up, g, wp);
@@ -931,6 +935,24 @@ __device__ __forceinline__ void entropy_jump(const NodeState& um, const NodeStat
 #pragma unroll
   for (int m = 0; m < DIM; ++m) D[1 + m] = v[m] * (c0 + rh * dw[DIM + 1]) + p * dw[1 + m];
   D[DIM + 1] = E * dw[0] + rh * vdw + (rh * rh / r - g * p * p / (r * (g - 1.0))) * dw[DIM + 1];
+  if constexpr (MAT) {
+    const double a = sqrt(g * p / r), h = rh / r;
+    double vn = 0.0, adn = 0.0;
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) {
+      vn += v[m] * nu[m];
+      adn += nu[m] * dw[1 + m];
+    }
+    const double avn = fabs(vn);
+    // r_+- . [w] = dw_0 + v.dw_v +- a n.dw_v + (h +- a v.n) dw_E
+    const double base = dw[0] + vdw + h * dw[DIM + 1], sh = a * (adn + vn * dw[DIM + 1]);
+    const double km = (fabs(vn - a) - avn) * r / (2.0 * g) * (base - sh);
+    const double kp = (fabs(vn + a) - avn) * r / (2.0 * g) * (base + sh);
+    D[0] = avn * D[0] + km + kp;
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) D[1 + m] = avn * D[1 + m] + km * (v[m] - a * nu[m]) + kp * (v[m] + a * nu[m]);
+    D[DIM + 1] = avn * D[DIM + 1] + km * (h - a * vn) + kp * (h + a * vn);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -939,7 +961,7 @@ __device__ __forceinline__ void entropy_jump(const NodeState& um, const NodeStat
 // neighbour's trace at the permuted node.  Both sides of a face evaluate it with their
 // own normals; the arithmetic per side does not depend on the partition.
 // ------------------------------------------------------------------------------------------------
-template <int DIM, int N>
+template <int DIM, int N, int ES>  // ES = IfaceArgs::es
 __global__ void __launch_bounds__(256) iface_kernel(DevRef R, IfaceArgs A) {
   using S = Sz<DIM, N>;
   constexpr int NC = S::NC, Nqf = S::Nqf, NF = S::NF, Nf = S::Nf;
@@ -982,7 +1004,7 @@ __global__ void __launch_bounds__(256) iface_kernel(DevRef R, IfaceArgs A) {
   for (int m = 0; m < DIM; ++m) nu[m] = Jn[m] / Jf;
   double F[NC];
   ec_flux_v2<DIM>(um, up, nu, gm1inv, F);
-  if (A.es) {  // dissipation with Davis's wave speed
+  if constexpr (ES != 0) {  // dissipation with Davis's wave speed
     double vnm = 0.0, vnp = 0.0;
 #pragma unroll
     for (int m = 0; m < DIM; ++m) {
@@ -991,17 +1013,20 @@ __global__ void __launch_bounds__(256) iface_kernel(DevRef R, IfaceArgs A) {
     }
     const double lam = fmax(fabs(vnm), fabs(vnp)) + fmax(sqrt(g * um.p / um.r), sqrt(g * up.p / up.r));
     double D[NC];
-    if (A.es == 1) {  // local Lax-Friedrichs on the conservative jump
+    if constexpr (ES == 1) {  // local Lax-Friedrichs on the conservative jump
       double Um[NC], Up[NC];
       cons_of<DIM>(um.r, um.v, um.p, gm1inv, Um);
       cons_of<DIM>(up.r, up.v, up.p, gm1inv, Up);
 #pragma unroll
       for (int v = 0; v < NC; ++v) D[v] = Up[v] - Um[v];
-    } else {  // entropy-jump scalar dissipation (reading R27): (du/dw)(u(wbar)) [w]
+    } else if constexpr (ES == 2) {  // entropy-jump scalar dissipation (reading R27): (du/dw)(u(wbar)) [w]
       entropy_jump<DIM>(um, up, g, D);
+    } else {  // matrix dissipation (reading R28): |A_n| (du/dw) [w] at u(wbar), no lambda
+      entropy_jump<DIM, true>(um, up, g, D, nu);
     }
+    const double sc = ES == 3 ? 0.5 : 0.5 * lam;
 #pragma unroll
-    for (int v = 0; v < NC; ++v) F[v] -= 0.5 * lam * D[v];
+    for (int v = 0; v < NC; ++v) F[v] -= sc * D[v];
   }
   const double bj = __ldg(&R.Bf[fz]) * Jf;
   double* out = A.fstar + (size_t)(e * Nf + z) * NC * Nqf + f;

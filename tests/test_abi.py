@@ -53,7 +53,7 @@ def test_setup_rejects_bad_arguments_without_gpu(es):
 
 
 def test_setup_rejects_unknown_interface_flux_without_gpu(es):
-    # es_options.interface_flux outside {0, 1, 2} is a configuration error, found before any CUDA call
+    # es_options.interface_flux outside {0, 1, 2, 3} is a configuration error, found before any CUDA call
     import numpy as np
     import es_inputs as I
     mesh = I.split_cartesian(2, 3, 1.0)
@@ -62,7 +62,7 @@ def test_setup_rejects_unknown_interface_flux_without_gpu(es):
     per = np.ascontiguousarray(mesh["period"], np.float64)
     m = es.es_mesh(2, len(ev), ev.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                    evx.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), per.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
-    for bad in (3, -1):
+    for bad in (4, -1):
         o = es.es_options(1.4, bad, 0, 1, None, None, 0, 0, 0)
         h = ctypes.c_void_p()
         rc = es.es_setup(ctypes.byref(h), ctypes.byref(m), 2, es.es_map_fn(0), None, ctypes.byref(o))

@@ -28,10 +28,12 @@ def test_tgv_entropy_history(es):
     ec, _ = H.run(es, I, torch, 3, 3, 0.3, 60, 20, 0, warp="paper")
     esh, _ = H.run(es, I, torch, 3, 3, 0.3, 60, 20, 1, warp="paper")
     ejh, _ = H.run(es, I, torch, 3, 3, 0.3, 60, 20, 2, warp="paper")  # entropy-jump dissipation (R27)
-    for h in ejh:
-        assert h["dSdt"] < 0.0, h
-    S_ej = [h["S"] for h in ejh]
-    assert all(b < a for a, b in zip(S_ej, S_ej[1:])), S_ej
+    mdh, _ = H.run(es, I, torch, 3, 3, 0.3, 60, 20, 3, warp="paper")  # matrix dissipation (R28)
+    for hist in (ejh, mdh):
+        for h in hist:
+            assert h["dSdt"] < 0.0, h
+        S = [h["S"] for h in hist]
+        assert all(b < a for a, b in zip(S, S[1:])), S
     for h in ec:
         assert abs(h["dSdt"]) <= 1e-12 * h["dSdt_scale"], h
     for h in esh:
@@ -40,7 +42,7 @@ def test_tgv_entropy_history(es):
     assert all(b < a for a, b in zip(S_es, S_es[1:])), S_es
     S_ec = [h["S"] for h in ec]
     assert abs(S_ec[-1] - S_ec[0]) < 1e-3 * abs(S_es[-1] - S_es[0]) + 1e-12 * abs(S_ec[0]), (S_ec, S_es)
-    for hist in (ec, esh, ejh):
+    for hist in (ec, esh, ejh, mdh):
         t0 = hist[0]["totals"]
         for h in hist[1:]:
             for a, b in zip(t0, h["totals"]):

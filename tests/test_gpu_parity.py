@@ -100,6 +100,9 @@ CASES = [
     (2, 3, 4, "paper", "wave", 2),     # entropy-jump dissipation (R27)
     (3, 3, 3, "paper", "tgv3", 2),
     (3, 3, 8, "bj", "tgv", 2),
+    (2, 3, 4, "paper", "vortex", 3),   # matrix dissipation (R28)
+    (3, 3, 3, "paper", "tgv3", 3),
+    (3, 3, 8, "bj", "tgv", 3),
 ]
 
 
@@ -152,7 +155,7 @@ def test_geometry_and_nodes_parity(es, d, p):
     assert np.abs(um.cpu().numpy() - ref).max() < 1e-12 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("d,p,fm", [(2, 3, 1), (3, 2, 0), (3, 3, 1), (2, 3, 2), (3, 3, 2)])
+@pytest.mark.parametrize("d,p,fm", [(2, 3, 1), (3, 2, 0), (3, 3, 1), (2, 3, 2), (3, 3, 2), (2, 3, 3), (3, 3, 3)])
 def test_entropy_production_parity(es, d, p, fm):
     mesh, om, ctx, u = _setup(es, d, 3, p, "paper", "wave" if d == 2 else "tgv3", fm)
     ref, st = om.rhs(u, flux_mode=fm, variant=1)
