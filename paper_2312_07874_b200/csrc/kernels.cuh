@@ -206,6 +206,31 @@ __device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const d
       x1[i] *= ok ? sc1[i * sin] : 0.0;
     }
   }
+  if constexpr (!TR && OC % 2 == 1) {
+    // odd chunk width: all N outputs at once, each table row read as 16-byte pairs (padded rows);
+    // every output is an independent chain over the inputs (no = N on this path)
+    double a0[N], a1[N];
+#pragma unroll
+    for (int o = 0; o < N; ++o) a0[o] = a1[o] = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int q2 = 0; q2 < NP / 2; ++q2) {
+        const double2 pv = *reinterpret_cast<const double2*>(ps + i * NP + 2 * q2);
+        a0[2 * q2] = fma(pv.x, x0[i], a0[2 * q2]);
+        a1[2 * q2] = fma(pv.x, x1[i], a1[2 * q2]);
+        if (2 * q2 + 1 < N) {
+          a0[2 * q2 + 1] = fma(pv.y, x0[i], a0[2 * q2 + 1]);
+          a1[2 * q2 + 1] = fma(pv.y, x1[i], a1[2 * q2 + 1]);
+        }
+      }
+#pragma unroll
+    for (int o = 0; o < N; ++o) {
+      out0[o * sout] = a0[o];
+      if (has1) out1[o * sout] = a1[o];
+    }
+    return;
+  }
   // all output chunks in flight (independent chains); for N a multiple of OC ptxas hoists every
   // table load of every chunk (register blow-up), so the chunks stay sequential there
 #pragma unroll(N == 8 ? 1 : N)
@@ -274,6 +299,30 @@ __device__ __forceinline__ void fiberK(const double* ps, const double* const* in
       x[k][i] = in[k][i * sin];
       if (sc) x[k][i] *= sc[k][i * sin];
     }
+  if constexpr (!TR && OC % 2 == 1) {  // whole rows as 16-byte pairs (see fiber2)
+    double a[K][N];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int o = 0; o < N; ++o) a[k][o] = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int q2 = 0; q2 < NP / 2; ++q2) {
+        const double2 pv = *reinterpret_cast<const double2*>(ps + i * NP + 2 * q2);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          a[k][2 * q2] = fma(pv.x, x[k][i], a[k][2 * q2]);
+          if (2 * q2 + 1 < N) a[k][2 * q2 + 1] = fma(pv.y, x[k][i], a[k][2 * q2 + 1]);
+        }
+      }
+#pragma unroll
+    for (int o = 0; o < N; ++o)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (k < nk) out[k][o * sout] = a[k][o];
+    return;
+  }
 #pragma unroll(N == 8 ? 1 : N)
   for (int o0 = 0; o0 < N; o0 += OC) {  // output chunks in flight (see fiber2)
     double a[K][OC];
