@@ -71,6 +71,9 @@ def lib():
         L.ora_rhs.argtypes = [ctypes.c_void_p, _dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _lp,
                               ctypes.c_int, ctypes.POINTER(Stats)]
         L.ora_rk4.argtypes = [ctypes.c_void_p, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.ora_dp54_tableau.argtypes = [_dp, _dp, _dp, _dp]
+        L.ora_dp54.argtypes = [ctypes.c_void_p, _dp, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                               ctypes.c_int, _dp, _dp]
         _lib = L
     return _lib
 
@@ -216,6 +219,12 @@ def wave_speed(Ua, Ub, nunit, gamma=1.4):
     return lib().ora_wave_speed(len(Ua) - 2, gamma, _d(Ua), _d(Ub), _d(nunit))
 
 
+def dp54_tableau():
+    c, a, b, bh = np.zeros(7), np.zeros((7, 7)), np.zeros(7), np.zeros(7)
+    lib().ora_dp54_tableau(_d(c), _d(a), _d(b), _d(bh))
+    return c, a, b, bh
+
+
 def ln_mean(x, y):
     return lib().ora_ln_mean(x, y)
 
@@ -329,6 +338,16 @@ class Mesh:
         if rc:
             raise RuntimeError(f"ora_rhs failed ({rc})")
         return out, st
+
+    def dp54(self, u, dt, rtol=1e-6, atol=1e-8, flux_mode=1, nthreads=0):
+        """one Dormand-Prince 5(4) step: (u5, scaled RMS error estimate)"""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        u5 = np.zeros_like(u)
+        err = ctypes.c_double()
+        rc = lib().ora_dp54(self.h, _d(u), dt, rtol, atol, flux_mode, nthreads, _d(u5), ctypes.byref(err))
+        if rc:
+            raise RuntimeError(f"ora_dp54 failed ({rc})")
+        return u5, err.value
 
     def rk4(self, u, dt, nsteps, flux_mode=1, nthreads=0):
         u = np.array(u, dtype=np.float64, copy=True, order="C")

@@ -1687,6 +1687,61 @@ int ora_rhs(const ora_mesh* m, const double* u_modal, double* dudt, int flux_mod
   return 0;
 }
 
+// Dormand-Prince 5(4) (Hairer, Norsett & Wanner I, Table II.5.2; the paper integrates with DP8 of
+// the same family): c, a (lower triangle, row-major 7x7), b (5th order), bh (embedded 4th)
+static const double DP_C[7] = {0.0, 1.0 / 5.0, 3.0 / 10.0, 4.0 / 5.0, 8.0 / 9.0, 1.0, 1.0};
+static const double DP_A[7][7] = {
+    {0, 0, 0, 0, 0, 0, 0},
+    {1.0 / 5.0, 0, 0, 0, 0, 0, 0},
+    {3.0 / 40.0, 9.0 / 40.0, 0, 0, 0, 0, 0},
+    {44.0 / 45.0, -56.0 / 15.0, 32.0 / 9.0, 0, 0, 0, 0},
+    {19372.0 / 6561.0, -25360.0 / 2187.0, 64448.0 / 6561.0, -212.0 / 729.0, 0, 0, 0},
+    {9017.0 / 3168.0, -355.0 / 33.0, 46732.0 / 5247.0, 49.0 / 176.0, -5103.0 / 18656.0, 0, 0},
+    {35.0 / 384.0, 0.0, 500.0 / 1113.0, 125.0 / 192.0, -2187.0 / 6784.0, 11.0 / 84.0, 0}};
+static const double DP_B[7] = {35.0 / 384.0, 0.0, 500.0 / 1113.0, 125.0 / 192.0, -2187.0 / 6784.0, 11.0 / 84.0, 0.0};
+static const double DP_BH[7] = {5179.0 / 57600.0, 0.0, 7571.0 / 16695.0, 393.0 / 640.0, -92097.0 / 339200.0,
+                                187.0 / 2100.0, 1.0 / 40.0};
+
+void ora_dp54_tableau(double* c, double* a, double* b, double* bh) {
+  for (int i = 0; i < 7; ++i) {
+    c[i] = DP_C[i];
+    b[i] = DP_B[i];
+    bh[i] = DP_BH[i];
+    for (int j = 0; j < 7; ++j) a[i * 7 + j] = DP_A[i][j];
+  }
+}
+
+// one Dormand-Prince 5(4) step of size dt from u (not modified): u5 = 5th-order solution, *err =
+// sqrt(mean_i (e_i / (atol + rtol max(|u_i|, |u5_i|)))^2) with e_i = dt sum_j (b_j - bh_j) k_j
+// (Hairer-Norsett-Wanner I, eq. II.4.11), k_7 = f(u5) (first same as last)
+int ora_dp54(const ora_mesh* m, const double* u, double dt, double rtol, double atol, int flux_mode,
+             int nthreads, double* u5, double* err) {
+  size_t N = (size_t)m->ne * m->Nc * m->ref.Np;
+  vector<vector<double>> k(7, vector<double>(N));
+  vector<double> us(N);
+  int rc;
+  for (int st = 0; st < 7; ++st) {
+    for (size_t i = 0; i < N; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < st; ++j) s += DP_A[st][j] * k[j][i];
+      us[i] = u[i] + dt * s;
+    }
+    if ((rc = ora_rhs(m, us.data(), k[st].data(), flux_mode, 1, 0, nullptr, nthreads, nullptr))) return rc;
+  }
+  // the last stage input is the 5th-order solution (a_7j = b_j)
+  double sq = 0.0;
+  for (size_t i = 0; i < N; ++i) {
+    u5[i] = us[i];
+    double e = 0.0;
+    for (int j = 0; j < 7; ++j) e += (DP_B[j] - DP_BH[j]) * k[j][i];
+    e *= dt;
+    double sc = atol + rtol * std::max(std::fabs(u[i]), std::fabs(u5[i]));
+    sq += (e / sc) * (e / sc);
+  }
+  *err = std::sqrt(sq / (double)N);
+  return 0;
+}
+
 int ora_rk4(const ora_mesh* m, double* u, double dt, int nsteps, int flux_mode, int nthreads) {
   // classical four-stage Runge-Kutta (R17)
   size_t N = (size_t)m->ne * m->Nc * m->ref.Np;

@@ -107,6 +107,11 @@ int ora_rhs(const ora_mesh* m, const double* u_modal, double* dudt, int flux_mod
             int64_t n_out, const int64_t* out_elems, int nthreads, ora_stats* stats);
 /* nsteps classical RK4 steps of size dt on all elements (R17), in place. */
 int ora_rk4(const ora_mesh* m, double* u_modal, double dt, int nsteps, int flux_mode, int nthreads);
+/* Dormand-Prince 5(4) (Hairer-Norsett-Wanner I, II.5): tableau (c[7], a[7][7], b[7], bh[7]) and one step
+ * of size dt from u_modal (unchanged) -> u5 (5th order) and the scaled RMS error estimate *err */
+void ora_dp54_tableau(double* c, double* a, double* b, double* bh);
+int ora_dp54(const ora_mesh* m, const double* u_modal, double dt, double rtol, double atol, int flux_mode,
+             int nthreads, double* u5, double* err);
 
 #ifdef __cplusplus
 }

@@ -115,6 +115,54 @@ def test_rk4_free_stream_and_order():
     assert 3.6 < order < 4.6, order
 
 
+def _rk_generic(f, y, h, n, A, b):
+    """n explicit Runge-Kutta steps with tableau (A, b) -- the textbook definition"""
+    s = len(b)
+    for _ in range(n):
+        k = []
+        for i in range(s):
+            k.append(f(y + h * sum(A[i, j] * k[j] for j in range(i))))
+        y = y + h * sum(b[i] * k[i] for i in range(s))
+    return y
+
+
+def test_dp54_tableau_order():
+    # Dormand-Prince 5(4) (Hairer-Norsett-Wanner I, II.5): consistency and FSAL exactly; the observed
+    # convergence order on a nonlinear ODE is 5 for b and 4 for the embedded bh (a wrong coefficient
+    # drops the order)
+    c, A, b, bh = O.dp54_tableau()
+    np.testing.assert_allclose(A.sum(1), c, atol=1e-15)
+    assert abs(b.sum() - 1) < 1e-15 and abs(bh.sum() - 1) < 1e-15
+    np.testing.assert_array_equal(A[6, :6], b[:6])
+    for k in range(1, 6):  # quadrature conditions sum b c^(k-1) = 1/k
+        assert abs(b @ c ** (k - 1) - 1.0 / k) < 1e-15
+    # Lotka-Volterra; reference by scipy's DOP853 at tight tolerance
+    f = lambda y: np.array([y[0] * (1 - y[1]), y[1] * (y[0] - 1)])  # noqa: E731
+    from scipy.integrate import solve_ivp
+    T, y0 = 2.0, np.array([1.5, 0.5])
+    ref = solve_ivp(lambda t, y: f(y), (0, T), y0, method="DOP853", rtol=3e-14, atol=1e-15).y[:, -1]
+    for bb, lo, hi in ((b, 4.6, 6.0), (bh, 3.6, 4.5)):
+        e = [np.abs(_rk_generic(f, y0, T / n, n, A, bb) - ref).max() for n in (20, 40)]
+        assert lo < math.log2(e[0] / e[1]) < hi, (lo, e)
+
+
+def test_dp54_step_free_stream_and_error_scaling():
+    mesh, om, L = _mesh(2, 3, 2, warp="paper")
+    u = om.project(I.free_stream(om.node_coords(), 2))
+    u5, err = om.dp54(u, 1e-2)
+    assert np.abs(u5 - u).max() < 1e-13 and err < 1e-6
+    u = I.perturb_modal(om.project(I.density_wave(om.node_coords(), L)), 2, 2, seed=2, amp=1e-2)
+    # one DP5 step is much closer to a fine RK4 solution than one RK4 step; the embedded estimate
+    # scales like dt^5
+    dt = 0.005
+    ref = om.rk4(u, dt / 32, 32)
+    u5, _ = om.dp54(u, dt)
+    assert np.abs(u5 - ref).max() < 0.2 * np.abs(om.rk4(u, dt, 1) - ref).max()
+    e1 = om.dp54(u, dt, rtol=0.0, atol=1.0)[1]
+    e2 = om.dp54(u, dt / 2, rtol=0.0, atol=1.0)[1]
+    assert 4.3 < math.log2(e1 / e2) < 5.7, (e1, e2)
+
+
 def _l2_density_error(om, u, L, t, d):
     V = O.ref_get(d, om.p, "V")
     W = O.ref_get(d, om.p, "W")
