@@ -116,6 +116,14 @@ es_status es_set_state(es_context* ctx, const double* u_modal);
 es_status es_get_state(es_context* ctx, double* u_modal);
 /* nsteps classical RK4 steps of size dt on the library state (R17). */
 es_status es_step(es_context* ctx, double dt, int nsteps);
+/* One Dormand-Prince 5(4) step of size dt on the library state (Hairer-Norsett-Wanner I, II.5; the
+ * paper integrates with DP8 of the same family).  *err = sqrt(mean_i (e_i / (atol + rtol
+ * max(|y0_i|, |y5_i|)))^2) over all modal coefficients of all ranks, e = y5 - y4 the embedded
+ * estimate.  *accepted = (*err <= 1): the state advances to the 5th-order solution y5; otherwise it is
+ * unchanged (the caller retries with a smaller dt).  First-same-as-last: f(y5) is reused by the next
+ * call unless es_set_state / es_step intervene.  Allocates 8 state-sized buffers on first use.
+ * Synchronous (reads err); ES_ERR_ARG for dt <= 0, negative tolerances or NULL outputs. */
+es_status es_step_dp54(es_context* ctx, double dt, double rtol, double atol, double* err, int* accepted);
 
 /* Entropy production sum_k sum_e w^T r = d/dt sum_k 1^T W J~ s, global over ranks,
  * its absolute scale sum |w_i r_i| (computed modally as sum |w~_i (V^T r)_i|), and the global

@@ -62,6 +62,8 @@ es_rhs_host = _sig("es_rhs_host", _i, _vp, _vp, _vp)
 es_set_state = _sig("es_set_state", _i, _vp, _vp)
 es_get_state = _sig("es_get_state", _i, _vp, _vp)
 es_step = _sig("es_step", _i, _vp, ctypes.c_double, _i)
+es_step_dp54 = _sig("es_step_dp54", _i, _vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, _dp,
+                    ctypes.POINTER(_i))
 es_entropy_production = _sig("es_entropy_production", _i, _vp, _vp, _dp, _dp, _dp)
 es_flux_counts = _sig("es_flux_counts", _i, _vp, _lp, _lp, _lp, _dp)
 es_node_coords = _sig("es_node_coords", _i, _vp, _vp)
@@ -125,6 +127,30 @@ def declared_symbols():
     """Every function name declared in include/es.h."""
     txt = open(HEADER).read()
     return sorted(set(re.findall(r"\b(es_[a-z_]+)\s*\(", txt)) - {"es_map_fn"})
+
+
+def dp54_controller(step, T, dt0, rtol, atol, max_steps=1000000, safety=0.9, facmin=0.2, facmax=5.0):
+    """Step-size control of Hairer-Norsett-Wanner I, eq. II.4.13 for an embedded pair of orders 5(4):
+    dt_new = dt min(facmax, max(facmin, safety err^(-1/5))), facmax = 1 right after a rejection;
+    the last step lands on T exactly.  `step(dt, rtol, atol) -> (err, accepted)` advances the state
+    when accepted.  Returns (accepted, rejected, dt)."""
+    t, dt, nacc, nrej, after_reject = 0.0, float(dt0), 0, 0, False
+    while t < T * (1.0 - 1e-14):
+        if nacc + nrej >= max_steps:
+            raise ESError(-1, f"dp54: more than {max_steps} steps before T")
+        h = min(dt, T - t)
+        err, ok = step(h, rtol, atol)
+        fac = safety * err ** -0.2 if err > 0.0 else facmax
+        fac = min(1.0 if after_reject else facmax, max(facmin, fac))
+        if ok:
+            t += h
+            nacc += 1
+            after_reject = False
+        else:
+            nrej += 1
+            after_reject = True
+        dt = h * fac
+    return nacc, nrej, dt
 
 
 class ESError(RuntimeError):
@@ -227,6 +253,17 @@ class Context:
 
     def step(self, dt, nsteps=1):
         self._check(es_step(self.h, float(dt), int(nsteps)))
+
+    def step_dp54(self, dt, rtol=1e-6, atol=1e-8):
+        """one Dormand-Prince 5(4) step (es_step_dp54): (scaled error, accepted)"""
+        err, acc = ctypes.c_double(), _i()
+        self._check(es_step_dp54(self.h, float(dt), float(rtol), float(atol), ctypes.byref(err), ctypes.byref(acc)))
+        return err.value, bool(acc.value)
+
+    def integrate_dp54(self, T, dt0, rtol=1e-6, atol=1e-8, max_steps=1000000):
+        """adaptive Dormand-Prince 5(4) integration of the library state over [0, T] (host step-size
+        control, see dp54_controller); returns (accepted steps, rejected steps, last dt)"""
+        return dp54_controller(self.step_dp54, T, dt0, rtol, atol, max_steps)
 
     def entropy_production(self, u):
         r, a = ctypes.c_double(), ctypes.c_double()

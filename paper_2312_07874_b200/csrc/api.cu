@@ -59,6 +59,9 @@ struct es_context {
   int* face_reflect = nullptr;
   int* bad = nullptr;
   double *U = nullptr, *ACC = nullptr, *US = nullptr, *hin = nullptr, *hout = nullptr, *send_buf = nullptr;
+  double* dpk[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // DP5(4) stage slopes
+  double *dpy = nullptr, *dppart = nullptr;  // DP5(4) 5th-order solution, error partials
+  bool dp_fsal = false;                      // dpk[0] holds f(U) (first same as last)
   ncclComm_t comm = nullptr;
   int64_t launches = 0;
   bool timing = false;
@@ -304,7 +307,10 @@ void es_destroy(es_context* c) {
                   (void*)c->prim, (void*)c->trace, (void*)c->wt, (void*)c->part, (void*)c->red,
                   (void*)c->face_slot, (void*)c->d_interior, (void*)c->d_boundary, (void*)c->d_send,
                   (void*)c->face_reflect, (void*)c->bad, (void*)c->U, (void*)c->ACC, (void*)c->US,
-                  (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg, (void*)c->fstar})
+                  (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg, (void*)c->fstar,
+                  (void*)c->dpy, (void*)c->dppart})
+    if (p) cudaFree(p);
+  for (double* p : c->dpk)
     if (p) cudaFree(p);
   for (auto& t : c->tev) {
     cudaEventDestroy(t.a);
@@ -529,6 +535,7 @@ es_status es_rhs_host(es_context* c, const double* uh, double* duh) {
 }
 
 es_status es_set_state(es_context* c, const double* u) {
+  c->dp_fsal = false;
   POISON_CHECK();
   CK(cudaSetDevice(c->device));
   CK(cudaMemcpyAsync(c->U, u, (size_t)c->nloc * c->NC * c->Np * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -543,6 +550,7 @@ es_status es_get_state(es_context* c, double* u) {
 
 es_status es_step(es_context* c, double dt, int nsteps) {
   POISON_CHECK();
+  c->dp_fsal = false;
   CK(cudaSetDevice(c->device));
   for (int st = 0; st < nsteps; ++st) {
     for (int s = 0; s < 4; ++s) {  // classical RK4 (R17), stage update fused in the RHS epilogue
@@ -556,6 +564,88 @@ es_status es_step(es_context* c, double dt, int nsteps) {
       es_status r = rhs_pass(c, s == 0 ? c->U : c->US, A, nullptr);
       if (r != ES_OK) return r;
     }
+  }
+  if (c->check_adm) return check_bad(c);
+  return ES_OK;
+}
+
+// Dormand-Prince 5(4) (Hairer-Norsett-Wanner I, Table II.5.2; the paper uses DP8 of the same family,
+// P:889).  Stage inputs and the solution are streamed combinations of the slopes (rk_comb_kernel);
+// the slopes are full RHS evaluations (mode 0).  FSAL: the last slope f(y5) is the next step's first.
+namespace {
+const double DPA[7][6] = {{0, 0, 0, 0, 0, 0},
+                          {1.0 / 5.0, 0, 0, 0, 0, 0},
+                          {3.0 / 40.0, 9.0 / 40.0, 0, 0, 0, 0},
+                          {44.0 / 45.0, -56.0 / 15.0, 32.0 / 9.0, 0, 0, 0},
+                          {19372.0 / 6561.0, -25360.0 / 2187.0, 64448.0 / 6561.0, -212.0 / 729.0, 0, 0},
+                          {9017.0 / 3168.0, -355.0 / 33.0, 46732.0 / 5247.0, 49.0 / 176.0, -5103.0 / 18656.0, 0},
+                          {35.0 / 384.0, 0.0, 500.0 / 1113.0, 125.0 / 192.0, -2187.0 / 6784.0, 11.0 / 84.0}};
+// b - bh (5th-order weights minus the embedded 4th-order ones)
+const double DPE[7] = {35.0 / 384.0 - 5179.0 / 57600.0,     0.0, 500.0 / 1113.0 - 7571.0 / 16695.0,
+                       125.0 / 192.0 - 393.0 / 640.0,        -2187.0 / 6784.0 + 92097.0 / 339200.0,
+                       11.0 / 84.0 - 187.0 / 2100.0,         -1.0 / 40.0};
+}  // namespace
+
+es_status es_step_dp54(es_context* c, double dt, double rtol, double atol, double* err, int* accepted) {
+  POISON_CHECK();
+  if (!err || !accepted || !(dt > 0.0) || !(rtol >= 0.0) || !(atol >= 0.0) || !(rtol > 0.0 || atol > 0.0))
+    return fail(c, ES_ERR_ARG, "es_step_dp54: dt > 0, rtol, atol >= 0 (not both 0), err and accepted required");
+  CK(cudaSetDevice(c->device));
+  const int64_t n = c->nloc * (int64_t)c->NC * c->Np;
+  if (!c->dpy) {
+    for (auto& p : c->dpk) CK(cudaMalloc((void**)&p, (size_t)n * sizeof(double)));
+    CK(cudaMalloc((void**)&c->dpy, (size_t)n * sizeof(double)));
+    CK(cudaMalloc((void**)&c->dppart, RK_ERR_BLOCKS * sizeof(double)));
+    c->dp_fsal = false;
+  }
+  auto slope = [&](const double* y, double* k) -> es_status {
+    RhsArgs A = base_rhs_args(c);
+    A.mode = 0;
+    A.out = k;
+    return rhs_pass(c, y, A, nullptr);
+  };
+  es_status r;
+  if (!c->dp_fsal && (r = slope(c->U, c->dpk[0])) != ES_OK) return r;
+  for (int st = 1; st < 7; ++st) {
+    RkComb kc{};
+    kc.nk = st;
+    for (int j = 0; j < st; ++j) {
+      kc.k[j] = c->dpk[j];
+      kc.c[j] = dt * DPA[st][j];
+    }
+    double* ys = st == 6 ? c->dpy : c->US;  // the last stage input is the 5th-order solution
+    CK(launch_rk_comb(c->U, kc, ys, n, c->stream));
+    c->launches++;
+    if ((r = slope(ys, c->dpk[st])) != ES_OK) return r;
+  }
+  RkComb ec{};
+  ec.nk = 7;
+  for (int j = 0; j < 7; ++j) {
+    ec.k[j] = c->dpk[j];
+    ec.c[j] = dt * DPE[j];
+  }
+  CK(launch_rk_err(c->U, c->dpy, ec, rtol, atol, n, c->dppart, c->stream));
+  CK(launch_reduce_parts(c->dppart, RK_ERR_BLOCKS, 1, c->red, c->stream));
+  c->launches += 2;
+  double hsum[2] = {0.0, (double)n};
+  CK(cudaMemcpyAsync(hsum, c->red, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->world > 1) {
+    if (!c->comm) return fail(c, ES_ERR_CONFIG, "es_step_dp54 with world > 1 needs the NCCL communicator");
+    double* d2 = c->red;
+    CK(cudaMemcpyAsync(d2, hsum, 2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    NK(ncclAllReduce(d2, d2, 2, ncclDouble, ncclSum, c->comm, c->stream));
+    CK(cudaMemcpyAsync(hsum, d2, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  *err = sqrt(hsum[0] / hsum[1]);
+  *accepted = *err <= 1.0;
+  if (*accepted) {  // y5 becomes the state, f(y5) the next first slope
+    std::swap(c->U, c->dpy);
+    std::swap(c->dpk[0], c->dpk[6]);
+    c->dp_fsal = true;
+  } else {
+    c->dp_fsal = true;  // dpk[0] = f(U) still holds
   }
   if (c->check_adm) return check_bad(c);
   return ES_OK;

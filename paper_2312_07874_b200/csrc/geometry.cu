@@ -212,6 +212,47 @@ __global__ void reduce_parts_kernel(const double* part, int64_t ne, int w, doubl
   }
 }
 
+// Runge-Kutta stage input / solution: out = y0 + sum_j c_j k_j (k and c by value)
+__global__ void rk_comb_kernel(const double* __restrict__ y0, RkComb kc, double* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < kc.nk; ++j) s = fma(kc.c[j], kc.k[j][i], s);
+    out[i] = y0[i] + s;
+  }
+}
+// scaled squared error partials (Hairer-Norsett-Wanner I, eq. II.4.11), block-fixed order
+__global__ void __launch_bounds__(256) rk_err_kernel(const double* __restrict__ y0, const double* __restrict__ y1,
+                                                     RkComb ec, double rtol, double atol, int64_t n, double* part) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double e = 0.0;
+    for (int j = 0; j < ec.nk; ++j) e = fma(ec.c[j], ec.k[j][i], e);
+    const double sc = atol + rtol * fmax(fabs(y0[i]), fabs(y1[i]));
+    const double r = e / sc;
+    s = fma(r, r, s);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+cudaError_t launch_rk_comb(const double* y0, const RkComb& kc, double* out, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int64_t b = (n + 255) / 256;
+  rk_comb_kernel<<<(unsigned)(b < 148 * 16 ? b : 148 * 16), 256, 0, st>>>(y0, kc, out, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_rk_err(const double* y0, const double* y1, const RkComb& ec, double rtol, double atol,
+                          int64_t n, double* part, cudaStream_t st) {
+  rk_err_kernel<<<RK_ERR_BLOCKS, 256, 0, st>>>(y0, y1, ec, rtol, atol, n, part);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_geometry(const GeoArgs& g, int64_t ne, cudaStream_t st) {
   if (ne <= 0) return cudaSuccess;
   size_t sm = ((size_t)g.Npg * g.dim + 2 * (size_t)g.Npg + (size_t)g.Ncl * 18) * sizeof(double);

@@ -38,4 +38,18 @@ cudaError_t launch_pack(const double* trace, const int64_t* slots, int64_t nsend
                         cudaStream_t st);
 cudaError_t launch_reduce_parts(const double* part, int64_t ne, int w, double* out, cudaStream_t st);
 
+// explicit Runge-Kutta combinations over the modal state (HBM-bound streams)
+struct RkComb {
+  const double* k[7];
+  double c[7];  // coefficients of k_j (already multiplied by dt)
+  int nk;
+};
+// out = y0 + sum_j c_j k_j
+cudaError_t launch_rk_comb(const double* y0, const RkComb& kc, double* out, int64_t n, cudaStream_t st);
+// per-block partial sums of (e_i / (atol + rtol max(|y0_i|, |y1_i|)))^2, e = sum_j c_j k_j, over a
+// fixed grid of RK_ERR_BLOCKS blocks (deterministic order) -> part[RK_ERR_BLOCKS]
+constexpr int RK_ERR_BLOCKS = 1184;
+cudaError_t launch_rk_err(const double* y0, const double* y1, const RkComb& ec, double rtol, double atol,
+                          int64_t n, double* part, cudaStream_t st);
+
 }  // namespace esb

@@ -188,6 +188,52 @@ def test_rk4_steps_parity(es, d, p):
     assert (inc < 1e-10).all(), inc
 
 
+@pytest.mark.parametrize("d,p", [(2, 3), (3, 2)])
+def test_dp54_step_parity(es, d, p):
+    # es_step_dp54 against the oracle's Dormand-Prince 5(4) step: the 5th-order solution, the scaled
+    # error estimate, rejection leaving the state unchanged, and first-same-as-last over two steps
+    mesh, om, ctx, u = _setup(es, d, 3, p, "paper", "wave" if d == 2 else "tgv3", 1)
+    dt, rtol, atol = 2e-3, 1e-9, 1e-11
+    u1, e1 = om.dp54(u, dt, rtol, atol, flux_mode=1)
+    u2, e2 = om.dp54(u1, dt, rtol, atol, flux_mode=1)
+    ut = torch.from_numpy(u).cuda()
+    ctx.set_state(ut)
+    out = torch.empty_like(ut)
+    # a tolerance far below reach: rejected, state unchanged
+    err, ok = ctx.step_dp54(dt, 0.0, 1e-300)
+    assert not ok and err > 1.0
+    ctx.get_state(out)
+    ctx.synchronize()
+    assert np.array_equal(out.cpu().numpy(), u)
+    for ref, eref in ((u1, e1), (u2, e2)):
+        err, ok = ctx.step_dp54(dt, rtol, atol)
+        assert ok == (eref <= 1.0) and abs(err - eref) < 1e-9 * eref, (err, eref)
+        ctx.get_state(out)
+        ctx.synchronize()
+        got = out.cpu().numpy()
+        assert np.abs(got - ref).max() < 1e-13 * np.abs(ref).max()
+        inc = _relerr(got - u, ref - u)
+        assert (inc < 1e-10).all(), inc
+
+
+def test_dp54_adaptive_density_wave(es):
+    # adaptive DP5(4) over the density wave: reaches T; the solution matches a fine RK4 run
+    mesh, om, ctx, u = _setup(es, 2, 4, 3, "paper", "wave", 1)
+    T = 0.05
+    ut = torch.from_numpy(u).cuda()
+    ctx.set_state(ut)
+    nacc, nrej, _ = ctx.integrate_dp54(T, 1e-4, rtol=1e-10, atol=1e-12)
+    out = torch.empty_like(ut)
+    ctx.get_state(out)
+    ctx.set_state(ut)
+    ctx.step(T / 400, 400)
+    ref = torch.empty_like(ut)
+    ctx.get_state(ref)
+    ctx.synchronize()
+    assert nacc >= 3
+    assert (out - ref).abs().max().item() < 1e-8 * ref.abs().max().item()
+
+
 def test_host_entry_point_matches_device(es):
     mesh, om, ctx, u = _setup(es, 2, 4, 4, "bj", "wave", 1)
     got = _gpu_rhs(ctx, u)
