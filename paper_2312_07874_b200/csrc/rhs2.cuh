@@ -875,8 +875,18 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   for (int64_t idx = blockIdx.x, it = 0; idx < A.n_elem; idx += gridDim.x, ++it) k2_element<DIM, N, EQ>(A, idx, (unsigned)it);
 }
 
+// resident CTAs per SM the register budget is sized for: about 16 warps per SM where shared memory
+// allows (small-degree elements have few line slots per CTA), one CTA otherwise
 template <int DIM, int N>
-__global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
+__host__ __device__ constexpr int k2_min_blocks() {
+  constexpr int smem_fit = (227 * 1024) / (int)(rhs2_smem_doubles<DIM, N>() * 8 + 1024);
+  constexpr int want = 16 / Lw<DIM, N>::NW;
+  constexpr int b = want < smem_fit ? want : smem_fit;
+  return b < 1 ? 1 : b;
+}
+
+template <int DIM, int N>
+__global__ void __launch_bounds__(Lw<DIM, N>::NT, k2_min_blocks<DIM, N>()) rhs2_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
   rhs2_body<DIM, N, false>(R, A);
 }
 // ablation: the paper's Eq. num_fluxes per-operator fluxes (es_options.volume_mode = 1)
