@@ -548,8 +548,18 @@ __host__ __device__ constexpr size_t project_smem_doubles() {
   return ProjSmem<DIM, N>::total;
 }
 
+// resident CTAs per SM the register budget is sized for: about 20 warps per SM where shared memory
+// allows (small elements have small CTAs), at least 2
 template <int DIM, int N>
-__global__ void __launch_bounds__(Sz<DIM, N>::NT, 2) project_kernel(DevRef R, ProjArgs A) {
+__host__ __device__ constexpr int k1_min_blocks() {
+  constexpr int smem_fit = (227 * 1024) / (int)(project_smem_doubles<DIM, N>() * 8 + 1024);
+  constexpr int want = 20 / (Sz<DIM, N>::NT / 32);
+  constexpr int b = want < smem_fit ? want : smem_fit;
+  return b < 2 ? 2 : b;
+}
+
+template <int DIM, int N>
+__global__ void __launch_bounds__(Sz<DIM, N>::NT, k1_min_blocks<DIM, N>()) project_kernel(DevRef R, ProjArgs A) {
   using S = Sz<DIM, N>;
   using L = ProjSmem<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf;
