@@ -875,12 +875,12 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   for (int64_t idx = blockIdx.x, it = 0; idx < A.n_elem; idx += gridDim.x, ++it) k2_element<DIM, N, EQ>(A, idx, (unsigned)it);
 }
 
-// resident CTAs per SM the register budget is sized for: about 16 warps per SM where shared memory
+// resident CTAs per SM the register budget is sized for: about 18 warps per SM where shared memory
 // allows (small-degree elements have few line slots per CTA), one CTA otherwise
 template <int DIM, int N>
 __host__ __device__ constexpr int k2_min_blocks() {
   constexpr int smem_fit = (227 * 1024) / (int)(rhs2_smem_doubles<DIM, N>() * 8 + 1024);
-  constexpr int want = 16 / Lw<DIM, N>::NW;
+  constexpr int want = 18 / Lw<DIM, N>::NW;
   constexpr int b = want < smem_fit ? want : smem_fit;
   return b < 1 ? 1 : b;
 }
