@@ -78,7 +78,11 @@ typedef struct {
   int volume_mode;                      /* 0: line-wise flux differencing (the default);
                                            1: ablation -- one flux per operator S^(l) with a
                                            nonzero on the line, the paper's Eq. num_fluxes
-                                           iteration; same result up to rounding */
+                                           iteration; same result up to rounding;
+                                           2: ablation -- brute force over every node pair with
+                                           the dense operators, zeros included (SURVEY 8(f) rank
+                                           2; O(N_q^2) per element, small configurations only);
+                                           other values: ES_ERR_CONFIG */
 } es_options;
 
 /* Builds tables, geometry (exact metrics in 2D, conservative curl metrics in 3D, P:345-364;

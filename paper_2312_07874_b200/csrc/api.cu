@@ -54,7 +54,9 @@ struct es_context {
   double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr, *fstar = nullptr;
   int num_sms = 148, proj_ctas = 296;
   bool external = false;
-  int eq56 = 0;  // volume_mode 1  // world > 1 without NCCL: the caller moves the halo (es_rhs_stage1/2)
+  int eq56 = 0;   // volume_mode 1: per-operator fluxes (Eq. num_fluxes ablation)
+  int dense = 0;  // volume_mode 2: brute force over all node pairs (dense operators)
+  double *sdense = nullptr, *rbdense = nullptr;
   int64_t *face_slot = nullptr, *d_interior = nullptr, *d_boundary = nullptr, *d_send = nullptr;
   int* face_reflect = nullptr;
   int* bad = nullptr;
@@ -220,6 +222,9 @@ RhsArgs base_rhs_args(es_context* c) {
   A.fstar = c->fstar;
   A.max_ctas = c->num_sms;
   A.eq56 = c->eq56;
+  A.sdense = c->sdense;
+  A.rbdense = c->rbdense;
+  A.nhat = c->R.nhat;
   return A;
 }
 
@@ -308,7 +313,7 @@ void es_destroy(es_context* c) {
                   (void*)c->face_slot, (void*)c->d_interior, (void*)c->d_boundary, (void*)c->d_send,
                   (void*)c->face_reflect, (void*)c->bad, (void*)c->U, (void*)c->ACC, (void*)c->US,
                   (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg, (void*)c->fstar,
-                  (void*)c->dpy, (void*)c->dppart})
+                  (void*)c->dpy, (void*)c->dppart, (void*)c->sdense, (void*)c->rbdense})
     if (p) cudaFree(p);
   for (double* p : c->dpk)
     if (p) cudaFree(p);
@@ -337,6 +342,8 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   c->es = opt->interface_flux;
   c->check_adm = opt->check_admissibility;
   c->eq56 = opt->volume_mode == 1;
+  c->dense = opt->volume_mode == 2;
+  if (opt->volume_mode < 0 || opt->volume_mode > 2) return fail(c, ES_ERR_CONFIG, "volume_mode must be 0, 1 or 2");
   c->rank = opt->rank;
   c->world = opt->world < 1 ? 1 : opt->world;
   c->device = opt->device;
@@ -375,6 +382,14 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   CK(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
   es_status s = upload_tables(c);
   if (s != ES_OK) return s;
+  if (c->dense) {  // volume_mode 2: dense operators for the brute-force ablation
+    std::vector<double> S, RB;
+    build_dense_tables(c->T, S, RB);
+    CK(cudaMalloc((void**)&c->sdense, S.size() * sizeof(double)));
+    CK(cudaMalloc((void**)&c->rbdense, RB.size() * sizeof(double)));
+    CK(cudaMemcpy(c->sdense, S.data(), S.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->rbdense, RB.data(), RB.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   // ---- mapping nodes: affine images of the degree-p lattice, then the user map ----
   const int d = c->d, nv = d + 1, Npg = c->T.Npg;
   std::vector<double> xin((size_t)c->nloc * Npg * d), xmap(xin.size());
@@ -685,13 +700,15 @@ es_status es_flux_counts(const es_context* c, int64_t* vol, int64_t* fac, int64_
   if (c->d == 2) {
     // line-wise: one flux per pair on each eta line, n(n-1)/2 pairs per line, n lines per direction;
     // Eq. num_fluxes mode: one per operator with a nonzero on the line (2 on eta1, 1 on eta2 lines)
-    if (vol) *vol = c->eq56 ? 3 * q * n * n / 2 : q * n * n;
-    if (fac) *fac = 3 * n * n;                 // n volume nodes per facet node, 3 facets
+    if (vol) *vol = c->dense ? n * n * (n * n - 1) : c->eq56 ? 3 * q * n * n / 2 : q * n * n;
+    if (fac) *fac = c->dense ? 2 * (n * n) * (3 * n)  // every (node, facet node) pair, from both sides
+                             : 3 * n * n;             // n volume nodes per facet node, 3 facets
     if (eq56) *eq56 = 3 * n * n * (q + 2) / 2; // sum_l nnz(S^(l))/2 + sum nnz(R^T B)
     if (iface) *iface = 3.0 * n;               // per element side
   } else {
-    if (vol) *vol = c->eq56 ? 3 * q * n * n * n : 3 * q * n * n * n / 2;  // (3 + 2 + 1) vs 3 line directions
-    if (fac) *fac = 3 * n * n * n + n * n * n * n;
+    if (vol) *vol = c->dense ? n * n * n * (n * n * n - 1)  // brute force: every ordered pair
+                             : c->eq56 ? 3 * q * n * n * n : 3 * q * n * n * n / 2;  // (3 + 2 + 1) vs 3 line directions
+    if (fac) *fac = c->dense ? 2 * (n * n * n) * (4 * n * n) : 3 * n * n * n + n * n * n * n;
     if (eq56) *eq56 = 4 * n * n * n * n;
     if (iface) *iface = 4.0 * n * n;
   }

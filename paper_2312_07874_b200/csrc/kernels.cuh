@@ -83,6 +83,9 @@ struct RhsArgs {
   const double* fstar;        // [nloc][Nf][NC][Nqf] B J_f f* from the interface kernel
   int max_ctas;               // number of SMs (the launcher multiplies by resident CTAs per SM)
   int eq56;                   // 1: per-operator fluxes (Eq. num_fluxes ablation), 0: line-wise
+  const double* sdense;       // volume_mode 2: dense S^(l) [l][j][i]
+  const double* rbdense;      // volume_mode 2: dense (R^(z)T B) [z][f][i]
+  const double* nhat;         // [Nf][3] reference outward normals
 };
 
 struct IfaceArgs {

@@ -256,7 +256,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 __shared__ uint64_t k2_barA, k2_barB;
 
 // one element of the flux kernel (the body of the persistent loop)
-template <int DIM, int N, bool EQ>
+template <int DIM, int N, bool EQ, bool DN = false>
 __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsigned it) {
   using S = Sz<DIM, N>;
   using W = Lw<DIM, N>;
@@ -667,11 +667,112 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
       pass(I1{}, tc, ec, I1{}, Yes{}, 0);
     }
   };
-  // the ablation (EQ) is its own kernel instantiation: the production path keeps its registers
-  if (all_taylor)  // uniform over the CTA
-    passes(std::true_type{}, std::integral_constant<bool, EQ>{});
-  else
-    passes(std::false_type{}, std::integral_constant<bool, EQ>{});
+  // brute-force ablation (volume_mode 2): every ordered pair (i, j) of volume
+  // nodes with the dense S^(l) (zeros included) and every (node, facet node) pair with the dense
+  // R^T B; node i owns r_i = -sum_j f#(u_i, u_j, n_ij) - sum_(z,f) f#(u_i, u_f, n_if) (each pair is
+  // evaluated from both sides, S skew), facet node f owns s_f -= sum_i f#(u_i, u_f, n_if)
+  auto dense_passes = [&]() {
+    // all lanes run every iteration (flux_batch takes a warp vote): idle lanes and the i = j pair
+    // evaluate with a zero normal, which makes F exactly zero
+    const double* Sd = A.sdense;
+    const double* RBd = A.rbdense;
+    for (int i0 = 0; i0 < Nq; i0 += NT) {
+      const int ii = i0 + tid;
+      const bool ok = ii < Nq;
+      const int i = ok ? ii : 0;
+      const NodeState me = state_at(i);
+      double gl[3][3], acc[NC];
+#pragma unroll
+      for (int l = 0; l < DIM; ++l)
+#pragma unroll
+        for (int m = 0; m < DIM; ++m) gl[l][m] = Gat(l, m, i);
+#pragma unroll
+      for (int v = 0; v < NC; ++v) acc[v] = 0.0;
+      for (int j = 0; j < Nq; ++j) {
+        const bool use = ok && j != i;
+        Job<DIM> jb[1];
+        jb[0].base = sP;
+        jb[0].bb = sP + (DIM + 2) * Nq;
+        jb[0].stride = Nq;
+        jb[0].idx = j;
+#pragma unroll
+        for (int m = 0; m < DIM; ++m) {
+          double nm = 0.0;
+#pragma unroll
+          for (int l = 0; l < DIM; ++l) nm += __ldg(&Sd[((size_t)l * Nq + j) * Nq + i]) * (gl[l][m] + Gat(l, m, j));
+          jb[0].n[m] = use ? nm : 0.0;
+        }
+        double F[1][NC];
+        flux_batch<DIM, 1, true>(me, jb, gm1inv, F);
+#pragma unroll
+        for (int v = 0; v < NC; ++v) acc[v] -= F[0][v];
+      }
+      for (int fz = 0; fz < NF; ++fz) {
+        const int z = fz / Nqf, f = fz - z * Nqf;
+        const double c2 = ok ? 0.5 * __ldg(&RBd[(size_t)fz * Nq + i]) : 0.0;
+        Job<DIM> jb[1];
+        jb[0].base = fP + z * NC * Nqf;
+        jb[0].bb = fB + z * Nqf;
+        jb[0].stride = Nqf;
+        jb[0].idx = f;
+#pragma unroll
+        for (int m = 0; m < DIM; ++m) {
+          double gtn = 0.0;
+#pragma unroll
+          for (int l = 0; l < DIM; ++l) gtn += A.nhat[z * 3 + l] * gl[l][m];
+          jb[0].n[m] = c2 * (gtn + fJ[(z * DIM + m) * Nqf + f]);
+        }
+        double F[1][NC];
+        flux_batch<DIM, 1, true>(me, jb, gm1inv, F);
+#pragma unroll
+        for (int v = 0; v < NC; ++v) acc[v] -= F[0][v];
+      }
+      if (ok)
+#pragma unroll
+        for (int v = 0; v < NC; ++v) sR[v * Nq + i] = acc[v];
+    }
+    for (int f0 = 0; f0 < NF; f0 += NT) {
+      const int fzz = f0 + tid;
+      const bool ok = fzz < NF;
+      const int fz = ok ? fzz : 0, z = fz / Nqf, f = fz - z * Nqf;
+      double sacc[NC];
+#pragma unroll
+      for (int v = 0; v < NC; ++v) sacc[v] = 0.0;
+      for (int i = 0; i < Nq; ++i) {
+        const NodeState me = state_at(i);
+        const double c2 = ok ? 0.5 * __ldg(&RBd[(size_t)fz * Nq + i]) : 0.0;
+        Job<DIM> jb[1];
+        jb[0].base = fP + z * NC * Nqf;
+        jb[0].bb = fB + z * Nqf;
+        jb[0].stride = Nqf;
+        jb[0].idx = f;
+#pragma unroll
+        for (int m = 0; m < DIM; ++m) {
+          double gtn = 0.0;
+#pragma unroll
+          for (int l = 0; l < DIM; ++l) gtn += A.nhat[z * 3 + l] * Gat(l, m, i);
+          jb[0].n[m] = c2 * (gtn + fJ[(z * DIM + m) * Nqf + f]);
+        }
+        double F[1][NC];
+        flux_batch<DIM, 1, true>(me, jb, gm1inv, F);
+#pragma unroll
+        for (int v = 0; v < NC; ++v) sacc[v] += F[0][v];
+      }
+      if (ok)
+#pragma unroll
+        for (int v = 0; v < NC; ++v) fS[(z * NC + v) * Nqf + f] -= sacc[v];
+    }
+    __syncthreads();
+  };
+  if constexpr (DN) {
+    dense_passes();
+  } else {
+    // the ablation (EQ) is its own kernel instantiation: the production path keeps its registers
+    if (all_taylor)  // uniform over the CTA
+      passes(std::true_type{}, std::integral_constant<bool, EQ>{});
+    else
+      passes(std::false_type{}, std::integral_constant<bool, EQ>{});
+  }
   // states, metrics and facet inputs are dead: the next element's copies land during the epilogue
   if (tid == 0 && has_next) issue_A(elem_of(nidx), (it + 1) & 1);
   stamp(5);
@@ -789,7 +890,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   stamp(11);
 }
 
-template <int DIM, int N, bool EQ>
+template <int DIM, int N, bool EQ, bool DN = false>
 __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   using S = Sz<DIM, N>;
   using W = Lw<DIM, N>;
@@ -872,7 +973,7 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   __syncthreads();  // mbarriers initialised and tables staged before anyone uses them
 
 #pragma unroll 1
-  for (int64_t idx = blockIdx.x, it = 0; idx < A.n_elem; idx += gridDim.x, ++it) k2_element<DIM, N, EQ>(A, idx, (unsigned)it);
+  for (int64_t idx = blockIdx.x, it = 0; idx < A.n_elem; idx += gridDim.x, ++it) k2_element<DIM, N, EQ, DN>(A, idx, (unsigned)it);
 }
 
 // resident CTAs per SM the register budget is sized for: about 18 warps per SM where shared memory
@@ -893,6 +994,11 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, k2_min_blocks<DIM, N>()) rhs2_
 template <int DIM, int N>
 __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_eq56_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
   rhs2_body<DIM, N, true>(R, A);
+}
+// ablation: brute force over all node pairs with the dense operators (es_options.volume_mode = 2)
+template <int DIM, int N>
+__global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_dense_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
+  rhs2_body<DIM, N, false, true>(R, A);
 }
 
 // entropy variables of a primitive state (App. B, R7): w = ((g - s)/(g - 1) - b|v|^2/2, b v, -b),

@@ -500,4 +500,62 @@ bool build_ref_tables(int d, int p, RefTables& t, std::string& err) {
   return true;
 }
 
+// Dense operators for the brute-force ablation (es_options.volume_mode = 2):
+// S^(l)_ij assembled from the line operators exactly as the line-wise kernel applies them (the
+// eta_k-line coefficients of DESIGN.md section 5.3), stored transposed [l][j][i]; (R^(z)T B)_if as
+// [z][f][i].  Entries off the lines are zero and are evaluated anyway by the brute-force kernel.
+void build_dense_tables(const RefTables& t, std::vector<double>& S, std::vector<double>& RB) {
+  const int d = t.d, N = t.n, Nq = t.Nq, Nqf = t.Nqf, Nf = t.Nf;
+  S.assign((size_t)d * Nq * Nq, 0.0);
+  RB.assign((size_t)Nf * Nqf * Nq, 0.0);
+  auto s_at = [&](int l, int i, int j) -> double& { return S[((size_t)l * Nq + j) * Nq + i]; };
+  auto rb_at = [&](int z, int f, int i) -> double& { return RB[((size_t)z * Nqf + f) * Nq + i]; };
+  if (d == 2) {
+    for (int b = 0; b < N; ++b)
+      for (int a = 0; a < N; ++a) {
+        const int i = a + N * b;
+        for (int a2 = 0; a2 < N; ++a2) {  // eta1 line
+          const int j = a2 + N * b, ix = a * N + a2;
+          s_at(0, i, j) += t.w[b] * t.skQ1[ix];
+          s_at(1, i, j) += t.w[b] * t.skA1[ix];
+        }
+        for (int b2 = 0; b2 < N; ++b2) {  // eta2 line
+          const int j = a + N * b2;
+          s_at(1, i, j) += t.w[a] * t.skA2[b * N + b2];
+        }
+        rb_at(0, a, i) = t.lL[b] * t.Bf[0 * Nqf + a];
+        rb_at(1, b, i) = t.lR[a] * t.Bf[1 * Nqf + b];
+        rb_at(2, b, i) = t.lL[a] * t.Bf[2 * Nqf + b];
+      }
+  } else {
+    for (int c = 0; c < N; ++c)
+      for (int b = 0; b < N; ++b)
+        for (int a = 0; a < N; ++a) {
+          const int i = a + N * b + N * N * c;
+          const double c0 = 0.5 * t.w[b] * t.w3[c], c1 = 0.5 * t.w[a] * t.w3[c],
+                       c2 = 0.125 * t.w[a] * t.w[b] * (1.0 - t.eta[b]);
+          for (int a2 = 0; a2 < N; ++a2) {  // eta1 line: S^(0), S^(1), S^(2)
+            const int j = a2 + N * b + N * N * c, ix = a * N + a2;
+            s_at(0, i, j) += c0 * t.skQ1[ix];
+            s_at(1, i, j) += c0 * t.skA1[ix];
+            s_at(2, i, j) += c0 * t.skA1[ix];
+          }
+          for (int b2 = 0; b2 < N; ++b2) {  // eta2 line: S^(1), S^(2)
+            const int j = a + N * b2 + N * N * c, ix = b * N + b2;
+            s_at(1, i, j) += c1 * t.skA2[ix];
+            s_at(2, i, j) += c1 * t.skA3[ix];
+          }
+          for (int c2i = 0; c2i < N; ++c2i) {  // eta3 line: S^(2)
+            const int j = a + N * b + N * N * c2i;
+            s_at(2, i, j) += c2 * t.skA4[c * N + c2i];
+          }
+          rb_at(0, a + N * c, i) = t.lL[b] * t.Bf[0 * Nqf + a + N * c];
+          rb_at(1, b + N * c, i) = t.lR[a] * t.Bf[1 * Nqf + b + N * c];
+          rb_at(2, b + N * c, i) = t.lL[a] * t.Bf[2 * Nqf + b + N * c];
+          for (int j4 = 0; j4 < N; ++j4)
+            rb_at(3, a + N * j4, i) = t.l3L[c] * t.lint4[j4 * N + b] * t.Bf[3 * Nqf + a + N * j4];
+        }
+  }
+}
+
 }  // namespace esb

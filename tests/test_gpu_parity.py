@@ -318,3 +318,24 @@ def test_eq56_ablation_parity(es, d, M, p, warp, ic, fm):
     c = ctx.flux_counts()
     assert (c["volume"] + c["facet"]) * om.ne == st.volume_pairs + st.facet_pairs  # Eq. 56 count
     assert c["volume"] + c["facet"] == c["eq56"]
+
+
+@pytest.mark.parametrize("d,M,p,warp,ic,fm", [(2, 3, 3, "paper", "wave", 1), (3, 3, 2, "paper", "tgv3", 1),
+                                              (3, 3, 4, "bj", "tgv", 0)])
+def test_dense_ablation_parity(es, d, M, p, warp, ic, fm):
+    # volume_mode 2: brute force over all node pairs with the dense operators (zeros included) --
+    # the same RHS as the oracle's dense variant (2), with N_q (N_q - 1) ordered volume evaluations
+    # and 2 N_q N_f N_qf facet evaluations per element
+    L = _L(d)
+    mesh = I.split_cartesian(d, M, L)
+    w = _warp(warp, d, L, M)
+    om = O.Mesh(mesh, p, warp=w)
+    u = I.perturb_modal(om.project(_ic(ic, om.node_coords(), d, L)), d, p, seed=1, amp=1e-2)
+    ref, st = om.rhs(u, flux_mode=fm, variant=2)
+    ctx = es.Context(mesh, p, warp=w, interface_flux=fm, volume_mode=2)
+    got = _gpu_rhs(ctx, u)
+    assert (_relerr(got, ref) <= TOL).all(), _relerr(got, ref)
+    n = p + 1
+    Nq, NF = n ** d, (d + 1) * n ** (d - 1)
+    c = ctx.flux_counts()
+    assert c["volume"] == Nq * (Nq - 1) and c["facet"] == 2 * Nq * NF
