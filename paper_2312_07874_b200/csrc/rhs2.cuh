@@ -1078,7 +1078,7 @@ __device__ __forceinline__ void entropy_jump(const NodeState& um, const NodeStat
 // own normals; the arithmetic per side does not depend on the partition.
 // ------------------------------------------------------------------------------------------------
 template <int DIM, int N, int ES>  // ES = IfaceArgs::es
-__global__ void __launch_bounds__(256) iface_kernel(DevRef R, IfaceArgs A) {
+__global__ void __launch_bounds__(256, 4) iface_kernel(DevRef R, IfaceArgs A) {
   using S = Sz<DIM, N>;
   constexpr int NC = S::NC, Nqf = S::Nqf, NF = S::NF, Nf = S::Nf;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
