@@ -586,24 +586,22 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
 #pragma unroll
           for (int v = 0; v < NC; ++v) facc[v] = 0.0;
           const double h3 = 0.5 * tl3[cc] * vmask;  // job-independent part of (R^T B)_if / 2
-#pragma unroll 1
-          for (int t0 = 0; t0 < N; t0 += 2) {
-            Job<DIM> jq[2];
+          // B consecutive steps t0 .. t0 + B - 1 in one flux batch
+          auto f4batch = [&](auto bc, int t0) {
+            constexpr int B = decltype(bc)::value;
+            Job<DIM> jq[B];
 #pragma unroll
-            for (int tt = 0; tt < 2; ++tt) {
-              const int t = t0 + tt;
-              int jf = pos + (t < N ? t : 0);
+            for (int tt = 0; tt < B; ++tt) {
+              int jf = pos + t0 + tt;
               if (jf >= N) jf -= N;
               const int f4 = ca + N * jf;
-              fjob_h(jq[tt], 3, f4, t < N ? (h3 * tli4[jf * N + cb]) * tB[3 * Nqf + f4] : 0.0, gt4);
+              fjob_h(jq[tt], 3, f4, (h3 * tli4[jf * N + cb]) * tB[3 * Nqf + f4], gt4);
             }
-            double Fb[2][NC];
-            flux_batch<DIM, 2, CHK>(me, jq, gm1inv, Fb);
+            double Fb[B][NC];
+            flux_batch<DIM, B, CHK>(me, jq, gm1inv, Fb);
 #pragma unroll
-            for (int tt = 0; tt < 2; ++tt) {
-              const int t = t0 + tt;
-              if (t >= N) break;
-              int p0 = pos - t;
+            for (int tt = 0; tt < B; ++tt) {
+              int p0 = pos - (t0 + tt);
               if (p0 < 0) p0 += N;
               const int src = grp * N + p0;
 #pragma unroll
@@ -612,7 +610,10 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
                 facc[v] += shfl_d(Fb[tt][v], src);
               }
             }
-          }
+          };
+#pragma unroll 1
+          for (int t0 = 0; t0 + 1 < N; t0 += 2) f4batch(std::integral_constant<int, 2>{}, t0);
+          if constexpr (N % 2 == 1) f4batch(std::integral_constant<int, 1>{}, N - 1);  // no masked job
           if (valid)  // partial over b of facet node (a, j = pos) on line c
 #pragma unroll
             for (int v = 0; v < NC; ++v) pt[((v * N + pos) * N + ca) * N + cc] = facc[v];
