@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT, k1_min_blocks<DIM, N>()) proje
       out[0] = r;
 #pragma unroll
       for (int m = 0; m < DIM; ++m) out[1 + m] = vel[m];
-      out[DIM + 1] = r * ib;
+      out[DIM + 1] = 0.5 * (r * ib);  // p / 2: the flux uses half pressures (exact scaling)
       out[DIM + 2] = b;
       return (b > 0.0 && r > 0.0) ? 0 : 1;
     };

@@ -101,6 +101,7 @@ __device__ __forceinline__ double inv_ln_mean_v2(double x, double y) {
   return log(y / x) / (y - x);
 }
 
+// entropy-projected node state: rho, v, p (p / 2 in the flux kernel's rows, see flux_batch), beta
 struct NodeState {
   double r, v[3], p, b;
 };
@@ -136,15 +137,14 @@ __device__ __forceinline__ double shfl_d(double x, int src) {
   return __hiloint2double(hi, lo);
 }
 
-// reciprocal: hardware approximation refined by two Newton steps (quadratic convergence from the
-// ~2^-23 seed; arguments are positive and normal)
+// reciprocal: hardware approximation refined by one cubic step r (1 + e + e^2), e = 1 - s r (error
+// e^3 ~ 1e-18 from the seed's 9.9e-7; within 1 ulp of the correctly rounded 1/s over 2^26 arguments,
+// tools/rcp_check.cu, profiles/r01_v47_rcp_check.json); arguments are positive and normal
 __device__ __forceinline__ double rcp_nr(double s) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
-  double e = fma(-s, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-s, r, 1.0);
-  return fma(r, e, r);
+  const double e = fma(-s, r, 1.0);
+  return fma(r, fma(e, e, e), r);
 }
 
 // one Newton step: relative error ~2^-44 from the ~2^-22 seed.  Used where the reciprocal only
@@ -219,13 +219,14 @@ __device__ __forceinline__ void flux_batch(const NodeState& me, const Job<DIM>* 
       vbn += o[t].v[m] * n[m];
       vdot += me.v[m] * o[t].v[m];
     }
-    const double pav = 0.5 * (me.p + o[t].p);
+    // the p fields hold p / 2: <p> = p_a/2 + p_b/2, (p_a v_b.n + p_b v_a.n)/2 below (exact scalings)
+    const double pav = me.p + o[t].p;
     const double fr = rl[t] * (0.5 * (van + vbn));
     const double hfr = 0.5 * fr;
     F[t][0] = fr;
 #pragma unroll
     for (int m = 0; m < DIM; ++m) F[t][1 + m] = hfr * (me.v[m] + o[t].v[m]) + pav * n[m];
-    F[t][DIM + 1] = fr * (0.5 * vdot + ib[t] * gm1inv) + 0.5 * (me.p * vbn + o[t].p * van);
+    F[t][DIM + 1] = fr * (0.5 * vdot + ib[t] * gm1inv) + (me.p * vbn + o[t].p * van);
   }
 }
 
@@ -323,10 +324,11 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   };
   stamp(0);
   mbar_wait(&k2_barA, it & 1);
-  // facet beta = rho / p (the volume beta rows and the element's all-Taylor flag come from K1)
+  // facet beta = rho / p = (rho / (p/2)) / 2 (the volume beta rows and the element's all-Taylor flag
+  // come from K1; the state rows hold p / 2)
   for (int fz = tid; fz < NF; fz += NT) {
     const double* q = fP + (fz / Nqf) * NC * Nqf + fz % Nqf;
-    fB[fz] = q[0] / q[(DIM + 1) * Nqf];
+    fB[fz] = 0.5 * (q[0] / q[(DIM + 1) * Nqf]);
   }
   mbar_wait(&k2_barB, it & 1);  // f* is updated in place by the passes
   __syncthreads();
@@ -1105,8 +1107,8 @@ __global__ void __launch_bounds__(256, 4) iface_kernel(DevRef R, IfaceArgs A) {
     um.v[m] = tm[(1 + m) * Nqf];
     up.v[m] = tp[(1 + m) * Nqf];
   }
-  um.p = tm[(DIM + 1) * Nqf];
-  up.p = tp[(DIM + 1) * Nqf];
+  um.p = 2.0 * tm[(DIM + 1) * Nqf];  // the trace rows hold p / 2
+  up.p = 2.0 * tp[(DIM + 1) * Nqf];
   um.b = um.r / um.p;
   up.b = up.r / up.p;
   double Jn[DIM], Jf = 0.0;
