@@ -72,9 +72,20 @@ def rhs_kernel_flops(dim, p, vol=None, fac=None):
     nc = dim + 2
     f = (vol or c["vol"]) * (FLUX_FLOPS[dim] + VOL_NORMAL_FLOPS[dim] + ACC_FLOPS[dim])
     f += (fac or c["fac"]) * (FLUX_FLOPS[dim] + FAC_NORMAL_FLOPS[dim] + ACC_FLOPS[dim])
-    f += 2 * 3 * nc * c["sf"]  # V^T, V, V^T of the weight-adjusted inverse
-    f += nc * c["Nq"] * (2 * (dim + 1) + 1)  # lifting R^T s and W/J~ scaling
+    if dim == 2:  # the 2D flux kernel also applies the weight-adjusted inverse (3D: K3, wadj_kernel_flops)
+        f += 2 * 3 * nc * c["sf"]  # V^T, V, V^T of the weight-adjusted inverse
+        f += nc * c["Nq"]  # W/J~ scaling
+    f += nc * c["Nq"] * 2 * (dim + 1)  # lifting R^T s
     return f
+
+
+def wadj_kernel_flops(dim, p):
+    """algorithmic flops per element of the 3D weight-adjusted inverse kernel K3: three
+    sum-factorised transforms V^T, V, V^T (2 flops per MAC, exact triangular loop bounds) and the
+    W/J~ scaling"""
+    c = counts(dim, p)
+    nc = dim + 2
+    return 2 * 3 * nc * c["sf"] + nc * c["Nq"]
 
 
 def ncu_traffic_per_element():
@@ -347,6 +358,7 @@ def run(args):
     k2_ms, k2_n = ctx.timing_read(1)
     k1_ms, k1_n = ctx.timing_read(0)
     kf_ms, kf_n = ctx.timing_read(2)
+    k3_ms, k3_n = ctx.timing_read(3)
     launches = ctx.launch_count()
     ctx.timing_enable(False)
     if world > 1:
@@ -414,6 +426,10 @@ def run(args):
                      "projection_share_of_step": k1_ms / args.steps / ms_step,
                      "iface_kernel_ms_avg": kf_ms / max(kf_n, 1),
                      "iface_share_of_step": kf_ms / args.steps / ms_step,
+                     "wadj_kernel_ms_avg": k3_ms / max(k3_n, 1),
+                     "wadj_share_of_step": k3_ms / args.steps / ms_step,
+                     "wadj_tflops": (wadj_kernel_flops(dim, p) * (ne / world) / (k3_ms / max(k3_n, 1) * 1e-3) / 1e12
+                                     if k3_n else None),
                      "peak_basis": "148 SM x 64 DFMA/clk x 2 x sm_max_mhz (DESIGN.md 5.4)"},
         "e2e": {"value": e2e_value, "unit": "flux_evals/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                 "api": "cudaMemcpyAsync(pinned->device) + es_set_state + es_step + es_get_state + copy back"},

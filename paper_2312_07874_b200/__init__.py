@@ -8,6 +8,7 @@ passes raw pointers.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import re
 
@@ -140,8 +141,11 @@ def dp54_controller(step, T, dt0, rtol, atol, max_steps=1000000, safety=0.9, fac
             raise ESError(-1, f"dp54: more than {max_steps} steps before T")
         h = min(dt, T - t)
         err, ok = step(h, rtol, atol)
-        fac = safety * err ** -0.2 if err > 0.0 else facmax
-        fac = min(1.0 if after_reject else facmax, max(facmin, fac))
+        if not math.isfinite(err):  # a trial stage blew up (or 0/0): reject and shrink
+            ok, fac = False, facmin
+        else:
+            fac = safety * err ** -0.2 if err > 0.0 else facmax
+            fac = min(1.0 if after_reject else facmax, max(facmin, fac))
         if ok:
             t += h
             nacc += 1

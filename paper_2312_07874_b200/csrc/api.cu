@@ -15,6 +15,7 @@
 #include "geometry.cuh"
 #include "internal.h"
 #include "kernels.cuh"
+#include "xform3.cuh"
 
 namespace esb {
 cudaError_t launch_project_2d(int n, const DevRef& R, const ProjArgs& A, cudaStream_t st);
@@ -27,6 +28,10 @@ cudaError_t launch_projnodal_2d(int n, const DevRef& R, int64_t ne, const double
 cudaError_t launch_projnodal_3d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st);
 cudaError_t launch_evalnodal_2d(int n, const DevRef& R, int64_t ne, const double* um, double* un, cudaStream_t st);
 cudaError_t launch_evalnodal_3d(int n, const DevRef& R, int64_t ne, const double* um, double* un, cudaStream_t st);
+cudaError_t upload_psi_3d(int n, const double* p1, const double* p2, const double* p3);
+cudaError_t launch_wadj_3d(int n, const WadjArgs& A, cudaStream_t st);
+cudaError_t launch_wjinv_permute_3d(int n, const double* geo_vol, int gvs, int row, int64_t ne, double* out,
+                                    cudaStream_t st);
 }  // namespace esb
 
 using namespace esb;
@@ -52,6 +57,7 @@ struct es_context {
   void* d_tables = nullptr;
   double *geo_vol = nullptr, *geo_face = nullptr, *xq = nullptr, *jt = nullptr;
   double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr, *fstar = nullptr;
+  double *rbuf = nullptr, *wjk3 = nullptr;  // 3D: nodal residual for K3, W / J~ in K3's layout
   int num_sms = 148, proj_ctas = 296;
   bool external = false;
   int eq56 = 0;   // volume_mode 1: per-operator fluxes (Eq. num_fluxes ablation)
@@ -187,6 +193,20 @@ cudaError_t run_rhs(es_context* c, RhsArgs A, int64_t n, const int64_t* list) {
     cudaEventRecord(te.b, c->stream);
     c->tev.push_back(te);
   }
+  if (e != cudaSuccess || c->d == 2) return e;
+  // 3D: weight-adjusted inverse and the RK / entropy epilogue, batched over elements (K3)
+  WadjArgs W{n, c->rbuf, c->wjk3, A.mode, A.out, A.u0, A.acc, A.ustage, A.dt, A.wt, A.part, A.c0};
+  TimedEvent t3{};
+  if (c->timing) {
+    t3 = {get_event(c), get_event(c), 3};
+    cudaEventRecord(t3.a, c->stream);
+  }
+  c->launches++;
+  e = launch_wadj_3d(c->n, W, c->stream);
+  if (c->timing) {
+    cudaEventRecord(t3.b, c->stream);
+    c->tev.push_back(t3);
+  }
   return e;
 }
 
@@ -225,6 +245,7 @@ RhsArgs base_rhs_args(es_context* c) {
   A.sdense = c->sdense;
   A.rbdense = c->rbdense;
   A.nhat = c->R.nhat;
+  A.rbuf = c->rbuf;
   return A;
 }
 
@@ -313,7 +334,8 @@ void es_destroy(es_context* c) {
                   (void*)c->face_slot, (void*)c->d_interior, (void*)c->d_boundary, (void*)c->d_send,
                   (void*)c->face_reflect, (void*)c->bad, (void*)c->U, (void*)c->ACC, (void*)c->US,
                   (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg, (void*)c->fstar,
-                  (void*)c->dpy, (void*)c->dppart, (void*)c->sdense, (void*)c->rbdense})
+                  (void*)c->dpy, (void*)c->dppart, (void*)c->sdense, (void*)c->rbdense, (void*)c->rbuf,
+                  (void*)c->wjk3})
     if (p) cudaFree(p);
   for (double* p : c->dpk)
     if (p) cudaFree(p);
@@ -476,6 +498,13 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   CK(cudaMalloc((void**)&c->ACC, nmod * sizeof(double)));
   CK(cudaMalloc((void**)&c->US, nmod * sizeof(double)));
   CK(cudaMemset(c->U, 0, nmod * sizeof(double)));
+  if (c->d == 3) {  // K3: nodal residual buffer, W / J~ in its layout, PKD tables in constant memory
+    CK(cudaMalloc((void**)&c->rbuf, (size_t)c->nloc * c->NC * c->Nq * sizeof(double)));
+    CK(cudaMalloc((void**)&c->wjk3, (size_t)c->nloc * c->Nq * sizeof(double)));
+    CK(launch_wjinv_permute_3d(c->n, c->geo_vol, even_up((NG + 2) * c->Nq), NG + 1, c->nloc, c->wjk3, c->stream));
+    CK(upload_psi_3d(c->n, c->T.psi1.data(), c->T.psi2.data(), c->T.psi3.data()));
+    c->launches++;
+  }
   if (std::getenv("ES_PHASE_TIMING")) {
     CK(cudaMalloc((void**)&c->dbg, 2 * 4096 * 16 * sizeof(long long)));
     CK(cudaMemset(c->dbg, 0, 2 * 4096 * 16 * sizeof(long long)));
@@ -550,8 +579,8 @@ es_status es_rhs_host(es_context* c, const double* uh, double* duh) {
 }
 
 es_status es_set_state(es_context* c, const double* u) {
-  c->dp_fsal = false;
   POISON_CHECK();
+  c->dp_fsal = false;
   CK(cudaSetDevice(c->device));
   CK(cudaMemcpyAsync(c->U, u, (size_t)c->nloc * c->NC * c->Np * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   return ES_OK;
@@ -670,9 +699,9 @@ es_status es_entropy_production(es_context* c, const double* u, double* rate, do
                                  double* cons) {
   POISON_CHECK();
   CK(cudaSetDevice(c->device));
-  const size_t nmod = (size_t)c->nloc * c->NC * c->Np;
+  // a flag left by an earlier unchecked call (check_admissibility = 0) must not be reported here
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
   double* scratch = c->ACC;  // the RK accumulator is free between steps
-  (void)nmod;
   RhsArgs A = base_rhs_args(c);
   A.mode = 5;
   A.out = scratch;

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256) rk_err_kernel(const double* __restrict__ 
     double e = 0.0;
     for (int j = 0; j < ec.nk; ++j) e = fma(ec.c[j], ec.k[j][i], e);
     const double sc = atol + rtol * fmax(fabs(y0[i]), fabs(y1[i]));
-    const double r = e / sc;
+    const double r = e == 0.0 ? 0.0 : e / sc;  // atol = 0 with a coefficient that stays 0: no 0/0
     s = fma(r, r, s);
   }
   red[threadIdx.x] = s;

@@ -86,6 +86,7 @@ struct RhsArgs {
   const double* sdense;       // volume_mode 2: dense S^(l) [l][j][i]
   const double* rbdense;      // volume_mode 2: dense (R^(z)T B) [z][f][i]
   const double* nhat;         // [Nf][3] reference outward normals
+  double* rbuf;               // 3D: nodal residual [nloc][NC][N(b)][N(a)][N(c)] for the batched K3
 };
 
 struct IfaceArgs {

@@ -46,13 +46,14 @@ struct Rhs2Smem {
   using W = Lw<DIM, N>;
   // per-CTA constants (staged once by the persistent CTA)
   static constexpr int TB = 5 * N * N + 6 * N + N * N + S::NF;  // line operators, weights, extrapolation, B
-  static constexpr int PS = psi_smem_doubles<DIM, N>();         // PKD sum-factorisation tables
+  // PKD sum-factorisation tables: 2D only (3D hands the nodal residual to the batched K3, xform3.cuh)
+  static constexpr int PS = DIM == 2 ? psi_smem_doubles<DIM, N>() : 0;
   // per element
   static constexpr int PR = S::PRS;                  // rho, v, p, beta, flag (bulk copy of prim)
   static constexpr int GG = ev2(S::NG * S::Nq);      // G_lm              (bulk copy)
   static constexpr int RR = ev2(S::NC * S::Nq);      // nodal residual r; first transform buffer
   static constexpr int PT = DIM == 3 ? S::NC * N * N * N : 0;  // facet-4 partial sums [v][j][a][c]
-  static constexpr int UM = ev2(S::NC * S::Np) + (DIM == 3 ? S::NC * N * N : 0);  // modal result, facet-4 lift
+  static constexpr int UM = DIM == 2 ? ev2(S::NC * S::Np) : S::NC * N * N;  // 2D modal result / 3D facet-4 lift
   static constexpr int FP = S::Nf * S::NC * S::Nqf;  // facet states [z][rho, v, p][f] (bulk copy)
   static constexpr int FB = ev2(S::NF);              // facet beta = rho / p
   static constexpr int FJ = S::Nf * DIM * S::Nqf;    // J n at facet nodes [z][m][f] (bulk copy)
@@ -69,7 +70,7 @@ struct Rhs2Smem {
   static constexpr int o_tb = 0, o_ps = ev2(o_tb + TB), o_pr = ev2(o_ps + PS), o_g = o_pr + PR, o_r = ev2(o_g + GG),
                        o_pt = ev2(o_r + RR), o_fp = ev2(o_pt + PB), o_fb = ev2(o_fp + FP),
                        o_fj = ev2(o_fb + FB), o_fs = ev2(o_fj + FJ), o_sc = ev2(o_fs + FS), o_um = o_sc, o_wj = ev2(o_sc + SCU),
-                       total = ev2(o_wj + 2 * ev2(WJN));  // W/J~ double-buffered by element parity
+                       total = ev2(o_wj + (DIM == 2 ? 2 * ev2(WJN) : 0));  // 2D: W/J~ double-buffered by element parity
   static_assert(S::PRS <= PR, "prim copy");
   static_assert(total * 8 <= 227 * 1024 - 256, "shared memory");
 };
@@ -256,6 +257,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // mbarriers of the flux kernel: element data for the passes (A) / interface fluxes and W/J~ (B)
 __shared__ uint64_t k2_barA, k2_barB;
 
+template <int DIM, int N>
+__device__ __forceinline__ void k2_epilogue_2d(const RhsArgs& A, int64_t e, unsigned it);
+
 // one element of the flux kernel (the body of the persistent loop)
 template <int DIM, int N, bool EQ, bool DN = false>
 __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsigned it) {
@@ -293,14 +297,15 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
   // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers
   auto issue_A = [&](int64_t e, unsigned buf) {
-    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8, bW = L::WJN * 8;
+    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8,
+                       bW = DIM == 2 ? L::WJN * 8 : 0;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&k2_barA, bP + bG + bF + bJ + bW);
     bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &k2_barA);
     bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &k2_barA);
     bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &k2_barA);
     bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &k2_barA);
-    bulk_g2s(smk2 + L::o_wj + buf * ev2(L::WJN), A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barA);
+    if constexpr (DIM == 2) bulk_g2s(smk2 + L::o_wj + buf * ev2(L::WJN), A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barA);
   };
   auto issue_B = [&](int64_t e) {
     constexpr unsigned bS = L::FS * 8;
@@ -781,7 +786,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   stamp(5);
   // ---- lifting r -= R^T s; facet 4 sum-factorised: t4[v][a][b] = sum_j l_b(eta3_j) s4[v][a + N j] ----
   if constexpr (DIM == 3) {
-    double* t4 = sU + L::UM - NC * N * N;
+    double* t4 = sU;
     for (int q = tid; q < NC * N * N; q += NT) {
       const int v = q / (N * N), b = (q / N) % N, a = q % N;
       const double* s4 = fS + (3 * NC + v) * Nqf + a;
@@ -792,26 +797,59 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     }
     __syncthreads();
   }
-  for (int i = tid; i < Nq; i += NT) {
-    const int a = i % N, b = (i / N) % N, c = DIM == 3 ? i / (N * N) : 0;
-#pragma unroll
-    for (int v = 0; v < NC; ++v) {
-      double t;
-      if constexpr (DIM == 2) {
-        t = tlL[b] * fS[(0 * NC + v) * Nqf + a] + tlR[a] * fS[(1 * NC + v) * Nqf + b] +
-            tlL[a] * fS[(2 * NC + v) * Nqf + b];
-      } else {
-        const double* t4 = sU + ev2(NC * Np);
-        t = tlL[b] * fS[(0 * NC + v) * Nqf + a + N * c] + tlR[a] * fS[(1 * NC + v) * Nqf + b + N * c] +
-            tlL[a] * fS[(2 * NC + v) * Nqf + b + N * c] + tl3[c] * t4[(v * N + b) * N + a];
-      }
-      sR[v * Nq + i] -= t;
+  if constexpr (DIM == 3) {
+    // nodal residual r = sR - R^T s, written as r[e][v][b][a][c] (c fastest: the layout the batched
+    // weight-adjusted inverse K3 reads coalesced, xform3.cuh); K3 applies P:593 and the RK update
+    const double* t4 = sU;
+    double* rg = A.rbuf + (size_t)e * NC * Nq;
+    for (int q = tid; q < NC * Nq; q += NT) {
+      const int v = q / Nq, rq = q - v * Nq, b = rq / (N * N), a = (rq / N) % N, c = rq % N;
+      const int i = a + N * b + N * N * c;
+      const double t = tlL[b] * fS[(0 * NC + v) * Nqf + a + N * c] + tlR[a] * fS[(1 * NC + v) * Nqf + b + N * c] +
+                       tlL[a] * fS[(2 * NC + v) * Nqf + b + N * c] + tl3[c] * t4[(v * N + b) * N + a];
+      rg[q] = sR[v * Nq + i] - t;
     }
+    __syncthreads();
+    stamp(7);
+    if (tid == 0 && has_next) issue_B(elem_of(nidx));
+    return;
+  } else {
+    for (int i = tid; i < Nq; i += NT) {
+      const int a = i % N, b = (i / N) % N;
+#pragma unroll
+      for (int v = 0; v < NC; ++v) {
+        const double t = tlL[b] * fS[(0 * NC + v) * Nqf + a] + tlR[a] * fS[(1 * NC + v) * Nqf + b] +
+                         tlL[a] * fS[(2 * NC + v) * Nqf + b];
+        sR[v * Nq + i] -= t;
+      }
+    }
+    __syncthreads();
+    stamp(7);
+    // the interface fluxes are consumed: the next element's copy lands during the transforms
+    if (tid == 0 && has_next) issue_B(elem_of(nidx));
+    k2_epilogue_2d<DIM, N>(A, e, it);
   }
-  __syncthreads();
-  stamp(7);
-  // the interface fluxes are consumed: the next element's copy lands during the transforms
-  if (tid == 0 && has_next) issue_B(elem_of(nidx));
+}
+
+// 2D epilogue of the flux kernel: d u~/dt = V^T W/J~ V (V^T r) in place, then the output /
+// RK4 stage update / entropy partials (3D runs this in the batched K3, xform3.cuh)
+template <int DIM, int N>
+__device__ __forceinline__ void k2_epilogue_2d(const RhsArgs& A, int64_t e, unsigned it) {
+  using S = Sz<DIM, N>;
+  using W = Lw<DIM, N>;
+  using L = Rhs2Smem<DIM, N>;
+  constexpr int NC = S::NC, Np = S::Np, NT = W::NT;
+  double* sR = smk2 + L::o_r;
+  double* pt = smk2 + L::o_pt;
+  double* sU = smk2 + L::o_um;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto stamp = [&](int k) {
+#ifdef ES_STAMPS
+    if (A.dbg && tid == 0 && e < 4096) A.dbg[e * 16 + k] = clock64();
+#else
+    (void)k;
+#endif
+  };
   const double* sWJ = smk2 + L::o_wj + (it & 1) * ev2(L::WJN) + L::WJOFF;  // [Nq] W / J~
 
   // ---- d u~/dt = V^T W/J~ V (V^T r), transforms in place in sR ----
@@ -929,14 +967,15 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
   // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers
   auto issue_A = [&](int64_t e, unsigned buf) {
-    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8, bW = L::WJN * 8;
+    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8,
+                       bW = DIM == 2 ? L::WJN * 8 : 0;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&k2_barA, bP + bG + bF + bJ + bW);
     bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &k2_barA);
     bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &k2_barA);
     bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &k2_barA);
     bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &k2_barA);
-    bulk_g2s(smk2 + L::o_wj + buf * ev2(L::WJN), A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barA);
+    if constexpr (DIM == 2) bulk_g2s(smk2 + L::o_wj + buf * ev2(L::WJN), A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barA);
   };
   auto issue_B = [&](int64_t e) {
     constexpr unsigned bS = L::FS * 8;
@@ -972,7 +1011,7 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
     if constexpr (DIM == 3) tl3[k] = R.l3L[k];
   }
   for (int k = tid; k < NF; k += NT) tB[k] = R.Bf[k];
-  const PsiS T = stage_psi<DIM, N>(R, smk2 + L::o_ps);
+  if constexpr (DIM == 2) stage_psi<DIM, N>(R, smk2 + L::o_ps);  // 3D: no PKD tables in this kernel
   __syncthreads();  // mbarriers initialised and tables staged before anyone uses them
 
 #pragma unroll 1

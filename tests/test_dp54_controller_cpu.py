@@ -62,3 +62,17 @@ def test_controller_step_limit():
     m = MockDP(lambda t, y: -y, [1.0])
     with pytest.raises(es.ESError):
         es.dp54_controller(m.step, 10.0, 1e-3, rtol=1e-12, atol=1e-14, max_steps=5)
+
+
+def test_controller_non_finite_error_is_a_rejection_that_shrinks_the_step():
+    # a trial step that blew up reports err = nan: the controller must reject it and
+    # shrink dt by facmin, not grow it by facmax
+    calls = []
+
+    def step(dt, rtol, atol):
+        calls.append(dt)
+        return (float("nan"), True) if dt > 0.05 else (0.5, True)
+
+    nacc, nrej, _ = es.dp54_controller(step, 0.2, 0.1, rtol=1e-6, atol=1e-9)
+    assert nrej == 1 and calls[1] == pytest.approx(0.1 * 0.2)
+    assert nacc >= 1

@@ -49,7 +49,7 @@ def build_oracle(force=False):
 
 def lib_sources():
     c = os.path.join(PKG, "csrc")
-    return sorted(os.path.join(c, f) for f in os.listdir(c) if f.endswith((".cu", ".cpp", ".h", ".cuh"))) + \
+    return sorted(os.path.join(c, f) for f in os.listdir(c) if f.endswith((".cu", ".cpp", ".h", ".cuh", ".inc"))) + \
         [os.path.join(ROOT, "include", "es.h")]
 
 
