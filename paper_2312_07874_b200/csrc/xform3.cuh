@@ -40,10 +40,19 @@ struct X3 {
   // shared-memory banks two deep (mode A) and B-mode lanes hit distinct bank pairs
   static constexpr int SEV = NPAIR * N + ((N - NPAIR * N) % 16 + 16) % 16;
   static constexpr int SPE = NC * SEV;  // S doubles per element: [v][pr][c] (+ pad)
-  static constexpr int UPE = NC * Np;   // modal doubles per element: [v][k]
+  static constexpr int UPE = NC * Np;  // modal result [v][k] (the element's W / J~ [b][a][c] before that)
+  static_assert(NC * Np >= Nq, "W / J~ staging fits the modal buffer");
   static constexpr int PPE = NC * (2 * NPAIR + 1);  // entropy partials per element
-  // elements per CTA: the mode-A lanes (5 E N) fill whole warps of a CTA of at most 384 threads
-  static constexpr int E = (384 / (NC * N)) < 1 ? 1 : (384 / (NC * N));
+  // elements per CTA: the mode-A lanes (5 E N) fill whole warps of a CTA of at most 192 threads
+  // (two CTAs per SM, so that one CTA's global loads and barriers overlap the other's arithmetic)
+#ifndef ES_K3_THREADS
+#define ES_K3_THREADS 192
+#endif
+#ifndef ES_K3_MINB
+#define ES_K3_MINB 2
+#endif
+  static constexpr int MINB = ES_K3_MINB;  // resident CTAs per SM the register budget is sized for
+  static constexpr int E = (ES_K3_THREADS / (NC * N)) < 1 ? 1 : (ES_K3_THREADS / (NC * N));
   static constexpr int NT = ((NC * E * N + 31) / 32) * 32;
   static constexpr size_t SMEM = (size_t)E * (SPE + UPE + PPE) * sizeof(double);
 };
@@ -73,10 +82,57 @@ struct WadjArgs {
   double c0;
 };
 
-// ---- mode A: one c-slab ----
+// ---- mode A: one c-slab, lane = (element, variable, c) ----
+// Fully unrolled: every table read is a compile-time constant-memory operand (uniform registers).
+// even-odd (parity) form of the psi1 contractions: the Legendre nodes are symmetric (eta_{N-1-a} =
+// -eta_a) and psi1^{a1} has the parity of a1, so psi1[a1][N-1-a] = (-1)^{a1} psi1[a1][a] and
+//   u[a] = ue[a] + uo[a], u[N-1-a] = ue[a] - uo[a],  ue = even-a1 sums, uo = odd-a1 sums, a < N/2
+// halves the multiply-adds of the largest sum-factorisation step (checked on the host at setup)
+template <int N>
+__device__ __forceinline__ void psi1_apply_eo(const double* t2, double* u) {  // u[a] = sum_a1 psi1[a1][a] t2[a1]
+  constexpr int H = N / 2, M = N % 2;
+#pragma unroll
+  for (int a = 0; a < H + M; ++a) {
+    double ue = 0.0, uo = 0.0;
+#pragma unroll
+    for (int a1 = 0; a1 < N; a1 += 2) ue = fma(c_psi<N>.p1[a1 * N + a], t2[a1], ue);
+    if (a < H) {
+#pragma unroll
+      for (int a1 = 1; a1 < N; a1 += 2) uo = fma(c_psi<N>.p1[a1 * N + a], t2[a1], uo);
+      u[a] = ue + uo;
+      u[N - 1 - a] = ue - uo;
+    } else {
+      u[a] = ue;  // middle node: the odd functions vanish there
+    }
+  }
+}
+template <int N>
+__device__ __forceinline__ void psi1T_apply_eo(const double* y, double* s2) {  // s2[a1] = sum_a psi1[a1][a] y[a]
+  constexpr int H = N / 2, M = N % 2;
+  double yp[H + M], ym[H > 0 ? H : 1];
+#pragma unroll
+  for (int a = 0; a < H; ++a) {
+    yp[a] = y[a] + y[N - 1 - a];
+    ym[a] = y[a] - y[N - 1 - a];
+  }
+  if (M) yp[H] = y[H];
+#pragma unroll
+  for (int a1 = 0; a1 < N; ++a1) {
+    double t = 0.0;
+    if (a1 % 2 == 0) {
+#pragma unroll
+      for (int a = 0; a < H + M; ++a) t = fma(c_psi<N>.p1[a1 * N + a], yp[a], t);
+    } else {
+#pragma unroll
+      for (int a = 0; a < H; ++a) t = fma(c_psi<N>.p1[a1 * N + a], ym[a], t);
+    }
+    s2[a1] = t;
+  }
+}
+
 // V^T steps 1-2 from the global residual: s1[pr] = sum_b psi2[a1][a2][b] sum_a psi1[a1][a] r[b][a][c]
 template <int N>
-__device__ __forceinline__ void modeA_vt12_global(const double* __restrict__ rr, double* S, bool ok) {
+__device__ __forceinline__ void modeA_vt12_global(const double* __restrict__ rr, double* S, bool ok, bool act) {
   constexpr int NPAIR = X3<N>::NPAIR;
   double s1[NPAIR];
 #pragma unroll
@@ -86,27 +142,26 @@ __device__ __forceinline__ void modeA_vt12_global(const double* __restrict__ rr,
     double x[N], s2[N];
 #pragma unroll
     for (int a = 0; a < N; ++a) x[a] = ok ? __ldg(rr + (b * N + a) * N) : 0.0;
-#pragma unroll
-    for (int a1 = 0; a1 < N; ++a1) {
-      double t = 0.0;
-#pragma unroll
-      for (int a = 0; a < N; ++a) t = fma(c_psi<N>.p1[a1 * N + a], x[a], t);
-      s2[a1] = t;
-    }
+    psi1T_apply_eo<N>(x, s2);
 #pragma unroll
     for (int a1 = 0; a1 < N; ++a1)
 #pragma unroll
       for (int a2 = 0; a2 < N - a1; ++a2)
         s1[pr_of(N, a1, a2)] = fma(c_psi<N>.p2[(a1 * N + a2) * N + b], s2[a1], s1[pr_of(N, a1, a2)]);
   }
+  if (act)
 #pragma unroll
-  for (int q = 0; q < NPAIR; ++q) S[q * N] = s1[q];
+    for (int q = 0; q < NPAIR; ++q) S[q * N] = s1[q];
 }
 
-// V steps 2-3 of one c-slab, W / J~ scaling, V^T steps 1-2: S (t1 in) -> S (s1 out), same slots
+// V steps 2-3 of one c-slab, W / J~ scaling, V^T steps 1-2: S (t1 in) -> S (s1 out), same slots;
+// wj: the element's W / J~ [b][a][c] in shared memory at the lane's c.  The t1 column is re-read
+// from shared memory for every b (volatile: not hoisted into 2 x 45 registers beside the 45
+// accumulators s1)
 template <int N>
-__device__ __forceinline__ void modeA_mid(double* S, const double* __restrict__ wj, bool ok) {
+__device__ __forceinline__ void modeA_mid(double* S, const double* wj, bool act) {
   constexpr int NPAIR = X3<N>::NPAIR;
+  const volatile double* Sv = S;
   double s1[NPAIR];
 #pragma unroll
   for (int q = 0; q < NPAIR; ++q) s1[q] = 0.0;
@@ -117,31 +172,22 @@ __device__ __forceinline__ void modeA_mid(double* S, const double* __restrict__ 
     for (int a1 = 0; a1 < N; ++a1) {
       double t = 0.0;
 #pragma unroll
-      for (int a2 = 0; a2 < N - a1; ++a2) t = fma(c_psi<N>.p2[(a1 * N + a2) * N + b], S[pr_of(N, a1, a2) * N], t);
+      for (int a2 = 0; a2 < N - a1; ++a2) t = fma(c_psi<N>.p2[(a1 * N + a2) * N + b], Sv[pr_of(N, a1, a2) * N], t);
       t2[a1] = t;
     }
+    psi1_apply_eo<N>(t2, y);
 #pragma unroll
-    for (int a = 0; a < N; ++a) {
-      double t = 0.0;
-#pragma unroll
-      for (int a1 = 0; a1 < N; ++a1) t = fma(c_psi<N>.p1[a1 * N + a], t2[a1], t);
-      y[a] = t * (ok ? __ldg(wj + (b * N + a) * N) : 0.0);
-    }
-#pragma unroll
-    for (int a1 = 0; a1 < N; ++a1) {
-      double t = 0.0;
-#pragma unroll
-      for (int a = 0; a < N; ++a) t = fma(c_psi<N>.p1[a1 * N + a], y[a], t);
-      s2[a1] = t;
-    }
+    for (int a = 0; a < N; ++a) y[a] *= wj[(b * N + a) * N];
+    psi1T_apply_eo<N>(y, s2);
 #pragma unroll
     for (int a1 = 0; a1 < N; ++a1)
 #pragma unroll
       for (int a2 = 0; a2 < N - a1; ++a2)
         s1[pr_of(N, a1, a2)] = fma(c_psi<N>.p2[(a1 * N + a2) * N + b], s2[a1], s1[pr_of(N, a1, a2)]);
   }
+  if (act)
 #pragma unroll
-  for (int q = 0; q < NPAIR; ++q) S[q * N] = s1[q];
+    for (int q = 0; q < NPAIR; ++q) S[q * N] = s1[q];
 }
 
 // ---- mode B: one (pr) fibre over c, length N3 = N - s of the modal index a3 ----
@@ -211,22 +257,31 @@ __device__ __forceinline__ void pr_by_rank(int rank, int& a1, int& a2) {
 }
 
 template <int N>
-__global__ void __launch_bounds__(X3<N>::NT) wadj3_kernel(const WadjArgs A) {
+__global__ void __launch_bounds__(X3<N>::NT, X3<N>::MINB) wadj3_kernel(const WadjArgs A) {
   using Z = X3<N>;
   constexpr int NC = Z::NC, NPAIR = Z::NPAIR, Np = Z::Np, E = Z::E, NT = Z::NT, SPE = Z::SPE, UPE = Z::UPE;
   extern __shared__ __align__(16) double smx[];
   double* S = smx;            // [E][NC][NPAIR][N]
-  double* U = smx + E * SPE;  // [E][NC][Np] modal result; entropy partials before that
+  double* U = smx + E * SPE;  // [E][NC][Np] modal result, then the entropy partials
   const int tid = threadIdx.x;
   const int64_t e0 = (int64_t)blockIdx.x * E;
   const int ne = (int)((A.n_elem - e0) < E ? (A.n_elem - e0) : E);
   const bool ent_mode = A.mode == 5;
+  // W / J~ of the CTA's elements into the (not yet used) modal buffer U[e] ([b][a][c], 8-byte
+  // asynchronous copies: the element stride of U is odd), consumed by A2
+  for (int k = tid; k < ne * Z::Nq; k += NT) {
+    const int e = k / Z::Nq, q = k - e * Z::Nq;
+    cp_async8(U + e * UPE + q, A.wjinv + (e0 + e) * Z::Nq + q);
+  }
+  cp_async_commit();
 
-  // ---- A1: V^T steps 1-2 of r, lane = (e, v, c) ----
-  if (tid < NC * E * N) {
-    const int ev = tid / N, c = tid - ev * N, e = ev / NC;
-    const bool ok = e < ne;
-    modeA_vt12_global<N>(A.r + ((size_t)e0 * NC + (ok ? ev : 0)) * Z::Nq + c, S + ev * Z::SEV + c, ok);
+  // ---- A1: V^T steps 1-2 of r, lane = (e, v, c); every thread runs it (warp-convergent, so that the
+  // b-dependent table rows are uniform-register constant loads), idle lanes on zeros without stores
+  {
+    const bool act = tid < NC * E * N;
+    const int ev = act ? tid / N : 0, c = act ? tid - ev * N : 0, e = ev / NC;
+    const bool ok = act && e < ne;
+    modeA_vt12_global<N>(A.r + ((size_t)e0 * NC + (ok ? ev : 0)) * Z::Nq + c, S + ev * Z::SEV + c, ok, act);
   }
   __syncthreads();
   // ---- B1: V^T step 3 (r^ = V^T r) and V step 1, lane = (pr rank, e, v) ----
@@ -259,11 +314,13 @@ __global__ void __launch_bounds__(X3<N>::NT) wadj3_kernel(const WadjArgs A) {
       for (int v = 0; v < NC; ++v) pp[2 + v] = pe[E * NC * NPAIR * 2 + e * NC + v] / A.c0;
     }
   }
-  // ---- A2: V steps 2-3, W / J~, V^T steps 1-2, lane = (e, v, c) ----
-  if (tid < NC * E * N) {
-    const int ev = tid / N, c = tid - ev * N, e = ev / NC;
-    const bool ok = e < ne;
-    modeA_mid<N>(S + ev * Z::SEV + c, A.wjinv + (e0 + (ok ? e : 0)) * Z::Nq + c, ok);
+  // ---- A2: V steps 2-3, W / J~, V^T steps 1-2, lane = (e, v, c) (all threads, as A1) ----
+  cp_async_wait_all();
+  __syncthreads();
+  {
+    const bool act = tid < NC * E * N;
+    const int ev = act ? tid / N : 0, c = act ? tid - ev * N : 0, e = ev / NC;
+    modeA_mid<N>(S + ev * Z::SEV + c, U + e * UPE + c, act);
   }
   __syncthreads();
   // ---- B2: V^T step 3 -> du~/dt in U[e][v][k] ----

@@ -65,6 +65,8 @@ def build_lib(force=False, jobs=8):
     inc = ["-I", os.path.join(ROOT, "include"), "-I", c]
     if os.environ.get("ES_STAMPS"):  # per-element clock stamps (ES_PHASE_TIMING diagnostics)
         inc = ["-DES_STAMPS"] + inc
+    if os.environ.get("ES_NVCC_DEFS"):  # tuning experiments, e.g. "-DES_K3_THREADS=192 -DES_K3_MINB=2"
+        inc = os.environ["ES_NVCC_DEFS"].split() + inc
     nd = nccl_dir()
     if nd:
         inc = ["-I", os.path.join(nd, "include")] + inc
