@@ -88,12 +88,34 @@ def wadj_kernel_flops(dim, p):
     return 2 * 3 * nc * c["sf"] + nc * c["Nq"]
 
 
-def ncu_traffic_per_element():
-    """DRAM bytes per element of K2 from the committed ncu --set full capture (profiles/)."""
+def project_kernel_flops(dim, p):
+    """algorithmic flops per element of the entropy-projection kernel K1: five
+    sum-factorised transforms (V, V^T, V, V^T, V; 2 flops per multiply-add, exact loop bounds), the
+    facet extrapolation, the entropy variables at the volume nodes (~35 flops each, logs and divisions
+    counted as one) and the entropy-projected states at volume and facet nodes (~20 each)"""
+    c = counts(dim, p)
+    nc, n = dim + 2, p + 1
+    nf = (dim + 1) * n ** (dim - 1)
+    traces = 5 * n ** 3 if dim == 3 else 3 * n * n
+    return 2 * 5 * nc * c["sf"] + 2 * nc * traces + 35 * c["Nq"] + 20 * (c["Nq"] + nf)
+
+
+def iface_bytes_per_element(dim, p):
+    """algorithmic HBM bytes per element of the interface kernel: own and neighbour traces (rho, v,
+    p/2 at every facet node), J n at the facet nodes, B J_f f* written"""
+    n = p + 1
+    nf = (dim + 1) * n ** (dim - 1)
+    nc = dim + 2
+    return 8 * nf * (2 * nc + dim + nc)
+
+
+def ncu_traffic_per_element(kernel="K2"):
+    """DRAM bytes per element and launch of a kernel from the committed ncu --set full capture (profiles/)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             d = json.load(fh)
-        return d["rhs2_kernel"]["dram_bytes_per_element"], d["source"]
+        key = {"K2": "rhs2_kernel", "K1": "project_kernel", "K3": "wadj3_kernel", "iface": "iface_kernel"}[kernel]
+        return d[key]["dram_bytes_per_element"], d["source"]
     except Exception:
         return None, None
 
@@ -344,9 +366,9 @@ def run(args):
     sampler = ClockSampler(local)
     sampler.start()
     ctx.reset_launch_count()
-    ctx.timing_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    # ---- timed region: K RK4 steps (CUDA-graph replays on one rank, es_set_graphs) ----
     e0.record(stream)
     for _ in range(args.steps):
         ctx.step(dt, 1)
@@ -355,14 +377,9 @@ def run(args):
     barrier()
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1)
-    k2_ms, k2_n = ctx.timing_read(1)
-    k1_ms, k1_n = ctx.timing_read(0)
-    kf_ms, kf_n = ctx.timing_read(2)
-    k3_ms, k3_n = ctx.timing_read(3)
     launches = ctx.launch_count()
-    ctx.timing_enable(False)
     if world > 1:
-        tt = torch.tensor([ms, k2_ms / max(k2_n, 1)], device="cuda", dtype=torch.float64)
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt[0].item())
     ms_step = ms / args.steps
@@ -370,41 +387,73 @@ def run(args):
     evals_step = rhs_per_step * ne * (c["vol"] + c["fac"])
     value = evals_step / (ms_step * 1e-3)
     dof = ne * c["Np"] * (dim + 2)
-    # ---- end to end through the public API with host buffers ----
+    # ---- per-kernel breakdown: the same K steps again, eager, CUDA events around every launch on the
+    # context stream (the launching stream of all kernels) ----
+    ctx.timing_enable(True)
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e4.record(stream)
+    for _ in range(args.steps):
+        ctx.step(dt, 1)
+    e5.record(stream)
+    ctx.synchronize()
+    eager_ms_step = e4.elapsed_time(e5) / args.steps
+    kt = {}
+    for cls, name in ((0, "K1"), (1, "K2"), (2, "iface"), (3, "K3")):
+        tms, tn = ctx.timing_read(cls)
+        kt[name] = (tms / max(tn, 1), tn / args.steps)  # ms per launch, launches per step
+    ctx.timing_enable(False)
+    # ---- end to end through the public C-ABI host-buffer call (es_step_host): every step copies the
+    # state from pinned host memory to the device and the result back ----
     state = torch.empty_like(um)
     ctx.get_state(state)
     ctx.synchronize()
     host_in = state.cpu().pin_memory()
     host_out = torch.empty_like(host_in).pin_memory()
-    dev = torch.empty_like(um)
     barrier()
-    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2.record(stream)
     esteps = max(1, min(args.steps, 3))
-    with torch.cuda.stream(stream):
-        for _ in range(esteps):
-            dev.copy_(host_in, non_blocking=True)
-            ctx.set_state(dev)
-            ctx.step(dt, 1)
-            ctx.get_state(dev)
-            host_out.copy_(dev, non_blocking=True)
-    e3.record(stream)
-    ctx.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(esteps):
+        ctx.step_host(host_in, host_out, dt, 1)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / esteps
     barrier()
-    e2e_ms = e2.elapsed_time(e3) / esteps
     if world > 1:
         tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt[0].item())
     e2e_value = evals_step / (e2e_ms * 1e-3)
     nbytes = host_in.numel() * 8
-    # ---- roofline of the dominant kernel (K2) ----
-    k2_avg_ms = k2_ms / max(k2_n, 1)
-    k2_flops = rhs_kernel_flops(dim, p, c["vol"], c["fac"]) * (ne / world) / (k2_n / max(1, args.steps * 4))
-    achieved = k2_flops / (k2_avg_ms * 1e-3) / 1e12
-    tpe, traffic_src = ncu_traffic_per_element()
-    traffic = tpe * (ne / world) / (k2_n / max(1, args.steps * 4)) if tpe else None
-    peak = fp64_peak_tflops()
+    # ---- roofline: each kernel against the bound that applies ----
+    nloc = ne / world
+    peak_fp64 = fp64_peak_tflops()
+    hbm = measured_peaks().get("hbm_gbs", 6544.3)
+    kernels = {}
+
+    def add_alu(name, label, flops_el):
+        ms_l, per_step = kt[name]
+        if per_step == 0:
+            return
+        units = nloc * rhs_per_step / per_step  # elements per launch
+        ach = flops_el * units / (ms_l * 1e-3) / 1e12
+        kernels[name] = {"kernel": label, "bound": "alu", "ms_avg": ms_l, "launches_per_step": per_step,
+                         "share_of_step": ms_l * per_step / eager_ms_step, "algorithmic_flops_per_element": flops_el,
+                         "achieved": ach, "peak": peak_fp64, "unit": "TFLOP/s", "frac": ach / peak_fp64}
+    add_alu("K2", "rhs2_kernel (line-wise flux differencing, facet correction, lifting)",
+            rhs_kernel_flops(dim, p, c["vol"], c["fac"]))
+    add_alu("K1", "project_kernel (entropy projection, traces)", project_kernel_flops(dim, p))
+    if dim == 3:
+        add_alu("K3", "wadj3_kernel (weight-adjusted inverse, RK update)", wadj_kernel_flops(dim, p))
+    ms_f, per_f = kt["iface"]
+    if per_f:
+        b_el = iface_bytes_per_element(dim, p)
+        ach = b_el * nloc * rhs_per_step / per_f / (ms_f * 1e-3) / 1e9
+        kernels["iface"] = {"kernel": "iface_kernel (entropy-stable interface flux)", "bound": "hbm", "ms_avg": ms_f,
+                            "launches_per_step": per_f, "share_of_step": ms_f * per_f / eager_ms_step,
+                            "algorithmic_bytes_per_element": b_el, "achieved": ach, "peak": hbm, "unit": "GB/s",
+                            "frac": ach / hbm}
+    dom = max(kernels, key=lambda k: kernels[k]["share_of_step"])
+    tpe, traffic_src = ncu_traffic_per_element(dom)
+    k = kernels[dom]
+    units = nloc * rhs_per_step / k["launches_per_step"]
     line = {
         "metric": "EC two-point flux evals/s", "value": value, "unit": "flux_evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -413,26 +462,19 @@ def run(args):
                    "dof": dof, "dt": dt, "l2": "inputs larger than L2 (no flush needed)" if dof * 8 > 126e6 else
                    "inputs smaller than L2",
                    "parallelism": f"element partition over {world} GPU(s), NCCL face-trace halo",
-                   "setup_s": t_setup},
+                   "cuda_graphs": world == 1, "setup_s": t_setup},
         "dof_rhs_per_s": dof * rhs_per_step / (ms_step * 1e-3),
         "rhs_per_s": rhs_per_step / (ms_step * 1e-3),
         "eq56_equivalent_evals_per_s": rhs_per_step * ne * c["eq56"] / (ms_step * 1e-3),
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "rhs2_kernel (K2, flux differencing)",
-                     "kernel_ms_avg": k2_avg_ms, "kernel_share_of_step": k2_ms / args.steps / ms_step,
+        "roofline": {"bound": k["bound"], "achieved": k["achieved"], "peak": k["peak"], "unit": k["unit"],
+                     "frac": k["frac"], "traffic": tpe * units if tpe else None, "kernel": k["kernel"],
+                     "kernel_ms_avg": k["ms_avg"], "kernel_share_of_step": k["share_of_step"],
                      "traffic_source": traffic_src,
-                     "algorithmic_flops_per_element": rhs_kernel_flops(dim, p, c["vol"], c["fac"]),
-                     "projection_kernel_ms_avg": k1_ms / max(k1_n, 1),
-                     "projection_share_of_step": k1_ms / args.steps / ms_step,
-                     "iface_kernel_ms_avg": kf_ms / max(kf_n, 1),
-                     "iface_share_of_step": kf_ms / args.steps / ms_step,
-                     "wadj_kernel_ms_avg": k3_ms / max(k3_n, 1),
-                     "wadj_share_of_step": k3_ms / args.steps / ms_step,
-                     "wadj_tflops": (wadj_kernel_flops(dim, p) * (ne / world) / (k3_ms / max(k3_n, 1) * 1e-3) / 1e12
-                                     if k3_n else None),
-                     "peak_basis": "148 SM x 64 DFMA/clk x 2 x sm_max_mhz (DESIGN.md 5.4)"},
+                     "peak_basis": ("148 SM x 64 DFMA/clk x 2 x sm_max_mhz (DESIGN.md 5.4)" if k["bound"] == "alu"
+                                    else "MEASURED_PEAKS.json hbm_gbs"),
+                     "eager_ms_per_step": eager_ms_step, "kernels": kernels},
         "e2e": {"value": e2e_value, "unit": "flux_evals/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                "api": "cudaMemcpyAsync(pinned->device) + es_set_state + es_step + es_get_state + copy back"},
+                "api": "es_step_host (C ABI): pinned host state -> device, RK4 step, device -> pinned host"},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }

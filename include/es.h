@@ -120,6 +120,16 @@ es_status es_set_state(es_context* ctx, const double* u_modal);
 es_status es_get_state(es_context* ctx, double* u_modal);
 /* nsteps classical RK4 steps of size dt on the library state (R17). */
 es_status es_step(es_context* ctx, double dt, int nsteps);
+
+/* End to end through host buffers (the e2e measurement path): copies u_host (HOST, [n_local][N_c][N_p*],
+ * pinned for an asynchronous copy) into the library state, advances nsteps classical RK4 steps of
+ * size dt (es_step) and copies the state back into u_host_out (HOST).  Synchronous. */
+es_status es_step_host(es_context* ctx, const double* u_host, double* u_host_out, double dt, int nsteps);
+
+/* CUDA graphs for es_step (default on): with world == 1 and no per-kernel timing the launches of one
+ * RK4 step are captured once per dt into a CUDA graph and replayed.  on = 0 launches them eagerly
+ * (the same kernels and arguments: results are bitwise identical). */
+es_status es_set_graphs(es_context* ctx, int on);
 /* One Dormand-Prince 5(4) step of size dt on the library state (Hairer-Norsett-Wanner I, II.5; the
  * paper integrates with DP8 of the same family).  *err = sqrt(mean_i (e_i / (atol + rtol
  * max(|y0_i|, |y5_i|)))^2) over all modal coefficients of all ranks, e = y5 - y4 the embedded
@@ -142,6 +152,17 @@ es_status es_entropy_production(es_context* ctx, const double* u_modal, double* 
 es_status es_flux_counts(const es_context* ctx, int64_t* volume_pairs_per_el,
                          int64_t* facet_pairs_per_el, int64_t* eq56_per_el,
                          double* interface_per_el);
+
+/* Flux evaluations COUNTED IN THE KERNELS (P:563-567 Eq. num_fluxes; BASELINE north_star "integer
+ * counts must match exactly"): runs one RHS on u_modal (device) with the counting instantiation of
+ * the flux kernel (same arithmetic, per-element counters) and writes counts[n_local][4] (HOST):
+ *   [0] volume two-point flux evaluations with a nonzero operator coefficient (line-wise pairs, or
+ *       per-operator evaluations with volume_mode 1),
+ *   [1] facet-correction evaluations (nonzeros of R^T B),
+ *   [2] every evaluation the kernel's lanes issued, masked jobs included (idle-lane diagnostic),
+ *   [3] interface flux evaluations (one per facet node of the element; both sides of a face count).
+ * Synchronous.  volume_mode 2 (brute force) is not instrumented: ES_ERR_CONFIG. */
+es_status es_count_fluxes(es_context* ctx, const double* u_modal, int64_t* counts);
 
 /* Physical coordinates of the volume quadrature nodes, device pointer [n_local][N_q][dim]. */
 es_status es_node_coords(es_context* ctx, double* x_dev);

@@ -67,6 +67,9 @@ es_step_dp54 = _sig("es_step_dp54", _i, _vp, ctypes.c_double, ctypes.c_double, c
                     ctypes.POINTER(_i))
 es_entropy_production = _sig("es_entropy_production", _i, _vp, _vp, _dp, _dp, _dp)
 es_flux_counts = _sig("es_flux_counts", _i, _vp, _lp, _lp, _lp, _dp)
+es_count_fluxes = _sig("es_count_fluxes", _i, _vp, _vp, _lp)
+es_step_host = _sig("es_step_host", _i, _vp, _vp, _vp, ctypes.c_double, _i)
+es_set_graphs = _sig("es_set_graphs", _i, _vp, _i)
 es_node_coords = _sig("es_node_coords", _i, _vp, _vp)
 es_project_nodal = _sig("es_project_nodal", _i, _vp, _vp, _vp)
 es_eval_nodal = _sig("es_eval_nodal", _i, _vp, _vp, _vp)
@@ -281,6 +284,20 @@ class Context:
         i = ctypes.c_double()
         self._check(es_flux_counts(self.h, ctypes.byref(v), ctypes.byref(f), ctypes.byref(e), ctypes.byref(i)))
         return dict(volume=v.value, facet=f.value, eq56=e.value, interface=i.value)
+
+    def step_host(self, u_host_in, u_host_out, dt, nsteps=1):
+        """es_step_host: host state in -> nsteps RK4 steps -> host state out (synchronous)"""
+        self._check(es_step_host(self.h, _ptr(u_host_in), _ptr(u_host_out), dt, nsteps))
+
+    def set_graphs(self, on=True):
+        self._check(es_set_graphs(self.h, 1 if on else 0))
+
+    def count_fluxes(self, u):
+        """flux evaluations counted in the kernels on one RHS of u (device tensor): int64 array
+        [n_local][4] = volume, facet correction, issued (masked included), interface (es_count_fluxes)"""
+        out = np.zeros((self.nloc, 4), np.int64)
+        self._check(es_count_fluxes(self.h, _ptr(u), out.ctypes.data_as(_lp)))
+        return out
 
     def node_coords(self, x):
         self._check(es_node_coords(self.h, _ptr(x)))

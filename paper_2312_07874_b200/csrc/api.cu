@@ -29,6 +29,8 @@ cudaError_t launch_projnodal_3d(int n, const DevRef& R, int64_t ne, const double
 cudaError_t launch_evalnodal_2d(int n, const DevRef& R, int64_t ne, const double* um, double* un, cudaStream_t st);
 cudaError_t launch_evalnodal_3d(int n, const DevRef& R, int64_t ne, const double* um, double* un, cudaStream_t st);
 cudaError_t upload_psi_3d(int n, const double* p1, const double* p2, const double* p3);
+cudaError_t launch_rhs_count_2d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
+cudaError_t launch_rhs_count_3d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
 cudaError_t launch_wadj_3d(int n, const WadjArgs& A, cudaStream_t st);
 cudaError_t launch_wjinv_permute_3d(int n, const double* geo_vol, int gvs, int row, int64_t ne, double* out,
                                     cudaStream_t st);
@@ -58,6 +60,13 @@ struct es_context {
   double *geo_vol = nullptr, *geo_face = nullptr, *xq = nullptr, *jt = nullptr;
   double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr, *fstar = nullptr;
   double *rbuf = nullptr, *wjk3 = nullptr;  // 3D: nodal residual for K3, W / J~ in K3's layout
+  unsigned long long* dcounts = nullptr;    // es_count_fluxes: per-element flux-evaluation counters
+  bool counting = false;
+  // CUDA graph of one classical RK4 step (4 right-hand sides, 12-16 launches) replayed by es_step
+  cudaGraphExec_t step_graph = nullptr;
+  double step_graph_dt = 0.0;
+  int64_t step_graph_launches = 0;
+  bool use_graphs = true;
   int num_sms = 148, proj_ctas = 296;
   bool external = false;
   int eq56 = 0;   // volume_mode 1: per-operator fluxes (Eq. num_fluxes ablation)
@@ -188,7 +197,11 @@ cudaError_t run_rhs(es_context* c, RhsArgs A, int64_t n, const int64_t* list) {
     cudaEventRecord(te.a, c->stream);
   }
   c->launches++;
-  cudaError_t e = c->d == 2 ? launch_rhs_2d(c->n, c->R, A, c->stream) : launch_rhs_3d(c->n, c->R, A, c->stream);
+  if (c->counting) A.counts = c->dcounts;
+  cudaError_t e = c->counting ? (c->d == 2 ? launch_rhs_count_2d(c->n, c->R, A, c->stream)
+                                           : launch_rhs_count_3d(c->n, c->R, A, c->stream))
+                              : (c->d == 2 ? launch_rhs_2d(c->n, c->R, A, c->stream)
+                                           : launch_rhs_3d(c->n, c->R, A, c->stream));
   if (c->timing) {
     cudaEventRecord(te.b, c->stream);
     c->tev.push_back(te);
@@ -212,7 +225,8 @@ cudaError_t run_rhs(es_context* c, RhsArgs A, int64_t n, const int64_t* list) {
 
 cudaError_t run_iface(es_context* c, int64_t n, const int64_t* list) {
   if (n <= 0) return cudaSuccess;
-  IfaceArgs I{n, list, c->trace, c->geo_face, c->face_slot, c->face_reflect, c->fstar, c->gamma, c->es};
+  IfaceArgs I{n, list, c->trace, c->geo_face, c->face_slot, c->face_reflect, c->fstar, c->gamma, c->es,
+              c->counting ? c->dcounts : nullptr};
   TimedEvent te{};
   if (c->timing) {
     te = {get_event(c), get_event(c), 2};
@@ -335,7 +349,7 @@ void es_destroy(es_context* c) {
                   (void*)c->face_reflect, (void*)c->bad, (void*)c->U, (void*)c->ACC, (void*)c->US,
                   (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg, (void*)c->fstar,
                   (void*)c->dpy, (void*)c->dppart, (void*)c->sdense, (void*)c->rbdense, (void*)c->rbuf,
-                  (void*)c->wjk3})
+                  (void*)c->wjk3, (void*)c->dcounts})
     if (p) cudaFree(p);
   for (double* p : c->dpk)
     if (p) cudaFree(p);
@@ -346,6 +360,7 @@ void es_destroy(es_context* c) {
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev_packed) cudaEventDestroy(c->ev_packed);
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+  if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -592,24 +607,85 @@ es_status es_get_state(es_context* c, double* u) {
   return ES_OK;
 }
 
+namespace {
+// one classical RK4 step (R17): four right-hand sides, the stage update fused in the epilogue
+es_status rk4_step_launches(es_context* c, double dt) {
+  for (int s = 0; s < 4; ++s) {
+    RhsArgs A = base_rhs_args(c);
+    A.mode = 1 + s;
+    A.dt = dt;
+    A.u0 = c->U;
+    A.acc = c->ACC;
+    A.ustage = c->US;
+    A.out = c->U;
+    es_status r = rhs_pass(c, s == 0 ? c->U : c->US, A, nullptr);
+    if (r != ES_OK) return r;
+  }
+  return ES_OK;
+}
+}  // namespace
+
 es_status es_step(es_context* c, double dt, int nsteps) {
   POISON_CHECK();
   c->dp_fsal = false;
   CK(cudaSetDevice(c->device));
-  for (int st = 0; st < nsteps; ++st) {
-    for (int s = 0; s < 4; ++s) {  // classical RK4 (R17), stage update fused in the RHS epilogue
-      RhsArgs A = base_rhs_args(c);
-      A.mode = 1 + s;
-      A.dt = dt;
-      A.u0 = c->U;
-      A.acc = c->ACC;
-      A.ustage = c->US;
-      A.out = c->U;
-      es_status r = rhs_pass(c, s == 0 ? c->U : c->US, A, nullptr);
+  // single rank, no per-kernel timing: the step's launches are captured once into a CUDA graph (per
+  // dt, a kernel argument) and replayed -- small meshes are launch-latency bound
+  const bool graph = c->use_graphs && c->world == 1 && !c->timing && !c->dbg && nsteps > 0;
+  if (graph) {
+    if (!c->step_graph || c->step_graph_dt != dt) {
+      if (c->step_graph) {
+        CK(cudaGraphExecDestroy(c->step_graph));
+        c->step_graph = nullptr;
+      }
+      cudaGraph_t g = nullptr;
+      const int64_t l0 = c->launches;
+      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+      es_status r = rk4_step_launches(c, dt);
+      cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+      if (r != ES_OK) {
+        if (g) cudaGraphDestroy(g);
+        return r;
+      }
+      CK(ce);
+      ce = cudaGraphInstantiate(&c->step_graph, g, 0);
+      cudaGraphDestroy(g);
+      CK(ce);
+      c->step_graph_dt = dt;
+      c->step_graph_launches = c->launches - l0;
+      c->launches = l0;
+    }
+    for (int st = 0; st < nsteps; ++st) {
+      CK(cudaGraphLaunch(c->step_graph, c->stream));
+      c->launches += c->step_graph_launches;
+    }
+  } else {
+    for (int st = 0; st < nsteps; ++st) {
+      es_status r = rk4_step_launches(c, dt);
       if (r != ES_OK) return r;
     }
   }
   if (c->check_adm) return check_bad(c);
+  return ES_OK;
+}
+
+es_status es_step_host(es_context* c, const double* u_host, double* u_host_out, double dt, int nsteps) {
+  POISON_CHECK();
+  if (!u_host || !u_host_out) return fail(c, ES_ERR_ARG, "null buffer");
+  CK(cudaSetDevice(c->device));
+  const size_t bytes = (size_t)c->nloc * c->NC * c->Np * sizeof(double);
+  CK(cudaMemcpyAsync(c->U, u_host, bytes, cudaMemcpyHostToDevice, c->stream));
+  c->dp_fsal = false;
+  es_status s = es_step(c, dt, nsteps);
+  if (s != ES_OK) return s;
+  CK(cudaMemcpyAsync(u_host_out, c->U, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return ES_OK;
+}
+
+es_status es_set_graphs(es_context* c, int on) {
+  POISON_CHECK();
+  c->use_graphs = on != 0;
   return ES_OK;
 }
 
@@ -741,6 +817,28 @@ es_status es_flux_counts(const es_context* c, int64_t* vol, int64_t* fac, int64_
     if (eq56) *eq56 = 4 * n * n * n * n;
     if (iface) *iface = 4.0 * n * n;
   }
+  return ES_OK;
+}
+
+es_status es_count_fluxes(es_context* c, const double* u, int64_t* counts) {
+  POISON_CHECK();
+  if (!u || !counts) return fail(c, ES_ERR_ARG, "null buffer");
+  if (c->dense) return fail(c, ES_ERR_CONFIG, "es_count_fluxes: volume_mode 2 is not instrumented");
+  CK(cudaSetDevice(c->device));
+  const size_t nb = (size_t)c->nloc * 4 * sizeof(unsigned long long);
+  if (!c->dcounts) CK(cudaMalloc((void**)&c->dcounts, nb));
+  CK(cudaMemsetAsync(c->dcounts, 0, nb, c->stream));
+  RhsArgs A = base_rhs_args(c);
+  A.mode = 0;
+  A.out = c->ACC;  // scratch: the RK accumulator is free between steps
+  c->counting = true;
+  es_status s = rhs_pass(c, u, A, nullptr);
+  c->counting = false;
+  if (s != ES_OK) return s;
+  std::vector<unsigned long long> h((size_t)c->nloc * 4);
+  CK(cudaMemcpyAsync(h.data(), c->dcounts, nb, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (size_t k = 0; k < h.size(); ++k) counts[k] = (int64_t)h[k];
   return ES_OK;
 }
 

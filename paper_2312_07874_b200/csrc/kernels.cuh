@@ -87,6 +87,7 @@ struct RhsArgs {
   const double* rbdense;      // volume_mode 2: dense (R^(z)T B) [z][f][i]
   const double* nhat;         // [Nf][3] reference outward normals
   double* rbuf;               // 3D: nodal residual [nloc][NC][N(b)][N(a)][N(c)] for the batched K3
+  unsigned long long* counts; // counting launch: [nloc][4] volume / facet-correction / issued flux evaluations
 };
 
 struct IfaceArgs {
@@ -99,6 +100,7 @@ struct IfaceArgs {
   double* fstar;              // [nloc][Nf][NC][Nqf]
   double gamma;
   int es;
+  unsigned long long* counts; // counting launch: [nloc][4], slot 3 = interface flux evaluations
 };
 
 // ------------------------------------------------------------------------------------------------

@@ -261,7 +261,7 @@ template <int DIM, int N>
 __device__ __forceinline__ void k2_epilogue_2d(const RhsArgs& A, int64_t e, unsigned it);
 
 // one element of the flux kernel (the body of the persistent loop)
-template <int DIM, int N, bool EQ, bool DN = false>
+template <int DIM, int N, bool EQ, bool DN = false, bool CNT = false>
 __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsigned it) {
   using S = Sz<DIM, N>;
   using W = Lw<DIM, N>;
@@ -351,6 +351,10 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   };
   auto Gat = [&](int l, int m, int i) { return sG[(l * DIM + m) * Nq + i]; };
 
+  // flux-evaluation counters of the counting instantiation (CNT): evaluations with a nonzero operator
+  // coefficient in the volume (cv) and facet-correction (cf) passes, and every evaluation the lane
+  // issued, masked or not (ci) -- observed in the kernel, compared with the oracle's counted loops
+  int cv = 0, cf = 0, ci = 0;
   // ---- direction passes, one specialisation per direction k ----
   // DST: 0 = sR = acc (first pass), 1 = sR += acc, 2 = pt = acc (the pt buffer holds a second
   // residual so that two passes can run without a barrier between them); SYNC: end with a barrier
@@ -418,6 +422,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           jb.idx = j;
           const bool half = (N % 2 == 0) && (s == NS);
           const double mk = (s <= NS && !(half && pos >= N / 2)) ? vmask : 0.0;
+          if constexpr (CNT) cv += (mk != 0.0) ? NLOP : 0;
           // term l of n_ij = sum_l c A (g_i^(l) + g_j^(l)) goes to slot min(l', NLOP - 1)
           auto put = [&](int slot, int m, double val) {
             if (EQ56)
@@ -476,6 +481,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
             for (int m = 0; m < DIM; ++m) jv[t].n[m] = nl[t][op][m];
           double Fo[W::VB][NC];
           flux_batch<DIM, W::VB, CHK>(me, jv, gm1inv, Fo);
+          if constexpr (CNT) ci += W::VB;
 #pragma unroll
           for (int t = 0; t < W::VB; ++t)
 #pragma unroll
@@ -549,6 +555,10 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           fjob(jf[1], 2, cb, tlL[ca] * tB[2 * Nqf + cb], gtn3);
           double Fc[2][NC];
           flux_batch<DIM, 2, CHK>(me, jf, gm1inv, Fc);
+          if constexpr (CNT) {
+            ci += 2;
+            cf += valid ? 2 : 0;
+          }
           line_sums(Fc[0], [&](int Lq, int v) { return fS + (1 * NC + v) * Nqf + Lq; });
           line_sums(Fc[1], [&](int Lq, int v) { return fS + (2 * NC + v) * Nqf + Lq; });
         } else {  // eta2 = -1 (facet 1): facet node a
@@ -556,6 +566,10 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           fjob(jf[0], 0, ca, tlL[cb] * tB[0 * Nqf + ca], gtn);
           double Fc[1][NC];
           flux_batch<DIM, 1, CHK>(me, jf, gm1inv, Fc);
+          if constexpr (CNT) {
+            ci += 1;
+            cf += valid ? 1 : 0;
+          }
           line_sums(Fc[0], [&](int Lq, int v) { return fS + (0 * NC + v) * Nqf + Lq; });
         }
       } else {
@@ -573,6 +587,10 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           fjob(jf[1], 2, f, tlL[ca] * tB[2 * Nqf + f], gtn3);
           double Fc[2][NC];
           flux_batch<DIM, 2, CHK>(me, jf, gm1inv, Fc);
+          if constexpr (CNT) {
+            ci += 2;
+            cf += valid ? 2 : 0;
+          }
           line_sums(Fc[0], [&](int Lq, int v) { return fS + (1 * NC + v) * Nqf + Lq; });
           line_sums(Fc[1], [&](int Lq, int v) { return fS + (2 * NC + v) * Nqf + Lq; });
         } else if (k == 1) {  // facet 1 (eta2 = -1): node (a, c) = line; facet 4 (eta3 = -1): nodes (a, j)
@@ -584,6 +602,10 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
             fjob(j1[0], 0, f, tlL[cb] * tB[0 * Nqf + f], gtn);
             double F1[1][NC];
             flux_batch<DIM, 1, CHK>(me, j1, gm1inv, F1);
+            if constexpr (CNT) {
+              ci += 1;
+              cf += valid ? 1 : 0;
+            }
             line_sums(F1[0], [&](int Lq, int v) { return fS + (0 * NC + v) * Nqf + Lq; });
           }
           // facet 4, rotating schedule: at step t lane pos pairs its node (a, b = pos, c) with the
@@ -606,6 +628,10 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
             }
             double Fb[B][NC];
             flux_batch<DIM, B, CHK>(me, jq, gm1inv, Fb);
+            if constexpr (CNT) {
+              ci += B;
+              cf += valid ? B : 0;
+            }
 #pragma unroll
             for (int tt = 0; tt < B; ++tt) {
               int p0 = pos - (t0 + tt);
@@ -781,6 +807,16 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     else
       passes(std::false_type{}, std::integral_constant<bool, EQ>{});
   }
+  if constexpr (CNT) {  // per-element totals: warp sums, one atomic per warp and counter
+    cv = __reduce_add_sync(0xffffffffu, cv);
+    cf = __reduce_add_sync(0xffffffffu, cf);
+    ci = __reduce_add_sync(0xffffffffu, ci);
+    if (lane == 0) {
+      atomicAdd(A.counts + e * 4 + 0, (unsigned long long)cv);
+      atomicAdd(A.counts + e * 4 + 1, (unsigned long long)cf);
+      atomicAdd(A.counts + e * 4 + 2, (unsigned long long)ci);
+    }
+  }
   // states, metrics and facet inputs are dead: the next element's copies land during the epilogue
   if (tid == 0 && has_next) issue_A(elem_of(nidx), (it + 1) & 1);
   stamp(5);
@@ -931,7 +967,7 @@ __device__ __forceinline__ void k2_epilogue_2d(const RhsArgs& A, int64_t e, unsi
   stamp(11);
 }
 
-template <int DIM, int N, bool EQ, bool DN = false>
+template <int DIM, int N, bool EQ, bool DN = false, bool CNT = false>
 __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   using S = Sz<DIM, N>;
   using W = Lw<DIM, N>;
@@ -1015,7 +1051,7 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   __syncthreads();  // mbarriers initialised and tables staged before anyone uses them
 
 #pragma unroll 1
-  for (int64_t idx = blockIdx.x, it = 0; idx < A.n_elem; idx += gridDim.x, ++it) k2_element<DIM, N, EQ, DN>(A, idx, (unsigned)it);
+  for (int64_t idx = blockIdx.x, it = 0; idx < A.n_elem; idx += gridDim.x, ++it) k2_element<DIM, N, EQ, DN, CNT>(A, idx, (unsigned)it);
 }
 
 // resident CTAs per SM the register budget is sized for: about 18 warps per SM where shared memory
@@ -1031,6 +1067,15 @@ __host__ __device__ constexpr int k2_min_blocks() {
 template <int DIM, int N>
 __global__ void __launch_bounds__(Lw<DIM, N>::NT, k2_min_blocks<DIM, N>()) rhs2_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
   rhs2_body<DIM, N, false>(R, A);
+}
+// counting instantiation (es_count_fluxes): the production kernel with per-element flux counters
+template <int DIM, int N>
+__global__ void __launch_bounds__(Lw<DIM, N>::NT, k2_min_blocks<DIM, N>()) rhs2_count_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
+  rhs2_body<DIM, N, false, false, true>(R, A);
+}
+template <int DIM, int N>
+__global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_eq56_count_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
+  rhs2_body<DIM, N, true, false, true>(R, A);
 }
 // ablation: the paper's Eq. num_fluxes per-operator fluxes (es_options.volume_mode = 1)
 template <int DIM, int N>
@@ -1186,6 +1231,7 @@ __global__ void __launch_bounds__(256, 4) iface_kernel(DevRef R, IfaceArgs A) {
 #pragma unroll
     for (int v = 0; v < NC; ++v) F[v] -= sc * D[v];
   }
+  if (A.counts) atomicAdd(A.counts + e * 4 + 3, 1ull);  // counting launch only (es_count_fluxes)
   const double bj = __ldg(&R.Bf[fz]) * Jf;
   double* out = A.fstar + (size_t)(e * Nf + z) * NC * Nqf + f;
 #pragma unroll

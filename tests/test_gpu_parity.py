@@ -119,9 +119,24 @@ def test_rhs_parity(es, d, M, p, warp, ic, fm):
     ref, st = om.rhs(u, flux_mode=fm, variant=1)
     err = _relerr(got, ref)
     assert (err <= TOL).all(), err
+    _check_counts(ctx, om, u, st, st0)
+
+
+def _check_counts(ctx, om, u, st, st0=None):
+    # flux evaluations COUNTED IN THE KERNELS (es_count_fluxes), per element, against the pairs the
+    # oracle's loops counted (R22): exact integers, identical for every element
+    cnt = ctx.count_fluxes(torch.from_numpy(u).cuda())
+    ne = om.ne
+    assert (cnt[:, 0] == cnt[0, 0]).all() and (cnt[:, 1] == cnt[0, 1]).all()
+    assert cnt[:, 0].sum() == st.volume_pairs, (cnt[0], st.volume_pairs / ne)
+    assert cnt[:, 1].sum() == st.facet_pairs, (cnt[0], st.facet_pairs / ne)
+    assert cnt[:, 3].sum() == st.interface_evals, (cnt[0], st.interface_evals / ne)
+    assert (cnt[:, 2] >= cnt[:, 0] + cnt[:, 1]).all()  # issued includes masked jobs
+    # the closed forms the library reports agree with what the kernel did
     c = ctx.flux_counts()
-    assert c["volume"] * om.ne == st.volume_pairs
-    assert c["facet"] * om.ne == st.facet_pairs
+    assert c["volume"] == cnt[0, 0] and c["facet"] == cnt[0, 1]
+    if st0 is not None:  # the paper's Eq. num_fluxes count from the oracle's variant 0
+        assert c["eq56"] * ne == st0.volume_pairs + st0.facet_pairs
 
 
 def test_free_stream_gpu(es):
@@ -232,6 +247,31 @@ def test_dp54_step_parity(es, d, p):
         assert (inc < 1e-10).all(), inc
 
 
+@pytest.mark.parametrize("d,p", [(2, 2), (3, 3)])
+def test_graph_step_bitwise_equals_eager(es, d, p):
+    # es_step replays a captured CUDA graph on one rank: bitwise the eager launches, also over two
+    # dt values (re-capture); es_step_host (host buffers in and out) gives the same state
+    mesh, om, ctx, u = _setup(es, d, 3, p, "paper", "wave" if d == 2 else "tgv3", 1)
+    ut = torch.from_numpy(u).cuda()
+    out = []
+    for graphs in (True, False):
+        ctx.set_graphs(graphs)
+        ctx.set_state(ut)
+        ctx.step(1e-3, 3)
+        ctx.step(5e-4, 2)
+        o = torch.empty_like(ut)
+        ctx.get_state(o)
+        ctx.synchronize()
+        out.append(o.cpu().numpy())
+    assert np.array_equal(out[0], out[1])
+    ctx.set_graphs(True)
+    hin = torch.from_numpy(u).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    ctx.step_host(hin, hout, 1e-3, 3)
+    ctx.step_host(hout.clone().pin_memory(), hout, 5e-4, 2)
+    assert np.array_equal(hout.numpy(), out[0])
+
+
 def test_dp54_adaptive_density_wave(es):
     # adaptive DP5(4) over the density wave: reaches T; the solution matches a fine RK4 run
     mesh, om, ctx, u = _setup(es, 2, 4, 3, "paper", "wave", 1)
@@ -331,8 +371,10 @@ def test_eq56_ablation_parity(es, d, M, p, warp, ic, fm):
     got = _gpu_rhs(ctx, u)
     assert (_relerr(got, ref) <= TOL).all()
     c = ctx.flux_counts()
-    assert (c["volume"] + c["facet"]) * om.ne == st.volume_pairs + st.facet_pairs  # Eq. 56 count
     assert c["volume"] + c["facet"] == c["eq56"]
+    # kernel-counted per-operator evaluations = the Eq. 56 nonzero loops of the oracle
+    cnt = ctx.count_fluxes(torch.from_numpy(u).cuda())
+    assert cnt[:, 0].sum() == st.volume_pairs and cnt[:, 1].sum() == st.facet_pairs, (cnt[0], st.volume_pairs / om.ne)
 
 
 @pytest.mark.parametrize("d,M,p,warp,ic,fm", [(2, 3, 3, "paper", "wave", 1), (3, 3, 2, "paper", "tgv3", 1),

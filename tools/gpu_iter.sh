@@ -18,10 +18,9 @@ for C in ${@:-C5}; do
 import json
 try:
     d = json.load(open("gpurun_out/${TAG}_bench_${C}.json"))
-    r = d["roofline"]
-    print("$C", "ms/step %.2f" % d["ms_per_step"], "value %.3e" % d["value"], "K2 %.2f ms frac %.3f" % (r["kernel_ms_avg"], r["frac"]),
-          "K1 %.2f ms" % r["projection_kernel_ms_avg"], "iface %.2f ms" % r["iface_kernel_ms_avg"],
-          "K3 %.2f ms %s TF" % (r.get("wadj_kernel_ms_avg", 0), r.get("wadj_tflops")))
+    r = d["roofline"]; k = r["kernels"]
+    print("$C", "ms/step %.2f" % d["ms_per_step"], "eager %.2f" % r["eager_ms_per_step"], "value %.3e" % d["value"],
+          " ".join("%s %.2f ms %.3f" % (n, v["ms_avg"], v["frac"]) for n, v in k.items()), "e2e %.3e" % d["e2e"]["value"])
 except Exception as ex:
     print("bench parse failed", ex); print(open("gpurun_out/${TAG}_bench_${C}.err").read()[-2000:])
 PY
