@@ -164,6 +164,20 @@ es_status es_flux_counts(const es_context* ctx, int64_t* volume_pairs_per_el,
  * Synchronous.  volume_mode 2 (brute force) is not instrumented: ES_ERR_CONFIG. */
 es_status es_count_fluxes(es_context* ctx, const double* u_modal, int64_t* counts);
 
+/* Loopback groups (one-GPU emulation of world > 1, tests): ctxs[r] (r = 0..n-1) are the n ranks of one
+ * mesh, each created with world = n, rank = r and nccl_unique_id = NULL, on one device in this process.
+ * These calls run the complete multi-rank path of es_rhs / es_step / es_entropy_production -- K1, pack
+ * of the boundary traces, interior-element interface fluxes overlapping the exchange, the wait, the
+ * boundary-element interface fluxes, flux kernel, K3 -- with the NCCL send/recv replaced by one
+ * cudaMemcpyAsync per (receiver, sender) pair on the receiver's communication stream, ordered after
+ * the sender's pack by an event, and the allreduce by a host sum over ranks.  u[r] / dudt[r]: device
+ * pointers of rank r's local block.  es_group_step advances every rank's library state (es_set_state).
+ * Asynchronous except es_group_entropy_production (synchronous). */
+es_status es_group_rhs(es_context** ctxs, int n, const double* const* u, double* const* dudt);
+es_status es_group_step(es_context** ctxs, int n, double dt, int nsteps);
+es_status es_group_entropy_production(es_context** ctxs, int n, const double* const* u, double* rate,
+                                      double* abs_scale, double* conservation);
+
 /* Physical coordinates of the volume quadrature nodes, device pointer [n_local][N_q][dim]. */
 es_status es_node_coords(es_context* ctx, double* x_dev);
 /* Reference L2 projection u~ = V^T W u (M = I): u_nodal device [n_local][N_q][N_c] ->

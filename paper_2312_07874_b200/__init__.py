@@ -70,6 +70,10 @@ es_flux_counts = _sig("es_flux_counts", _i, _vp, _lp, _lp, _lp, _dp)
 es_count_fluxes = _sig("es_count_fluxes", _i, _vp, _vp, _lp)
 es_step_host = _sig("es_step_host", _i, _vp, _vp, _vp, ctypes.c_double, _i)
 es_set_graphs = _sig("es_set_graphs", _i, _vp, _i)
+es_group_rhs = _sig("es_group_rhs", _i, ctypes.POINTER(_vp), _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp))
+es_group_step = _sig("es_group_step", _i, ctypes.POINTER(_vp), _i, ctypes.c_double, _i)
+es_group_entropy_production = _sig("es_group_entropy_production", _i, ctypes.POINTER(_vp), _i, ctypes.POINTER(_vp),
+                                   _dp, _dp, _dp)
 es_node_coords = _sig("es_node_coords", _i, _vp, _vp)
 es_project_nodal = _sig("es_project_nodal", _i, _vp, _vp, _vp)
 es_eval_nodal = _sig("es_eval_nodal", _i, _vp, _vp, _vp)
@@ -158,6 +162,40 @@ def dp54_controller(step, T, dt0, rtol, atol, max_steps=1000000, safety=0.9, fac
             after_reject = True
         dt = h * fac
     return nacc, nrej, dt
+
+
+def _group(ctxs):
+    arr = (_vp * len(ctxs))(*[c.h.value if hasattr(c.h, "value") else c.h for c in ctxs])
+    return arr, len(ctxs)
+
+
+def _ptrs(ts):
+    return (_vp * len(ts))(*[_ptr(t).value for t in ts])
+
+
+def group_rhs(ctxs, us, dudts):
+    """es_group_rhs: the loopback multi-rank RHS of contexts ranks 0..n-1 (one device, no NCCL)"""
+    g, n = _group(ctxs)
+    rc = es_group_rhs(g, n, _ptrs(us), _ptrs(dudts))
+    if rc != ES_OK:
+        raise ESError(rc, es_last_error(ctxs[0].h).decode())
+
+
+def group_step(ctxs, dt, nsteps=1):
+    g, n = _group(ctxs)
+    rc = es_group_step(g, n, float(dt), int(nsteps))
+    if rc != ES_OK:
+        raise ESError(rc, es_last_error(ctxs[0].h).decode())
+
+
+def group_entropy_production(ctxs, us):
+    g, n = _group(ctxs)
+    rate, sc = ctypes.c_double(), ctypes.c_double()
+    cons = np.zeros(ctxs[0].d + 2)
+    rc = es_group_entropy_production(g, n, _ptrs(us), ctypes.byref(rate), ctypes.byref(sc), cons.ctypes.data_as(_dp))
+    if rc != ES_OK:
+        raise ESError(rc, es_last_error(ctxs[0].h).decode())
+    return rate.value, sc.value, cons
 
 
 class ESError(RuntimeError):

@@ -292,16 +292,24 @@ es_status rhs_second(es_context* c, RhsArgs A) {
   return ES_OK;
 }
 
-// one right-hand side: projection, halo exchange overlapped with the interface fluxes of interior
-// elements, then the boundary elements' interface fluxes and the flux kernel
-es_status rhs_pass(es_context* c, const double* u, RhsArgs A, double* wt) {
-  if (c->external) return fail(c, ES_ERR_CONFIG, "world > 1 without NCCL: use es_rhs_stage1 / es_rhs_stage2");
+// One right-hand side in three phases; with world > 1:
+//   (a) projection K1 on all local elements, pack of the boundary traces, the communication stream
+//       waits for the pack;
+//   (b) the halo exchange on the communication stream: NCCL grouped send/recv (rhs_phase_b_nccl), or
+//       for a group of contexts in one process on one device one cudaMemcpyAsync per (receiver,
+//       sender) pair (rhs_phase_b_loopback, es_group_*);
+//   (c) interface fluxes of elements without remote neighbours (overlapping the exchange), wait for
+//       the exchange, interface fluxes of the boundary elements, flux kernel (+ K3 in 3D).
+es_status rhs_phase_a(es_context* c, const double* u, double* wt) {
   es_status s0 = rhs_first(c, u, wt);
-  if (s0 != ES_OK) return s0;
-  if (c->world == 1) return rhs_second(c, A);
-  const int per_face = c->NC * c->Nqf;
+  if (s0 != ES_OK || c->world == 1) return s0;
   CK(cudaEventRecord(c->ev_packed, c->stream));
   CK(cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
+  return ES_OK;
+}
+
+es_status rhs_phase_b_nccl(es_context* c) {
+  const int per_face = c->NC * c->Nqf;
   NK(ncclGroupStart());
   for (int r = 0; r < c->world; ++r) {
     if (r == c->rank) continue;
@@ -314,12 +322,42 @@ es_status rhs_pass(es_context* c, const double* u, RhsArgs A, double* wt) {
   }
   NK(ncclGroupEnd());
   CK(cudaEventRecord(c->ev_comm, c->comm_stream));
+  return ES_OK;
+}
+
+// loopback transport: the receiver copies each sender's packed block (after the sender's pack)
+es_status rhs_phase_b_loopback(es_context* c, es_context* const* group) {
+  const int per_face = c->NC * c->Nqf;
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank || c->plan.recv_count[r] == 0) continue;
+    es_context* s = group[r];
+    CK(cudaStreamWaitEvent(c->comm_stream, s->ev_packed, 0));
+    CK(cudaMemcpyAsync(c->trace + (c->nloc * c->Nf + c->plan.recv_offset[r]) * per_face,
+                       s->send_buf + s->plan.send_offset[c->rank] * per_face,
+                       (size_t)c->plan.recv_count[r] * per_face * sizeof(double), cudaMemcpyDeviceToDevice,
+                       c->comm_stream));
+  }
+  CK(cudaEventRecord(c->ev_comm, c->comm_stream));
+  return ES_OK;
+}
+
+es_status rhs_phase_c(es_context* c, RhsArgs A) {
+  if (c->world == 1) return rhs_second(c, A);
   // interface fluxes of elements without remote neighbours overlap the exchange
   CK(run_iface(c, (int64_t)c->plan.interior.size(), c->d_interior));
   CK(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
   CK(run_iface(c, (int64_t)c->plan.boundary.size(), c->d_boundary));
   CK(run_rhs(c, A, c->nloc, nullptr));
   return ES_OK;
+}
+
+// one right-hand side of one context (NCCL transport when world > 1)
+es_status rhs_pass(es_context* c, const double* u, RhsArgs A, double* wt) {
+  if (c->external) return fail(c, ES_ERR_CONFIG, "world > 1 without NCCL: use es_rhs_stage1 / es_rhs_stage2 or es_group_*");
+  es_status s = rhs_phase_a(c, u, wt);
+  if (s != ES_OK) return s;
+  if (c->world > 1 && (s = rhs_phase_b_nccl(c)) != ES_OK) return s;
+  return rhs_phase_c(c, A);
 }
 
 es_status check_bad(es_context* c) {
@@ -979,6 +1017,132 @@ es_status es_rhs_stage2(es_context* c, double* dudt) {
   es_status s = rhs_second(c, A);
   if (s != ES_OK) return s;
   if (c->check_adm) return check_bad(c);
+  return ES_OK;
+}
+
+}  // extern "C"
+namespace {
+// a loopback group: world contexts of one mesh (ranks 0..world-1, each created without an NCCL id)
+// on one device in this process
+es_status group_check(es_context** g, int n) {
+  if (!g || n < 1) return ES_ERR_ARG;
+  for (int r = 0; r < n; ++r) {
+    es_context* c = g[r];
+    if (!c) return ES_ERR_ARG;
+    if (c->poisoned != ES_OK) return c->poisoned;
+    if (c->world != n || c->rank != r || c->device != g[0]->device || c->ne != g[0]->ne || c->p != g[0]->p)
+      return fail(c, ES_ERR_ARG, "es_group_*: contexts must be ranks 0..n-1 of one mesh on one device");
+  }
+  return ES_OK;
+}
+// one RHS of every context of the group with argument builder `args(r)`; the packs of round k wait
+// for every receiver's copies of round k-1 (the send buffers are reused)
+template <class F>
+es_status group_rhs_pass(es_context** g, int n, const double* const* u, F args, double* const* wt) {
+  for (int r = 0; r < n; ++r) {
+    es_context* c = g[r];
+    for (int q = 0; q < n; ++q)
+      if (q != r && n > 1) {
+        cudaError_t e = cudaStreamWaitEvent(c->stream, g[q]->ev_comm, 0);
+        if (e != cudaSuccess) return fail(c, ES_ERR_CUDA, std::string("cudaStreamWaitEvent: ") + cudaGetErrorString(e));
+      }
+    es_status s = rhs_phase_a(c, u[r], wt ? wt[r] : nullptr);
+    if (s != ES_OK) return s;
+  }
+  for (int r = 0; r < n && n > 1; ++r) {
+    es_status s = rhs_phase_b_loopback(g[r], g);
+    if (s != ES_OK) return s;
+  }
+  for (int r = 0; r < n; ++r) {
+    es_status s = rhs_phase_c(g[r], args(r));
+    if (s != ES_OK) return s;
+  }
+  return ES_OK;
+}
+}  // namespace
+extern "C" {
+
+es_status es_group_rhs(es_context** g, int n, const double* const* u, double* const* dudt) {
+  es_status s = group_check(g, n);
+  if (s != ES_OK) return s;
+  if (!u || !dudt) return ES_ERR_ARG;
+  return group_rhs_pass(g, n, u, [&](int r) {
+    RhsArgs A = base_rhs_args(g[r]);
+    A.mode = 0;
+    A.out = dudt[r];
+    return A;
+  }, nullptr);
+}
+
+es_status es_group_step(es_context** g, int n, double dt, int nsteps) {
+  es_status s = group_check(g, n);
+  if (s != ES_OK) return s;
+  std::vector<const double*> u0(n), us(n);
+  for (int r = 0; r < n; ++r) {
+    g[r]->dp_fsal = false;
+    u0[r] = g[r]->U;
+    us[r] = g[r]->US;
+  }
+  for (int st = 0; st < nsteps; ++st)
+    for (int k = 0; k < 4; ++k) {  // classical RK4 (R17), the stage update fused in the epilogue
+      s = group_rhs_pass(g, n, k == 0 ? u0.data() : us.data(), [&](int r) {
+        es_context* c = g[r];
+        RhsArgs A = base_rhs_args(c);
+        A.mode = 1 + k;
+        A.dt = dt;
+        A.u0 = c->U;
+        A.acc = c->ACC;
+        A.ustage = c->US;
+        A.out = c->U;
+        return A;
+      }, nullptr);
+      if (s != ES_OK) return s;
+    }
+  for (int r = 0; r < n; ++r)
+    if (g[r]->check_adm && (s = check_bad(g[r])) != ES_OK) return s;
+  return ES_OK;
+}
+
+es_status es_group_entropy_production(es_context** g, int n, const double* const* u, double* rate, double* abs_scale,
+                                      double* cons) {
+  es_status s = group_check(g, n);
+  if (s != ES_OK) return s;
+  if (!u) return ES_ERR_ARG;
+  std::vector<double*> wts(n);
+  for (int r = 0; r < n; ++r) {
+    es_context* c = g[r];
+    cudaError_t e = cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream);
+    if (e != cudaSuccess) return fail(c, ES_ERR_CUDA, cudaGetErrorString(e));
+    wts[r] = c->wt;
+  }
+  s = group_rhs_pass(g, n, u, [&](int r) {
+    es_context* c = g[r];
+    RhsArgs A = base_rhs_args(c);
+    A.mode = 5;
+    A.out = c->ACC;
+    A.wt = c->wt;
+    A.part = c->part;
+    return A;
+  }, wts.data());
+  if (s != ES_OK) return s;
+  // per-rank deterministic reductions, then the sum over ranks in rank order (the allreduce of
+  // es_entropy_production)
+  double tot[8] = {0};
+  for (int r = 0; r < n; ++r) {
+    es_context* c = g[r];
+    const int w = 2 + c->NC;
+    CK(launch_reduce_parts(c->part, c->nloc, w, c->red, c->stream));
+    c->launches++;
+    double h[8] = {0};
+    CK(cudaMemcpyAsync(h, c->red, w * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < w; ++k) tot[k] += h[k];
+    if ((s = check_bad(c)) != ES_OK) return s;
+  }
+  if (rate) *rate = tot[0];
+  if (abs_scale) *abs_scale = tot[1];
+  if (cons)
+    for (int v = 0; v < g[0]->NC; ++v) cons[v] = tot[2 + v];
   return ES_OK;
 }
 

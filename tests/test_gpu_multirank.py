@@ -98,3 +98,54 @@ def test_external_mode_requires_two_stage(es):
     with pytest.raises(es.ESError) as ex:
         c.rhs(u, torch.empty_like(u))
     assert ex.value.code == es.ES_ERR_CONFIG
+
+
+@pytest.mark.parametrize("d,M,p,world,fm", [(2, 4, 3, 2, 1), (2, 5, 4, 3, 0), (3, 3, 3, 3, 1), (3, 4, 4, 4, 1),
+                                           (3, 3, 8, 2, 1)])
+def test_group_multirank_path_bitwise(es, d, M, p, world, fm):
+    # es_group_*: the library's own world > 1 code path (pack, interior-element interface fluxes
+    # overlapping the exchange on the communication stream, event ordering, boundary-element interface
+    # fluxes, flux kernel, K3, RK4 stages, the reductions) with only the NCCL calls replaced by
+    # device-to-device copies; bitwise equal to one rank
+    L = 2.0 if d == 2 else 2.0 * math.pi
+    mesh = I.split_cartesian(d, M, L)
+    w = I.paper_warp(d, L)
+    om = O.Mesh(mesh, p, warp=w)
+    x = om.node_coords()
+    u0 = I.density_wave(x, L) if d == 2 else I.taylor_green(x, Ma=0.3)
+    u = I.perturb_modal(om.project(u0), d, p, seed=2, amp=1e-2)
+    ut = torch.from_numpy(u).cuda()
+    ctx1 = es.Context(mesh, p, warp=w, interface_flux=fm)
+    ref = torch.empty_like(ut)
+    ctx1.rhs(ut, ref)
+    dt = 1e-3
+    ctx1.set_state(ut)
+    ctx1.step(dt, 3)
+    ref_step = torch.empty_like(ut)
+    ctx1.get_state(ref_step)
+    rate1, sc1, cons1 = ctx1.entropy_production(ut)
+    ctx1.synchronize()
+    ctxs = [es.Context(mesh, p, warp=w, interface_flux=fm, rank=r, world=world, nccl_id=None) for r in range(world)]
+    assert any(len(es.plan(d, mesh["elem_vertices"], r, world)["send_slots"]) for r in range(world))
+    ins = [ut[c.first:c.first + c.nloc].contiguous() for c in ctxs]
+    outs = [torch.empty_like(t) for t in ins]
+    es.group_rhs(ctxs, ins, outs)
+    for c in ctxs:
+        c.synchronize()
+    got = torch.cat(outs).cpu().numpy()
+    assert np.array_equal(got, ref.cpu().numpy())  # bitwise
+    # three RK4 steps on the library states, twice (the send buffers are reused across stages)
+    for c, t in zip(ctxs, ins):
+        c.set_state(t)
+    es.group_step(ctxs, dt, 3)
+    st = []
+    for c, t in zip(ctxs, ins):
+        o = torch.empty_like(t)
+        c.get_state(o)
+        c.synchronize()
+        st.append(o)
+    assert np.array_equal(torch.cat(st).cpu().numpy(), ref_step.cpu().numpy())
+    # entropy production and conservation summed over ranks (the allreduce of es_entropy_production)
+    rate, sc, cons = es.group_entropy_production(ctxs, ins)
+    assert abs(rate - rate1) <= 1e-13 * sc1 and abs(sc - sc1) <= 1e-13 * sc1
+    assert np.abs(cons - cons1).max() <= 1e-13 * max(np.abs(cons1).max(), sc1)

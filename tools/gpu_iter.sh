@@ -13,6 +13,7 @@ elif [ "$K" != "none" ]; then
 fi
 [ -f gpurun_out/${TAG}_pytest_gpu.log ] && tail -15 gpurun_out/${TAG}_pytest_gpu.log
 for C in ${@:-C5}; do
+  [ "$C" == "none" ] && continue
   timeout 600 python bench.py --config $C --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_bench_${C}.json 2> gpurun_out/${TAG}_bench_${C}.err
   echo "bench $C rc=$?"; python - <<PY
 import json
