@@ -32,6 +32,7 @@ cudaError_t upload_psi_3d(int n, const double* p1, const double* p2, const doubl
 cudaError_t launch_rhs_count_2d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
 cudaError_t launch_rhs_count_3d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
 cudaError_t launch_wadj_3d(int n, const WadjArgs& A, cudaStream_t st);
+cudaError_t upload_psi_3d_k1(int n, const double* p1, const double* p2, const double* p3);
 cudaError_t launch_wjinv_permute_3d(int n, const double* geo_vol, int gvs, int row, int64_t ne, double* out,
                                     cudaStream_t st);
 }  // namespace esb
@@ -436,6 +437,14 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   c->Np = c->T.Np;
   c->NC = c->d + 2;
   c->c0 = c->d == 2 ? 1.0 / std::sqrt(2.0) : std::sqrt(0.75);
+  // the even-odd psi1 contractions (psi_const.cuh) need psi1[a1][N-1-a] = (-1)^a1 psi1[a1][a]: the
+  // Legendre nodes are symmetric and psi1^a1 has the parity of a1 (checked to 2 ulp here)
+  for (int a1 = 0; a1 < c->T.n; ++a1)
+    for (int a = 0; a < c->T.n; ++a) {
+      const double x = c->T.psi1[(size_t)a1 * c->T.n + a], y = c->T.psi1[(size_t)a1 * c->T.n + c->T.n - 1 - a];
+      if (std::fabs(x - (a1 % 2 ? -y : y)) > 4.5e-16 * std::fabs(x) + 1e-300)
+        return fail(c, ES_ERR_VERIFY, "psi1 table is not parity-symmetric (even-odd transform form)");
+    }
   c->ne = mesh->n_elements;
   if (c->ne < c->world) return fail(c, ES_ERR_CONFIG, "fewer elements than ranks");
   if (!build_mesh_plan(c->d, c->ne, mesh->elem_vertices, c->rank, c->world, c->plan, err))
@@ -556,6 +565,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
     CK(cudaMalloc((void**)&c->wjk3, (size_t)c->nloc * c->Nq * sizeof(double)));
     CK(launch_wjinv_permute_3d(c->n, c->geo_vol, even_up((NG + 2) * c->Nq), NG + 1, c->nloc, c->wjk3, c->stream));
     CK(upload_psi_3d(c->n, c->T.psi1.data(), c->T.psi2.data(), c->T.psi3.data()));
+    CK(upload_psi_3d_k1(c->n, c->T.psi1.data(), c->T.psi2.data(), c->T.psi3.data()));
     c->launches++;
   }
   if (std::getenv("ES_PHASE_TIMING")) {

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "psi_const.cuh"
+
 namespace esb {
 
 // ------------------------------------------------------------------------------------------------
@@ -425,21 +427,18 @@ __device__ void modal_to_nodal(const PsiS& T, const double* um, double* un, doub
                 nullptr, nullptr, t2 + ((v0 * N + a1) * N + c0) * N, t2 + ((v1 * N + a1) * N + c1) * N, 1, q1 != q0);
     }
     __syncthreads();
-    // u[v][a + N bc] = sum_a1 psi1[a1][a] t2[v][a1][bc]; items of FB (v, bc) fibers H apart
-    constexpr int NFB = NV * N * N, H = (NFB + FB - 1) / FB;
-    for (int it = tid; it < H; it += nt) {
-      const double* in[FB];
-      double* out[FB];
-      int nk = 0;
+    // u[v][a + N bc] = sum_a1 psi1[a1][a] t2[v][a1][bc]: one (v, bc) fibre per item, the psi1 table
+    // from constant memory (uniform operands) in the even-odd form (psi_const.cuh)
+    for (int q = tid; q < NV * N * N; q += nt) {
+      const int v = q / (N * N), bc = q - v * N * N;
+      const double* in = t2 + v * Nq + bc;
+      double x[N], o[N];
 #pragma unroll
-      for (int k = 0; k < FB; ++k) {
-        const int q = it + k * H < NFB ? it + k * H : it;
-        nk += it + k * H < NFB;
-        const int v = q / (N * N), bc = q - v * N * N;
-        in[k] = t2 + v * Nq + bc;
-        out[k] = un + v * Nq + N * bc;
-      }
-      fiberK<N, false, FB>(T.p1, in, N * N, nullptr, out, 1, nk);
+      for (int a1 = 0; a1 < N; ++a1) x[a1] = in[a1 * N * N];
+      psi1_apply_eo<N>(x, o);
+      double* out = un + v * Nq + N * bc;
+#pragma unroll
+      for (int a = 0; a < N; ++a) out[a] = o[a];
     }
     __syncthreads();
   }
@@ -471,23 +470,18 @@ __device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, doubl
     }
     __syncthreads();
   } else {
-    // s2[v][a1][bc] = sum_a psi1[a1][a] y[v][a + N bc]; items of FB (v, bc) fibers H apart
-    constexpr int NFB = NV * N * N, H = (NFB + FB - 1) / FB;
-    for (int it = tid; it < H; it += nt) {
-      const double* in[FB];
-      const double* sc[FB];
-      double* out[FB];
-      int nk = 0;
+    // s2[v][a1][bc] = sum_a psi1[a1][a] y[v][a + N bc] (optional per-node scale): one (v, bc) fibre per
+    // item, constant-memory psi1 in the even-odd form (psi_const.cuh)
+    for (int q = tid; q < NV * N * N; q += nt) {
+      const int v = q / (N * N), bc = q - v * N * N;
+      const double* in = y + v * Nq + N * bc;
+      double x[N], o[N];
 #pragma unroll
-      for (int k = 0; k < FB; ++k) {
-        const int q = it + k * H < NFB ? it + k * H : it;
-        nk += it + k * H < NFB;
-        const int v = q / (N * N), bc = q - v * N * N;
-        in[k] = y + v * Nq + N * bc;
-        sc[k] = scale ? scale + N * bc : nullptr;
-        out[k] = t2 + v * Nq + bc;
-      }
-      fiberK<N, true, FB>(T.p1, in, 1, scale ? sc : nullptr, out, N * N, nk);
+      for (int a = 0; a < N; ++a) x[a] = in[a] * (scale ? scale[N * bc + a] : 1.0);
+      psi1T_apply_eo<N>(x, o);
+      double* out = t2 + v * Nq + bc;
+#pragma unroll
+      for (int a1 = 0; a1 < N; ++a1) out[a1 * N * N] = o[a1];
     }
     __syncthreads();
     // s1[v][pr(a1,a2)][c] = sum_b psi2[a1][a2][b] s2[v][a1][c][b]; items (a1, pair of (v, c) fibers)

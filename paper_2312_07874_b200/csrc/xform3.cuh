@@ -21,17 +21,9 @@
 // so by the flux kernel) and W / J~ [e][b][a][c] (permuted copy made at setup).
 #pragma once
 #include "kernels.cuh"
+#include "psi_const.cuh"
 
 namespace esb {
-
-template <int N>
-struct PsiC {
-  double p1[N * N];      // psi1[a1][a]
-  double p2[N * N * N];  // psi2[a1][a2][b]
-  double p3[N * N * N];  // psi3[s][a3][c]
-};
-template <int N>
-__constant__ PsiC<N> c_psi;
 
 template <int N>
 struct X3 {
@@ -84,52 +76,6 @@ struct WadjArgs {
 
 // ---- mode A: one c-slab, lane = (element, variable, c) ----
 // Fully unrolled: every table read is a compile-time constant-memory operand (uniform registers).
-// even-odd (parity) form of the psi1 contractions: the Legendre nodes are symmetric (eta_{N-1-a} =
-// -eta_a) and psi1^{a1} has the parity of a1, so psi1[a1][N-1-a] = (-1)^{a1} psi1[a1][a] and
-//   u[a] = ue[a] + uo[a], u[N-1-a] = ue[a] - uo[a],  ue = even-a1 sums, uo = odd-a1 sums, a < N/2
-// halves the multiply-adds of the largest sum-factorisation step (checked on the host at setup)
-template <int N>
-__device__ __forceinline__ void psi1_apply_eo(const double* t2, double* u) {  // u[a] = sum_a1 psi1[a1][a] t2[a1]
-  constexpr int H = N / 2, M = N % 2;
-#pragma unroll
-  for (int a = 0; a < H + M; ++a) {
-    double ue = 0.0, uo = 0.0;
-#pragma unroll
-    for (int a1 = 0; a1 < N; a1 += 2) ue = fma(c_psi<N>.p1[a1 * N + a], t2[a1], ue);
-    if (a < H) {
-#pragma unroll
-      for (int a1 = 1; a1 < N; a1 += 2) uo = fma(c_psi<N>.p1[a1 * N + a], t2[a1], uo);
-      u[a] = ue + uo;
-      u[N - 1 - a] = ue - uo;
-    } else {
-      u[a] = ue;  // middle node: the odd functions vanish there
-    }
-  }
-}
-template <int N>
-__device__ __forceinline__ void psi1T_apply_eo(const double* y, double* s2) {  // s2[a1] = sum_a psi1[a1][a] y[a]
-  constexpr int H = N / 2, M = N % 2;
-  double yp[H + M], ym[H > 0 ? H : 1];
-#pragma unroll
-  for (int a = 0; a < H; ++a) {
-    yp[a] = y[a] + y[N - 1 - a];
-    ym[a] = y[a] - y[N - 1 - a];
-  }
-  if (M) yp[H] = y[H];
-#pragma unroll
-  for (int a1 = 0; a1 < N; ++a1) {
-    double t = 0.0;
-    if (a1 % 2 == 0) {
-#pragma unroll
-      for (int a = 0; a < H + M; ++a) t = fma(c_psi<N>.p1[a1 * N + a], yp[a], t);
-    } else {
-#pragma unroll
-      for (int a = 0; a < H; ++a) t = fma(c_psi<N>.p1[a1 * N + a], ym[a], t);
-    }
-    s2[a1] = t;
-  }
-}
-
 // V^T steps 1-2 from the global residual: s1[pr] = sum_b psi2[a1][a2][b] sum_a psi1[a1][a] r[b][a][c]
 template <int N>
 __device__ __forceinline__ void modeA_vt12_global(const double* __restrict__ rr, double* S, bool ok, bool act) {
