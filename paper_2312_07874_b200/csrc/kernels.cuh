@@ -295,6 +295,48 @@ __device__ __forceinline__ void fiber2(const double* ps, int ni, int no, const d
 
 // K fibers per work item (the flattened steps): x_k = in[k][i sin] (* sc[k][i sin]), outputs
 // out[k][o sout] for k < nk; same arithmetic as fiber2 (K = 2) with the table loads shared K ways.
+// one fibre, the modal side of runtime length m (the psi3 steps): TR = false: y[o] = sum_{i<m} A[i][o] x[i]
+// (N outputs); TR = true: y[o] = sum_i A[o][i] x[i] for o < m.  Loop bounds are compile-time N with the
+// modal side predicated (the tables vanish beyond m).
+template <int N, bool TR>
+__device__ __forceinline__ void fiberK_n(const double* ps, int m, const double* in, int sin, double* out, int sout) {
+  constexpr int NP = psi_np<N>();
+  double x[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) x[i] = (TR || i < m) ? in[i * sin] : 0.0;
+  if constexpr (!TR) {
+    double a[N];
+#pragma unroll
+    for (int o = 0; o < N; ++o) a[o] = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (i >= m) break;
+#pragma unroll
+      for (int q2 = 0; q2 < NP / 2; ++q2) {
+        const double2 pv = *reinterpret_cast<const double2*>(ps + i * NP + 2 * q2);
+        a[2 * q2] = fma(pv.x, x[i], a[2 * q2]);
+        if (2 * q2 + 1 < N) a[2 * q2 + 1] = fma(pv.y, x[i], a[2 * q2 + 1]);
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < N; ++o) out[o * sout] = a[o];
+  } else {
+#pragma unroll
+    for (int o = 0; o < N; ++o) {
+      if (o >= m) break;
+      const double* row = ps + o * NP;
+      double t = 0.0;
+#pragma unroll
+      for (int i2 = 0; i2 < NP / 2; ++i2) {
+        const double2 pv = *reinterpret_cast<const double2*>(row + 2 * i2);
+        t = fma(pv.x, x[2 * i2], t);
+        if (2 * i2 + 1 < N) t = fma(pv.y, x[2 * i2 + 1], t);
+      }
+      out[o * sout] = t;
+    }
+  }
+}
+
 template <int N, bool TR, int K>
 __device__ __forceinline__ void fiberK(const double* ps, const double* const* in, int sin, const double* const* sc,
                                        double* const* out, int sout, int nk) {
@@ -409,12 +451,14 @@ __device__ void modal_to_nodal(const PsiS& T, const double* um, double* un, doub
     }
     __syncthreads();
   } else {
-    // t1[v][pr][c] = sum_a3 psi3[s][a3][c] u[v][off(pr)+a3]; items (pr, variable pair)
-    for (int it = tid; it < NPAIR * NVP; it += nt) {
-      const int pr = it / NVP, v0 = 2 * (it - pr * NVP), v1 = v0 + 1 < NV ? v0 + 1 : v0;
+    // t1[v][pr][c] = sum_a3 psi3[s][a3][c] u[v][off(pr)+a3]; one (pr, v) fibre per item (225 items at
+    // N = 9 fit one round of the CTA: half the critical path of paired fibres)
+    for (int it = tid; it < NPAIR * NV; it += nt) {
+      const int pr = it / NV, v = it - pr * NV;
       const int sdeg = T.pa1[pr] + T.pa2[pr];
-      fiber2<N, false>(T.p3 + sdeg * N * psi_np<N>(), N - sdeg, N, um + v0 * Np + T.poff[pr], um + v1 * Np + T.poff[pr], 1, nullptr,
-                nullptr, t1 + (v0 * NPAIR + pr) * N, t1 + (v1 * NPAIR + pr) * N, 1, v1 != v0);
+      const double* in[1] = {um + v * Np + T.poff[pr]};
+      double* out[1] = {t1 + (v * NPAIR + pr) * N};
+      fiberK_n<N, false>(T.p3 + sdeg * N * psi_np<N>(), N - sdeg, in[0], 1, out[0], 1);
     }
     __syncthreads();
     // t2[v][a1][c][b] = sum_a2 psi2[a1][a2][b] t1[v][pr(a1,a2)][c]; items (a1, pair of (v, c) fibers)
@@ -494,12 +538,11 @@ __device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, doubl
                 nullptr, nullptr, t1 + (v0 * NPAIR + prs) * N + c0, t1 + (v1 * NPAIR + prs) * N + c1, N, q1 != q0);
     }
     __syncthreads();
-    // u[v][off(pr)+a3] = sum_c psi3[s][a3][c] s1[v][pr][c]; items (pr, variable pair)
-    for (int it = tid; it < NPAIR * NVP; it += nt) {
-      const int pr = it / NVP, v0 = 2 * (it - pr * NVP), v1 = v0 + 1 < NV ? v0 + 1 : v0;
+    // u[v][off(pr)+a3] = sum_c psi3[s][a3][c] s1[v][pr][c]; one (pr, v) fibre per item
+    for (int it = tid; it < NPAIR * NV; it += nt) {
+      const int pr = it / NV, v = it - pr * NV;
       const int sdeg = T.pa1[pr] + T.pa2[pr];
-      fiber2<N, true>(T.p3 + sdeg * N * psi_np<N>(), N, N - sdeg, t1 + (v0 * NPAIR + pr) * N, t1 + (v1 * NPAIR + pr) * N, 1, nullptr,
-                nullptr, um + v0 * Np + T.poff[pr], um + v1 * Np + T.poff[pr], 1, v1 != v0);
+      fiberK_n<N, true>(T.p3 + sdeg * N * psi_np<N>(), N - sdeg, t1 + (v * NPAIR + pr) * N, 1, um + v * Np + T.poff[pr], 1);
     }
     __syncthreads();
   }
