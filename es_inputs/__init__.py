@@ -273,3 +273,4 @@ def modal_state_from_centroids(mesh, p, kind, seed=0, amp=2e-2, gamma=GAMMA):
     scale[:, :, 0] = 0.0
     # keep the kinetic energy perturbation small relative to pressure for admissibility
     return u + scale * rng.standard_normal(u.shape)
+

@@ -187,6 +187,15 @@ es_status es_project_nodal(es_context* ctx, const double* u_nodal, double* u_mod
 /* Evaluation at the volume quadrature nodes u = V u~: u_modal device [n_local][N_c][N_p*]
  * -> u_nodal device [n_local][N_q][N_c].  (Error norms, output.) */
 es_status es_eval_nodal(es_context* ctx, const double* u_modal, double* u_nodal);
+/* Evaluation at arbitrary reference points (error norms with a rule of the caller's choice, e.g. the
+ * degree-35 collapsed Gauss rule behind the paper's L2 errors): xi_host[npts][dim] (HOST) on the
+ * reference simplex (vertices of P:177 / P:257).  Writes (device) u_out[n_local][npts][N_c] =
+ * sum_k u~_k psi_k(xi) (PKD basis), and when non-NULL x_out[n_local][npts][dim] = x^(kappa)(xi)
+ * (the degree-p_g mapping) and jac_out[n_local][npts] = det(dx/dxi) of that mapping (the
+ * exact Jacobian, not J~).  u_modal: device.  Synchronous. */
+es_status es_eval_points(es_context* ctx, const double* u_modal, int npts, const double* xi_host,
+                         double* u_out, double* x_out, double* jac_out);
+
 /* Quadrature weights of the volume nodes in physical space, W J~: device [n_local][N_q];
  * sum_k sum_i wj f(x_i) integrates f over the local elements (exact for the L2 norm of P_p data). */
 es_status es_node_weights(es_context* ctx, double* wj);

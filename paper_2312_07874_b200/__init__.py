@@ -70,6 +70,7 @@ es_flux_counts = _sig("es_flux_counts", _i, _vp, _lp, _lp, _lp, _dp)
 es_count_fluxes = _sig("es_count_fluxes", _i, _vp, _vp, _lp)
 es_step_host = _sig("es_step_host", _i, _vp, _vp, _vp, ctypes.c_double, _i)
 es_set_graphs = _sig("es_set_graphs", _i, _vp, _i)
+es_eval_points = _sig("es_eval_points", _i, _vp, _vp, _i, _dp, _vp, _vp, _vp)
 es_group_rhs = _sig("es_group_rhs", _i, ctypes.POINTER(_vp), _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp))
 es_group_step = _sig("es_group_step", _i, ctypes.POINTER(_vp), _i, ctypes.c_double, _i)
 es_group_entropy_production = _sig("es_group_entropy_production", _i, ctypes.POINTER(_vp), _i, ctypes.POINTER(_vp),
@@ -329,6 +330,18 @@ class Context:
 
     def set_graphs(self, on=True):
         self._check(es_set_graphs(self.h, 1 if on else 0))
+
+    def eval_points(self, u, xi, x_out=None, jac_out=None):
+        """es_eval_points: solution at reference points xi [npts][d] (host numpy) of every local element:
+        returns a device tensor [n_local][npts][N_c]; x_out / jac_out optional device tensors"""
+        import torch
+        xi = np.ascontiguousarray(xi, dtype=np.float64)
+        npts = xi.shape[0]
+        out = torch.empty((self.nloc, npts, self.d + 2), dtype=torch.float64, device=u.device)
+        self._check(es_eval_points(self.h, _ptr(u), npts, xi.ctypes.data_as(_dp), _ptr(out),
+                                   _ptr(x_out) if x_out is not None else None,
+                                   _ptr(jac_out) if jac_out is not None else None))
+        return out
 
     def count_fluxes(self, u):
         """flux evaluations counted in the kernels on one RHS of u (device tensor): int64 array

@@ -61,6 +61,7 @@ struct es_context {
   double *geo_vol = nullptr, *geo_face = nullptr, *xq = nullptr, *jt = nullptr;
   double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr, *fstar = nullptr;
   double *rbuf = nullptr, *wjk3 = nullptr;  // 3D: nodal residual for K3, W / J~ in K3's layout
+  double* xmapv = nullptr;                   // [nloc][Npg][dim] mapping-node positions (es_eval_points)
   unsigned long long* dcounts = nullptr;    // es_count_fluxes: per-element flux-evaluation counters
   bool counting = false;
   // CUDA graph of one classical RK4 step (4 right-hand sides, 12-16 launches) replayed by es_step
@@ -388,7 +389,7 @@ void es_destroy(es_context* c) {
                   (void*)c->face_reflect, (void*)c->bad, (void*)c->U, (void*)c->ACC, (void*)c->US,
                   (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg, (void*)c->fstar,
                   (void*)c->dpy, (void*)c->dppart, (void*)c->sdense, (void*)c->rbdense, (void*)c->rbuf,
-                  (void*)c->wjk3, (void*)c->dcounts})
+                  (void*)c->wjk3, (void*)c->dcounts, (void*)c->xmapv})
     if (p) cudaFree(p);
   for (double* p : c->dpk)
     if (p) cudaFree(p);
@@ -490,6 +491,7 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
     map(user, c->nloc * Npg, xin.data(), xmap.data());
   else
     xmap = xin;
+  CK(upload(&c->xmapv, xmap));  // absolute mapping-node positions, kept for es_eval_points
   // element-local coordinates (R25): metric terms are translation invariant, and local
   // coordinates avoid a cancellation of order (L/h)^2 in the curl-form metrics
   std::vector<double> shift((size_t)c->nloc * d);
@@ -887,6 +889,27 @@ es_status es_count_fluxes(es_context* c, const double* u, int64_t* counts) {
   CK(cudaMemcpyAsync(h.data(), c->dcounts, nb, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   for (size_t k = 0; k < h.size(); ++k) counts[k] = (int64_t)h[k];
+  return ES_OK;
+}
+
+es_status es_eval_points(es_context* c, const double* u, int npts, const double* xi, double* uo, double* xo,
+                         double* jo) {
+  POISON_CHECK();
+  if (!u || !xi || !uo || npts <= 0) return fail(c, ES_ERR_ARG, "es_eval_points: u, xi, u_out and npts > 0 required");
+  CK(cudaSetDevice(c->device));
+  std::vector<double> pkd, lm, dm;
+  if (!eval_point_tables(c->d, c->p, xi, npts, pkd, lm, dm)) return fail(c, ES_ERR_CONFIG, "point tables");
+  double *dp = nullptr, *dl = nullptr, *dd = nullptr;
+  CK(upload(&dp, pkd));
+  CK(upload(&dl, lm));
+  CK(upload(&dd, dm));
+  EvalPtsArgs a{c->d, c->NC, c->Np, c->T.Npg, npts, c->nloc, u, c->xmapv, dp, dl, dd, uo, xo, jo};
+  CK(launch_eval_points(a, c->stream));
+  c->launches++;
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(dp);
+  cudaFree(dl);
+  cudaFree(dd);
   return ES_OK;
 }
 

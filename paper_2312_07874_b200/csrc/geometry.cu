@@ -282,4 +282,50 @@ cudaError_t launch_reduce_parts(const double* part, int64_t ne, int w, double* o
   return cudaGetLastError();
 }
 
+// one thread per (element, point); the element's modal coefficients staged in shared memory
+__global__ void __launch_bounds__(128) eval_points_kernel(EvalPtsArgs a) {
+  extern __shared__ double su[];
+  const int64_t e = blockIdx.y;
+  const int nm = a.NC * a.Np;
+  for (int k = threadIdx.x; k < nm; k += blockDim.x) su[k] = a.um[e * nm + k];
+  __syncthreads();
+  const int pt = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pt >= a.npts) return;
+  const double* pk = a.pkd + (size_t)pt * a.Np;
+  for (int v = 0; v < a.NC; ++v) {
+    double s = 0.0;
+    for (int k = 0; k < a.Np; ++k) s = fma(su[v * a.Np + k], __ldg(pk + k), s);
+    a.u[((size_t)e * a.npts + pt) * a.NC + v] = s;
+  }
+  const double* X = a.xmap + (size_t)e * a.Npg * a.dim;
+  if (a.x) {
+    for (int m = 0; m < a.dim; ++m) {
+      double s = 0.0;
+      for (int i = 0; i < a.Npg; ++i) s = fma(__ldg(a.lmap + (size_t)pt * a.Npg + i), X[i * a.dim + m], s);
+      a.x[((size_t)e * a.npts + pt) * a.dim + m] = s;
+    }
+  }
+  if (a.jac) {
+    double A[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // A[m][l] = d x_m / d xi_l
+    for (int l = 0; l < a.dim; ++l)
+      for (int i = 0; i < a.Npg; ++i) {
+        const double g = __ldg(a.dmap + ((size_t)l * a.npts + pt) * a.Npg + i);
+        for (int m = 0; m < a.dim; ++m) A[m][l] = fma(g, X[i * a.dim + m], A[m][l]);
+      }
+    const double J = a.dim == 2 ? A[0][0] * A[1][1] - A[0][1] * A[1][0]
+                                : A[0][0] * (A[1][1] * A[2][2] - A[1][2] * A[2][1]) -
+                                      A[0][1] * (A[1][0] * A[2][2] - A[1][2] * A[2][0]) +
+                                      A[0][2] * (A[1][0] * A[2][1] - A[1][1] * A[2][0]);
+    a.jac[(size_t)e * a.npts + pt] = J;
+  }
+}
+
+cudaError_t launch_eval_points(const EvalPtsArgs& a, cudaStream_t st) {
+  if (a.ne <= 0 || a.npts <= 0) return cudaSuccess;
+  const size_t sm = (size_t)a.NC * a.Np * sizeof(double);
+  dim3 grid((unsigned)((a.npts + 127) / 128), (unsigned)a.ne);
+  eval_points_kernel<<<grid, 128, sm, st>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace esb

@@ -36,6 +36,21 @@ cudaError_t launch_geometry(const GeoArgs& g, int64_t ne, cudaStream_t st);
 cudaError_t launch_face_check(const FaceCheckArgs& a, cudaStream_t st);
 cudaError_t launch_pack(const double* trace, const int64_t* slots, int64_t nsend, int per_face, double* buf,
                         cudaStream_t st);
+// evaluation at arbitrary reference points (es_eval_points): u = sum_k u~_k psi_k(xi) per variable,
+// x = sum_i l_i(xi) X_i, jac = det(sum_i grad l_i(xi) X_i^T) over the element's mapping nodes X
+struct EvalPtsArgs {
+  int dim, NC, Np, Npg, npts;
+  int64_t ne;
+  const double* um;    // [ne][NC][Np]
+  const double* xmap;  // [ne][Npg][dim] mapping-node positions
+  const double* pkd;   // [npts][Np]
+  const double* lmap;  // [npts][Npg]
+  const double* dmap;  // [dim][npts][Npg]
+  double* u;           // [ne][npts][NC]
+  double* x;           // optional [ne][npts][dim]
+  double* jac;         // optional [ne][npts]
+};
+cudaError_t launch_eval_points(const EvalPtsArgs& a, cudaStream_t st);
 cudaError_t launch_reduce_parts(const double* part, int64_t ne, int w, double* out, cudaStream_t st);
 
 // explicit Runge-Kutta combinations over the modal state (HBM-bound streams)

@@ -50,6 +50,9 @@ struct RefTables {
 bool build_ref_tables(int d, int p, RefTables& t, std::string& err);
 // dense S^(l) [l][j][i] and (R^(z)T B) [z][f][i] for the brute-force ablation (volume_mode 2)
 void build_dense_tables(const RefTables& t, std::vector<double>& S, std::vector<double>& RB);
+// PKD basis, mapping Lagrange basis and its reference gradients at arbitrary points (es_eval_points)
+bool eval_point_tables(int d, int p, const double* xi, int npts, std::vector<double>& pkd, std::vector<double>& lmap,
+                       std::vector<double>& dmap);
 
 // ----------------------------------------------------------------------------------------------
 // Host mesh plan: connectivity with the orientation rule R11, and the partition/halo

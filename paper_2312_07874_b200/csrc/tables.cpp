@@ -83,70 +83,46 @@ Q pnorm_q(int n, Q a, Q b, Q x) {
   return pc;
 }
 
-// symmetric tridiagonal eigen-decomposition (implicit QL with Wilkinson-type shifts)
-bool tridiag_eig(std::vector<double>& dg, std::vector<double> e, int n, std::vector<double>& z) {
-  z.assign((size_t)n * n, 0.0);
-  for (int i = 0; i < n; ++i) z[(size_t)i * n + i] = 1.0;
-  e.resize(n, 0.0);
-  e[n - 1] = 0.0;
-  for (int l = 0; l < n; ++l) {
-    int iter = 0, m;
-    do {
-      for (m = l; m < n - 1; ++m) {
-        double dd = std::fabs(dg[m]) + std::fabs(dg[m + 1]);
-        if (std::fabs(e[m]) <= 1e-300 + 2.2e-16 * dd) break;
-      }
-      if (m != l) {
-        if (iter++ == 100) return false;
-        double g = (dg[l + 1] - dg[l]) / (2.0 * e[l]);
-        double r = std::hypot(g, 1.0);
-        g = dg[m] - dg[l] + e[l] / (g + std::copysign(r, g));
-        double s = 1.0, c = 1.0, pp = 0.0;
-        int i;
-        bool early = false;
-        for (i = m - 1; i >= l; --i) {
-          double f = s * e[i], bb = c * e[i];
-          r = std::hypot(f, g);
-          e[i + 1] = r;
-          if (r == 0.0) {
-            dg[i + 1] -= pp;
-            e[m] = 0.0;
-            early = true;
-            break;
-          }
-          s = f / r;
-          c = g / r;
-          g = dg[i + 1] - pp;
-          r = (dg[i] - g) * s + 2.0 * c * bb;
-          pp = s * r;
-          dg[i + 1] = g + pp;
-          g = c * r - bb;
-          for (int k = 0; k < n; ++k) {
-            double t = z[(size_t)k * n + i + 1];
-            z[(size_t)k * n + i + 1] = s * z[(size_t)k * n + i] + c * t;
-            z[(size_t)k * n + i] = c * z[(size_t)k * n + i] - s * t;
-          }
-        }
-        if (early) continue;
-        dg[l] -= pp;
-        e[l] = g;
-        e[m] = 0.0;
-      }
-    } while (m != l);
+// Eigenvalues of the symmetric tridiagonal Jacobi matrix (diagonal dg, off-diagonal e) by bisection on
+// the Sturm count: the number of negative pivots of the LDL^T factorisation of (J - t I) equals the
+// number of eigenvalues below t.  Only the eigenvalues are needed (starting values of the binary128
+// Newton polish in gauss_rule); they all lie in [-1, 1] for the Jacobi weights on [-1, 1].
+int sturm_below(const std::vector<double>& dg, const std::vector<double>& e, int n, double t) {
+  int cnt = 0;
+  double q = 1.0;
+  for (int k = 0; k < n; ++k) {
+    q = dg[k] - t - (k > 0 ? e[k - 1] * e[k - 1] / q : 0.0);
+    if (q == 0.0) q = -1e-300;
+    if (q < 0.0) ++cnt;
+  }
+  return cnt;
+}
+bool tridiag_eigvals(const std::vector<double>& dg, const std::vector<double>& e, int n, std::vector<double>& lam) {
+  lam.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) {  // i-th smallest eigenvalue: count(below lo) <= i < count(below hi)
+    double lo = -1.0 - 1e-12, hi = 1.0 + 1e-12;
+    for (int it = 0; it < 200 && hi - lo > 1e-15; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (sturm_below(dg, e, n, mid) > i)
+        hi = mid;
+      else
+        lo = mid;
+    }
+    lam[i] = 0.5 * (lo + hi);
   }
   return true;
 }
 
-// Gauss rule w.r.t. (1-x)^a (1+x)^b with N nodes: Golub-Welsch eigenvalues as
-// starting values, Newton on the monic recurrence in binary128, Gauss-Christoffel weights
+// Gauss rule w.r.t. (1-x)^a (1+x)^b with N nodes: the eigenvalues of the Jacobi matrix
+// (Golub-Welsch) by Sturm bisection as starting values, Newton on the monic recurrence in binary128, Gauss-Christoffel weights
 //   w_i = ||p_{N-1}||^2 / (p_{N-1}(x_i) p_N'(x_i)).
 bool gauss_rule(int N, double a, double b, std::vector<Q>& x, std::vector<Q>& w) {
   Monic m = monic_coeffs(N + 1, a, b);
-  std::vector<double> dg(N), e(N, 0.0), z;
+  std::vector<double> dg(N), e(N, 0.0), lam;
   for (int k = 0; k < N; ++k) dg[k] = m.al[k];
   for (int k = 0; k + 1 < N; ++k) e[k] = std::sqrt(m.be[k + 1]);
-  if (!tridiag_eig(dg, e, N, z)) return false;
-  std::sort(dg.begin(), dg.end());
+  if (!tridiag_eigvals(dg, e, N, lam)) return false;
+  dg = lam;
   MonicQ mq = monic_q(N + 1, a, b);
   Q norm2 = mq.be[0];
   for (int k = 1; k < N; ++k) norm2 *= mq.be[k];
@@ -504,6 +480,55 @@ bool build_ref_tables(int d, int p, RefTables& t, std::string& err) {
 // S^(l)_ij assembled from the line operators exactly as the line-wise kernel applies them (the
 // eta_k-line coefficients of DESIGN.md section 5.3), stored transposed [l][j][i]; (R^(z)T B)_if as
 // [z][f][i].  Entries off the lines are zero and are evaluated anyway by the brute-force kernel.
+// PKD basis (the product of the psi tables' functions, modal order of the ABI) and the
+// mapping-lattice Lagrange basis with its gradients at arbitrary reference points xi[npts][d]:
+// pkd [npts][Np], lmap [npts][Npg], dmap [d][npts][Npg] (rounded from binary128)
+bool eval_point_tables(int d, int p, const double* xi, int npts, std::vector<double>& pkd, std::vector<double>& lmap,
+                       std::vector<double>& dmap) {
+  const int Np = d == 2 ? (p + 1) * (p + 2) / 2 : (p + 1) * (p + 2) * (p + 3) / 6;
+  pkd.assign((size_t)npts * Np, 0.0);
+  std::vector<double> X(xi, xi + (size_t)npts * d), L, D;
+  lattice_basis(d, p, X, npts, &L, &D);
+  const size_t nL = L.size() / 2, nD = D.size() / 2;
+  lmap.assign(nL, 0.0);
+  dmap.assign(nD, 0.0);
+  for (size_t k = 0; k < nL; ++k) lmap[k] = L[k] + L[nL + k];
+  for (size_t k = 0; k < nD; ++k) dmap[k] = D[k] + D[nD + k];
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int x = 0; x < npts; ++x) {
+    // collapsed coordinates (inverse of P:183 / P:263), singular vertices mapped to eta = 1
+    Q e1, e2, e3 = 0;
+    const double* q = xi + (size_t)x * d;
+    if (d == 2) {
+      e2 = q[1];
+      e1 = (std::fabs(1.0 - q[1]) < 1e-300) ? (Q)1 : (Q)2 * ((Q)1 + (Q)q[0]) / ((Q)1 - (Q)q[1]) - (Q)1;
+    } else {
+      e3 = q[2];
+      const Q den2 = (Q)1 - (Q)q[2];
+      e2 = (std::fabs((double)den2) < 1e-300) ? (Q)1 : (Q)2 * ((Q)1 + (Q)q[1]) / den2 - (Q)1;
+      const Q den1 = -(Q)q[1] - (Q)q[2];
+      e1 = (std::fabs((double)den1) < 1e-300) ? (Q)1 : (Q)2 * ((Q)1 + (Q)q[0]) / den1 - (Q)1;
+    }
+    int k = 0;
+    for (int a1 = 0; a1 <= p; ++a1) {
+      const Q f1 = qsqrt((Q)2) * pnorm_q(a1, 0, 0, e1);
+      for (int a2 = 0; a2 <= p - a1; ++a2) {
+        const Q f2 = powq((Q)1 - e2, (Q)a1) * pnorm_q(a2, (Q)(2 * a1 + 1), 0, e2);
+        if (d == 2) {
+          pkd[(size_t)x * Np + k++] = (double)(f1 * f2);
+          continue;
+        }
+        for (int a3 = 0; a3 <= p - a1 - a2; ++a3) {
+          const int sd = a1 + a2;
+          const Q f3 = (Q)2 * powq((Q)1 - e3, (Q)sd) * pnorm_q(a3, (Q)(2 * sd + 2), 0, e3);
+          pkd[(size_t)x * Np + k++] = (double)(f1 * f2 * f3);
+        }
+      }
+    }
+  }
+  return true;
+}
+
 void build_dense_tables(const RefTables& t, std::vector<double>& S, std::vector<double>& RB) {
   const int d = t.d, N = t.n, Nq = t.Nq, Nqf = t.Nqf, Nf = t.Nf;
   S.assign((size_t)d * Nq * Nq, 0.0);

@@ -56,6 +56,37 @@ def test_eval_nodal_and_weights(es, d, p):
 
 def test_density_wave_order(es):
     import convergence as C
-    errs = [C.run_case(es, I, torch, 2, 2, M, 0.1, "paper")[0] for M in (4, 8, 16)]
+    errs = [C.run_case(es, I, torch, 2, 2, M, 0.1, "paper")["l2_rho_error"] for M in (4, 8, 16)]
     orders = [math.log2(errs[k] / errs[k + 1]) for k in range(2)]
     assert orders[-1] > 2.4, (errs, orders)  # p + 1 = 3 expected
+
+
+@pytest.mark.parametrize("d,p,warp", [(2, 3, "paper"), (3, 2, "paper"), (3, 3, "bj")])
+def test_eval_points_against_oracle(es, d, p, warp):
+    # es_eval_points: the PKD expansion at arbitrary points against the oracle's PKD basis;
+    # at the scheme's own volume nodes the map reproduces the node coordinates and, for the BASELINE
+    # warp (rank-one displacement, J~ = J exactly, R13), the Jacobian equals J~ of the geometry
+    L = 2.0 if d == 2 else 2.0 * math.pi
+    M = 3
+    mesh = I.split_cartesian(d, M, L)
+    w = I.paper_warp(d, L) if warp == "paper" else I.bj_warp(d, L, M)
+    om = O.Mesh(mesh, p, warp=w)
+    u = I.perturb_modal(om.project(I.density_wave(om.node_coords(), L)), d, p, seed=3, amp=1e-2)
+    ctx = es.Context(mesh, p, warp=w)
+    ut = torch.from_numpy(u).cuda()
+    import quadrature as Q
+    xi, _ = Q.collapsed_gauss_rule(d, 5)
+    uq = ctx.eval_points(ut, xi).cpu().numpy()
+    V = O.pkd_eval(d, p, xi)[0]  # [npts][Np]
+    ref = np.einsum("qk,evk->eqv", V, u)
+    assert np.abs(uq - ref).max() < 1e-13 * np.abs(ref).max()
+    xiv = O.ref_get(d, p, "xi")  # the volume quadrature nodes [Nq][d]
+    x = torch.empty((ctx.nloc, len(xiv), d), dtype=torch.float64, device="cuda")
+    jac = torch.empty((ctx.nloc, len(xiv)), dtype=torch.float64, device="cuda")
+    ctx.eval_points(ut, xiv, x, jac)
+    xc = om.node_coords()
+    assert np.abs(x.cpu().numpy() - xc).max() < 1e-12 * L
+    if warp == "bj":
+        for e in (0, 5, om.ne - 1):
+            assert np.allclose(jac[e].cpu().numpy(), om.geometry(e)["Jt"], rtol=1e-11, atol=0)
+    assert float(jac.min()) > 0
