@@ -136,6 +136,42 @@ __device__ __forceinline__ void modeA_mid(double* S, const double* wj, bool act)
     for (int q = 0; q < NPAIR; ++q) S[q * N] = s1[q];
 }
 
+// modeA_mid with the t1 column held in registers (45 loads per lane instead of 45 per b): 90
+// accumulator + t1 doubles live, for CTAs sized to 1 per SM with a 224-register budget
+template <int N>
+__device__ __forceinline__ void modeA_mid_t1reg(double* S, const double* wj, bool act) {
+  constexpr int NPAIR = X3<N>::NPAIR;
+  double s1[NPAIR], t1[NPAIR];
+#pragma unroll
+  for (int q = 0; q < NPAIR; ++q) {
+    s1[q] = 0.0;
+    t1[q] = S[q * N];
+  }
+#pragma unroll
+  for (int b = 0; b < N; ++b) {
+    double t2[N], y[N], s2[N];
+#pragma unroll
+    for (int a1 = 0; a1 < N; ++a1) {
+      double t = 0.0;
+#pragma unroll
+      for (int a2 = 0; a2 < N - a1; ++a2) t = fma(c_psi<N>.p2[(a1 * N + a2) * N + b], t1[pr_of(N, a1, a2)], t);
+      t2[a1] = t;
+    }
+    psi1_apply_eo<N>(t2, y);
+#pragma unroll
+    for (int a = 0; a < N; ++a) y[a] *= wj[(b * N + a) * N];
+    psi1T_apply_eo<N>(y, s2);
+#pragma unroll
+    for (int a1 = 0; a1 < N; ++a1)
+#pragma unroll
+      for (int a2 = 0; a2 < N - a1; ++a2)
+        s1[pr_of(N, a1, a2)] = fma(c_psi<N>.p2[(a1 * N + a2) * N + b], s2[a1], s1[pr_of(N, a1, a2)]);
+  }
+  if (act)
+#pragma unroll
+    for (int q = 0; q < NPAIR; ++q) S[q * N] = s1[q];
+}
+
 // ---- mode B: one (pr) fibre over c, length N3 = N - s of the modal index a3 ----
 // V^T step 3 (u1[a3] = sum_c psi3[s][a3][c] x[c]) then, for FWD, V step 1 back into x (in place)
 template <int N, int N3, bool FWD>

@@ -177,15 +177,18 @@ def _l2_density_error(om, u, L, t, d):
 
 
 def test_density_wave_h_convergence():
-    # ES scheme, density wave translating with v = (1,1), order ~ p+1
-    d, p, L, T = 2, 2, 2.0, 0.1
+    # ES scheme, density wave translating with v = (1,1) over one period T = 2 on the
+    # paper's curved triangles, p = 3: the observed order at M = 8 -> 16 is within 0.3 of p + 1
+    # (the GPU study in profiles/r02_density_wave_convergence.jsonl measures 3.81 there with
+    # the degree-35 rule)
+    d, p, L, T = 2, 3, 2.0, 2.0
     errs = []
-    for M in (4, 8):
+    for M in (8, 16):
         mesh, om, _ = _mesh(d, M, p, warp="paper")
         u = om.project(I.density_wave(om.node_coords(), L))
         h = L / M
-        nst = int(math.ceil(T / (0.05 * h)))
+        nst = int(math.ceil(T / (0.1 * h / ((2 * p + 1) * 3.05))))  # CFL 0.1 (R16)
         u = om.rk4(u, T / nst, nst, flux_mode=1)
         errs.append(_l2_density_error(om, u, L, T, d))
     order = math.log2(errs[0] / errs[1])
-    assert order > 2.4, (errs, order)
+    assert abs(order - (p + 1)) <= 0.3, (errs, order)

@@ -11,29 +11,24 @@
 
 using namespace esb;
 
-template <int N, int VAR, int MINB>
-__global__ void __launch_bounds__(192, MINB) bench_mid(double* out, int reps, int zero) {
+template <int N, int VAR, int MINB, int NTH = 192>
+__global__ void __launch_bounds__(NTH, MINB) bench_mid(double* out, int reps, int zero) {
   using Z = X3<N>;
   extern __shared__ __align__(16) double sm[];
-  const int E = 192 / (5 * N);
+  const int E = NTH / (5 * N);
   double* S = sm;                  // [E*5][SEV]
   double* W = S + E * 5 * Z::SEV;  // [E][Nq]
-  double* p2T = W + E * Z::Nq + 2; // [N][P2S]
-  p2T = (double*)(((uintptr_t)p2T + 15) & ~(uintptr_t)15);
   const int tid = threadIdx.x;
   for (int k = tid; k < E * 5 * Z::SEV; k += blockDim.x) S[k] = 1.0 + 1e-3 * (k % 17);
   for (int k = tid; k < E * Z::Nq; k += blockDim.x) W[k] = 0.5 + 1e-3 * (k % 13);
-  for (int k = tid; k < N * Z::P2S; k += blockDim.x) p2T[k] = 1e-2 * (k % 7);
   __syncthreads();
   const bool act = tid < 5 * E * N;
   const int ev = act ? tid / N : 0, c = act ? tid - ev * N : 0, e = ev / 5;
   for (int r = 0; r < reps; ++r) {
-    if constexpr (VAR == 0)
-      modeA_mid<N>(S + ev * Z::SEV + c, W + e * Z::Nq + c, p2T, act, zero);
-    else if constexpr (VAR == 1)
-      modeA_mid_unrolled<N>(S + ev * Z::SEV + c, W + e * Z::Nq + c, act);
+    if constexpr (VAR == 2)
+      modeA_mid<N>(S + ev * Z::SEV + c, W + e * Z::Nq + c, act);
     else
-      modeA_mid_eo<N>(S + ev * Z::SEV + c, W + e * Z::Nq + c, act);
+      modeA_mid_t1reg<N>(S + ev * Z::SEV + c, W + e * Z::Nq + c, act);
     __syncwarp();
   }
   if (tid == 0) out[blockIdx.x] = S[0];
@@ -51,23 +46,25 @@ int main() {
   cudaMemcpyToSymbol(c_psi<N>, &h, sizeof(h));
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int E = 192 / (5 * N);
-  size_t smem = (E * 5 * Z::SEV + E * Z::Nq + 4 + N * Z::P2S) * 8;
   double* out;
   cudaMalloc(&out, sizeof(double) * sms * 64);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const int reps = 200;
-  const char* names[6] = {"unrolled-168reg", "unrolled-255reg", "evenodd-168reg", "evenodd-255reg", "loop-168reg", "loop-255reg"};
-  for (int var = 0; var < 6; ++var) {
-    auto k = var == 0 ? bench_mid<N, 1, 2> : var == 1 ? bench_mid<N, 1, 1> : var == 2 ? bench_mid<N, 2, 2> :
-             var == 3 ? bench_mid<N, 2, 1> : var == 4 ? bench_mid<N, 0, 2> : bench_mid<N, 0, 1>;
+  const char* names[3] = {"evenodd-168reg-192thr", "t1reg-224reg-288thr", "t1reg-255reg-256thr"};
+  const int nths[3] = {192, 288, 256};
+  for (int var = 0; var < 3; ++var) {
+    auto k = var == 0 ? bench_mid<N, 2, 2, 192> : var == 1 ? bench_mid<N, 3, 1, 288> : bench_mid<N, 3, 1, 256>;
+    const int nth = nths[var];
+    const int E = nth / (5 * N);
+    const size_t smem = (E * 5 * Z::SEV + E * Z::Nq + 4 + N * 46) * 8;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     for (int cps : {1, 2}) {
-      k<<<sms * cps, 192, smem>>>(out, 2, 0);
+      if (var > 0 && cps > 1) continue;
+      k<<<sms * cps, nth, smem>>>(out, 2, 0);
       cudaEventRecord(a);
-      k<<<sms * cps, 192, smem>>>(out, reps, 0);
+      k<<<sms * cps, nth, smem>>>(out, reps, 0);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
