@@ -72,6 +72,7 @@ def lib():
                               ctypes.c_int, ctypes.POINTER(Stats)]
         L.ora_rk4.argtypes = [ctypes.c_void_p, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.ora_dp54_tableau.argtypes = [_dp, _dp, _dp, _dp]
+        L.ora_advection_rhs.argtypes = [ctypes.c_void_p, _dp, _dp, ctypes.c_int, ctypes.c_int, _dp, _dp]
         L.ora_dp54.argtypes = [ctypes.c_void_p, _dp, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                ctypes.c_int, _dp, _dp]
         _lib = L
@@ -348,6 +349,30 @@ class Mesh:
         if rc:
             raise RuntimeError(f"ora_dp54 failed ({rc})")
         return u5, err.value
+
+    def advection_rhs(self, u, a, flux_mode=1, form=0):
+        """linear advection (P:425-436): u [ne][Np] (or [ne][1][Np]) modal scalar, velocity a [d];
+        form 0 skew-symmetric [eq:rhs_skew], 1 conservative; flux_mode 0 central, 1 upwind.
+        Returns (dudt [ne][Np], energy rate sum u^T r, energy scale sum |u_i r_i|)."""
+        u = _c(np.asarray(u).reshape(self.ne, -1))
+        av = _c(np.asarray(a, dtype=np.float64).reshape(-1))
+        out = np.zeros_like(u)
+        en = np.zeros(2)
+        rc = lib().ora_advection_rhs(self.h, _d(u), _d(av), flux_mode, form, _d(out), _d(en))
+        if rc:
+            raise RuntimeError(f"ora_advection_rhs failed ({rc})")
+        return out, en[0], en[1]
+
+    def advection_rk4(self, u, a, dt, nsteps, flux_mode=1, form=0):
+        """classical RK4 (R17) on the advection right-hand side (Python loop over the oracle's RHS)"""
+        u = np.array(np.asarray(u).reshape(self.ne, -1), dtype=np.float64)
+        for _ in range(nsteps):
+            k1 = self.advection_rhs(u, a, flux_mode, form)[0]
+            k2 = self.advection_rhs(u + 0.5 * dt * k1, a, flux_mode, form)[0]
+            k3 = self.advection_rhs(u + 0.5 * dt * k2, a, flux_mode, form)[0]
+            k4 = self.advection_rhs(u + dt * k3, a, flux_mode, form)[0]
+            u = u + dt / 6.0 * (k1 + 2 * k2 + 2 * k3 + k4)
+        return u
 
     def rk4(self, u, dt, nsteps, flux_mode=1, nthreads=0):
         u = np.array(u, dtype=np.float64, copy=True, order="C")

@@ -1687,6 +1687,86 @@ int ora_rhs(const ora_mesh* m, const double* u_modal, double* dudt, int flux_mod
   return 0;
 }
 
+// ---- linear advection, du/dt + div(a u) = 0: the skew-symmetric weak form
+// P:431-436 [eq:rhs_skew], or the conservative form P:425-426 [eq:rhs_cons], with dense operators ----
+//   r = 1/2 sum_l ( Q^(l)T sum_m G^(l,m) f^(m) - sum_m G^(l,m) Q^(l) f^(m) )
+//       - sum_z R^(z)T B^(z) J^(z) ( f* - 1/2 sum_m N^(z,m) R^(z) f^(m) ),   f^(m) = a_m u   (skew)
+//   r = sum_l Q^(l)T sum_m G^(l,m) f^(m) - sum_z R^(z)T B^(z) J^(z) f*                          (conservative)
+// f* = (a.n) (u- + u+)/2 (central, flux_mode 0) or minus |a.n| (u+ - u-)/2 (upwind, flux_mode 1),
+// n the unit outward normal J n / J_f; d u~/dt = M~^{-1} V^T r.  energy[0] = sum_k u^T r
+// = d/dt sum_k u~^T M~ u~ / 2, energy[1] = sum_k |u_i r_i|.
+int ora_advection_rhs(const ora_mesh* m, const double* u_modal /*[ne][Np]*/, const double* a, int flux_mode,
+                      int form, double* dudt, double* energy) {
+  const Ref& r = m->ref;
+  const int d = m->d, Nq = r.Nq, Np = r.Np, Nf = r.Nf, Nqf = r.Nqf, n = r.n;
+  const int64_t ne = m->ne;
+  for (int64_t e = 0; e < ne; ++e)
+    if (!m->has_geom[e]) return -1;
+  // nodal values u = V u~ and traces R^(z) u at every facet node
+  vector<double> un((size_t)ne * Nq), ut((size_t)ne * Nf * Nqf);
+  for (int64_t e = 0; e < ne; ++e) {
+    Vapply(r, u_modal + (size_t)e * Np, &un[(size_t)e * Nq]);
+    for (int z = 0; z < Nf; ++z)
+      for (int f = 0; f < Nqf; ++f) {
+        double t = 0.0;
+        for (int i = 0; i < Nq; ++i) t += r.R[((size_t)z * Nqf + f) * Nq + i] * un[(size_t)e * Nq + i];
+        ut[((size_t)e * Nf + z) * Nqf + f] = t;
+      }
+  }
+  double er = 0.0, ea = 0.0;
+  vector<double> res(Nq), c((size_t)d * Nq);
+  for (int64_t e = 0; e < ne; ++e) {
+    const double* u = &un[(size_t)e * Nq];
+    const vector<double>& G = m->G[e];
+    for (int l = 0; l < d; ++l)  // c_l = sum_m G_lm a_m, so that sum_m G^(l,m) f^(m) = c_l u
+      for (int i = 0; i < Nq; ++i) {
+        double t = 0.0;
+        for (int mm = 0; mm < d; ++mm) t += G[((size_t)i * d + l) * d + mm] * a[mm];
+        c[(size_t)l * Nq + i] = t;
+      }
+    for (int i = 0; i < Nq; ++i) {
+      double t = 0.0;
+      for (int l = 0; l < d; ++l) {
+        const double* Q = &r.Q[(size_t)l * Nq * Nq];
+        const double* cl = &c[(size_t)l * Nq];
+        for (int j = 0; j < Nq; ++j) {
+          const double qt = Q[(size_t)j * Nq + i] * cl[j] * u[j];  // (Q^T (c u))_i
+          t += form == 0 ? 0.5 * (qt - cl[i] * Q[(size_t)i * Nq + j] * u[j]) : qt;
+        }
+      }
+      res[i] = t;
+    }
+    for (int z = 0; z < Nf; ++z) {
+      const int64_t o = m->nbr[e * Nf + z];
+      const int zo = m->nbr_face[e * Nf + z], rf = m->reflect[e * Nf + z];
+      for (int f = 0; f < Nqf; ++f) {
+        const int i1 = f % n, i2 = f / n;
+        const int fo = (d == 2) ? (rf ? n - 1 - f : f) : ((rf ? n - 1 - i1 : i1) + n * i2);
+        const double um = ut[((size_t)e * Nf + z) * Nqf + f], up = ut[((size_t)o * Nf + zo) * Nqf + fo];
+        const double* Jn = &m->Jn[e][((size_t)z * Nqf + f) * d];
+        double Jf = 0.0, an = 0.0;
+        for (int k = 0; k < d; ++k) Jf += Jn[k] * Jn[k];
+        Jf = std::sqrt(Jf);
+        for (int k = 0; k < d; ++k) an += a[k] * Jn[k] / Jf;
+        double fs = an * 0.5 * (um + up);
+        if (flux_mode == 1) fs -= 0.5 * std::fabs(an) * (up - um);
+        const double sv = r.B[z * Nqf + f] * Jf * (form == 0 ? fs - 0.5 * an * um : fs);
+        for (int i = 0; i < Nq; ++i) res[i] -= r.R[((size_t)z * Nqf + f) * Nq + i] * sv;
+      }
+    }
+    for (int i = 0; i < Nq; ++i) {
+      er += u[i] * res[i];
+      ea += std::fabs(u[i] * res[i]);
+    }
+    wadg(*m, e, res.data(), dudt + (size_t)e * Np);
+  }
+  if (energy) {
+    energy[0] = er;
+    energy[1] = ea;
+  }
+  return 0;
+}
+
 // Dormand-Prince 5(4) (Hairer, Norsett & Wanner I, Table II.5.2; the paper integrates with DP8 of
 // the same family): c, a (lower triangle, row-major 7x7), b (5th order), bh (embedded 4th)
 static const double DP_C[7] = {0.0, 1.0 / 5.0, 3.0 / 10.0, 4.0 / 5.0, 8.0 / 9.0, 1.0, 1.0};

@@ -113,6 +113,13 @@ void ora_dp54_tableau(double* c, double* a, double* b, double* bh);
 int ora_dp54(const ora_mesh* m, const double* u_modal, double dt, double rtol, double atol, int flux_mode,
              int nthreads, double* u5, double* err);
 
+/* Linear advection du/dt + div(a u) = 0: scalar modal state
+ * u_modal[ne][Np], constant velocity a[dim]; form 0 = skew-symmetric [eq:rhs_skew], 1 = conservative
+ * [eq:rhs_cons]; flux_mode 0 central, 1 upwind.  dudt[ne][Np] = M~^{-1} V^T r; energy[2] = (sum u^T r,
+ * sum |u_i r_i|).  Requires geometry for every element. */
+int ora_advection_rhs(const ora_mesh* m, const double* u_modal, const double* a, int flux_mode, int form,
+                      double* dudt, double* energy);
+
 #ifdef __cplusplus
 }
 #endif
