@@ -178,6 +178,19 @@ es_status es_group_step(es_context** ctxs, int n, double dt, int nsteps);
 es_status es_group_entropy_production(es_context** ctxs, int n, const double* const* u, double* rate,
                                       double* abs_scale, double* conservation);
 
+/* Linear-advection workload: du/dt + div(a u) = 0 with constant velocity a on the
+ * context's mesh and geometry, in the skew-symmetric weak form of P:431-436 [eq:rhs_skew] (form 0; energy
+ * stable on curved meshes) or the conservative form P:425-426 [eq:rhs_cons] (form 1), with the central
+ * (flux_mode 0) or upwind (1) numerical flux, and the weight-adjusted inverse mass matrix.  The
+ * scalar state is u_modal[n_local][N_p*] (device).  Single rank (ES_ERR_CONFIG otherwise).
+ *   es_adv_configure: velocity a[dim], flux and form; allocates the workload's buffers.
+ *   es_adv_rhs: du~/dt; energy (HOST, may be NULL) receives (sum_k u^T r, sum_k |u_i r_i|), the rate
+ *     d/dt of sum_k u~^T M~ u~ / 2 and its scale (synchronous when energy != NULL).
+ *   es_adv_step: nsteps classical RK4 steps (R17) of u_modal in place (asynchronous). */
+es_status es_adv_configure(es_context* ctx, const double* a, int flux_mode, int form);
+es_status es_adv_rhs(es_context* ctx, const double* u_modal, double* dudt_modal, double* energy);
+es_status es_adv_step(es_context* ctx, double* u_modal, double dt, int nsteps);
+
 /* Physical coordinates of the volume quadrature nodes, device pointer [n_local][N_q][dim]. */
 es_status es_node_coords(es_context* ctx, double* x_dev);
 /* Reference L2 projection u~ = V^T W u (M = I): u_nodal device [n_local][N_q][N_c] ->

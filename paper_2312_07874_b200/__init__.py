@@ -71,6 +71,9 @@ es_count_fluxes = _sig("es_count_fluxes", _i, _vp, _vp, _lp)
 es_step_host = _sig("es_step_host", _i, _vp, _vp, _vp, ctypes.c_double, _i)
 es_set_graphs = _sig("es_set_graphs", _i, _vp, _i)
 es_eval_points = _sig("es_eval_points", _i, _vp, _vp, _i, _dp, _vp, _vp, _vp)
+es_adv_configure = _sig("es_adv_configure", _i, _vp, _dp, _i, _i)
+es_adv_rhs = _sig("es_adv_rhs", _i, _vp, _vp, _vp, _dp)
+es_adv_step = _sig("es_adv_step", _i, _vp, _vp, ctypes.c_double, _i)
 es_group_rhs = _sig("es_group_rhs", _i, ctypes.POINTER(_vp), _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp))
 es_group_step = _sig("es_group_step", _i, ctypes.POINTER(_vp), _i, ctypes.c_double, _i)
 es_group_entropy_production = _sig("es_group_entropy_production", _i, ctypes.POINTER(_vp), _i, ctypes.POINTER(_vp),
@@ -342,6 +345,22 @@ class Context:
                                    _ptr(x_out) if x_out is not None else None,
                                    _ptr(jac_out) if jac_out is not None else None))
         return out
+
+    def adv_configure(self, a, flux_mode=1, form=0):
+        """linear-advection workload (es_adv_configure): velocity a [d], flux 0 central / 1 upwind,
+        form 0 skew-symmetric / 1 conservative"""
+        av = np.zeros(3)
+        av[:len(a)] = a
+        self._check(es_adv_configure(self.h, av.ctypes.data_as(_dp), int(flux_mode), int(form)))
+
+    def adv_rhs(self, u, dudt, energy=False):
+        """es_adv_rhs on device tensors [n_local][N_p]; returns (rate, scale) when energy"""
+        en = np.zeros(2)
+        self._check(es_adv_rhs(self.h, _ptr(u), _ptr(dudt), en.ctypes.data_as(_dp) if energy else None))
+        return (en[0], en[1]) if energy else None
+
+    def adv_step(self, u, dt, nsteps=1):
+        self._check(es_adv_step(self.h, _ptr(u), float(dt), int(nsteps)))
 
     def count_fluxes(self, u):
         """flux evaluations counted in the kernels on one RHS of u (device tensor): int64 array

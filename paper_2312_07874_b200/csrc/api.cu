@@ -16,6 +16,7 @@
 #include "internal.h"
 #include "kernels.cuh"
 #include "xform3.cuh"
+#include "advect.cuh"
 
 namespace esb {
 cudaError_t launch_project_2d(int n, const DevRef& R, const ProjArgs& A, cudaStream_t st);
@@ -33,6 +34,9 @@ cudaError_t launch_rhs_count_2d(int n, const DevRef& R, const RhsArgs& A, cudaSt
 cudaError_t launch_rhs_count_3d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
 cudaError_t launch_wadj_3d(int n, const WadjArgs& A, cudaStream_t st);
 cudaError_t upload_psi_3d_k1(int n, const double* p1, const double* p2, const double* p3);
+cudaError_t upload_psi_adv_3d(int n, const double* p1, const double* p2, const double* p3);
+cudaError_t launch_adv_2d(int n, const DevRef& R, const AdvArgs& A, cudaStream_t st);
+cudaError_t launch_adv_3d(int n, const DevRef& R, const AdvArgs& A, cudaStream_t st);
 cudaError_t launch_wjinv_permute_3d(int n, const double* geo_vol, int gvs, int row, int64_t ne, double* out,
                                     cudaStream_t st);
 }  // namespace esb
@@ -69,6 +73,12 @@ struct es_context {
   double step_graph_dt = 0.0;
   int64_t step_graph_launches = 0;
   bool use_graphs = true;
+  // linear-advection workload (es_adv_*): velocity, flux, form, buffers
+  double adv_a[3] = {0, 0, 0};
+  int adv_flux = 1, adv_form = 0;
+  bool adv_ready = false;
+  double *adv_unod = nullptr, *adv_trace = nullptr, *adv_X = nullptr, *adv_acc = nullptr, *adv_us = nullptr,
+         *adv_part = nullptr;
   int num_sms = 148, proj_ctas = 296;
   bool external = false;
   int eq56 = 0;   // volume_mode 1: per-operator fluxes (Eq. num_fluxes ablation)
@@ -389,7 +399,8 @@ void es_destroy(es_context* c) {
                   (void*)c->face_reflect, (void*)c->bad, (void*)c->U, (void*)c->ACC, (void*)c->US,
                   (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg, (void*)c->fstar,
                   (void*)c->dpy, (void*)c->dppart, (void*)c->sdense, (void*)c->rbdense, (void*)c->rbuf,
-                  (void*)c->wjk3, (void*)c->dcounts, (void*)c->xmapv})
+                  (void*)c->wjk3, (void*)c->dcounts, (void*)c->xmapv, (void*)c->adv_unod, (void*)c->adv_trace,
+                  (void*)c->adv_X, (void*)c->adv_acc, (void*)c->adv_us, (void*)c->adv_part})
     if (p) cudaFree(p);
   for (double* p : c->dpk)
     if (p) cudaFree(p);
@@ -913,6 +924,94 @@ es_status es_eval_points(es_context* c, const double* u, int npts, const double*
   return ES_OK;
 }
 
+// ---- linear advection, single rank ----
+es_status es_adv_configure(es_context* c, const double* a, int flux_mode, int form) {
+  POISON_CHECK();
+  if (!a || flux_mode < 0 || flux_mode > 1 || form < 0 || form > 1)
+    return fail(c, ES_ERR_ARG, "es_adv_configure: velocity, flux_mode 0/1, form 0/1");
+  if (c->world != 1) return fail(c, ES_ERR_CONFIG, "es_adv_*: single rank only");
+  CK(cudaSetDevice(c->device));
+  for (int m = 0; m < 3; ++m) c->adv_a[m] = m < c->d ? a[m] : 0.0;
+  c->adv_flux = flux_mode;
+  c->adv_form = form;
+  if (!c->adv_unod) {
+    const int n = c->n;
+    CK(cudaMalloc((void**)&c->adv_unod, (size_t)c->nloc * c->Nq * sizeof(double)));
+    CK(cudaMalloc((void**)&c->adv_trace, (size_t)c->nloc * c->Nf * c->Nqf * sizeof(double)));
+    CK(cudaMalloc((void**)&c->adv_acc, (size_t)c->nloc * c->Np * sizeof(double)));
+    CK(cudaMalloc((void**)&c->adv_us, (size_t)c->nloc * c->Np * sizeof(double)));
+    CK(cudaMalloc((void**)&c->adv_part, (size_t)c->nloc * 2 * sizeof(double)));
+    std::vector<double> X((size_t)5 * n * n, 0.0);
+    const std::vector<double>* src[5] = {&c->T.fQ1, &c->T.fA1, &c->T.fA2, &c->T.fA3, &c->T.fA4};
+    for (int k = 0; k < 5; ++k)
+      if (!src[k]->empty()) std::memcpy(&X[(size_t)k * n * n], src[k]->data(), (size_t)n * n * sizeof(double));
+    CK(upload(&c->adv_X, X));
+    if (c->d == 3) CK(upload_psi_adv_3d(c->n, c->T.psi1.data(), c->T.psi2.data(), c->T.psi3.data()));
+  }
+  c->adv_ready = true;
+  return ES_OK;
+}
+
+namespace {
+AdvArgs adv_args(es_context* c, const double* u, int mode) {
+  AdvArgs A{};
+  A.n_elem = c->nloc;
+  A.u = u;
+  A.unod = c->adv_unod;
+  A.trace = c->adv_trace;
+  A.geo_vol = c->geo_vol;
+  A.geo_face = c->geo_face;
+  A.face_slot = c->face_slot;
+  A.face_reflect = c->face_reflect;
+  A.X = c->adv_X;
+  for (int m = 0; m < 3; ++m) A.a[m] = c->adv_a[m];
+  A.flux_mode = c->adv_flux;
+  A.form = c->adv_form;
+  A.mode = mode;
+  return A;
+}
+cudaError_t adv_launch(es_context* c, const AdvArgs& A) {
+  c->launches += 2;
+  return c->d == 2 ? launch_adv_2d(c->n, c->R, A, c->stream) : launch_adv_3d(c->n, c->R, A, c->stream);
+}
+}  // namespace
+
+es_status es_adv_rhs(es_context* c, const double* u, double* dudt, double* energy) {
+  POISON_CHECK();
+  if (!c->adv_ready) return fail(c, ES_ERR_CONFIG, "es_adv_rhs: call es_adv_configure first");
+  if (!u || !dudt) return fail(c, ES_ERR_ARG, "null buffer");
+  CK(cudaSetDevice(c->device));
+  AdvArgs A = adv_args(c, u, 0);
+  A.out = dudt;
+  A.part = energy ? c->adv_part : nullptr;
+  CK(adv_launch(c, A));
+  if (energy) {
+    CK(launch_reduce_parts(c->adv_part, c->nloc, 2, c->red, c->stream));
+    c->launches++;
+    CK(cudaMemcpyAsync(energy, c->red, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  return ES_OK;
+}
+
+es_status es_adv_step(es_context* c, double* u, double dt, int nsteps) {
+  POISON_CHECK();
+  if (!c->adv_ready) return fail(c, ES_ERR_CONFIG, "es_adv_step: call es_adv_configure first");
+  if (!u) return fail(c, ES_ERR_ARG, "null buffer");
+  CK(cudaSetDevice(c->device));
+  for (int st = 0; st < nsteps; ++st)
+    for (int s = 0; s < 4; ++s) {  // classical RK4 (R17), the stage update fused in the epilogue
+      AdvArgs A = adv_args(c, s == 0 ? u : c->adv_us, 1 + s);
+      A.dt = dt;
+      A.u0 = u;
+      A.acc = c->adv_acc;
+      A.ustage = c->adv_us;
+      A.out = u;
+      CK(adv_launch(c, A));
+    }
+  return ES_OK;
+}
+
 es_status es_node_coords(es_context* c, double* x) {
   POISON_CHECK();
   CK(cudaSetDevice(c->device));
@@ -988,6 +1087,11 @@ es_status es_ref_table(int dim, int p, const char* name, double* out, int64_t ca
   else if (nm == "skA2") v = &t.skA2;
   else if (nm == "skA3") v = &t.skA3;
   else if (nm == "skA4") v = &t.skA4;
+  else if (nm == "fQ1") v = &t.fQ1;
+  else if (nm == "fA1") v = &t.fA1;
+  else if (nm == "fA2") v = &t.fA2;
+  else if (nm == "fA3") v = &t.fA3;
+  else if (nm == "fA4") v = &t.fA4;
   else if (nm == "lL") v = &t.lL;
   else if (nm == "lR") v = &t.lR;
   else if (nm == "l3L") v = &t.l3L;

@@ -23,6 +23,7 @@ struct RefTables {
   std::vector<double> skA2;  // skew(diag(w (1-eta)/2) D)
   std::vector<double> skA3;  // skew(diag(w (1-eta^2)/4) D)            (tet)
   std::vector<double> skA4;  // skew(diag(w3 (1-eta3)) D3)              (tet)
+  std::vector<double> fQ1, fA1, fA2, fA3, fA4;  // the unskewed X (Q^(l) line blocks, linear advection)
   std::vector<double> lL, lR;    // LG Lagrange basis at -1 and +1 (n)
   std::vector<double> l3L;       // GJ(1,0) Lagrange basis at -1 (n)       (tet)
   std::vector<double> lint4;     // [j][b] LG basis l_b at eta3_j         (tet facet 4)

@@ -344,6 +344,13 @@ bool build_ref_tables(int d, int p, RefTables& t, std::string& err) {
   t.skA2 = skew_of(A2, n);
   t.skA3 = skew_of(A3, n);
   t.skA4 = skew_of(A4, n);
+  // the full line matrices (Q^(l) restricted to a line = coefficient x X, used by the linear-advection
+  // workload's skew-symmetric form P:431-436)
+  t.fQ1 = rnd(Q1);
+  t.fA1 = rnd(A1);
+  t.fA2 = rnd(A2);
+  t.fA3 = rnd(A3);
+  t.fA4 = rnd(A4);
   t.lL = rnd(lagrange_at(e, (Q)-1));
   t.lR = rnd(lagrange_at(e, (Q)1));
   t.l3L = rnd(lagrange_at(e3, (Q)-1));

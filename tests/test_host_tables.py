@@ -38,14 +38,14 @@ def test_rules_weights_nodes(es, d, p):
     assert np.abs(es.ref_table(d, p, "xi_vol") - xi.ravel()).max() < 4e-16
 
 
-def _lines(d, n, k):
+def _lines(d, n, k, diagonal=False):
     """node index pairs (i, j, pos_i, pos_j, fixed coords) along eta_k lines"""
     import itertools
     out = []
     for fixed in itertools.product(range(n), repeat=d - 1):
         for a in range(n):
             for b in range(n):
-                if a == b:
+                if a == b and not diagonal:
                     continue
                 ci, cj, it = [0] * d, [0] * d, iter(fixed)
                 for t in range(d):
@@ -96,6 +96,37 @@ def test_line_factorisation_matches_dense_S(es, d, p):
             mask[i, j] = True
     for l in range(d):
         assert np.abs(S[l][~mask]).max() < 1e-14 * scale
+
+
+@pytest.mark.parametrize("d,p", CASES)
+def test_line_factorisation_matches_dense_Q(es, d, p):
+    # Q^(l) = W D^(l) is the sum over line directions of coefficient x X with
+    # the unskewed 1D matrices (the linear-advection workload's skew-symmetric form uses Q itself)
+    n = p + 1
+    Qd = O.ref_get(d, p, "Q")
+    w = es.ref_table(d, p, "w")
+    w3 = es.ref_table(d, p, "w3")
+    eta = es.ref_table(d, p, "eta")
+    X = {nm: es.ref_table(d, p, nm).reshape(n, n) for nm in ("fQ1", "fA1", "fA2")}
+    if d == 3:
+        X.update({nm: es.ref_table(d, p, nm).reshape(n, n) for nm in ("fA3", "fA4")})
+    Qa = np.zeros_like(Qd)
+    for k in range(d):
+        for i, j, a, b, c in _lines(d, n, k, diagonal=True):
+            if d == 2:
+                ex = [w[c[1]] * X["fQ1"][a, b], w[c[1]] * X["fA1"][a, b]] if k == 0 else [0.0, w[c[0]] * X["fA2"][a, b]]
+            elif k == 0:
+                cl = 0.5 * w[c[1]] * w3[c[2]]
+                ex = [cl * X["fQ1"][a, b], cl * X["fA1"][a, b], cl * X["fA1"][a, b]]
+            elif k == 1:
+                cl = 0.5 * w[c[0]] * w3[c[2]]
+                ex = [0.0, cl * X["fA2"][a, b], cl * X["fA3"][a, b]]
+            else:
+                cl = 0.125 * w[c[0]] * w[c[1]] * (1 - eta[c[1]])
+                ex = [0.0, 0.0, cl * X["fA4"][a, b]]
+            for l in range(d):
+                Qa[l, i, j] += ex[l]
+    assert np.abs(Qa - Qd).max() < 2e-14 * np.abs(Qd).max()
 
 
 @pytest.mark.parametrize("d,p", [(2, 3), (2, 6), (3, 2), (3, 4)])
