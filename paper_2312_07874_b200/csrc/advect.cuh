@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(128) adv_rhs_kernel(DevRef R, AdvArgs A) {
   double* y = t2 + ((t2_size<DIM, N>() + 1) & ~1);  // [Nq]
   double* um = y + ((Nq + 1) & ~1);                // [Np]
   double* X = um + ((Np + 1) & ~1);                // [5][N][N]
-  double* ps = X + 5 * N * N;
+  double* ps = X + ((5 * N * N + 1) & ~1);  // 16-byte aligned psi rows
   const PsiS T = stage_psi<DIM, N>(R, ps);
   const int64_t e = blockIdx.x;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -252,7 +252,7 @@ template <int DIM, int N>
 __host__ __device__ constexpr size_t adv_rhs_smem_doubles() {
   using S = Sz<DIM, N>;
   return ((S::Nq + 1) & ~1) * 3 + ((DIM * S::Nq + 1) & ~1) + ((S::NF + 1) & ~1) + ((t1_size<DIM, N>() + 1) & ~1) +
-         ((t2_size<DIM, N>() + 1) & ~1) + ((S::Np + 1) & ~1) + 5 * N * N + psi_smem_doubles<DIM, N>();
+         ((t2_size<DIM, N>() + 1) & ~1) + ((S::Np + 1) & ~1) + ((5 * N * N + 1) & ~1) + psi_smem_doubles<DIM, N>();
 }
 
 }  // namespace esb
