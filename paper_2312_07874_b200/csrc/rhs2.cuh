@@ -35,7 +35,10 @@ struct Lw {  // line-group layout
   static constexpr int NW = SLOTS <= ES_K2_NWMAX ? SLOTS : ES_K2_NWMAX;
   static constexpr int NT = NW * 32;
   static constexpr int NS = N / 2;                            // shifts
-  static constexpr int VB = 2;  // volume pair jobs per flux batch (ILP vs registers: 4 spills at N = 9)
+#ifndef ES_K2_VB
+#define ES_K2_VB 2
+#endif
+  static constexpr int VB = ES_K2_VB;  // volume pair jobs per flux batch (ILP vs registers: 4 spills at N = 9)
 };
 
 __host__ __device__ constexpr int ev2(int x) { return (x + 1) & ~1; }
@@ -60,7 +63,10 @@ struct Rhs2Smem {
   static constexpr int FS = S::Nf * S::NC * S::Nqf;  // B J_f f* (bulk copy), then s = B J_f f* - C^T 1
   // per-warp reduction scratch of the line sums: SCV variables per round, sized to fit the region
   // it shares with the modal result (all NC at once when there is room)
-  static constexpr int SCV = W::NW * S::NC * 32 <= UM ? S::NC : (UM / (W::NW * 32) >= 1 ? UM / (W::NW * 32) : 1);
+  // (all NC variables per round: the facet-side line sums are a latency chain per round, and in 3D
+  // the region no longer holds the modal result, so it is sized for the scratch)
+  static constexpr int SCV_FIT = W::NW * S::NC * 32 <= UM ? S::NC : (UM / (W::NW * 32) >= 1 ? UM / (W::NW * 32) : 1);
+  static constexpr int SCV = DIM == 3 ? S::NC : SCV_FIT;
   static constexpr int SC = W::NW * SCV * 32;
   static constexpr int WJ0 = ((S::NG * S::Nq) % 2 == 0) ? S::NG * S::Nq : (S::NG + 1) * S::Nq;  // first even row
   static constexpr int WJN = ((S::NG * S::Nq) % 2 == 0) ? 2 * S::Nq : ev2(S::Nq);                // doubles copied
