@@ -23,8 +23,6 @@ cudaError_t launch_project_2d(int n, const DevRef& R, const ProjArgs& A, cudaStr
 cudaError_t launch_project_3d(int n, const DevRef& R, const ProjArgs& A, cudaStream_t st);
 cudaError_t launch_rhs_2d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
 cudaError_t launch_rhs_3d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st);
-cudaError_t launch_iface_2d(int n, const DevRef& R, const IfaceArgs& A, cudaStream_t st);
-cudaError_t launch_iface_3d(int n, const DevRef& R, const IfaceArgs& A, cudaStream_t st);
 cudaError_t launch_projnodal_2d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st);
 cudaError_t launch_projnodal_3d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st);
 cudaError_t launch_evalnodal_2d(int n, const DevRef& R, int64_t ne, const double* um, double* un, cudaStream_t st);
@@ -63,7 +61,7 @@ struct es_context {
   DevRef R{};
   void* d_tables = nullptr;
   double *geo_vol = nullptr, *geo_face = nullptr, *xq = nullptr, *jt = nullptr;
-  double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr, *fstar = nullptr;
+  double *prim = nullptr, *trace = nullptr, *wt = nullptr, *part = nullptr, *red = nullptr;
   double *rbuf = nullptr, *wjk3 = nullptr;  // 3D: nodal residual for K3, W / J~ in K3's layout
   double* xmapv = nullptr;                   // [nloc][Npg][dim] mapping-node positions (es_eval_points)
   unsigned long long* dcounts = nullptr;    // es_count_fluxes: per-element flux-evaluation counters
@@ -199,7 +197,9 @@ cudaError_t run_project(es_context* c, const double* u, int64_t n, const int64_t
   return c->d == 2 ? launch_project_2d(c->n, c->R, A, c->stream) : launch_project_3d(c->n, c->R, A, c->stream);
 }
 
-cudaError_t run_rhs(es_context* c, RhsArgs A, int64_t n, const int64_t* list) {
+// K2 (interface fluxes, line-wise flux differencing, facet correction, lifting; + the 2D epilogue) on
+// n elements (all, or an element list)
+cudaError_t run_k2(es_context* c, RhsArgs A, int64_t n, const int64_t* list) {
   A.n_elem = n;
   A.elem_list = list;
   if (n <= 0) return cudaSuccess;
@@ -218,37 +218,23 @@ cudaError_t run_rhs(es_context* c, RhsArgs A, int64_t n, const int64_t* list) {
     cudaEventRecord(te.b, c->stream);
     c->tev.push_back(te);
   }
-  if (e != cudaSuccess || c->d == 2) return e;
-  // 3D: weight-adjusted inverse and the RK / entropy epilogue, batched over elements (K3)
-  WadjArgs W{n, c->rbuf, c->wjk3, A.mode, A.out, A.u0, A.acc, A.ustage, A.dt, A.wt, A.part, A.c0};
+  return e;
+}
+
+// 3D: weight-adjusted inverse and the RK / entropy epilogue, batched over all local elements (K3)
+cudaError_t run_k3(es_context* c, const RhsArgs& A) {
+  if (c->d == 2) return cudaSuccess;
+  WadjArgs W{c->nloc, c->rbuf, c->wjk3, A.mode, A.out, A.u0, A.acc, A.ustage, A.dt, A.wt, A.part, A.c0};
   TimedEvent t3{};
   if (c->timing) {
     t3 = {get_event(c), get_event(c), 3};
     cudaEventRecord(t3.a, c->stream);
   }
   c->launches++;
-  e = launch_wadj_3d(c->n, W, c->stream);
+  cudaError_t e = launch_wadj_3d(c->n, W, c->stream);
   if (c->timing) {
     cudaEventRecord(t3.b, c->stream);
     c->tev.push_back(t3);
-  }
-  return e;
-}
-
-cudaError_t run_iface(es_context* c, int64_t n, const int64_t* list) {
-  if (n <= 0) return cudaSuccess;
-  IfaceArgs I{n, list, c->trace, c->geo_face, c->face_slot, c->face_reflect, c->fstar, c->gamma, c->es,
-              c->counting ? c->dcounts : nullptr};
-  TimedEvent te{};
-  if (c->timing) {
-    te = {get_event(c), get_event(c), 2};
-    cudaEventRecord(te.a, c->stream);
-  }
-  c->launches++;
-  cudaError_t e = c->d == 2 ? launch_iface_2d(c->n, c->R, I, c->stream) : launch_iface_3d(c->n, c->R, I, c->stream);
-  if (c->timing) {
-    cudaEventRecord(te.b, c->stream);
-    c->tev.push_back(te);
   }
   return e;
 }
@@ -265,7 +251,6 @@ RhsArgs base_rhs_args(es_context* c) {
   A.es = c->es;
   A.c0 = c->c0;
   A.dbg = c->dbg;
-  A.fstar = c->fstar;
   A.max_ctas = c->num_sms;
   A.eq56 = c->eq56;
   A.sdense = c->sdense;
@@ -299,8 +284,8 @@ es_status rhs_first(es_context* c, const double* u, double* wt) {
 
 // second half: interface fluxes (halo slots filled) and the flux-differencing kernel
 es_status rhs_second(es_context* c, RhsArgs A) {
-  CK(run_iface(c, c->nloc, nullptr));
-  CK(run_rhs(c, A, c->nloc, nullptr));
+  CK(run_k2(c, A, c->nloc, nullptr));
+  CK(run_k3(c, A));
   return ES_OK;
 }
 
@@ -355,11 +340,12 @@ es_status rhs_phase_b_loopback(es_context* c, es_context* const* group) {
 
 es_status rhs_phase_c(es_context* c, RhsArgs A) {
   if (c->world == 1) return rhs_second(c, A);
-  // interface fluxes of elements without remote neighbours overlap the exchange
-  CK(run_iface(c, (int64_t)c->plan.interior.size(), c->d_interior));
+  // the flux kernel on elements without remote neighbours overlaps the exchange (SURVEY 8(e),
+  // north_star: "overlapped with the volume kernel"), then the boundary elements, then K3 on all
+  CK(run_k2(c, A, (int64_t)c->plan.interior.size(), c->d_interior));
   CK(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
-  CK(run_iface(c, (int64_t)c->plan.boundary.size(), c->d_boundary));
-  CK(run_rhs(c, A, c->nloc, nullptr));
+  CK(run_k2(c, A, (int64_t)c->plan.boundary.size(), c->d_boundary));
+  CK(run_k3(c, A));
   return ES_OK;
 }
 
@@ -397,7 +383,7 @@ void es_destroy(es_context* c) {
                   (void*)c->prim, (void*)c->trace, (void*)c->wt, (void*)c->part, (void*)c->red,
                   (void*)c->face_slot, (void*)c->d_interior, (void*)c->d_boundary, (void*)c->d_send,
                   (void*)c->face_reflect, (void*)c->bad, (void*)c->U, (void*)c->ACC, (void*)c->US,
-                  (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg, (void*)c->fstar,
+                  (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg,
                   (void*)c->dpy, (void*)c->dppart, (void*)c->sdense, (void*)c->rbdense, (void*)c->rbuf,
                   (void*)c->wjk3, (void*)c->dcounts, (void*)c->xmapv, (void*)c->adv_unod, (void*)c->adv_trace,
                   (void*)c->adv_X, (void*)c->adv_acc, (void*)c->adv_us, (void*)c->adv_part})
@@ -565,7 +551,6 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   const size_t nmod = (size_t)c->nloc * c->NC * c->Np;
   CK(cudaMalloc((void**)&c->prim, (size_t)c->nloc * even_up((c->NC + 1) * c->Nq + 1) * sizeof(double)));
   CK(cudaMalloc((void**)&c->trace, (size_t)c->nslots * c->NC * c->Nqf * sizeof(double)));
-  CK(cudaMalloc((void**)&c->fstar, (size_t)c->nloc * c->Nf * c->NC * c->Nqf * sizeof(double)));
   CK(cudaMalloc((void**)&c->wt, nmod * sizeof(double)));
   CK(cudaMalloc((void**)&c->part, (size_t)c->nloc * (2 + c->NC) * sizeof(double)));
   CK(cudaMalloc((void**)&c->red, 8 * sizeof(double)));

@@ -82,7 +82,6 @@ struct RhsArgs {
   double* part;               // entropy mode: [nloc][2 + NC]
   double c0;                  // value of the constant PKD mode (1/sqrt|ref|)
   long long* dbg;             // optional [4096][16] phase clock stamps (diagnostics)
-  const double* fstar;        // [nloc][Nf][NC][Nqf] B J_f f* from the interface kernel
   int max_ctas;               // number of SMs (the launcher multiplies by resident CTAs per SM)
   int eq56;                   // 1: per-operator fluxes (Eq. num_fluxes ablation), 0: line-wise
   const double* sdense;       // volume_mode 2: dense S^(l) [l][j][i]
@@ -92,18 +91,6 @@ struct RhsArgs {
   unsigned long long* counts; // counting launch: [nloc][4] volume / facet-correction / issued flux evaluations
 };
 
-struct IfaceArgs {
-  int64_t n_elem;
-  const int64_t* elem_list;
-  const double* trace;        // [slots][NC][Nqf] entropy-projected primitive states at facet nodes
-  const double* geo_face;     // [nloc][Nf][DIM][Nqf] J n
-  const int64_t* face_slot;   // [nloc][Nf]
-  const int* face_reflect;    // [nloc][Nf]
-  double* fstar;              // [nloc][Nf][NC][Nqf]
-  double gamma;
-  int es;
-  unsigned long long* counts; // counting launch: [nloc][4], slot 3 = interface flux evaluations
-};
 
 // ------------------------------------------------------------------------------------------------
 // physics: the two-point flux and the logarithmic mean live in rhs2.cuh

@@ -22,7 +22,6 @@ namespace esb {
 
 cudaError_t launch_project_2d(int n, const DevRef& R, const ProjArgs& A, cudaStream_t st) { ES_CASES(do_project, R, A, st) }
 cudaError_t launch_rhs_2d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st) { ES_CASES(do_rhs, R, A, st) }
-cudaError_t launch_iface_2d(int n, const DevRef& R, const IfaceArgs& A, cudaStream_t st) { ES_CASES(do_iface, R, A, st) }
 cudaError_t launch_projnodal_2d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st) {
   ES_CASES(do_projnodal, R, ne, un, um, st)
 }

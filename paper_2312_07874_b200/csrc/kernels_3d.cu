@@ -47,7 +47,6 @@ cudaError_t upload_psi_3d_k1(int n, const double* p1, const double* p2, const do
 
 cudaError_t launch_project_3d(int n, const DevRef& R, const ProjArgs& A, cudaStream_t st) { ES_CASES(do_project, R, A, st) }
 cudaError_t launch_rhs_3d(int n, const DevRef& R, const RhsArgs& A, cudaStream_t st) { ES_CASES(do_rhs, R, A, st) }
-cudaError_t launch_iface_3d(int n, const DevRef& R, const IfaceArgs& A, cudaStream_t st) { ES_CASES(do_iface, R, A, st) }
 cudaError_t launch_projnodal_3d(int n, const DevRef& R, int64_t ne, const double* un, double* um, cudaStream_t st) {
   ES_CASES(do_projnodal, R, ne, un, um, st)
 }

@@ -60,7 +60,8 @@ struct Rhs2Smem {
   static constexpr int FP = S::Nf * S::NC * S::Nqf;  // facet states [z][rho, v, p][f] (bulk copy)
   static constexpr int FB = ev2(S::NF);              // facet beta = rho / p
   static constexpr int FJ = S::Nf * DIM * S::Nqf;    // J n at facet nodes [z][m][f] (bulk copy)
-  static constexpr int FS = S::Nf * S::NC * S::Nqf;  // B J_f f* (bulk copy), then s = B J_f f* - C^T 1
+  static constexpr int FS = S::Nf * S::NC * S::Nqf;  // B J_f f* (computed in the prologue), then s = B J_f f* - C^T 1
+  static constexpr int FN = S::Nf * S::NC * S::Nqf;  // neighbour traces at this element's facet nodes (cp.async)
   // per-warp reduction scratch of the line sums: SCV variables per round, sized to fit the region
   // it shares with the modal result (all NC at once when there is room)
   // (all NC variables per round: the facet-side line sums are a latency chain per round, and in 3D
@@ -75,7 +76,7 @@ struct Rhs2Smem {
   static constexpr int SCU = SC > UM ? SC : UM;   // warp scratch, then modal result + facet-4 lifting
   static constexpr int o_tb = 0, o_ps = ev2(o_tb + TB), o_pr = ev2(o_ps + PS), o_g = o_pr + PR, o_r = ev2(o_g + GG),
                        o_pt = ev2(o_r + RR), o_fp = ev2(o_pt + PB), o_fb = ev2(o_fp + FP),
-                       o_fj = ev2(o_fb + FB), o_fs = ev2(o_fj + FJ), o_sc = ev2(o_fs + FS), o_um = o_sc, o_wj = ev2(o_sc + SCU),
+                       o_fj = ev2(o_fb + FB), o_fs = ev2(o_fj + FJ), o_fn = ev2(o_fs + FS), o_sc = ev2(o_fn + FN), o_um = o_sc, o_wj = ev2(o_sc + SCU),
                        total = ev2(o_wj + (DIM == 2 ? 2 * ev2(WJN) : 0));  // 2D: W/J~ double-buffered by element parity
   static_assert(S::PRS <= PR, "prim copy");
   static_assert(total * 8 <= 227 * 1024 - 256, "shared memory");
@@ -261,7 +262,137 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 }
 
 // mbarriers of the flux kernel: element data for the passes (A) / interface fluxes and W/J~ (B)
-__shared__ uint64_t k2_barA, k2_barB;
+__shared__ uint64_t k2_barA;
+
+// entropy variables of a primitive state (App. B, R7): w = ((g - s)/(g - 1) - b|v|^2/2, b v, -b),
+// s = ln p - g ln rho, b = rho / p
+template <int DIM>
+__device__ __forceinline__ void wvars(const NodeState& a, double g, double* w) {
+  double v2 = 0.0;
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) v2 += a.v[m] * a.v[m];
+  const double s = log(a.p) - g * log(a.r);
+  w[0] = (g - s) / (g - 1.0) - 0.5 * a.b * v2;
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) w[1 + m] = a.b * a.v[m];
+  w[DIM + 1] = -a.b;
+}
+// D = (du/dw)(u(wbar)) (w+ - w-), wbar the mean of the two sides' entropy variables (reading R27).
+// du/dw in primitive form, applied without forming the matrix:
+//   D_0   = rho (dw_0 + v.dw_v) + E dw_E
+//   D_v   = rho v (dw_0 + v.dw_v) + p dw_v + rho h v dw_E
+//   D_E   = E dw_0 + rho h v.dw_v + (rho h^2 - g p^2 / (rho (g - 1))) dw_E,  h = (E + p) / rho
+// MAT (reading R28): D = |A_n| (du/dw) [w] at the same state, with the Barth-scaled eigenvectors:
+//   |v.n| (du/dw)[w] + sum_{+,-} (|v.n +- a| - |v.n|) rho/(2g) (r_+- . [w]) r_+-,
+//   r_+- = (1, v +- a n, h +- a v.n), a^2 = g p / rho; lam is unused then
+template <int DIM, bool MAT = false>
+__device__ __forceinline__ void entropy_jump(const NodeState& um, const NodeState& up, double g, double* D,
+                                             const double* nu = nullptr) {
+  double wm[DIM + 2], wp[DIM + 2], wb[DIM + 2], dw[DIM + 2];
+  wvars<DIM>(um, g, wm);
+  wvars<DIM>(up, g, wp);
+#pragma unroll
+  for (int k = 0; k < DIM + 2; ++k) {
+    wb[k] = 0.5 * (wm[k] + wp[k]);
+    dw[k] = wp[k] - wm[k];
+  }
+  // u(wbar): b = -w_last, v = w_v / b, s = g - (g - 1)(w_0 + b|v|^2/2), rho = (b e^s)^(1/(1-g))
+  const double b = -wb[DIM + 1];
+  double v[DIM], v2 = 0.0, vdw = 0.0;
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) {
+    v[m] = wb[1 + m] / b;
+    v2 += v[m] * v[m];
+  }
+  const double s = g - (g - 1.0) * (wb[0] + 0.5 * b * v2);
+  const double r = exp((s + log(b)) / (1.0 - g)), p = r / b;
+  const double E = p / (g - 1.0) + 0.5 * r * v2, rh = E + p;
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) vdw += v[m] * dw[1 + m];
+  const double c0 = r * (dw[0] + vdw);
+  D[0] = c0 + E * dw[DIM + 1];
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) D[1 + m] = v[m] * (c0 + rh * dw[DIM + 1]) + p * dw[1 + m];
+  D[DIM + 1] = E * dw[0] + rh * vdw + (rh * rh / r - g * p * p / (r * (g - 1.0))) * dw[DIM + 1];
+  if constexpr (MAT) {
+    const double a = sqrt(g * p / r), h = rh / r;
+    double vn = 0.0, adn = 0.0;
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) {
+      vn += v[m] * nu[m];
+      adn += nu[m] * dw[1 + m];
+    }
+    const double avn = fabs(vn);
+    // r_+- . [w] = dw_0 + v.dw_v +- a n.dw_v + (h +- a v.n) dw_E
+    const double base = dw[0] + vdw + h * dw[DIM + 1], sh = a * (adn + vn * dw[DIM + 1]);
+    const double km = (fabs(vn - a) - avn) * r / (2.0 * g) * (base - sh);
+    const double kp = (fabs(vn + a) - avn) * r / (2.0 * g) * (base + sh);
+    D[0] = avn * D[0] + km + kp;
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) D[1 + m] = avn * D[1 + m] + km * (v[m] - a * nu[m]) + kp * (v[m] + a * nu[m]);
+    D[DIM + 1] = avn * D[DIM + 1] + km * (h - a * vn) + kp * (h + a * vn);
+  }
+}
+
+
+// interface flux at one facet node (Davis' wave speed P:839): EC flux in the unit normal
+// n = J n / J_f of this side plus the dissipation of mode ES (0 none, 1 LLF, 2 entropy jump R27, 3
+// matrix R28); returns B J_f f* in out[v * ostride].  um / up: own and neighbour traces (rho, v, p/2) at
+// the node with strides; both sides of a face evaluate it with their own normals (partition-independent)
+template <int DIM>
+__device__ __forceinline__ void iface_node_flux(int es, const double* tm, int sm_, const double* tp, int sp,
+                                                const double* Jn, double Bf, double g, double* out, int ostride) {
+  constexpr int NC = DIM + 2;
+  const double gm1inv = 1.0 / (g - 1.0);
+  NodeState um, up;
+  um.r = tm[0];
+  up.r = tp[0];
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) {
+    um.v[m] = tm[(1 + m) * sm_];
+    up.v[m] = tp[(1 + m) * sp];
+  }
+  um.p = 2.0 * tm[(DIM + 1) * sm_];  // the trace rows hold p / 2
+  up.p = 2.0 * tp[(DIM + 1) * sp];
+  um.b = um.r / um.p;
+  up.b = up.r / up.p;
+  double Jf = 0.0;
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) Jf += Jn[m] * Jn[m];
+  Jf = sqrt(Jf);
+  double nu[DIM];
+#pragma unroll
+  for (int m = 0; m < DIM; ++m) nu[m] = Jn[m] / Jf;
+  double F[NC];
+  ec_flux_v2<DIM>(um, up, nu, gm1inv, F);
+  if (es != 0) {  // dissipation with Davis's wave speed
+    double vnm = 0.0, vnp = 0.0;
+#pragma unroll
+    for (int m = 0; m < DIM; ++m) {
+      vnm += um.v[m] * nu[m];
+      vnp += up.v[m] * nu[m];
+    }
+    const double lam = fmax(fabs(vnm), fabs(vnp)) + fmax(sqrt(g * um.p / um.r), sqrt(g * up.p / up.r));
+    double D[NC];
+    if (es == 1) {  // local Lax-Friedrichs on the conservative jump
+      double Um[NC], Up[NC];
+      cons_of<DIM>(um.r, um.v, um.p, gm1inv, Um);
+      cons_of<DIM>(up.r, up.v, up.p, gm1inv, Up);
+#pragma unroll
+      for (int v = 0; v < NC; ++v) D[v] = Up[v] - Um[v];
+    } else if (es == 2) {  // entropy-jump scalar dissipation (R27): (du/dw)(u(wbar)) [w]
+      entropy_jump<DIM>(um, up, g, D);
+    } else {  // matrix dissipation (R28): |A_n| (du/dw) [w] at u(wbar), no lambda
+      entropy_jump<DIM, true>(um, up, g, D, nu);
+    }
+    const double sc = es == 3 ? 0.5 : 0.5 * lam;
+#pragma unroll
+    for (int v = 0; v < NC; ++v) F[v] -= sc * D[v];
+  }
+  const double bj = Bf * Jf;
+#pragma unroll
+  for (int v = 0; v < NC; ++v) out[v * ostride] = bj * F[v];
+}
 
 template <int DIM, int N>
 __device__ __forceinline__ void k2_epilogue_2d(const RhsArgs& A, int64_t e, unsigned it);
@@ -313,11 +444,19 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &k2_barA);
     if constexpr (DIM == 2) bulk_g2s(smk2 + L::o_wj + buf * ev2(L::WJN), A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barA);
   };
-  auto issue_B = [&](int64_t e) {
-    constexpr unsigned bS = L::FS * 8;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&k2_barB, bS);
-    bulk_g2s(fS, A.fstar + (size_t)e * L::FS, bS, &k2_barB);
+  // the neighbour traces of an element's facet nodes, gathered by 8-byte asynchronous copies in this
+  // element's node order (the face permutation P:736-741 applied by the copy); they land during the
+  // previous element's passes
+  auto prefetch_nbr = [&](int64_t e) {
+    double* fN = smk2 + L::o_fn;
+    for (int q = tid; q < S::Nf * NC * Nqf; q += NT) {
+      const int z = q / (NC * Nqf), r = q - z * NC * Nqf, v = r / Nqf, f = r - v * Nqf;
+      const int64_t slot = A.face_slot[e * S::Nf + z];
+      const int rf = A.face_reflect[e * S::Nf + z];
+      const int fo = DIM == 2 ? (rf ? N - 1 - f : f) : (rf ? (N - 1 - f % N) + N * (f / N) : f);
+      cp_async8(fN + q, A.trace + (size_t)slot * NC * Nqf + v * Nqf + fo);
+    }
+    cp_async_commit();
   };
   const int grp = lane / N, pos = lane - grp * N;
   const bool lane_ok = grp < W::LPW;
@@ -333,6 +472,11 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     (void)k;
 #endif
   };
+  // flux-evaluation counters of the counting instantiation (CNT): evaluations with a nonzero operator
+  // coefficient in the volume (cv) and facet-correction (cf) passes, every evaluation the lane issued,
+  // masked or not (ci), and the interface fluxes (cI) -- observed in the kernel, compared with the
+  // oracle's counted loops
+  int cv = 0, cf = 0, ci = 0, cI = 0;
   stamp(0);
   mbar_wait(&k2_barA, it & 1);
   // facet beta = rho / p = (rho / (p/2)) / 2 (the volume beta rows and the element's all-Taylor flag
@@ -341,8 +485,24 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     const double* q = fP + (fz / Nqf) * NC * Nqf + fz % Nqf;
     fB[fz] = 0.5 * (q[0] / q[(DIM + 1) * Nqf]);
   }
-  mbar_wait(&k2_barB, it & 1);  // f* is updated in place by the passes
+  cp_async_wait_all();  // this element's neighbour traces
   __syncthreads();
+  // interface fluxes at the element's facet nodes, B J_f f* into fS (the
+  // facet-correction passes then subtract C^T 1 in place)
+  {
+    const double* fN = smk2 + L::o_fn;
+    for (int fz = tid; fz < NF; fz += NT) {
+      const int z = fz / Nqf, f = fz - z * Nqf;
+      double Jn[DIM];
+#pragma unroll
+      for (int m = 0; m < DIM; ++m) Jn[m] = fJ[(z * DIM + m) * Nqf + f];
+      iface_node_flux<DIM>(A.es, fP + z * NC * Nqf + f, Nqf, fN + z * NC * Nqf + f, Nqf, Jn, tB[fz], g,
+                           fS + z * NC * Nqf + f, Nqf);
+      if constexpr (CNT) ++cI;
+    }
+  }
+  __syncthreads();
+  if (has_next) prefetch_nbr(elem_of(nidx));  // fN is consumed
   const bool all_taylor = sP[(DIM + 3) * Nq] != 0.0;
   stamp(1);
 
@@ -357,10 +517,6 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   };
   auto Gat = [&](int l, int m, int i) { return sG[(l * DIM + m) * Nq + i]; };
 
-  // flux-evaluation counters of the counting instantiation (CNT): evaluations with a nonzero operator
-  // coefficient in the volume (cv) and facet-correction (cf) passes, and every evaluation the lane
-  // issued, masked or not (ci) -- observed in the kernel, compared with the oracle's counted loops
-  int cv = 0, cf = 0, ci = 0;
   // ---- direction passes, one specialisation per direction k ----
   // DST: 0 = sR = acc (first pass), 1 = sR += acc, 2 = pt = acc (the pt buffer holds a second
   // residual so that two passes can run without a barrier between them); SYNC: end with a barrier
@@ -817,7 +973,9 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     cv = __reduce_add_sync(0xffffffffu, cv);
     cf = __reduce_add_sync(0xffffffffu, cf);
     ci = __reduce_add_sync(0xffffffffu, ci);
+    cI = __reduce_add_sync(0xffffffffu, cI);
     if (lane == 0) {
+      atomicAdd(A.counts + e * 4 + 3, (unsigned long long)cI);
       atomicAdd(A.counts + e * 4 + 0, (unsigned long long)cv);
       atomicAdd(A.counts + e * 4 + 1, (unsigned long long)cf);
       atomicAdd(A.counts + e * 4 + 2, (unsigned long long)ci);
@@ -853,7 +1011,6 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     }
     __syncthreads();
     stamp(7);
-    if (tid == 0 && has_next) issue_B(elem_of(nidx));
     return;
   } else {
     for (int i = tid; i < Nq; i += NT) {
@@ -867,8 +1024,6 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     }
     __syncthreads();
     stamp(7);
-    // the interface fluxes are consumed: the next element's copy lands during the transforms
-    if (tid == 0 && has_next) issue_B(elem_of(nidx));
     k2_epilogue_2d<DIM, N>(A, e, it);
   }
 }
@@ -1019,21 +1174,26 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
     bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &k2_barA);
     if constexpr (DIM == 2) bulk_g2s(smk2 + L::o_wj + buf * ev2(L::WJN), A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barA);
   };
-  auto issue_B = [&](int64_t e) {
-    constexpr unsigned bS = L::FS * 8;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&k2_barB, bS);
-    bulk_g2s(fS, A.fstar + (size_t)e * L::FS, bS, &k2_barB);
+  // the neighbour traces of an element's facet nodes, gathered by 8-byte asynchronous copies in this
+  // element's node order (the face permutation P:736-741 applied by the copy); they land during the
+  // previous element's passes
+  auto prefetch_nbr = [&](int64_t e) {
+    double* fN = smk2 + L::o_fn;
+    for (int q = tid; q < S::Nf * NC * Nqf; q += NT) {
+      const int z = q / (NC * Nqf), r = q - z * NC * Nqf, v = r / Nqf, f = r - v * Nqf;
+      const int64_t slot = A.face_slot[e * S::Nf + z];
+      const int rf = A.face_reflect[e * S::Nf + z];
+      const int fo = DIM == 2 ? (rf ? N - 1 - f : f) : (rf ? (N - 1 - f % N) + N * (f / N) : f);
+      cp_async8(fN + q, A.trace + (size_t)slot * NC * Nqf + v * Nqf + fo);
+    }
+    cp_async_commit();
   };
   // ---- per-CTA: barriers, first element's copies, constant tables ----
   if (tid == 0) {
     mbar_init(&k2_barA, 1);
-    mbar_init(&k2_barB, 1);
-    if ((int64_t)blockIdx.x < A.n_elem) {
-      issue_A(elem_of(blockIdx.x), 0);
-      issue_B(elem_of(blockIdx.x));
-    }
+    if ((int64_t)blockIdx.x < A.n_elem) issue_A(elem_of(blockIdx.x), 0);
   }
+  if ((int64_t)blockIdx.x < A.n_elem) prefetch_nbr(elem_of(blockIdx.x));
   for (int k = tid; k < N * N; k += NT) {
     tQ1[k] = R.skQ1[k];
     tA1[k] = R.skA1[k];
@@ -1092,156 +1252,6 @@ __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_eq56_kernel(DevRef R, 
 template <int DIM, int N>
 __global__ void __launch_bounds__(Lw<DIM, N>::NT, 1) rhs2_dense_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
   rhs2_body<DIM, N, false, true>(R, A);
-}
-
-// entropy variables of a primitive state (App. B, R7): w = ((g - s)/(g - 1) - b|v|^2/2, b v, -b),
-// s = ln p - g ln rho, b = rho / p
-template <int DIM>
-__device__ __forceinline__ void wvars(const NodeState& a, double g, double* w) {
-  double v2 = 0.0;
-#pragma unroll
-  for (int m = 0; m < DIM; ++m) v2 += a.v[m] * a.v[m];
-  const double s = log(a.p) - g * log(a.r);
-  w[0] = (g - s) / (g - 1.0) - 0.5 * a.b * v2;
-#pragma unroll
-  for (int m = 0; m < DIM; ++m) w[1 + m] = a.b * a.v[m];
-  w[DIM + 1] = -a.b;
-}
-// D = (du/dw)(u(wbar)) (w+ - w-), wbar the mean of the two sides' entropy variables (reading R27).
-// du/dw in primitive form, applied without forming the matrix:
-//   D_0   = rho (dw_0 + v.dw_v) + E dw_E
-//   D_v   = rho v (dw_0 + v.dw_v) + p dw_v + rho h v dw_E
-//   D_E   = E dw_0 + rho h v.dw_v + (rho h^2 - g p^2 / (rho (g - 1))) dw_E,  h = (E + p) / rho
-// MAT (reading R28): D = |A_n| (du/dw) [w] at the same state, with the Barth-scaled eigenvectors:
-//   |v.n| (du/dw)[w] + sum_{+,-} (|v.n +- a| - |v.n|) rho/(2g) (r_+- . [w]) r_+-,
-//   r_+- = (1, v +- a n, h +- a v.n), a^2 = g p / rho; lam is unused then
-template <int DIM, bool MAT = false>
-__device__ __forceinline__ void entropy_jump(const NodeState& um, const NodeState& up, double g, double* D,
-                                             const double* nu = nullptr) {
-  double wm[DIM + 2], wp[DIM + 2], wb[DIM + 2], dw[DIM + 2];
-  wvars<DIM>(um, g, wm);
-  wvars<DIM>(up, g, wp);
-#pragma unroll
-  for (int k = 0; k < DIM + 2; ++k) {
-    wb[k] = 0.5 * (wm[k] + wp[k]);
-    dw[k] = wp[k] - wm[k];
-  }
-  // u(wbar): b = -w_last, v = w_v / b, s = g - (g - 1)(w_0 + b|v|^2/2), rho = (b e^s)^(1/(1-g))
-  const double b = -wb[DIM + 1];
-  double v[DIM], v2 = 0.0, vdw = 0.0;
-#pragma unroll
-  for (int m = 0; m < DIM; ++m) {
-    v[m] = wb[1 + m] / b;
-    v2 += v[m] * v[m];
-  }
-  const double s = g - (g - 1.0) * (wb[0] + 0.5 * b * v2);
-  const double r = exp((s + log(b)) / (1.0 - g)), p = r / b;
-  const double E = p / (g - 1.0) + 0.5 * r * v2, rh = E + p;
-#pragma unroll
-  for (int m = 0; m < DIM; ++m) vdw += v[m] * dw[1 + m];
-  const double c0 = r * (dw[0] + vdw);
-  D[0] = c0 + E * dw[DIM + 1];
-#pragma unroll
-  for (int m = 0; m < DIM; ++m) D[1 + m] = v[m] * (c0 + rh * dw[DIM + 1]) + p * dw[1 + m];
-  D[DIM + 1] = E * dw[0] + rh * vdw + (rh * rh / r - g * p * p / (r * (g - 1.0))) * dw[DIM + 1];
-  if constexpr (MAT) {
-    const double a = sqrt(g * p / r), h = rh / r;
-    double vn = 0.0, adn = 0.0;
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) {
-      vn += v[m] * nu[m];
-      adn += nu[m] * dw[1 + m];
-    }
-    const double avn = fabs(vn);
-    // r_+- . [w] = dw_0 + v.dw_v +- a n.dw_v + (h +- a v.n) dw_E
-    const double base = dw[0] + vdw + h * dw[DIM + 1], sh = a * (adn + vn * dw[DIM + 1]);
-    const double km = (fabs(vn - a) - avn) * r / (2.0 * g) * (base - sh);
-    const double kp = (fabs(vn + a) - avn) * r / (2.0 * g) * (base + sh);
-    D[0] = avn * D[0] + km + kp;
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) D[1 + m] = avn * D[1 + m] + km * (v[m] - a * nu[m]) + kp * (v[m] + a * nu[m]);
-    D[DIM + 1] = avn * D[DIM + 1] + km * (h - a * vn) + kp * (h + a * vn);
-  }
-}
-
-// ------------------------------------------------------------------------------------------------
-// interface flux (Davis wave speed P:839): one thread per (element, facet node);
-// writes B J_f f*(u-, u+, n) with the element's own unit normal n = J n / J_f and the
-// neighbour's trace at the permuted node.  Both sides of a face evaluate it with their
-// own normals; the arithmetic per side does not depend on the partition.
-// ------------------------------------------------------------------------------------------------
-template <int DIM, int N, int ES>  // ES = IfaceArgs::es
-__global__ void __launch_bounds__(256, 4) iface_kernel(DevRef R, IfaceArgs A) {
-  using S = Sz<DIM, N>;
-  constexpr int NC = S::NC, Nqf = S::Nqf, NF = S::NF, Nf = S::Nf;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= A.n_elem * NF) return;
-  const int64_t idx = t / NF;
-  const int fz = (int)(t - idx * NF), z = fz / Nqf, f = fz - z * Nqf;
-  const int64_t e = A.elem_list ? A.elem_list[idx] : idx;
-  const int64_t slot = A.face_slot[e * Nf + z];
-  const int rf = A.face_reflect[e * Nf + z];
-  int fo;
-  if constexpr (DIM == 2)
-    fo = rf ? N - 1 - f : f;
-  else
-    fo = rf ? (N - 1 - f % N) + N * (f / N) : f;
-  const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
-  const double* tm = A.trace + (size_t)(e * Nf + z) * NC * Nqf + f;
-  const double* tp = A.trace + (size_t)slot * NC * Nqf + fo;
-  NodeState um, up;
-  um.r = tm[0];
-  up.r = tp[0];
-#pragma unroll
-  for (int m = 0; m < DIM; ++m) {
-    um.v[m] = tm[(1 + m) * Nqf];
-    up.v[m] = tp[(1 + m) * Nqf];
-  }
-  um.p = 2.0 * tm[(DIM + 1) * Nqf];  // the trace rows hold p / 2
-  up.p = 2.0 * tp[(DIM + 1) * Nqf];
-  um.b = um.r / um.p;
-  up.b = up.r / up.p;
-  double Jn[DIM], Jf = 0.0;
-#pragma unroll
-  for (int m = 0; m < DIM; ++m) {
-    Jn[m] = A.geo_face[((size_t)(e * Nf + z) * DIM + m) * Nqf + f];
-    Jf += Jn[m] * Jn[m];
-  }
-  Jf = sqrt(Jf);
-  double nu[DIM];
-#pragma unroll
-  for (int m = 0; m < DIM; ++m) nu[m] = Jn[m] / Jf;
-  double F[NC];
-  ec_flux_v2<DIM>(um, up, nu, gm1inv, F);
-  if constexpr (ES != 0) {  // dissipation with Davis's wave speed
-    double vnm = 0.0, vnp = 0.0;
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) {
-      vnm += um.v[m] * nu[m];
-      vnp += up.v[m] * nu[m];
-    }
-    const double lam = fmax(fabs(vnm), fabs(vnp)) + fmax(sqrt(g * um.p / um.r), sqrt(g * up.p / up.r));
-    double D[NC];
-    if constexpr (ES == 1) {  // local Lax-Friedrichs on the conservative jump
-      double Um[NC], Up[NC];
-      cons_of<DIM>(um.r, um.v, um.p, gm1inv, Um);
-      cons_of<DIM>(up.r, up.v, up.p, gm1inv, Up);
-#pragma unroll
-      for (int v = 0; v < NC; ++v) D[v] = Up[v] - Um[v];
-    } else if constexpr (ES == 2) {  // entropy-jump scalar dissipation (reading R27): (du/dw)(u(wbar)) [w]
-      entropy_jump<DIM>(um, up, g, D);
-    } else {  // matrix dissipation (reading R28): |A_n| (du/dw) [w] at u(wbar), no lambda
-      entropy_jump<DIM, true>(um, up, g, D, nu);
-    }
-    const double sc = ES == 3 ? 0.5 : 0.5 * lam;
-#pragma unroll
-    for (int v = 0; v < NC; ++v) F[v] -= sc * D[v];
-  }
-  if (A.counts) atomicAdd(A.counts + e * 4 + 3, 1ull);  // counting launch only (es_count_fluxes)
-  const double bj = __ldg(&R.Bf[fz]) * Jf;
-  double* out = A.fstar + (size_t)(e * Nf + z) * NC * Nqf + f;
-#pragma unroll
-  for (int v = 0; v < NC; ++v) out[v * Nqf] = bj * F[v];
 }
 
 }  // namespace esb
