@@ -487,22 +487,32 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   }
   cp_async_wait_all();  // this element's neighbour traces
   __syncthreads();
-  // interface fluxes at the element's facet nodes, B J_f f* into fS (the
-  // facet-correction passes then subtract C^T 1 in place)
-  {
-    const double* fN = smk2 + L::o_fn;
-    for (int fz = tid; fz < NF; fz += NT) {
+  // interface fluxes at the element's facet nodes, B J_f f*: computed in place
+  // over the neighbour traces in fN by threads [t0, t0 + nth)
+  double* fN = smk2 + L::o_fn;
+  auto compute_fstar = [&](int t, int nth, double* dst) {
+    for (int fz = t; fz < NF; fz += nth) {
       const int z = fz / Nqf, f = fz - z * Nqf;
       double Jn[DIM];
 #pragma unroll
       for (int m = 0; m < DIM; ++m) Jn[m] = fJ[(z * DIM + m) * Nqf + f];
       iface_node_flux<DIM>(A.es, fP + z * NC * Nqf + f, Nqf, fN + z * NC * Nqf + f, Nqf, Jn, tB[fz], g,
-                           fS + z * NC * Nqf + f, Nqf);
+                           dst + z * NC * Nqf + f, Nqf);
       if constexpr (CNT) ++cI;
     }
+  };
+  // HIDE (3D line-wise): the warps with one pass-1 slot fewer than the others (27 slots on 16 warps at
+  // N = 9) compute the interface fluxes in the slack of pass 1; fS starts from zero, collects -C^T 1
+  // in the passes, and f* is added before the lifting.  Otherwise f* goes into fS before the passes.
+  constexpr bool HIDE = DIM == 3 && !DN && (W::SLOTS % W::NW != 0) && (W::SLOTS > W::NW);
+  if constexpr (HIDE) {
+    for (int q = tid; q < S::Nf * NC * Nqf; q += NT) fS[q] = 0.0;
+  } else {
+    compute_fstar(tid, NT, fS);
   }
   __syncthreads();
-  if (has_next) prefetch_nbr(elem_of(nidx));  // fN is consumed
+  if constexpr (!HIDE)
+    if (has_next) prefetch_nbr(elem_of(nidx));  // fN is consumed
   const bool all_taylor = sP[(DIM + 3) * Nq] != 0.0;
   stamp(1);
 
@@ -843,7 +853,15 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   // two residuals are added
   auto passes = [&](auto tc, auto ec) {
     if constexpr (DIM == 3) {
-      pass(I1{}, tc, ec, I0{}, Yes{}, 0);
+      if constexpr (HIDE) {
+        pass(I1{}, tc, ec, I0{}, No{}, 0);
+        constexpr int extra = W::SLOTS % W::NW;  // warps below carry one pass-1 slot more
+        if (warp >= extra) compute_fstar(tid - extra * 32, (W::NW - extra) * 32, fN);
+        __syncthreads();
+        stamp(3);
+      } else {
+        pass(I1{}, tc, ec, I0{}, Yes{}, 0);
+      }
       for (int q = tid; q < NC * N * N; q += NT) {  // facet 4: C^T 1 at (a, j) = sum over c of partials
         const int v = q / (N * N), jf = (q / N) % N, a = q % N;
         double s = 0.0;
@@ -857,7 +875,11 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
       pass(I2{}, tc, ec, I2{}, No{}, 0);
       pass(I0{}, tc, ec, I1{}, Yes{}, W::SLOTS % W::NW);
       for (int q = tid; q < NC * Nq; q += NT) sR[q] += pt[q];
+      if constexpr (HIDE)  // s = B J_f f* - C^T 1
+        for (int q = tid; q < S::Nf * NC * Nqf; q += NT) fS[q] += fN[q];
       __syncthreads();
+      if constexpr (HIDE)
+        if (has_next) prefetch_nbr(elem_of(nidx));  // fN is consumed
     } else {
       pass(I0{}, tc, ec, I0{}, Yes{}, 0);
       pass(I1{}, tc, ec, I1{}, Yes{}, 0);
