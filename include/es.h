@@ -126,6 +126,14 @@ es_status es_step(es_context* ctx, double dt, int nsteps);
  * size dt (es_step) and copies the state back into u_host_out (HOST).  Synchronous. */
 es_status es_step_host(es_context* ctx, const double* u_host, double* u_host_out, double dt, int nsteps);
 
+/* One or more explicit Runge-Kutta steps with a caller-supplied Butcher tableau (s <= 16 stages; A[s][s]
+ * strictly lower triangular, row-major, b[s]; HOST arrays): U <- U + dt sum_j b_j k_j with
+ * k_j = f(U + dt sum_{l<j} a_jl k_l), on the library state.  Passing the coefficients of Dormand-Prince
+ * 8 (Hairer-Norsett-Wanner I, II.5 -- the paper's integrator) from a published table gives the
+ * paper's time integration at a fixed step.  Allocates s state-sized slope buffers on first use.
+ * Asynchronous (synchronous with check_admissibility). */
+es_status es_step_erk(es_context* ctx, double dt, int s, const double* A, const double* b, int nsteps);
+
 /* CUDA graphs for es_step (default on): with world == 1 and no per-kernel timing the launches of one
  * RK4 step are captured once per dt into a CUDA graph and replayed.  on = 0 launches them eagerly
  * (the same kernels and arguments: results are bitwise identical). */

@@ -71,6 +71,7 @@ es_count_fluxes = _sig("es_count_fluxes", _i, _vp, _vp, _lp)
 es_step_host = _sig("es_step_host", _i, _vp, _vp, _vp, ctypes.c_double, _i)
 es_set_graphs = _sig("es_set_graphs", _i, _vp, _i)
 es_eval_points = _sig("es_eval_points", _i, _vp, _vp, _i, _dp, _vp, _vp, _vp)
+es_step_erk = _sig("es_step_erk", _i, _vp, ctypes.c_double, _i, _dp, _dp, _i)
 es_adv_configure = _sig("es_adv_configure", _i, _vp, _dp, _i, _i)
 es_adv_rhs = _sig("es_adv_rhs", _i, _vp, _vp, _vp, _dp)
 es_adv_step = _sig("es_adv_step", _i, _vp, _vp, ctypes.c_double, _i)
@@ -361,6 +362,14 @@ class Context:
 
     def adv_step(self, u, dt, nsteps=1):
         self._check(es_adv_step(self.h, _ptr(u), float(dt), int(nsteps)))
+
+    def step_erk(self, dt, A, b, nsteps=1):
+        """es_step_erk: nsteps explicit Runge-Kutta steps with the Butcher tableau (A [s][s], b [s])"""
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        s = len(b)
+        assert A.shape == (s, s)
+        self._check(es_step_erk(self.h, float(dt), s, A.ctypes.data_as(_dp), b.ctypes.data_as(_dp), int(nsteps)))
 
     def count_fluxes(self, u):
         """flux evaluations counted in the kernels on one RHS of u (device tensor): int64 array

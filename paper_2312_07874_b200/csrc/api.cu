@@ -71,6 +71,9 @@ struct es_context {
   double step_graph_dt = 0.0;
   int64_t step_graph_launches = 0;
   bool use_graphs = true;
+  // es_step_erk: slopes of a caller-supplied explicit Runge-Kutta tableau, and the next-state buffer
+  std::vector<double*> erk_k;
+  double* erk_y = nullptr;
   // linear-advection workload (es_adv_*): velocity, flux, form, buffers
   double adv_a[3] = {0, 0, 0};
   int adv_flux = 1, adv_form = 0;
@@ -390,6 +393,9 @@ void es_destroy(es_context* c) {
     if (p) cudaFree(p);
   for (double* p : c->dpk)
     if (p) cudaFree(p);
+  for (double* p : c->erk_k)
+    if (p) cudaFree(p);
+  if (c->erk_y) cudaFree(c->erk_y);
   for (auto& t : c->tev) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
@@ -812,6 +818,56 @@ es_status es_step_dp54(es_context* c, double dt, double rtol, double atol, doubl
     c->dp_fsal = true;
   } else {
     c->dp_fsal = true;  // dpk[0] = f(U) still holds
+  }
+  if (c->check_adm) return check_bad(c);
+  return ES_OK;
+}
+
+es_status es_step_erk(es_context* c, double dt, int s, const double* A, const double* b, int nsteps) {
+  POISON_CHECK();
+  if (!A || !b || s < 1 || s > 16 || !(dt > 0.0))
+    return fail(c, ES_ERR_ARG, "es_step_erk: 1 <= s <= 16 stages, A[s][s], b[s], dt > 0");
+  for (int i = 0; i < s; ++i)
+    for (int j = i; j < s; ++j)
+      if (A[i * s + j] != 0.0) return fail(c, ES_ERR_ARG, "es_step_erk: A must be strictly lower triangular");
+  CK(cudaSetDevice(c->device));
+  c->dp_fsal = false;
+  const int64_t n = c->nloc * (int64_t)c->NC * c->Np;
+  while ((int)c->erk_k.size() < s) {
+    double* p = nullptr;
+    CK(cudaMalloc((void**)&p, (size_t)n * sizeof(double)));
+    c->erk_k.push_back(p);
+  }
+  if (!c->erk_y) CK(cudaMalloc((void**)&c->erk_y, (size_t)n * sizeof(double)));
+  for (int st = 0; st < nsteps; ++st) {
+    for (int i = 0; i < s; ++i) {  // k_i = f(U + dt sum_{l<i} a_il k_l)
+      const double* y = c->U;
+      RkComb kc{};
+      for (int l = 0; l < i; ++l)
+        if (A[i * s + l] != 0.0) {
+          kc.k[kc.nk] = c->erk_k[l];
+          kc.c[kc.nk++] = dt * A[i * s + l];
+        }
+      if (kc.nk > 0) {
+        CK(launch_rk_comb(c->U, kc, c->US, n, c->stream));
+        c->launches++;
+        y = c->US;
+      }
+      RhsArgs Ar = base_rhs_args(c);
+      Ar.mode = 0;
+      Ar.out = c->erk_k[i];
+      es_status r = rhs_pass(c, y, Ar, nullptr);
+      if (r != ES_OK) return r;
+    }
+    RkComb kc{};
+    for (int l = 0; l < s; ++l)
+      if (b[l] != 0.0) {
+        kc.k[kc.nk] = c->erk_k[l];
+        kc.c[kc.nk++] = dt * b[l];
+      }
+    CK(launch_rk_comb(c->U, kc, c->erk_y, n, c->stream));
+    c->launches++;
+    std::swap(c->U, c->erk_y);
   }
   if (c->check_adm) return check_bad(c);
   return ES_OK;

@@ -55,8 +55,8 @@ cudaError_t launch_reduce_parts(const double* part, int64_t ne, int w, double* o
 
 // explicit Runge-Kutta combinations over the modal state (HBM-bound streams)
 struct RkComb {
-  const double* k[7];
-  double c[7];  // coefficients of k_j (already multiplied by dt)
+  const double* k[16];
+  double c[16];  // coefficients of k_j (already multiplied by dt)
   int nk;
 };
 // out = y0 + sum_j c_j k_j

@@ -32,7 +32,11 @@ struct Sz {
   static constexpr int GVS = (NGV * Nq + 1) & ~1;  // geo_vol element stride (even, 16-B aligned)
   static constexpr int PRS = ((NC + 1) * Nq + 2) & ~1;  // prim element stride: rho, v, p, beta rows + flag
   static constexpr int KPT = (Nq + 383) / 384;
+#ifndef ES_K1_NT9  // tuning experiments: threads per CTA of the per-element kernels at 3D N = 9
   static constexpr int NT = ((Nq + KPT - 1) / KPT + 31) / 32 * 32;
+#else
+  static constexpr int NT = (DIM == 3 && N == 9) ? ES_K1_NT9 : ((Nq + KPT - 1) / KPT + 31) / 32 * 32;
+#endif
 };
 
 // device copy of the reference tables (pointers into one device allocation)

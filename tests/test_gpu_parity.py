@@ -396,3 +396,39 @@ def test_dense_ablation_parity(es, d, M, p, warp, ic, fm):
     Nq, NF = n ** d, (d + 1) * n ** (d - 1)
     c = ctx.flux_counts()
     assert c["volume"] == Nq * (Nq - 1) and c["facet"] == 2 * Nq * NF
+
+
+@pytest.mark.parametrize("d,p", [(2, 3), (3, 2)])
+def test_erk_dp8_step_parity(es, d, p):
+    # es_step_erk with the Dormand-Prince 8 tableau (the paper's integrator; tools/tableaux.py)
+    # against the same explicit Runge-Kutta loop over the oracle's right-hand side; and with the RK4
+    # tableau against the fused RK4 path (es_step)
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import tableaux as T
+    mesh, om, ctx, u = _setup(es, d, 3, p, "paper", "wave" if d == 2 else "tgv3", 1)
+    dt = 2e-3
+    A, b, c = T.dop853()
+    ref = u.copy()
+    for _ in range(2):
+        ref = T.erk_step(lambda t, y: om.rhs(y, flux_mode=1, variant=1)[0], 0.0, ref, dt, A, b, c)
+    ut = torch.from_numpy(u).cuda()
+    ctx.set_state(ut)
+    ctx.step_erk(dt, A, b, 2)
+    out = torch.empty_like(ut)
+    ctx.get_state(out)
+    ctx.synchronize()
+    got = out.cpu().numpy()
+    assert np.abs(got - ref).max() < 1e-13 * np.abs(ref).max()
+    assert (_relerr(got - u, ref - u) < 1e-10).all()
+    A4, b4, _ = T.rk4()
+    ctx.set_state(ut)
+    ctx.step_erk(dt, A4, b4, 3)
+    ctx.get_state(out)
+    o4 = torch.empty_like(ut)
+    ctx.set_state(ut)
+    ctx.step(dt, 3)
+    ctx.get_state(o4)
+    ctx.synchronize()
+    assert (_relerr(out.cpu().numpy() - u, o4.cpu().numpy() - u) < 1e-12).all()
