@@ -57,8 +57,9 @@ typedef struct {
 } es_mesh;
 
 /* Geometry map (P:327 [eq:poly_mapping]): called ONCE by es_setup with the affine images of the
- * degree-p equispaced lattice mapping nodes of the local elements, x_in host [n][dim] -> x_out host
- * [n][dim].  The returned positions define the isoparametric mapping.  */
+ * degree-p mapping nodes (es_options.mapping_nodes: equispaced lattice or warp & blend) of the local
+ * elements, x_in host [n][dim] -> x_out host [n][dim].  The returned positions define the
+ * isoparametric mapping.  */
 typedef void (*es_map_fn)(void* user, int64_t n, const double* x_in, double* x_out);
 
 typedef struct {
@@ -83,6 +84,12 @@ typedef struct {
                                            the dense operators, zeros included (SURVEY 8(f) rank
                                            2; O(N_q^2) per element, small configurations only);
                                            other values: ES_ERR_CONFIG */
+  int mapping_nodes;                    /* node family of the isoparametric map (degree p_g = p) and of
+                                           the 3D curl-metric interpolant (degree q + 1), P:845:
+                                           0: equispaced barycentric lattice (R10, the
+                                           default); 1: warp & blend -- Gauss-Lobatto-Legendre points
+                                           on the edges, Warburton's blend with alpha = 0 inside
+                                           (R32); other values: ES_ERR_CONFIG */
 } es_options;
 
 /* Builds tables, geometry (exact metrics in 2D, conservative curl metrics in 3D, P:345-364;

@@ -6,6 +6,7 @@ this module.  The product path (paper_2312_07874_b200/) never imports it and sha
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 
 import numpy as np
@@ -64,6 +65,10 @@ def lib():
         L.ora_mesh_create.restype = ctypes.c_void_p
         L.ora_mesh_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, _lp, _dp, _dp, MAPFN,
                                       ctypes.c_void_p, ctypes.c_double, ctypes.c_int64, _lp]
+        L.ora_mesh_create2.restype = ctypes.c_void_p
+        L.ora_mesh_create2.argtypes = L.ora_mesh_create.argtypes + [ctypes.c_int]
+        L.ora_nodes.restype = ctypes.c_int
+        L.ora_nodes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _dp]
         L.ora_mesh_destroy.argtypes = [ctypes.c_void_p]
         L.ora_mesh_geometry.argtypes = [ctypes.c_void_p, ctypes.c_int64, _dp, _dp, _dp, _dp, _dp]
         L.ora_mesh_conn.argtypes = [ctypes.c_void_p, _lp, _ip, _ip]
@@ -247,7 +252,7 @@ class Mesh:
     """Oracle mesh + geometry.  `mesh` is an es_inputs.split_cartesian dict, `warp` a callable
     [n,d] -> [n,d] (the user map).  `active`: optional element subset (plus neighbours)."""
 
-    def __init__(self, mesh, p, warp=None, gamma=1.4, active=None):
+    def __init__(self, mesh, p, warp=None, gamma=1.4, active=None, nodes=0):
         self.d = mesh["d"]
         self.p = p
         self.gamma = gamma
@@ -274,8 +279,8 @@ class Mesh:
         else:
             self._act = _c(active, np.int64)
             act_p, nact = self._act.ctypes.data_as(_lp), len(self._act)
-        h = lib().ora_mesh_create(d, p, self.ne, ev.ctypes.data_as(_lp), _d(evx), _d(per), self._cb, None,
-                                  gamma, nact, act_p)
+        h = lib().ora_mesh_create2(d, p, self.ne, ev.ctypes.data_as(_lp), _d(evx), _d(per), self._cb, None,
+                                   gamma, nact, act_p, int(nodes))
         if err:
             raise err[0]
         if not h:
@@ -380,3 +385,14 @@ class Mesh:
         if rc:
             raise RuntimeError(f"ora_rk4 failed ({rc})")
         return u
+
+
+def nodes(d, N, family):
+    """Mapping / curl-interpolation node set of degree N on the reference simplex: family 0 = the
+    equispaced lattice (R10), 1 = warp & blend (R32).  Returns (xi [M, d], lam [M, d+1])."""
+    M = math.comb(N + d, d)
+    xi = np.zeros((M, d))
+    lam = np.zeros((M, d + 1))
+    m = lib().ora_nodes(d, N, family, _d(xi), _d(lam))
+    assert m == M
+    return xi, lam

@@ -760,6 +760,116 @@ void lattice(int d, int N, vector<double>& xi, vector<double>& lam) {
 // so the oracle's metric terms are computed well below double-precision rounding and then rounded.
 typedef long double LD;
 
+// ---- warp & blend node family (P:845 names the interpolatory warp & blend of Chan & Warburton;
+// reading R32: Warburton's warp & blend with the blending parameter alpha = 0) ----
+// Gauss-Lobatto-Legendre points of degree N on [-1, 1], ascending: -1, the N - 1 roots of P_N', +1.
+// Newton on P_N' from the Chebyshev-Gauss-Lobatto points, with P_N' and P_N'' from the Legendre
+// recurrence and Legendre's equation (1 - x^2) P'' = 2 x P' - N (N + 1) P.
+vector<LD> gll_points(int N) {
+  vector<LD> x(N + 1);
+  x[0] = -1.0L;
+  x[N] = 1.0L;
+  for (int i = 1; i < N; ++i) {
+    LD t = -std::cos((LD)PI * (LD)i / (LD)N);
+    for (int it = 0; it < 100; ++it) {
+      LD p0 = 1.0L, p1 = t;  // P_0, P_1
+      for (int k = 2; k <= N; ++k) {
+        LD p2 = ((LD)(2 * k - 1) * t * p1 - (LD)(k - 1) * p0) / (LD)k;
+        p0 = p1;
+        p1 = p2;
+      }
+      // p1 = P_N, p0 = P_{N-1}
+      LD dp = (LD)N * (t * p1 - p0) / (t * t - 1.0L);
+      LD d2 = (2.0L * t * dp - (LD)N * (LD)(N + 1) * p1) / (1.0L - t * t);
+      LD dt = dp / d2;
+      t -= dt;
+      if (std::fabs(dt) < 1e-19L) break;
+    }
+    x[i] = t;
+  }
+  return x;
+}
+// 1D warp factor (Warburton 2006): w(r) = sum_i (r_i^GLL - r_i^eq) l_i^eq(r), the degree-N interpolant on
+// the equispaced points r_i^eq = -1 + 2i/N of the displacement to the GLL points, divided by 1 - r^2
+// (w vanishes at +-1); 0 at |r| = 1 where the blend vanishes
+LD warp_factor(int N, const vector<LD>& gll, LD r) {
+  if (std::fabs(r) > 1.0L - 1e-12L) return 0.0L;
+  LD w = 0.0L;
+  for (int i = 0; i <= N; ++i) {
+    LD ri = -1.0L + 2.0L * (LD)i / (LD)N, l = 1.0L;
+    for (int j = 0; j <= N; ++j)
+      if (j != i) {
+        LD rj = -1.0L + 2.0L * (LD)j / (LD)N;
+        l *= (r - rj) / (ri - rj);
+      }
+    w += (gll[i] - ri) * l;
+  }
+  return w / (1.0L - r * r);
+}
+// node family of degree N on the reference simplex: family 0 = the equispaced barycentric lattice
+// (R10), family 1 = warp & blend (R32).  lam [M][d+1] barycentric coordinates (lam_1 = 1 - sum, vertex
+// k+1 at xi_k = 1), xi [M][d] = -1 + 2 lam_{k+1}; same order as lattice().
+//   2D: lam += sum over the edges (i, j) of 2 lam_i lam_j wf(lam_j - lam_i) (e_j - e_i) -- the edge
+//       displacement w(r) along the edge, blended by 4 lam_i lam_j (= 1 - r^2 on the edge);
+//   3D: per face F (the vertex a opposite), the face's 2D warp W_F in the raw barycentrics of its
+//       vertices b, c, d, blended by lam_b lam_c lam_d / ((lam_b + lam_a/2)(lam_c + lam_a/2)(lam_d + lam_a/2));
+//       nodes on an edge take W_F itself (the two faces through the edge agree there).
+void node_set(int d, int N, int family, vector<LD>& xi, vector<LD>& lam) {
+  vector<double> xid, lamd;
+  lattice(d, N, xid, lamd);
+  const int nb = d + 1, M = (int)lamd.size() / nb;
+  lam.assign(lamd.size(), 0.0L);
+  for (int i = 0; i < M; ++i) {  // exact lattice barycentrics k / N
+    LD s = 0.0L;
+    for (int k = 1; k < nb; ++k) {
+      lam[(size_t)i * nb + k] = std::nearbyint(lamd[(size_t)i * nb + k] * N) / (LD)N;
+      s += lam[(size_t)i * nb + k];
+    }
+    lam[(size_t)i * nb] = 1.0L - s;
+  }
+  if (family == 1 && N >= 3) {  // N <= 2: the GLL points are equispaced, no warp
+    vector<LD> gll = gll_points(N);
+    const LD tol = 1e-10L;
+    for (int i = 0; i < M; ++i) {
+      LD* L = &lam[(size_t)i * nb];
+      LD shift[4] = {0, 0, 0, 0};
+      auto face_warp = [&](const int* vs, int nvs, LD* W) {  // 2D warp of the vertices vs
+        for (int k = 0; k < nb; ++k) W[k] = 0.0L;
+        for (int x = 0; x < nvs; ++x)
+          for (int y = x + 1; y < nvs; ++y) {
+            int a = vs[x], b = vs[y];
+            LD c = 2.0L * L[a] * L[b] * warp_factor(N, gll, L[b] - L[a]);
+            W[b] += c;
+            W[a] -= c;
+          }
+      };
+      if (d == 2) {
+        int vs[3] = {0, 1, 2};
+        face_warp(vs, 3, shift);
+      } else {
+        for (int a = 0; a < 4; ++a) {
+          int vs[3], q = 0;
+          for (int k = 0; k < 4; ++k)
+            if (k != a) vs[q++] = k;
+          LD W[4];
+          face_warp(vs, 3, W);
+          LD lb = L[vs[0]], lc = L[vs[1]], ld = L[vs[2]], la = L[a];
+          LD blend = lb * lc * ld, den = (lb + 0.5L * la) * (lc + 0.5L * la) * (ld + 0.5L * la);
+          if (den > tol) blend /= den;
+          for (int k = 0; k < 4; ++k) shift[k] += blend * W[k];
+          int npos = (lb > tol) + (lc > tol) + (ld > tol);
+          if (la < tol && npos < 3)
+            for (int k = 0; k < 4; ++k) shift[k] = W[k];
+        }
+      }
+      for (int k = 0; k < nb; ++k) L[k] += shift[k];
+    }
+  }
+  xi.assign((size_t)M * d, 0.0L);
+  for (int i = 0; i < M; ++i)
+    for (int k = 0; k < d; ++k) xi[(size_t)i * d + k] = -1.0L + 2.0L * lam[(size_t)i * nb + k + 1];
+}
+
 // polynomial interpolant on a lattice in the PKD basis: coefficients for nrhs fields
 struct Interp {
   int d, N, M;
@@ -767,15 +877,14 @@ struct Interp {
   vector<LD> xi;  // lattice points
   vector<LD> Vl;  // [M][M]
 };
-Interp make_interp(int d, int N) {
+Interp make_interp(int d, int N, int family = 0) {
   Interp I;
   I.d = d;
   I.N = N;
-  vector<double> lam, xid;
-  lattice(d, N, xid, lam);
-  // exact lattice coordinates -1 + 2 i/N in long double
-  I.xi.assign(xid.size(), 0.0L);
-  for (size_t k = 0; k < xid.size(); ++k) I.xi[k] = std::nearbyint((xid[k] + 1.0) * N / 2.0) * 2.0L / N - 1.0L;
+  vector<LD> lamq;
+  // interpolation points: the exact lattice coordinates -1 + 2 i/N in long double (family 0), or the
+  // warp & blend points (family 1, R32)
+  node_set(d, N, family, I.xi, lamq);
   I.al = multi_indices(d, N);
   I.M = (int)I.al.size() / d;
   I.Vl.assign((size_t)I.M * I.M, 0.0L);
@@ -1084,6 +1193,23 @@ void ora_entropy(int d, double g, int n, const double* U, double* S, double* Fen
 ora_mesh* ora_mesh_create(int d, int p, int64_t ne, const int64_t* elem_vertices,
                           const double* elem_vertex_coords, const double* period, ora_map_fn map,
                           void* user, double gamma, int64_t n_active, const int64_t* active) {
+  return ora_mesh_create2(d, p, ne, elem_vertices, elem_vertex_coords, period, map, user, gamma, n_active, active, 0);
+}
+
+int ora_nodes(int d, int N, int family, double* xi, double* lam) {
+  vector<LD> x, l;
+  node_set(d, N, family, x, l);
+  if (xi)
+    for (size_t k = 0; k < x.size(); ++k) xi[k] = (double)x[k];
+  if (lam)
+    for (size_t k = 0; k < l.size(); ++k) lam[k] = (double)l[k];
+  return (int)(l.size() / (d + 1));
+}
+
+ora_mesh* ora_mesh_create2(int d, int p, int64_t ne, const int64_t* elem_vertices,
+                           const double* elem_vertex_coords, const double* period, ora_map_fn map,
+                           void* user, double gamma, int64_t n_active, const int64_t* active, int node_family) {
+  if (node_family < 0 || node_family > 1) return nullptr;
   ora_mesh* m = new ora_mesh();
   m->d = d;
   m->p = p;
@@ -1165,11 +1291,12 @@ ora_mesh* ora_mesh_create(int d, int p, int64_t ne, const int64_t* elem_vertices
   for (int64_t e = 0; e < ne; ++e)
     if (act[e]) alist.push_back(e);
   // ---- mapping nodes: affine images of the degree-p_g lattice, then the user map ----
-  Interp Ipg = make_interp(d, p);
+  Interp Ipg = make_interp(d, p, node_family);
   Interp Icurl;
-  if (d == 3) Icurl = make_interp(d, p + 1);  // curl interpolation of degree q+1
-  vector<double> lxi, llam;
-  lattice(d, p, lxi, llam);
+  if (d == 3) Icurl = make_interp(d, p + 1, node_family);  // curl interpolation of degree q+1
+  vector<LD> lxiq, llamq;
+  node_set(d, p, node_family, lxiq, llamq);
+  vector<double> llam(llamq.begin(), llamq.end());
   int Npg = Ipg.M;
   vector<double> xin((size_t)alist.size() * Npg * d), xout(xin.size());
   for (size_t a = 0; a < alist.size(); ++a) {

@@ -87,6 +87,13 @@ typedef struct {
 ora_mesh* ora_mesh_create(int d, int p, int64_t ne, const int64_t* elem_vertices,
                           const double* elem_vertex_coords, const double* period, ora_map_fn map,
                           void* user, double gamma, int64_t n_active, const int64_t* active);
+/* as ora_mesh_create with the mapping / curl-interpolation node family: 0 = equispaced lattice
+ * (R10), 1 = warp & blend (R32) */
+ora_mesh* ora_mesh_create2(int d, int p, int64_t ne, const int64_t* elem_vertices,
+                           const double* elem_vertex_coords, const double* period, ora_map_fn map,
+                           void* user, double gamma, int64_t n_active, const int64_t* active, int node_family);
+/* node set of degree N (family as above): xi [M][d], lam [M][d+1] (either may be NULL); returns M */
+int ora_nodes(int d, int N, int family, double* xi, double* lam);
 void ora_mesh_destroy(ora_mesh* m);
 /* geometric factors of one element: G [Nq][d][d] (G_lm), Gf [Nf][Nqf][d][d], Jt [Nq], Jn
  * [Nf][Nqf][d], xq [Nq][d]; any pointer may be NULL. Returns 0, or -1 if geometry not built. */

@@ -433,7 +433,8 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   if (c->rank < 0 || c->rank >= c->world) return fail(c, ES_ERR_ARG, "rank out of range");
   c->external = c->world > 1 && !opt->nccl_unique_id;
   std::string err;
-  if (!build_ref_tables(c->d, p, c->T, err)) return fail(c, ES_ERR_CONFIG, err);
+  if (opt->mapping_nodes != 0 && opt->mapping_nodes != 1) return fail(c, ES_ERR_CONFIG, "mapping_nodes must be 0 or 1");
+  if (!build_ref_tables(c->d, p, c->T, err, opt->mapping_nodes)) return fail(c, ES_ERR_CONFIG, err);
   c->n = c->T.n;
   c->Nq = c->T.Nq;
   c->Nqf = c->T.Nqf;
@@ -950,7 +951,7 @@ es_status es_eval_points(es_context* c, const double* u, int npts, const double*
   if (!u || !xi || !uo || npts <= 0) return fail(c, ES_ERR_ARG, "es_eval_points: u, xi, u_out and npts > 0 required");
   CK(cudaSetDevice(c->device));
   std::vector<double> pkd, lm, dm;
-  if (!eval_point_tables(c->d, c->p, xi, npts, pkd, lm, dm)) return fail(c, ES_ERR_CONFIG, "point tables");
+  if (!eval_point_tables(c->d, c->p, xi, npts, pkd, lm, dm, c->T.nodes)) return fail(c, ES_ERR_CONFIG, "point tables");
   double *dp = nullptr, *dl = nullptr, *dd = nullptr;
   CK(upload(&dp, pkd));
   CK(upload(&dl, lm));
@@ -1116,6 +1117,16 @@ es_status es_ref_table(int dim, int p, const char* name, double* out, int64_t ca
   if (!name) return ES_ERR_ARG;
   RefTables t;
   std::string err;
+  if (!std::strcmp(name, "nodes0") || !std::strcmp(name, "nodes1")) {  // mapping-node barycentrics of degree p
+    if ((dim != 2 && dim != 3) || p < 1 || p > 12) return ES_ERR_ARG;
+    const std::vector<double> b = node_family_bary(dim, p, name[5] - '0');
+    if (n) *n = (int64_t)b.size();
+    if (out) {
+      if (cap < (int64_t)b.size()) return ES_ERR_ARG;
+      std::memcpy(out, b.data(), b.size() * sizeof(double));
+    }
+    return ES_OK;
+  }
   if (!build_ref_tables(dim, p, t, err)) return ES_ERR_CONFIG;
   std::string nm(name);
   const std::vector<double>* v = nullptr;

@@ -37,6 +37,7 @@ struct RefTables {
   std::vector<double> xi_face;   // [Nf][Nqf][d]
   // geometry interpolation (lattice of degree p for the map, q+1 for curl metrics, R10)
   int Npg = 0, Ncl = 0;
+  int nodes = 0;                 // node family of the map and the curl interpolant (0 lattice R10, 1 warp & blend R32)
   std::vector<double> lat_bary;  // [Npg][d+1] barycentric coordinates of mapping nodes
   std::vector<double> LmapV;     // [Nq][Npg]   Lagrange basis of the map at volume nodes
   std::vector<double> DmapV;     // [d][Nq][Npg] gradients at volume nodes (2D metrics)
@@ -48,12 +49,14 @@ struct RefTables {
   std::vector<double> DcurlF;    // [d][Nf*Nqf][Ncl]
 };
 
-bool build_ref_tables(int d, int p, RefTables& t, std::string& err);
+bool build_ref_tables(int d, int p, RefTables& t, std::string& err, int nodes = 0);
+// barycentric coordinates [M][d+1] of the degree-N mapping node family (0 lattice, 1 warp & blend)
+std::vector<double> node_family_bary(int d, int N, int family);
 // dense S^(l) [l][j][i] and (R^(z)T B) [z][f][i] for the brute-force ablation (volume_mode 2)
 void build_dense_tables(const RefTables& t, std::vector<double>& S, std::vector<double>& RB);
 // PKD basis, mapping Lagrange basis and its reference gradients at arbitrary points (es_eval_points)
 bool eval_point_tables(int d, int p, const double* xi, int npts, std::vector<double>& pkd, std::vector<double>& lmap,
-                       std::vector<double>& dmap);
+                       std::vector<double>& dmap, int nodes = 0);
 
 // ----------------------------------------------------------------------------------------------
 // Host mesh plan: connectivity with the orientation rule R11, and the partition/halo

@@ -66,9 +66,13 @@ struct Rhs2Smem {
   // it shares with the modal result (all NC at once when there is room)
   // (all NC variables per round: the facet-side line sums are a latency chain per round, and in 3D
   // the region no longer holds the modal result, so it is sized for the scratch)
-  static constexpr int SCV_FIT = W::NW * S::NC * 32 <= UM ? S::NC : (UM / (W::NW * 32) >= 1 ? UM / (W::NW * 32) : 1);
+  // row stride RS of the scratch (>= 32): the line sums read N consecutive doubles of row u at
+  // u RS + gq N; RS is chosen so that the LPW x SCV reading lanes fall into distinct shared-memory banks
+  // (bank model of tools/banksim.py: 9 instead of 45 wavefronts per round at N = 9)
+  static constexpr int RS = N == 9 ? 37 : (N == 3 ? 39 : 33);
+  static constexpr int SCV_FIT = W::NW * S::NC * RS <= UM ? S::NC : (UM / (W::NW * RS) >= 1 ? UM / (W::NW * RS) : 1);
   static constexpr int SCV = DIM == 3 ? S::NC : SCV_FIT;
-  static constexpr int SC = W::NW * SCV * 32;
+  static constexpr int SC = W::NW * SCV * RS;
   static constexpr int WJ0 = ((S::NG * S::Nq) % 2 == 0) ? S::NG * S::Nq : (S::NG + 1) * S::Nq;  // first even row
   static constexpr int WJN = ((S::NG * S::Nq) % 2 == 0) ? 2 * S::Nq : ev2(S::Nq);                // doubles copied
   static constexpr int WJOFF = ((S::NG * S::Nq) % 2 == 0) ? S::Nq : 0;  // W / J~ within the copied rows
@@ -394,6 +398,41 @@ __device__ __forceinline__ void iface_node_flux(int es, const double* tm, int sm
   for (int v = 0; v < NC; ++v) out[v * ostride] = bj * F[v];
 }
 
+// Line orderings of the direction passes.  The LPW line groups of a warp take consecutive line
+// indices L; (l0, l1) = (L mod N, L / N) name the two fixed coordinates of the line, swapped where that
+// lowers the shared-memory bank conflicts of the warp's LDS.64 of node data (served per half-warp:
+// the sixteen 8-byte addresses of a half should fall into distinct 8-byte bank slots mod 16).  Chosen
+// per (N, k) with the bank model of tools/banksim.py and confirmed by ncu (excess shared wavefronts
+// of the flux kernel 174M -> 91M at N = 9): the eta3 pass swaps (partner loads 4 -> 3 wavefronts per
+// instruction at N = 9), the eta2 pass swaps so that the facet-4 partner loads become broadcasts
+// across the warp's lines.
+__host__ __device__ constexpr bool line_swap(int DIM, int N, int k) {
+  return DIM == 3 && ((k == 1 && (N == 5 || N == 6 || N == 7 || N == 9)) || (k == 2 && (N == 7 || N == 9)));
+}
+template <int DIM, int N, int k>
+__device__ __forceinline__ void line_coords(int L, int pos, int& ca, int& cb, int& cc) {
+  int l0 = L % N, l1 = L / N;
+  if constexpr (line_swap(DIM, N, k)) {
+    const int t = l0;
+    l0 = l1;
+    l1 = t;
+  }
+  if constexpr (k == 0) {
+    ca = pos;
+    cb = l0;
+    cc = l1;
+  } else if constexpr (k == 1) {
+    ca = l0;
+    cb = pos;
+    cc = l1;
+  } else {
+    ca = l0;
+    cb = l1;
+    cc = pos;
+  }
+  if constexpr (DIM == 2) cc = 0;
+}
+
 template <int DIM, int N>
 __device__ __forceinline__ void k2_epilogue_2d(const RhsArgs& A, int64_t e, unsigned it);
 
@@ -429,7 +468,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   double* tB = tli4 + N * N;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* scr = smk2 + L::o_sc + warp * L::SCV * 32;
+  double* scr = smk2 + L::o_sc + warp * L::SCV * L::RS;
   const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
   auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
   // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers
@@ -544,26 +583,17 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     // warp w takes the slots s = w - woff (mod NW): the warps with an extra slot rotate between
     // passes that run back to back
     for (int slot = (warp + W::NW - woff) % W::NW; slot < W::SLOTS; slot += W::NW) {
-      const int Lidx = slot * W::LPW + grp;
+      // the lanes past the last line group (27..31 at N = 9) address the nodes of the last group,
+      // which shares their half-warp (same addresses: shared-memory broadcasts, no extra bank
+      // wavefronts), with a zero mask
+      const int Lidx = slot * W::LPW + (lane_ok ? grp : W::LPW - 1);
       const bool valid = lane_ok && Lidx < W::NL;
-      const int l0 = valid ? Lidx % N : 0, l1 = valid ? Lidx / N : 0;
-      // node coordinates (a, b, c) and index
+      const bool in_range = Lidx < W::NL;
+      // node coordinates (a, b, c) and index; line_coords orders the lines of a warp so that its
+      // node loads are free of bank conflicts (line_swap)
       int ca, cb, cc;
-      if (k == 0) {
-        ca = pos;
-        cb = l0;
-        cc = l1;
-      } else if (k == 1) {
-        ca = l0;
-        cb = pos;
-        cc = l1;
-      } else {
-        ca = l0;
-        cb = l1;
-        cc = pos;
-      }
-      if constexpr (DIM == 2) cc = 0;
-      const int i = valid ? ca + N * cb + N * N * cc : 0;
+      line_coords<DIM, N, k>(in_range ? Lidx : 0, pos, ca, cb, cc);
+      const int i = in_range ? ca + N * cb + N * N * cc : 0;
       const double vmask = valid ? 1.0 : 0.0;
       NodeState me = state_at(i);
       double gl[3][3];  // own metric rows g^(l)
@@ -585,7 +615,7 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           const int s = s0 + t;
           int pos2 = pos + (s <= NS ? s : 0);
           if (pos2 >= N) pos2 -= N;
-          const int j = valid ? i + (pos2 - pos) * stride : 0;
+          const int j = in_range ? i + (pos2 - pos) * stride : 0;
           const int ix = pos * N + pos2;
           Job<DIM>& jb = jv[t];
           jb.base = sP;
@@ -695,11 +725,11 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
         for (int v0 = 0; v0 < NC; v0 += SCV) {
 #pragma unroll
           for (int u = 0; u < SCV; ++u)
-            if (v0 + u < NC) scr[u * 32 + lane] = Fc[v0 + u];
+            if (v0 + u < NC) scr[u * L::RS + lane] = Fc[v0 + u];
           __syncwarp();
           for (int sidx = lane; sidx < W::LPW * SCV; sidx += 32) {
             const int gq = sidx / SCV, u = sidx - gq * SCV, v = v0 + u;
-            const double* src = scr + u * 32 + gq * N;
+            const double* src = scr + u * L::RS + gq * N;
             double tv[N];  // pairwise tree sum, depth ceil(log2 N)
 #pragma unroll
             for (int a = 0; a < N; ++a) tv[a] = src[a];
@@ -778,7 +808,11 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
               ci += 1;
               cf += valid ? 1 : 0;
             }
-            line_sums(F1[0], [&](int Lq, int v) { return fS + (0 * NC + v) * Nqf + Lq; });
+            line_sums(F1[0], [&](int Lq, int v) {  // facet node (a, c) of line Lq
+              int qa, qb, qc;
+              line_coords<DIM, N, 1>(Lq, 0, qa, qb, qc);
+              return fS + (0 * NC + v) * Nqf + qa + N * qc;
+            });
           }
           // facet 4, rotating schedule: at step t lane pos pairs its node (a, b = pos, c) with the
           // facet node (a, j = (pos + t) mod N); the facet-side value travels by shuffle to lane j,
@@ -1181,7 +1215,7 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   double* tB = tli4 + N * N;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* scr = smk2 + L::o_sc + warp * L::SCV * 32;
+  double* scr = smk2 + L::o_sc + warp * L::SCV * L::RS;
   const double g = A.gamma, gm1inv = 1.0 / (g - 1.0);
   auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
   // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers

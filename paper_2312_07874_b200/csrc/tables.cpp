@@ -7,6 +7,8 @@
 #include <quadmath.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <cstring>
 
@@ -231,23 +233,16 @@ void lattice_nodes(int d, int N, std::vector<T>& xi, std::vector<double>& bary) 
 }
 
 // Lagrange basis (and gradients) of the degree-N lattice evaluated at points X[npts][d] (reference
-// coordinates), stored as double-double pairs: out = [hi block | lo block]
-void lattice_basis(int d, int N, const std::vector<double>& X, int npts, std::vector<double>* L,
-                   std::vector<double>* Dg /*[d][npts][M]*/) {
+// coordinates, binary128): Lq [npts][M], Dq [d][npts][M]
+void lattice_basis_q(int d, int N, const std::vector<LD>& X, int npts, std::vector<LD>* Lq, std::vector<LD>* Dq) {
   std::vector<double> lxi, lb;
   lattice_nodes<double>(d, N, lxi, lb);
   const int nb = d + 1, M = (int)lb.size() / nb;
   std::vector<int> alpha((size_t)M * nb);
   for (int i = 0; i < M; ++i)
     for (int k = 0; k < nb; ++k) alpha[(size_t)i * nb + k] = (int)std::lround(lb[(size_t)i * nb + k] * N);
-  size_t nL = (size_t)npts * M, nD = (size_t)d * npts * M;
-  if (L) L->assign(2 * nL, 0.0);
-  if (Dg) Dg->assign(2 * nD, 0.0);
-  auto put = [](std::vector<double>& out, size_t n, size_t idx, LD v) {
-    double hi = (double)v;
-    out[idx] = hi;
-    out[n + idx] = (double)(v - (LD)hi);
-  };
+  if (Lq) Lq->assign((size_t)npts * M, (LD)0);
+  if (Dq) Dq->assign((size_t)d * npts * M, (LD)0);
 #pragma omp parallel for schedule(dynamic, 8)
   for (int x = 0; x < npts; ++x) {
     // barycentric coordinates: lam_{k+1} = (1 + xi_k)/2, lam_1 = 1 - sum; d lam_{k+1}/d xi_l = delta/2,
@@ -255,7 +250,7 @@ void lattice_basis(int d, int N, const std::vector<double>& X, int npts, std::ve
     LD lam[4];
     LD sum = 0;
     for (int k = 0; k < d; ++k) {
-      lam[k + 1] = ((LD)1 + (LD)X[(size_t)x * d + k]) / (LD)2;
+      lam[k + 1] = ((LD)1 + X[(size_t)x * d + k]) / (LD)2;
       sum += lam[k + 1];
     }
     lam[0] = (LD)1 - sum;
@@ -274,8 +269,8 @@ void lattice_basis(int d, int N, const std::vector<double>& X, int npts, std::ve
       }
       LD val = 1;
       for (int k = 0; k < nb; ++k) val *= f[k];
-      if (L) put(*L, nL, (size_t)x * M + i, val);
-      if (Dg) {
+      if (Lq) (*Lq)[(size_t)x * M + i] = val;
+      if (Dq) {
         for (int l = 0; l < d; ++l) {
           // d/dxi_l = 1/2 (d/dlam_{l+1} - d/dlam_0)
           LD g = 0;
@@ -286,12 +281,174 @@ void lattice_basis(int d, int N, const std::vector<double>& X, int npts, std::ve
               if (kk != k) prod *= f[kk];
             g += (k == 0) ? -prod : prod;
           }
-          put(*Dg, nD, ((size_t)l * npts + x) * M + i, g / (LD)2);
+          (*Dq)[((size_t)l * npts + x) * M + i] = g / (LD)2;
         }
       }
     }
   }
 }
+
+// ---------------- warp & blend node family (reading R32) ----------------
+// Warburton's warp & blend with the blending parameter alpha = 0, in barycentric form.  1D warp
+// factor wf(r) = w(r) / (1 - r^2), w the degree-N interpolant (barycentric Lagrange formula) on the
+// equispaced points of their displacement to the Gauss-Lobatto-Legendre points -- whose interior
+// points are the nodes of the Gauss-Jacobi (1,1) rule.  A triangle with barycentrics lam moves by
+// sum over its edges (u, v) of 2 lam_u lam_v wf(lam_v - lam_u) (e_v - e_u) (the edge warp blended by
+// 4 lam_u lam_v); a tetrahedron by the sum over its faces of the face's triangle warp (in the raw
+// barycentrics of its three vertices) times lam_b lam_c lam_d / prod(lam_x + lam_a / 2), a the opposite
+// vertex, except on edges, which take the face warp itself.  Nodes in lattice_nodes order.
+void node_bary(int d, int N, int family, std::vector<LD>& bary) {
+  std::vector<double> xi, b;
+  lattice_nodes<double>(d, N, xi, b);
+  const int nb = d + 1, M = (int)b.size() / nb;
+  bary.assign(b.size(), (LD)0);
+  for (int i = 0; i < M; ++i) {
+    LD s = 0;
+    for (int k = 1; k < nb; ++k) {
+      bary[(size_t)i * nb + k] = (LD)std::lround(b[(size_t)i * nb + k] * N) / (LD)N;
+      s += bary[(size_t)i * nb + k];
+    }
+    bary[(size_t)i * nb] = (LD)1 - s;
+  }
+  if (family != 1 || N < 3) return;  // N <= 2: the GLL points are equispaced
+  std::vector<LD> gx, gw, req(N + 1), disp(N + 1);
+  gauss_rule(N - 1, 1.0, 1.0, gx, gw);
+  std::sort(gx.begin(), gx.end());
+  for (int i = 0; i <= N; ++i) {
+    req[i] = (LD)(2 * i - N) / (LD)N;
+    const LD g = i == 0 ? (LD)-1 : (i == N ? (LD)1 : gx[i - 1]);
+    disp[i] = g - req[i];
+  }
+  auto wf = [&](LD r) -> LD {
+    const LD ar = r < 0 ? -r : r;
+    if (ar >= (LD)1 - (LD)1e-24) return 0;
+    const std::vector<LD> l = lagrange_at(req, r);
+    LD w = 0;
+    for (int i = 0; i <= N; ++i) w += disp[i] * l[i];
+    return w / ((LD)1 - r * r);
+  };
+  const LD tol = (LD)1e-10;
+  for (int i = 0; i < M; ++i) {
+    LD* L = &bary[(size_t)i * nb];
+    LD sh[4] = {0, 0, 0, 0};
+    auto tri_warp = [&](int a, int b2, int c, LD* W) {
+      for (int k = 0; k < 4; ++k) W[k] = 0;
+      const int ed[3][2] = {{a, b2}, {b2, c}, {a, c}};
+      for (const auto& e : ed) {
+        const LD t = 2 * L[e[0]] * L[e[1]] * wf(L[e[1]] - L[e[0]]);
+        W[e[1]] += t;
+        W[e[0]] -= t;
+      }
+    };
+    if (d == 2) {
+      tri_warp(0, 1, 2, sh);
+    } else {
+      for (int o = 0; o < 4; ++o) {
+        int v[3], q = 0;
+        for (int k = 0; k < 4; ++k)
+          if (k != o) v[q++] = k;
+        LD W[4];
+        tri_warp(v[0], v[1], v[2], W);
+        const LD la = L[o], half = la / 2;
+        LD blend = L[v[0]] * L[v[1]] * L[v[2]];
+        const LD den = (L[v[0]] + half) * (L[v[1]] + half) * (L[v[2]] + half);
+        if (den > tol) blend /= den;
+        const int inside = (L[v[0]] > tol) + (L[v[1]] > tol) + (L[v[2]] > tol);
+        for (int k = 0; k < 4; ++k) sh[k] = (la < tol && inside < 3) ? W[k] : sh[k] + blend * W[k];
+      }
+    }
+    for (int k = 0; k < nb; ++k) L[k] += sh[k];
+  }
+}
+
+// inverse of a dense M x M matrix in binary128 (Gauss-Jordan, partial pivoting)
+bool invert_q(std::vector<LD>& A, int M) {
+  std::vector<LD> I((size_t)M * M, (LD)0);
+  for (int i = 0; i < M; ++i) I[(size_t)i * M + i] = 1;
+  for (int c = 0; c < M; ++c) {
+    int pr = c;
+    for (int r = c + 1; r < M; ++r)
+      if (fabsq(A[(size_t)r * M + c]) > fabsq(A[(size_t)pr * M + c])) pr = r;
+    if (A[(size_t)pr * M + c] == 0) return false;
+    if (pr != c)
+      for (int k = 0; k < M; ++k) {
+        std::swap(A[(size_t)pr * M + k], A[(size_t)c * M + k]);
+        std::swap(I[(size_t)pr * M + k], I[(size_t)c * M + k]);
+      }
+    const LD iv = (LD)1 / A[(size_t)c * M + c];
+    for (int k = 0; k < M; ++k) {
+      A[(size_t)c * M + k] *= iv;
+      I[(size_t)c * M + k] *= iv;
+    }
+    for (int r = 0; r < M; ++r) {
+      if (r == c) continue;
+      const LD f = A[(size_t)r * M + c];
+      if (f == 0) continue;
+      for (int k = 0; k < M; ++k) {
+        A[(size_t)r * M + k] -= f * A[(size_t)c * M + k];
+        I[(size_t)r * M + k] -= f * I[(size_t)c * M + k];
+      }
+    }
+  }
+  A.swap(I);
+  return true;
+}
+
+// Lagrange basis (and gradients) of the degree-N node family at points X[npts][d] (binary128), stored
+// as double-double pairs: out = [hi block | lo block].  Family 0: the lattice's closed form.  Family 1
+// (warp & blend): l^wb(x) = l^lat(x) A^-1 with A_ij = l^lat_j(x^wb_i), A^-1 cached per (d, N).
+bool node_basis(int d, int N, int family, const std::vector<LD>& X, int npts, std::vector<double>* L,
+                std::vector<double>* Dg /*[d][npts][M]*/) {
+  std::vector<LD> Lq, Dq;
+  lattice_basis_q(d, N, X, npts, L ? &Lq : nullptr, Dg ? &Dq : nullptr);
+  const int M = d == 2 ? (N + 1) * (N + 2) / 2 : (N + 1) * (N + 2) * (N + 3) / 6;
+  if (family == 1 && N >= 3) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, std::vector<LD>> cache;
+    std::vector<LD> Ai;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = cache.find({d, N});
+      if (it == cache.end()) {
+        std::vector<LD> bw, xw((size_t)M * d), A;
+        node_bary(d, N, 1, bw);
+        for (int i = 0; i < M; ++i)
+          for (int k = 0; k < d; ++k) xw[(size_t)i * d + k] = 2 * bw[(size_t)i * (d + 1) + k + 1] - 1;
+        lattice_basis_q(d, N, xw, M, &A, nullptr);
+        if (!invert_q(A, M)) A.clear();
+        it = cache.emplace(std::make_pair(d, N), A).first;
+      }
+      Ai = it->second;
+    }
+    if (Ai.empty()) return false;  // singular (not for N <= 11: the family is unisolvent)
+    auto apply = [&](std::vector<LD>& B, int rows) {  // B [rows][M] <- B A^-1
+      std::vector<LD> out((size_t)rows * M, (LD)0);
+#pragma omp parallel for schedule(static)
+      for (int r = 0; r < rows; ++r)
+        for (int j = 0; j < M; ++j) {
+          const LD b = B[(size_t)r * M + j];
+          if (b == 0) continue;
+          for (int k = 0; k < M; ++k) out[(size_t)r * M + k] += b * Ai[(size_t)j * M + k];
+        }
+      B.swap(out);
+    };
+    if (L) apply(Lq, npts);
+    if (Dg) apply(Dq, d * npts);
+  }
+  auto pack = [](const std::vector<LD>& q, std::vector<double>& out) {
+    const size_t n = q.size();
+    out.assign(2 * n, 0.0);
+    for (size_t i = 0; i < n; ++i) {
+      const double hi = (double)q[i];
+      out[i] = hi;
+      out[n + i] = (double)(q[i] - (LD)hi);
+    }
+  };
+  if (L) pack(Lq, *L);
+  if (Dg) pack(Dq, *Dg);
+  return true;
+}
+std::vector<LD> to_q(const std::vector<double>& v) { return std::vector<LD>(v.begin(), v.end()); }
 
 void collapse(int d, const double* e, double* x) {
   if (d == 2) {
@@ -306,7 +463,7 @@ void collapse(int d, const double* e, double* x) {
 
 }  // namespace
 
-bool build_ref_tables(int d, int p, RefTables& t, std::string& err) {
+bool build_ref_tables(int d, int p, RefTables& t, std::string& err, int nodes) {
   if (!((d == 2 && p >= 1 && p <= 10) || (d == 3 && p >= 1 && p <= 8))) {
     err = "unsupported (dim, p)";
     return false;
@@ -464,23 +621,47 @@ bool build_ref_tables(int d, int p, RefTables& t, std::string& err) {
     double nh[12] = {0, -1, 0, r3, r3, r3, -1, 0, 0, 0, 0, -1};
     std::memcpy(t.nhat.data(), nh, sizeof(nh));
   }
-  // geometry interpolation matrices (P:327 mapping of degree p_g = p, P:349 curl lattice q+1)
-  std::vector<double> lxi;
-  lattice_nodes<double>(d, p, lxi, t.lat_bary);
-  t.Npg = (int)t.lat_bary.size() / (d + 1);
-  lattice_basis(d, p, t.xi_vol, t.Nq, &t.LmapV, d == 2 ? &t.DmapV : nullptr);
-  lattice_basis(d, p, lxi, t.Npg, nullptr, &t.DmapM);
-  if (d == 2) {
-    lattice_basis(d, p, t.xi_face, t.Nf * t.Nqf, nullptr, &t.DmapF);
-  } else {
-    std::vector<double> cxi, cb;
-    lattice_nodes<double>(d, p + 1, cxi, cb);
-    t.Ncl = (int)cb.size() / (d + 1);
-    lattice_basis(d, p, cxi, t.Ncl, &t.LmapC, &t.DmapC);
-    lattice_basis(d, p + 1, t.xi_vol, t.Nq, nullptr, &t.DcurlV);
-    lattice_basis(d, p + 1, t.xi_face, t.Nf * t.Nqf, nullptr, &t.DcurlF);
+  // geometry interpolation matrices (P:327 mapping of degree p_g = p, P:349 curl interpolation of
+  // degree q+1) on the node family `nodes` (0: equispaced lattice R10, 1: warp & blend R32)
+  if (nodes != 0 && nodes != 1) {
+    err = "mapping_nodes must be 0 or 1";
+    return false;
   }
-  return true;
+  t.nodes = nodes;
+  // reference coordinates of a node family: the lattice's as before (double), warp & blend in binary128
+  auto family_xi = [&](int N, std::vector<double>& bary) {
+    std::vector<LD> xq;
+    if (nodes == 0) {
+      std::vector<double> lxi;
+      lattice_nodes<double>(d, N, lxi, bary);
+      xq = to_q(lxi);
+    } else {
+      std::vector<LD> bq;
+      node_bary(d, N, 1, bq);
+      bary = rnd(bq);
+      const int M = (int)bq.size() / (d + 1);
+      xq.resize((size_t)M * d);
+      for (int i = 0; i < M; ++i)
+        for (int k = 0; k < d; ++k) xq[(size_t)i * d + k] = 2 * bq[(size_t)i * (d + 1) + k + 1] - 1;
+    }
+    return xq;
+  };
+  const std::vector<LD> mxi = family_xi(p, t.lat_bary), vxi = to_q(t.xi_vol), fxi = to_q(t.xi_face);
+  t.Npg = (int)t.lat_bary.size() / (d + 1);
+  bool ok = node_basis(d, p, nodes, vxi, t.Nq, &t.LmapV, d == 2 ? &t.DmapV : nullptr) &&
+            node_basis(d, p, nodes, mxi, t.Npg, nullptr, &t.DmapM);
+  if (d == 2) {
+    ok = ok && node_basis(d, p, nodes, fxi, t.Nf * t.Nqf, nullptr, &t.DmapF);
+  } else {
+    std::vector<double> cb;
+    const std::vector<LD> cxi = family_xi(p + 1, cb);
+    t.Ncl = (int)cb.size() / (d + 1);
+    ok = ok && node_basis(d, p, nodes, cxi, t.Ncl, &t.LmapC, &t.DmapC) &&
+         node_basis(d, p + 1, nodes, vxi, t.Nq, nullptr, &t.DcurlV) &&
+         node_basis(d, p + 1, nodes, fxi, t.Nf * t.Nqf, nullptr, &t.DcurlF);
+  }
+  if (!ok) err = "singular node-family Vandermonde";
+  return ok;
 }
 
 // Dense operators for the brute-force ablation (es_options.volume_mode = 2):
@@ -491,11 +672,11 @@ bool build_ref_tables(int d, int p, RefTables& t, std::string& err) {
 // mapping-lattice Lagrange basis with its gradients at arbitrary reference points xi[npts][d]:
 // pkd [npts][Np], lmap [npts][Npg], dmap [d][npts][Npg] (rounded from binary128)
 bool eval_point_tables(int d, int p, const double* xi, int npts, std::vector<double>& pkd, std::vector<double>& lmap,
-                       std::vector<double>& dmap) {
+                       std::vector<double>& dmap, int nodes) {
   const int Np = d == 2 ? (p + 1) * (p + 2) / 2 : (p + 1) * (p + 2) * (p + 3) / 6;
   pkd.assign((size_t)npts * Np, 0.0);
   std::vector<double> X(xi, xi + (size_t)npts * d), L, D;
-  lattice_basis(d, p, X, npts, &L, &D);
+  if (!node_basis(d, p, nodes, to_q(X), npts, &L, &D)) return false;
   const size_t nL = L.size() / 2, nD = D.size() / 2;
   lmap.assign(nL, 0.0);
   dmap.assign(nD, 0.0);
@@ -588,6 +769,13 @@ void build_dense_tables(const RefTables& t, std::vector<double>& S, std::vector<
             rb_at(3, a + N * j4, i) = t.l3L[c] * t.lint4[j4 * N + b] * t.Bf[3 * Nqf + a + N * j4];
         }
   }
+}
+
+// barycentric coordinates [M][d+1] of the degree-N node family (0: lattice, 1: warp & blend), rounded
+std::vector<double> node_family_bary(int d, int N, int family) {
+  std::vector<LD> b;
+  node_bary(d, N, family, b);
+  return rnd(b);
 }
 
 }  // namespace esb

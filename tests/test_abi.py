@@ -63,7 +63,7 @@ def test_setup_rejects_unknown_interface_flux_without_gpu(es):
     m = es.es_mesh(2, len(ev), ev.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                    evx.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), per.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     for bad in (4, -1):
-        o = es.es_options(1.4, bad, 0, 1, None, None, 0, 0, 0)
+        o = es.es_options(1.4, bad, 0, 1, None, None, 0, 0, 0, 0)
         h = ctypes.c_void_p()
         rc = es.es_setup(ctypes.byref(h), ctypes.byref(m), 2, es.es_map_fn(0), None, ctypes.byref(o))
         assert rc == es.ES_ERR_CONFIG

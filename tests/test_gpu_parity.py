@@ -432,3 +432,30 @@ def test_erk_dp8_step_parity(es, d, p):
     ctx.get_state(o4)
     ctx.synchronize()
     assert (_relerr(out.cpu().numpy() - u, o4.cpu().numpy() - u) < 1e-12).all()
+
+
+@pytest.mark.parametrize("d,M,p,warp,ic,fm", [(2, 3, 4, "paper", "wave", 1), (2, 3, 10, "bj", "vortex", 1),
+                                               (3, 3, 3, "paper", "tgv3", 1), (3, 3, 8, "bj", "tgv", 1),
+                                               (3, 3, 5, "paper", "tgv3", 0)])
+def test_warp_and_blend_mapping_parity(es, d, M, p, warp, ic, fm):
+    """es_options.mapping_nodes = 1 (warp & blend mapping and curl-interpolation nodes, R32):
+    geometry and RHS against the oracle built on its own warp & blend node set."""
+    L = _L(d)
+    mesh = I.split_cartesian(d, M, L)
+    w = _warp(warp, d, L, M)
+    om = O.Mesh(mesh, p, warp=w, nodes=1)
+    ctx = es.Context(mesh, p, warp=w, interface_flux=fm, mapping_nodes=1)
+    for e in (0, 7, om.ne - 1):
+        go, gg = om.geometry(e), ctx.element_geometry(e)
+        for k in ("G", "Jn", "Jt"):
+            assert np.abs(gg[k] - go[k]).max() < 1e-12 * np.abs(go[k]).max(), k
+    u = om.project(_ic(ic, om.node_coords(), d, L))
+    u = I.perturb_modal(u, d, p, seed=2, amp=1e-2)
+    got = _gpu_rhs(ctx, u)
+    ref0, _ = om.rhs(u, flux_mode=fm, variant=0)
+    err = _relerr(got, ref0)
+    assert (err <= TOL).all(), err
+    # the lattice-node map of the same warp is a different geometry: the RHS differs
+    ctx0 = es.Context(mesh, p, warp=w, interface_flux=fm, mapping_nodes=0)
+    if warp != "none":
+        assert np.abs(_gpu_rhs(ctx0, u) - got).max() > 1e-9 * np.abs(got).max()

@@ -159,3 +159,16 @@ def test_extrapolation_and_pkd_tables(es, d, p):
             if d == 3:
                 v *= p3[a[0] + a[1], a[2], C]
             assert abs(v - V[i, k]) < 1e-14 * max(1.0, abs(V[i, k]))
+
+
+@pytest.mark.parametrize("d,N", [(2, 3), (2, 8), (2, 11), (3, 3), (3, 6), (3, 9)])
+def test_warp_and_blend_nodes_match_oracle(es, d, N):
+    """The product's warp & blend mapping nodes (binary128, Gauss-Jacobi (1,1) interior GLL points,
+    barycentric Lagrange warp) equal the oracle's (long double, Newton on P_N') as sets (R32)."""
+    b = es.ref_table(d, N, "nodes1").reshape(-1, d + 1)
+    _, lo = O.nodes(d, N, 1)
+    key = lambda a: np.array(sorted(map(tuple, np.round(a, 12) + 0.0)))
+    assert b.shape == lo.shape
+    assert np.abs(key(b) - key(lo)).max() < 1e-15
+    b0 = es.ref_table(d, N, "nodes0").reshape(-1, d + 1)
+    assert np.abs(b0 * N - np.round(b0 * N)).max() < 1e-13
