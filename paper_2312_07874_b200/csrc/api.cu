@@ -96,6 +96,7 @@ struct es_context {
   int64_t launches = 0;
   bool timing = false;
   long long* dbg = nullptr;  // ES_PHASE_TIMING diagnostics
+  std::vector<double> psig_doubles;  // host copy of the padded psi tables (DevRef::psig)
   std::vector<TimedEvent> tev;
   std::vector<cudaEvent_t> ev_pool;
 };
@@ -181,6 +182,28 @@ es_status upload_tables(es_context* c) {
   size_t o_pa1 = add_i(t.pair_a1), o_pa2 = add_i(t.pair_a2), o_poff = add_i(t.pair_off), o_mpr = add_i(mode_pr),
          o_ml = add_i(mode_last);
   size_t o_B = add_d(t.Bf), o_nh = add_d(t.nhat), o_W = add_d(t.Wvol);
+  // the psi tables in the padded layout of stage_psi / psi_tables (kernels.cuh) for kernels that read
+  // them from global memory (L1) instead of staging them in shared memory (the slim K1)
+  {
+    const int n = t.n, NP = (n + 1) & ~1, npair = (int)t.pair_a1.size();
+    const int nd = n * NP + n * n * NP + (t.d == 3 ? n * n * NP : 0) + 48;  // + PSPAD
+    std::vector<double> pg(nd + (3 * npair + 1) / 2 + 1, 0.0);
+    for (int r = 0; r < n; ++r)
+      for (int q = 0; q < n; ++q) pg[(size_t)r * NP + q] = t.psi1[(size_t)r * n + q];
+    for (int r = 0; r < n * n; ++r)
+      for (int q = 0; q < n; ++q) {
+        pg[(size_t)n * NP + (size_t)r * NP + q] = t.psi2[(size_t)r * n + q];
+        if (t.d == 3) pg[(size_t)(n + n * n) * NP + (size_t)r * NP + q] = t.psi3[(size_t)r * n + q];
+      }
+    int* pi = reinterpret_cast<int*>(pg.data() + nd);
+    for (int k = 0; k < npair; ++k) {
+      pi[k] = t.pair_a1[k];
+      pi[npair + k] = t.pair_a2[k];
+      pi[2 * npair + k] = t.pair_off[k];
+    }
+    c->psig_doubles = pg;
+  }
+  size_t o_pg = add_d(c->psig_doubles);
   char* d = nullptr;
   CK(cudaMalloc((void**)&d, blob.size()));
   CK(cudaMemcpy(d, blob.data(), blob.size(), cudaMemcpyHostToDevice));
@@ -189,7 +212,7 @@ es_status upload_tables(es_context* c) {
   auto I = [&](size_t o) { return (const int*)(d + o); };
   c->R = DevRef{P(o_eta), P(o_w), P(o_eta3), P(o_w3), P(o_q1), P(o_a1), P(o_a2), P(o_a3), P(o_a4),
                 P(o_lL), P(o_lR), P(o_l3), P(o_li4), P(o_p1), P(o_p2), P(o_p3),
-                I(o_pa1), I(o_pa2), I(o_poff), I(o_mpr), I(o_ml), P(o_B), P(o_nh), P(o_W)};
+                I(o_pa1), I(o_pa2), I(o_poff), I(o_mpr), I(o_ml), P(o_B), P(o_nh), P(o_W), P(o_pg)};
   return ES_OK;
 }
 

@@ -47,6 +47,7 @@ struct DevRef {
   const double *psi1, *psi2, *psi3;
   const int *pair_a1, *pair_a2, *pair_off, *mode_pr, *mode_last;
   const double *Bf, *nhat, *Wvol;
+  const double* psig;  // the psi tables in the padded layout of psi_tables() (global memory)
 };
 
 struct ProjArgs {
@@ -452,14 +453,20 @@ __device__ void modal_to_nodal(const PsiS& T, const double* um, double* un, doub
       fiberK_n<N, false>(T.p3 + sdeg * N * psi_np<N>(), N - sdeg, in[0], 1, out[0], 1);
     }
     __syncthreads();
-    // t2[v][a1][c][b] = sum_a2 psi2[a1][a2][b] t1[v][pr(a1,a2)][c]; items (a1, pair of (v, c) fibers)
-    constexpr int NFC = NV * N, NPC = (NFC + 1) / 2;
-    for (int it = tid; it < N * NPC; it += nt) {
-      const int a1 = it / NPC, w = it - a1 * NPC, q0 = w, q1 = w + NPC < NFC ? w + NPC : w;
-      const int v0 = q0 / N, c0 = q0 - v0 * N, v1 = q1 / N, c1 = q1 - v1 * N;
-      const int prs = a1 * N - a1 * (a1 - 1) / 2;
-      fiber2<N, false>(T.p2 + a1 * N * psi_np<N>(), N - a1, N, t1 + (v0 * NPAIR + prs) * N + c0, t1 + (v1 * NPAIR + prs) * N + c1, N,
-                nullptr, nullptr, t2 + ((v0 * N + a1) * N + c0) * N, t2 + ((v1 * N + a1) * N + c1) * N, 1, q1 != q0);
+    // t2[v][a1][c][b] = sum_a2 psi2[a1][a2][b] t1[v][pr(a1,a2)][c]: one item = the (v, c) fibres of the
+    // rows a1 = k and N - 1 - k, N + 1 modal inputs per item whatever k (balanced: a fibre pair of one
+    // row a1 = 0 would take 2N); lanes of a warp share k, so the table reads are broadcasts
+    constexpr int NFC = NV * N, NK = (N + 1) / 2;
+    for (int it = tid; it < NK * NFC; it += nt) {
+      const int k = it / NFC, w = it - k * NFC, v = w / N, c = w - v * N;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a1 = h == 0 ? k : N - 1 - k;
+        if (h == 1 && a1 == k) break;
+        const int prs = a1 * N - a1 * (a1 - 1) / 2;
+        fiberK_n<N, false>(T.p2 + a1 * N * psi_np<N>(), N - a1, t1 + (v * NPAIR + prs) * N + c, N,
+                           t2 + ((v * N + a1) * N + c) * N, 1);
+      }
     }
     __syncthreads();
     // u[v][a + N bc] = sum_a1 psi1[a1][a] t2[v][a1][bc]: one (v, bc) fibre per item, the psi1 table
@@ -519,14 +526,19 @@ __device__ void nodal_to_modal(const PsiS& T, const double* y, double* um, doubl
       for (int a1 = 0; a1 < N; ++a1) out[a1 * N * N] = o[a1];
     }
     __syncthreads();
-    // s1[v][pr(a1,a2)][c] = sum_b psi2[a1][a2][b] s2[v][a1][c][b]; items (a1, pair of (v, c) fibers)
-    constexpr int NFC = NV * N, NPC = (NFC + 1) / 2;
-    for (int it = tid; it < N * NPC; it += nt) {
-      const int a1 = it / NPC, w = it - a1 * NPC, q0 = w, q1 = w + NPC < NFC ? w + NPC : w;
-      const int v0 = q0 / N, c0 = q0 - v0 * N, v1 = q1 / N, c1 = q1 - v1 * N;
-      const int prs = a1 * N - a1 * (a1 - 1) / 2;
-      fiber2<N, true>(T.p2 + a1 * N * psi_np<N>(), N, N - a1, t2 + ((v0 * N + a1) * N + c0) * N, t2 + ((v1 * N + a1) * N + c1) * N, 1,
-                nullptr, nullptr, t1 + (v0 * NPAIR + prs) * N + c0, t1 + (v1 * NPAIR + prs) * N + c1, N, q1 != q0);
+    // s1[v][pr(a1,a2)][c] = sum_b psi2[a1][a2][b] s2[v][a1][c][b]: one item = the (v, c) fibres of the
+    // rows a1 = k and N - 1 - k (N + 1 modal outputs per item, balanced as in modal_to_nodal)
+    constexpr int NFC = NV * N, NK = (N + 1) / 2;
+    for (int it = tid; it < NK * NFC; it += nt) {
+      const int k = it / NFC, w = it - k * NFC, v = w / N, c = w - v * N;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a1 = h == 0 ? k : N - 1 - k;
+        if (h == 1 && a1 == k) break;
+        const int prs = a1 * N - a1 * (a1 - 1) / 2;
+        fiberK_n<N, true>(T.p2 + a1 * N * psi_np<N>(), N - a1, t2 + ((v * N + a1) * N + c) * N, 1,
+                          t1 + (v * NPAIR + prs) * N + c, N);
+      }
     }
     __syncthreads();
     // u[v][off(pr)+a3] = sum_c psi3[s][a3][c] s1[v][pr][c]; one (pr, v) fibre per item
@@ -561,21 +573,40 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Slim K1 (experiment, off: ES_K1_SLIM=1 enables it for tetrahedra at N = 9): the shared-memory
+// footprint cut from 111 KB to 72 KB so that three
+// CTAs of 256 threads share an SM instead of two of 384 -- K1 is barrier-bound (one element's
+// transform steps give ~200-400 work items between barriers), and a third element in flight hides
+// more of it.  The facet values alias the second transform buffer, W J~ and W / J~ are read from
+// global memory where they are used, and the psi2 / psi3 tables come from a padded global copy (L1).
+#ifndef ES_K1_SLIM
+#define ES_K1_SLIM 0  // measured slower at C5: 19.7 vs 17.9 ms per RHS
+#endif
+template <int DIM, int N>
+__host__ __device__ constexpr bool k1_slim() {
+  return ES_K1_SLIM && DIM == 3 && N == 9;
+}
 template <int DIM, int N>
 struct ProjSmem {
   using S = Sz<DIM, N>;
+  static constexpr bool SLIM = k1_slim<DIM, N>();
   static constexpr int ev(int x) { return (x + 1) & ~1; }
   static constexpr int XB = S::NC * S::Nq;            // nodal buffer
   static constexpr int T2B = S::NC * S::Nq;           // second transform buffer
-  static constexpr int FWB = S::NC * S::NF;           // facet values
+  static constexpr int FWB = SLIM ? 0 : S::NC * S::NF;  // facet values (slim: in T2 after the facet-4 scratch)
   static constexpr int UMB = S::NC * S::Np;           // modal work buffer
-  static constexpr int INB = S::NC * S::Np + 2 * S::Nq;  // prefetched input: u~, W J~, W / J~
+  static constexpr int INB = S::NC * S::Np + (SLIM ? 0 : 2 * S::Nq);  // prefetched input: u~ (, W J~, W / J~)
   static constexpr int TBB = 3 * N + N * N;           // lL, lR, l3L, lint4
-  static constexpr int o_x = 0, o_t2 = ev(o_x + XB), o_fw = ev(o_t2 + T2B), o_um = ev(o_fw + FWB),
-                       o_in = ev(o_um + UMB), o_tb = ev(o_in + INB), o_ps = ev(o_tb + TBB),
-                       total = o_ps + psi_smem_doubles<DIM, N>();
+  static constexpr int o_x = 0, o_t2 = ev(o_x + XB), o_fw = SLIM ? o_t2 + ev(S::NC * N * N) : ev(o_t2 + T2B),
+                       o_um = ev(o_t2 + T2B + FWB), o_in = ev(o_um + UMB), o_tb = ev(o_in + INB), o_ps = ev(o_tb + TBB),
+                       total = o_ps + (SLIM ? 0 : psi_smem_doubles<DIM, N>());
   static_assert(S::NC * N * N <= T2B, "facet-4 scratch");
+  static_assert(!SLIM || ev(S::NC * N * N) + S::NC * S::NF <= T2B, "slim: facet values fit behind the facet-4 scratch");
 };
+template <int DIM, int N>
+__host__ __device__ constexpr int k1_threads() {
+  return k1_slim<DIM, N>() ? 256 : Sz<DIM, N>::NT;
+}
 
 template <int DIM, int N>
 __host__ __device__ constexpr size_t project_smem_doubles() {
@@ -587,13 +618,13 @@ __host__ __device__ constexpr size_t project_smem_doubles() {
 template <int DIM, int N>
 __host__ __device__ constexpr int k1_min_blocks() {
   constexpr int smem_fit = (227 * 1024) / (int)(project_smem_doubles<DIM, N>() * 8 + 1024);
-  constexpr int want = 20 / (Sz<DIM, N>::NT / 32);
+  constexpr int want = k1_slim<DIM, N>() ? 3 : 20 / (Sz<DIM, N>::NT / 32);
   constexpr int b = want < smem_fit ? want : smem_fit;
   return b < 2 ? 2 : b;
 }
 
 template <int DIM, int N>
-__global__ void __launch_bounds__(Sz<DIM, N>::NT, k1_min_blocks<DIM, N>()) project_kernel(DevRef R, ProjArgs A) {
+__global__ void __launch_bounds__(k1_threads<DIM, N>(), k1_min_blocks<DIM, N>()) project_kernel(DevRef R, ProjArgs A) {
   using S = Sz<DIM, N>;
   using L = ProjSmem<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf;
@@ -602,9 +633,9 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT, k1_min_blocks<DIM, N>()) proje
   double* T2 = sm + L::o_t2;  // [NC][Nq]
   double* FW = sm + L::o_fw;  // [NC][NF]
   double* um = sm + L::o_um;  // [NC][Np]
-  double* uin = sm + L::o_in;  // [NC][Np] u~, then W J~ [Nq], W / J~ [Nq]
-  double* wj = uin + NC * Np;
-  double* wjinv = wj + Nq;
+  double* uin = sm + L::o_in;  // [NC][Np] u~, then W J~ [Nq], W / J~ [Nq] (not slim)
+  const double* wj = uin + NC * Np;
+  const double* wjinv = wj + Nq;
   double* tlL = sm + L::o_tb;
   double* tlR = tlL + N;
   double* tl3 = tlR + N;
@@ -616,12 +647,14 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT, k1_min_blocks<DIM, N>()) proje
   auto prefetch = [&](int64_t e) {
     const double* src = A.u + (size_t)e * NC * Np;
     for (int k = tid; k < NC * Np; k += nt) cp_async8(uin + k, src + k);
-    const double* gv = A.geo_vol + (size_t)e * S::GVS + S::NG * Nq;
-    for (int k = tid; k < 2 * Nq; k += nt) cp_async8(wj + k, gv + k);
+    if constexpr (!L::SLIM) {
+      const double* gv = A.geo_vol + (size_t)e * S::GVS + S::NG * Nq;
+      for (int k = tid; k < 2 * Nq; k += nt) cp_async8(uin + NC * Np + k, gv + k);
+    }
     cp_async_commit();
   };
   if ((int64_t)blockIdx.x < A.n_elem) prefetch(elem_of(blockIdx.x));
-  const PsiS T = stage_psi<DIM, N>(R, sm + L::o_ps);
+  const PsiS T = L::SLIM ? psi_tables<DIM, N>(const_cast<double*>(R.psig)) : stage_psi<DIM, N>(R, sm + L::o_ps);
   for (int k = tid; k < N; k += nt) {
     tlL[k] = R.lL[k];
     tlR[k] = R.lR[k];
@@ -641,6 +674,10 @@ __global__ void __launch_bounds__(Sz<DIM, N>::NT, k1_min_blocks<DIM, N>()) proje
 #endif
     };
     stamp(0);
+    if constexpr (L::SLIM) {  // W J~ and W / J~ straight from global memory
+      wj = A.geo_vol + (size_t)e * S::GVS + S::NG * Nq;
+      wjinv = wj + Nq;
+    }
     cp_async_wait_all();
     __syncthreads();
     stamp(1);
