@@ -641,7 +641,7 @@ __global__ void __launch_bounds__(k1_threads<DIM, N>(), k1_min_blocks<DIM, N>())
   double* tl3 = tlR + N;
   double* tli4 = tl3 + N;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const double g = A.gamma, gm1 = g - 1.0, gm1inv = 1.0 / gm1;
+  const double g = A.gamma, gm1 = g - 1.0, gm1inv = 1.0 / gm1, i1mg = 1.0 / (1.0 - g);
   auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
   // asynchronous copies (cp.async) of one element's inputs into uin / wj / wjinv
   auto prefetch = [&](int64_t e) {
@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(k1_threads<DIM, N>(), k1_min_blocks<DIM, N>())
         v2 += vel[m] * vel[m];
       }
       const double s = g - gm1 * (w[0] + 0.5 * b * v2);
-      const double r = exp((s + log(b)) / (1.0 - g));
+      const double r = exp((s + log(b)) * i1mg);  // (b e^s)^(1/(1-g))
       out[0] = r;
 #pragma unroll
       for (int m = 0; m < DIM; ++m) out[1 + m] = vel[m];

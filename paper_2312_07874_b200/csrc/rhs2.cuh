@@ -23,6 +23,16 @@ namespace esb {
 // accesses compile to shared-memory loads and stores
 extern __shared__ __align__(16) double smk2[];
 
+// volume-job partner data by shuffle from the partner lane (1), or from shared memory (0); the default
+// (-1) shuffles for tetrahedra up to N = 7 (C4, N = 5: flux kernel 0.65 -> 0.63 ms) and loads at N = 9
+// (C5: 36.14 ms with loads, 36.38 with shuffles -- more spills at 128 registers)
+#ifndef ES_K2_SHFL
+#define ES_K2_SHFL -1
+#endif
+template <int DIM, int N>
+__host__ __device__ constexpr bool k2_shfl() {
+  return ES_K2_SHFL == 1 || (ES_K2_SHFL == -1 && DIM == 3 && N <= 7);
+}
 #ifndef ES_K2_NWMAX
 #define ES_K2_NWMAX 16  // warps per flux-kernel CTA (4 per SM sub-partition at <= 128 registers)
 #endif
@@ -186,11 +196,12 @@ struct Job {
 // both logarithmic means (element-wide bound on the spread of rho and beta), so the branch test
 // is dropped -- the arithmetic is identical to the checked path for such pairs.
 template <int DIM, int B, bool CHK = true>
+__device__ __forceinline__ void flux_batch_o(const NodeState& me, const NodeState* o, const Job<DIM>* jb, double gm1inv,
+                                             double (*F)[DIM + 2]);
+template <int DIM, int B, bool CHK = true>
 __device__ __forceinline__ void flux_batch(const NodeState& me, const Job<DIM>* jb, double gm1inv,
                                            double (*F)[DIM + 2]) {
   NodeState o[B];
-  double rl[B], ib[B], f2r[B], f2b[B];
-  bool need = false;
 #pragma unroll
   for (int t = 0; t < B; ++t) {
     const double* q = jb[t].base + jb[t].idx;
@@ -201,6 +212,14 @@ __device__ __forceinline__ void flux_batch(const NodeState& me, const Job<DIM>* 
     o[t].p = q[(DIM + 1) * st];
     o[t].b = jb[t].bb[jb[t].idx];
   }
+  flux_batch_o<DIM, B, CHK>(me, o, jb, gm1inv, F);
+}
+// the same with the other states already in registers (volume jobs: shuffled from the partner lanes)
+template <int DIM, int B, bool CHK>
+__device__ __forceinline__ void flux_batch_o(const NodeState& me, const NodeState* o, const Job<DIM>* jb, double gm1inv,
+                                             double (*F)[DIM + 2]) {
+  double rl[B], ib[B], f2r[B], f2b[B];
+  bool need = false;
 #pragma unroll
   for (int t = 0; t < B; ++t) {
     const double sr = me.r + o[t].r, isr = rcp_nr1(sr), ur = (me.r - o[t].r) * isr;
@@ -606,9 +625,13 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
       for (int v = 0; v < NC; ++v) acc[v] = 0.0;
 
       // -- volume pairs on this line: shifts in batches of VB (ILP), exchanged by shuffles --
+      // (ES_K2_SHFL: the partner node's state and metric rows come by shuffle from the partner lane,
+      // which holds them in registers, instead of from shared memory -- no bank conflicts, and the
+      // shared-memory pipe, 56-75 % busy, carries fewer wavefronts)
 #pragma unroll
       for (int s0 = 1; s0 <= NS; s0 += W::VB) {
         Job<DIM> jv[W::VB];
+        NodeState ov[W::VB];
         double nl[W::VB][NLOP][DIM];  // per-operator normals (summed unless EQ56)
 #pragma unroll
         for (int t = 0; t < W::VB; ++t) {
@@ -617,6 +640,20 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
           if (pos2 >= N) pos2 -= N;
           const int j = in_range ? i + (pos2 - pos) * stride : 0;
           const int ix = pos * N + pos2;
+          const int gsrc = (lane_ok ? grp : W::LPW - 1) * N + pos2;  // the partner node's lane
+          auto Gj = [&](int l, int m) -> double {
+            if constexpr (k2_shfl<DIM, N>())
+              return shfl_d(gl[l][m], gsrc);
+            else
+              return Gat(l, m, j);
+          };
+          if constexpr (k2_shfl<DIM, N>()) {
+            ov[t].r = shfl_d(me.r, gsrc);
+#pragma unroll
+            for (int m = 0; m < DIM; ++m) ov[t].v[m] = shfl_d(me.v[m], gsrc);
+            ov[t].p = shfl_d(me.p, gsrc);
+            ov[t].b = shfl_d(me.b, gsrc);
+          }
           Job<DIM>& jb = jv[t];
           jb.base = sP;
           jb.bb = sP + (DIM + 2) * Nq;
@@ -639,13 +676,13 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
               const double cl = mk * tw[cb], q1 = cl * tQ1[ix], a1 = cl * tA1[ix];
 #pragma unroll
               for (int m = 0; m < 2; ++m) {
-                put(0, m, q1 * (gl[0][m] + Gat(0, m, j)));
-                put(1, m, a1 * (gl[1][m] + Gat(1, m, j)));
+                put(0, m, q1 * (gl[0][m] + Gj(0, m)));
+                put(1, m, a1 * (gl[1][m] + Gj(1, m)));
               }
             } else {
               const double a2 = mk * tw[ca] * tA2[ix];
 #pragma unroll
-              for (int m = 0; m < 2; ++m) put(0, m, a2 * (gl[1][m] + Gat(1, m, j)));
+              for (int m = 0; m < 2; ++m) put(0, m, a2 * (gl[1][m] + Gj(1, m)));
             }
           } else {
             if (k == 0) {
@@ -653,24 +690,24 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
 #pragma unroll
               for (int m = 0; m < 3; ++m) {
                 if constexpr (EQ56) {
-                  put(0, m, q1 * (gl[0][m] + Gat(0, m, j)));
-                  put(1, m, a1 * (gl[1][m] + Gat(1, m, j)));
-                  put(2, m, a1 * (gl[2][m] + Gat(2, m, j)));
+                  put(0, m, q1 * (gl[0][m] + Gj(0, m)));
+                  put(1, m, a1 * (gl[1][m] + Gj(1, m)));
+                  put(2, m, a1 * (gl[2][m] + Gj(2, m)));
                 } else {  // metric row 1 holds g1 + g2 in this (last) pass
-                  put(0, m, q1 * (gl[0][m] + Gat(0, m, j)) + a1 * (gl[1][m] + Gat(1, m, j)));
+                  put(0, m, q1 * (gl[0][m] + Gj(0, m)) + a1 * (gl[1][m] + Gj(1, m)));
                 }
               }
             } else if (k == 1) {
               const double cl = mk * 0.5 * tw[ca] * tw3[cc], a2 = cl * tA2[ix], a3 = cl * tA3[ix];
 #pragma unroll
               for (int m = 0; m < 3; ++m) {
-                put(0, m, a2 * (gl[1][m] + Gat(1, m, j)));
-                put(1, m, a3 * (gl[2][m] + Gat(2, m, j)));
+                put(0, m, a2 * (gl[1][m] + Gj(1, m)));
+                put(1, m, a3 * (gl[2][m] + Gj(2, m)));
               }
             } else {
               const double a4 = mk * 0.125 * tw[ca] * tw[cb] * (1.0 - teta[cb]) * tA4[ix];
 #pragma unroll
-              for (int m = 0; m < 3; ++m) put(0, m, a4 * (gl[2][m] + Gat(2, m, j)));
+              for (int m = 0; m < 3; ++m) put(0, m, a4 * (gl[2][m] + Gj(2, m)));
             }
           }
         }
@@ -682,7 +719,10 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
 #pragma unroll
             for (int m = 0; m < DIM; ++m) jv[t].n[m] = nl[t][op][m];
           double Fo[W::VB][NC];
-          flux_batch<DIM, W::VB, CHK>(me, jv, gm1inv, Fo);
+          if constexpr (k2_shfl<DIM, N>())
+            flux_batch_o<DIM, W::VB, CHK>(me, ov, jv, gm1inv, Fo);
+          else
+            flux_batch<DIM, W::VB, CHK>(me, jv, gm1inv, Fo);
           if constexpr (CNT) ci += W::VB;
 #pragma unroll
           for (int t = 0; t < W::VB; ++t)
