@@ -99,6 +99,7 @@ struct es_context {
   std::vector<double> psig_doubles;  // host copy of the padded psi tables (DevRef::psig)
   std::vector<TimedEvent> tev;
   std::vector<cudaEvent_t> ev_pool;
+  std::vector<cudaEvent_t> pipe_ev;  // es_step_host pipeline: per chunk, copy done / kernel done
 };
 
 namespace {
@@ -424,6 +425,7 @@ void es_destroy(es_context* c) {
     cudaEventDestroy(t.b);
   }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (auto e : c->pipe_ev) cudaEventDestroy(e);
   if (c->ev_packed) cudaEventDestroy(c->ev_packed);
   if (c->ev_comm) cudaEventDestroy(c->ev_comm);
   if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
@@ -745,13 +747,97 @@ es_status es_step(es_context* c, double dt, int nsteps) {
   return ES_OK;
 }
 
+// es_step_host on one rank, pipelined: the host -> device copy of the state goes in NCH chunks on the
+// copy stream and the first stage's projection K1 runs on each chunk as soon as it has arrived (K1 is
+// element-local: pointer offsets select a contiguous element range); in 3D the last stage's batched
+// inverse K3 runs in chunks and each chunk's device -> host copy starts as soon as it is written.  The
+// arithmetic is that of es_step (same kernels, same per-element work): bitwise equal results.
+namespace {
+constexpr int NCH = 8;
+es_status step_host_pipelined(es_context* c, const double* u_host, double* u_host_out, double dt, int nsteps) {
+  const int64_t per = (int64_t)c->NC * c->Np, n = c->nloc;
+  if ((int)c->pipe_ev.size() < 2 * NCH)
+    while ((int)c->pipe_ev.size() < 2 * NCH) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->pipe_ev.push_back(e);
+    }
+  auto lo = [&](int k) { return n * k / NCH; };
+  const int64_t gvs = even_up((c->d * c->d + 2) * c->Nq), prs = even_up((c->NC + 1) * c->Nq + 1),
+                trs = (int64_t)c->Nf * c->NC * c->Nqf;
+  cudaStream_t cs = c->comm_stream;
+  // the previous call's copies are complete before the state is overwritten
+  CK(cudaEventRecord(c->pipe_ev[0], c->stream));
+  CK(cudaStreamWaitEvent(cs, c->pipe_ev[0], 0));
+  for (int st = 0; st < nsteps; ++st) {
+    for (int s = 0; s < 4; ++s) {
+      RhsArgs A = base_rhs_args(c);
+      A.mode = 1 + s;
+      A.dt = dt;
+      A.u0 = c->U;
+      A.acc = c->ACC;
+      A.ustage = c->US;
+      A.out = c->U;
+      const double* u = s == 0 ? c->U : c->US;
+      if (st == 0 && s == 0) {  // chunked H2D + K1
+        for (int k = 0; k < NCH; ++k) {
+          const int64_t e0 = lo(k), ne = lo(k + 1) - e0;
+          if (ne <= 0) continue;
+          CK(cudaMemcpyAsync(c->U + e0 * per, u_host + e0 * per, (size_t)ne * per * sizeof(double),
+                             cudaMemcpyHostToDevice, cs));
+          CK(cudaEventRecord(c->pipe_ev[k], cs));
+          CK(cudaStreamWaitEvent(c->stream, c->pipe_ev[k], 0));
+          ProjArgs P{ne, nullptr, c->U + e0 * per, c->geo_vol + e0 * gvs, c->prim + e0 * prs, c->trace + e0 * trs,
+                     nullptr, c->bad, c->gamma, nullptr, c->proj_ctas};
+          c->launches++;
+          CK(c->d == 2 ? launch_project_2d(c->n, c->R, P, c->stream) : launch_project_3d(c->n, c->R, P, c->stream));
+        }
+      } else {
+        CK(run_project(c, u, c->nloc, nullptr, nullptr));
+      }
+      const bool last = st == nsteps - 1 && s == 3;
+      if (!(last && c->d == 3)) {
+        CK(run_k2(c, A, c->nloc, nullptr));
+        CK(run_k3(c, A));
+        continue;
+      }
+      CK(run_k2(c, A, c->nloc, nullptr));
+      for (int k = 0; k < NCH; ++k) {  // chunked K3 + D2H
+        const int64_t e0 = lo(k), ne = lo(k + 1) - e0;
+        if (ne <= 0) continue;
+        WadjArgs W{ne, c->rbuf + e0 * (int64_t)c->NC * c->Nq, c->wjk3 + e0 * (int64_t)c->Nq, A.mode, A.out + e0 * per,
+                   A.u0 + e0 * per, A.acc + e0 * per, A.ustage + e0 * per, A.dt, nullptr, nullptr, A.c0};
+        c->launches++;
+        CK(launch_wadj_3d(c->n, W, c->stream));
+        CK(cudaEventRecord(c->pipe_ev[NCH + k], c->stream));
+        CK(cudaStreamWaitEvent(cs, c->pipe_ev[NCH + k], 0));
+        CK(cudaMemcpyAsync(u_host_out + e0 * per, c->U + e0 * per, (size_t)ne * per * sizeof(double),
+                           cudaMemcpyDeviceToHost, cs));
+      }
+    }
+  }
+  if (c->d == 2)
+    CK(cudaMemcpyAsync(u_host_out, c->U, (size_t)n * per * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(cs));
+  return ES_OK;
+}
+}  // namespace
+
 es_status es_step_host(es_context* c, const double* u_host, double* u_host_out, double dt, int nsteps) {
   POISON_CHECK();
   if (!u_host || !u_host_out) return fail(c, ES_ERR_ARG, "null buffer");
   CK(cudaSetDevice(c->device));
   const size_t bytes = (size_t)c->nloc * c->NC * c->Np * sizeof(double);
-  CK(cudaMemcpyAsync(c->U, u_host, bytes, cudaMemcpyHostToDevice, c->stream));
   c->dp_fsal = false;
+  // large states only (small meshes keep the single CUDA-graph replay of es_step)
+  if (c->world == 1 && nsteps >= 1 && !c->timing && !c->dbg && bytes >= ((size_t)64 << 20) && !c->eq56 && !c->dense) {
+    es_status s = step_host_pipelined(c, u_host, u_host_out, dt, nsteps);
+    if (s != ES_OK) return s;
+    if (c->check_adm) return check_bad(c);
+    return ES_OK;
+  }
+  CK(cudaMemcpyAsync(c->U, u_host, bytes, cudaMemcpyHostToDevice, c->stream));
   es_status s = es_step(c, dt, nsteps);
   if (s != ES_OK) return s;
   CK(cudaMemcpyAsync(u_host_out, c->U, bytes, cudaMemcpyDeviceToHost, c->stream));

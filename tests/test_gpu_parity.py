@@ -459,3 +459,27 @@ def test_warp_and_blend_mapping_parity(es, d, M, p, warp, ic, fm):
     ctx0 = es.Context(mesh, p, warp=w, interface_flux=fm, mapping_nodes=0)
     if warp != "none":
         assert np.abs(_gpu_rhs(ctx0, u) - got).max() > 1e-9 * np.abs(got).max()
+
+
+@pytest.mark.parametrize("d,M,p", [(3, 12, 8), (2, 128, 10)])
+def test_step_host_pipelined_bitwise(es, d, M, p):
+    """es_step_host on a state above 64 MB takes the pipelined path (chunked host -> device copies
+    overlapping the first stage's K1, in 3D chunked K3 + device -> host copies of the last stage): the
+    same kernels on the same elements, so the state equals es_step's bit for bit, for one and for
+    several steps per call."""
+    L = _L(d)
+    mesh = I.split_cartesian(d, M, L)
+    ctx = es.Context(mesh, p, warp=I.bj_warp(d, L, M), interface_flux=1)
+    u = I.modal_state_from_centroids(mesh, p, "tgv" if d == 3 else "vortex", seed=4)
+    assert u.nbytes >= 64 << 20
+    ut = torch.from_numpy(u).cuda()
+    for nsteps in (1, 2):
+        ctx.set_state(ut)
+        ctx.step(2e-4, nsteps)
+        ref = torch.empty_like(ut)
+        ctx.get_state(ref)
+        ctx.synchronize()
+        hin = torch.from_numpy(u).pin_memory()
+        hout = torch.full_like(hin, float("nan")).pin_memory()
+        ctx.step_host(hin, hout, 2e-4, nsteps)
+        assert np.array_equal(hout.numpy(), ref.cpu().numpy()), nsteps
