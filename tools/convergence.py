@@ -15,6 +15,7 @@ RK4 at these steps is below the spatial error (checked with --cfl 0.05 in DESIGN
 
     python tools/convergence.py --dim 2 --p 4 5 --M 4 8 16 32 [--T 2] [--flux 0 1]
     python tools/convergence.py --dim 3 --p 1 2 3 4 5 6 --M 4 --flux 1          (p-refinement)
+    python tools/convergence.py ... --nodes 1      (warp & blend mapping nodes)
 
 Prints one JSON line per run and the observed orders log2(e_M / e_2M).
 """
@@ -53,11 +54,11 @@ def l2_density_error(ctx, torch, u, d, L, t, xi, wq):
     return math.sqrt(err2), jmin
 
 
-def run_case(es, I, torch, d, p, M, T, warp="paper", fm=1, cfl=0.1, rule_n=18):
+def run_case(es, I, torch, d, p, M, T, warp="paper", fm=1, cfl=0.1, rule_n=18, nodes=0):
     L = 2.0
     mesh = I.split_cartesian(d, M, L)
     w = {"paper": I.paper_warp(d, L), "bj": I.bj_warp(d, L, M), "none": None}[warp]
-    ctx = es.Context(mesh, p, warp=w, interface_flux=fm)
+    ctx = es.Context(mesh, p, warp=w, interface_flux=fm, mapping_nodes=nodes)
     x = torch.empty((ctx.nloc, ctx.Nq, d), dtype=torch.float64, device="cuda")
     ctx.node_coords(x)
     ctx.synchronize()
@@ -80,6 +81,7 @@ def run_case(es, I, torch, d, p, M, T, warp="paper", fm=1, cfl=0.1, rule_n=18):
     rate, scale, cons = ctx.entropy_production(u)
     ctx.close()
     return dict(dim=d, p=p, M=M, h=h, T=T, steps=nsteps, dt=dt, cfl=cfl, warp=warp, flux="ES" if fm else "EC",
+                mapping_nodes=["lattice", "warp_and_blend"][nodes],
                 l2_rho_error=err, l2_rho_error_t0=e0, min_jacobian=jmin, entropy_rate=rate, entropy_scale=scale,
                 conservation=list(map(float, cons)), wall_s=wall, rule_degree=2 * rule_n - 1)
 
@@ -93,6 +95,7 @@ def main():
     ap.add_argument("--cfl", type=float, default=0.1)
     ap.add_argument("--warp", default="paper", choices=["paper", "bj", "none"])
     ap.add_argument("--flux", type=int, nargs="+", default=[1, 0], help="1 = entropy stable (LLF), 0 = entropy conservative")
+    ap.add_argument("--nodes", type=int, default=0, help="mapping nodes: 0 equispaced lattice (R10), 1 warp & blend (P:845, R32)")
     ap.add_argument("--out", default=None, help="JSONL file (appended)")
     args = ap.parse_args()
     import torch
@@ -111,14 +114,14 @@ def main():
         for p in args.p:
             errs = []
             for M in args.M:
-                rec = run_case(es, I, torch, args.dim, p, M, args.T, args.warp, fm, args.cfl)
+                rec = run_case(es, I, torch, args.dim, p, M, args.T, args.warp, fm, args.cfl, nodes=args.nodes)
                 errs.append(rec["l2_rho_error"])
                 emit(rec)
             if len(args.M) > 1:
                 orders = [math.log2(errs[k] / errs[k + 1]) * math.log(2) / math.log(args.M[k + 1] / args.M[k])
                           for k in range(len(errs) - 1)]
                 emit({"dim": args.dim, "p": p, "flux": "ES" if fm else "EC", "M": args.M, "observed_orders": orders,
-                      "expected": p + 1})
+                      "expected": p + 1, "mapping_nodes": ["lattice", "warp_and_blend"][args.nodes]})
 
 
 if __name__ == "__main__":
