@@ -100,6 +100,8 @@ struct es_context {
   std::vector<TimedEvent> tev;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<cudaEvent_t> pipe_ev;  // es_step_host pipeline: per chunk, copy done / kernel done
+  std::vector<int> pipe_dep;         // per chunk: the last chunk holding a face neighbour of its elements
+  int64_t* d_iota = nullptr;         // 0 .. nloc-1 (element lists of the pipeline's chunks)
 };
 
 namespace {
@@ -408,7 +410,7 @@ void es_destroy(es_context* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : {(void*)c->d_tables, (void*)c->geo_vol, (void*)c->geo_face, (void*)c->xq, (void*)c->jt,
                   (void*)c->prim, (void*)c->trace, (void*)c->wt, (void*)c->part, (void*)c->red,
-                  (void*)c->face_slot, (void*)c->d_interior, (void*)c->d_boundary, (void*)c->d_send,
+                  (void*)c->face_slot, (void*)c->d_interior, (void*)c->d_boundary, (void*)c->d_send, (void*)c->d_iota,
                   (void*)c->face_reflect, (void*)c->bad, (void*)c->U, (void*)c->ACC, (void*)c->US,
                   (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg,
                   (void*)c->dpy, (void*)c->dppart, (void*)c->sdense, (void*)c->rbdense, (void*)c->rbuf,
@@ -747,26 +749,41 @@ es_status es_step(es_context* c, double dt, int nsteps) {
   return ES_OK;
 }
 
-// es_step_host on one rank, pipelined: the host -> device copy of the state goes in NCH chunks on the
-// copy stream and the first stage's projection K1 runs on each chunk as soon as it has arrived (K1 is
-// element-local: pointer offsets select a contiguous element range); in 3D the last stage's batched
-// inverse K3 runs in chunks and each chunk's device -> host copy starts as soon as it is written.  The
-// arithmetic is that of es_step (same kernels, same per-element work): bitwise equal results.
+// es_step_host on one rank, pipelined: the host -> device copy of the state goes in NCH chunks of
+// contiguous elements on the copy stream; the first stage's projection K1 runs on each chunk as soon as
+// it has arrived (K1 is element-local), and the flux kernel K2 on a chunk as soon as K1 has run on every
+// chunk holding a face neighbour of its elements (pipe_dep; with periodic wrap-around the first chunk
+// comes last).  In the last stage K2 (+ K3 in 3D) run chunk by chunk and each chunk's device -> host
+// copy starts as soon as its new state is written.  Same kernels on the same elements as es_step:
+// bitwise equal results (test_step_host_pipelined_bitwise).
 namespace {
 constexpr int NCH = 8;
 es_status step_host_pipelined(es_context* c, const double* u_host, double* u_host_out, double dt, int nsteps) {
   const int64_t per = (int64_t)c->NC * c->Np, n = c->nloc;
-  if ((int)c->pipe_ev.size() < 2 * NCH)
+  auto lo = [&](int k) { return n * k / NCH; };
+  if ((int)c->pipe_ev.size() < 2 * NCH) {
     while ((int)c->pipe_ev.size() < 2 * NCH) {
       cudaEvent_t e;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       c->pipe_ev.push_back(e);
     }
-  auto lo = [&](int k) { return n * k / NCH; };
+    std::vector<int64_t> iota(n);
+    for (int64_t e = 0; e < n; ++e) iota[e] = e;
+    CK(upload(&c->d_iota, iota));
+    c->pipe_dep.assign(NCH, 0);
+    for (int k = 0; k < NCH; ++k)
+      for (int64_t e = lo(k); e < lo(k + 1); ++e)
+        for (int z = 0; z < c->Nf; ++z) {
+          const int64_t nb = c->plan.nbr[e * c->Nf + z];
+          int kk = 0;
+          while (kk + 1 < NCH && lo(kk + 1) <= nb) ++kk;
+          c->pipe_dep[k] = std::max(c->pipe_dep[k], std::max(kk, k));
+        }
+  }
   const int64_t gvs = even_up((c->d * c->d + 2) * c->Nq), prs = even_up((c->NC + 1) * c->Nq + 1),
                 trs = (int64_t)c->Nf * c->NC * c->Nqf;
   cudaStream_t cs = c->comm_stream;
-  // the previous call's copies are complete before the state is overwritten
+  // the copies wait for earlier work on the context stream (which may still use the state)
   CK(cudaEventRecord(c->pipe_ev[0], c->stream));
   CK(cudaStreamWaitEvent(cs, c->pipe_ev[0], 0));
   for (int st = 0; st < nsteps; ++st) {
@@ -778,37 +795,46 @@ es_status step_host_pipelined(es_context* c, const double* u_host, double* u_hos
       A.acc = c->ACC;
       A.ustage = c->US;
       A.out = c->U;
-      const double* u = s == 0 ? c->U : c->US;
-      if (st == 0 && s == 0) {  // chunked H2D + K1
+      const bool first = st == 0 && s == 0, last = st == nsteps - 1 && s == 3;
+      if (first) {  // chunked H2D -> K1, K2 as soon as the neighbours' traces exist, then K3
+        std::vector<char> done(NCH, 0);
         for (int k = 0; k < NCH; ++k) {
           const int64_t e0 = lo(k), ne = lo(k + 1) - e0;
-          if (ne <= 0) continue;
-          CK(cudaMemcpyAsync(c->U + e0 * per, u_host + e0 * per, (size_t)ne * per * sizeof(double),
-                             cudaMemcpyHostToDevice, cs));
-          CK(cudaEventRecord(c->pipe_ev[k], cs));
-          CK(cudaStreamWaitEvent(c->stream, c->pipe_ev[k], 0));
-          ProjArgs P{ne, nullptr, c->U + e0 * per, c->geo_vol + e0 * gvs, c->prim + e0 * prs, c->trace + e0 * trs,
-                     nullptr, c->bad, c->gamma, nullptr, c->proj_ctas};
-          c->launches++;
-          CK(c->d == 2 ? launch_project_2d(c->n, c->R, P, c->stream) : launch_project_3d(c->n, c->R, P, c->stream));
+          if (ne > 0) {
+            CK(cudaMemcpyAsync(c->U + e0 * per, u_host + e0 * per, (size_t)ne * per * sizeof(double),
+                               cudaMemcpyHostToDevice, cs));
+            CK(cudaEventRecord(c->pipe_ev[k], cs));
+            CK(cudaStreamWaitEvent(c->stream, c->pipe_ev[k], 0));
+            ProjArgs P{ne, nullptr, c->U + e0 * per, c->geo_vol + e0 * gvs, c->prim + e0 * prs, c->trace + e0 * trs,
+                       nullptr, c->bad, c->gamma, nullptr, c->proj_ctas};
+            c->launches++;
+            CK(c->d == 2 ? launch_project_2d(c->n, c->R, P, c->stream) : launch_project_3d(c->n, c->R, P, c->stream));
+          }
+          for (int i = 0; i < NCH; ++i)
+            if (!done[i] && c->pipe_dep[i] <= k) {
+              CK(run_k2(c, A, lo(i + 1) - lo(i), c->d_iota + lo(i)));
+              done[i] = 1;
+            }
         }
-      } else {
-        CK(run_project(c, u, c->nloc, nullptr, nullptr));
+        CK(run_k3(c, A));
+        continue;
       }
-      const bool last = st == nsteps - 1 && s == 3;
-      if (!(last && c->d == 3)) {
+      CK(run_project(c, s == 0 ? c->U : c->US, c->nloc, nullptr, nullptr));
+      if (!last) {
         CK(run_k2(c, A, c->nloc, nullptr));
         CK(run_k3(c, A));
         continue;
       }
-      CK(run_k2(c, A, c->nloc, nullptr));
-      for (int k = 0; k < NCH; ++k) {  // chunked K3 + D2H
+      for (int k = 0; k < NCH; ++k) {  // chunked K2 (+ K3) -> D2H
         const int64_t e0 = lo(k), ne = lo(k + 1) - e0;
         if (ne <= 0) continue;
-        WadjArgs W{ne, c->rbuf + e0 * (int64_t)c->NC * c->Nq, c->wjk3 + e0 * (int64_t)c->Nq, A.mode, A.out + e0 * per,
-                   A.u0 + e0 * per, A.acc + e0 * per, A.ustage + e0 * per, A.dt, nullptr, nullptr, A.c0};
-        c->launches++;
-        CK(launch_wadj_3d(c->n, W, c->stream));
+        CK(run_k2(c, A, ne, c->d_iota + e0));
+        if (c->d == 3) {
+          WadjArgs W{ne, c->rbuf + e0 * (int64_t)c->NC * c->Nq, c->wjk3 + e0 * (int64_t)c->Nq, A.mode, A.out + e0 * per,
+                     A.u0 + e0 * per, A.acc + e0 * per, A.ustage + e0 * per, A.dt, nullptr, nullptr, A.c0};
+          c->launches++;
+          CK(launch_wadj_3d(c->n, W, c->stream));
+        }
         CK(cudaEventRecord(c->pipe_ev[NCH + k], c->stream));
         CK(cudaStreamWaitEvent(cs, c->pipe_ev[NCH + k], 0));
         CK(cudaMemcpyAsync(u_host_out + e0 * per, c->U + e0 * per, (size_t)ne * per * sizeof(double),
@@ -816,8 +842,6 @@ es_status step_host_pipelined(es_context* c, const double* u_host, double* u_hos
       }
     }
   }
-  if (c->d == 2)
-    CK(cudaMemcpyAsync(u_host_out, c->U, (size_t)n * per * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaStreamSynchronize(cs));
   return ES_OK;
