@@ -326,11 +326,27 @@ es_status rhs_second(es_context* c, RhsArgs A) {
 //       sender) pair (rhs_phase_b_loopback, es_group_*);
 //   (c) interface fluxes of elements without remote neighbours (overlapping the exchange), wait for
 //       the exchange, interface fluxes of the boundary elements, flux kernel (+ K3 in 3D).
+// With world > 1 the projection runs on the boundary elements (those with a remote neighbour) first,
+// so that their traces are packed and the exchange starts while K1 runs on the interior elements.
 es_status rhs_phase_a(es_context* c, const double* u, double* wt) {
-  es_status s0 = rhs_first(c, u, wt);
-  if (s0 != ES_OK || c->world == 1) return s0;
+  if (c->world == 1) return rhs_first(c, u, wt);
+  TimedEvent te{};
+  if (c->timing) {
+    te = {get_event(c), get_event(c), 0};
+    cudaEventRecord(te.a, c->stream);
+  }
+  CK(run_project(c, u, (int64_t)c->plan.boundary.size(), c->d_boundary, wt));
+  const int per_face = c->NC * c->Nqf;
+  const int64_t nsend = (int64_t)c->plan.send_slots.size();
+  CK(launch_pack(c->trace, c->d_send, nsend, per_face, c->send_buf, c->stream));
+  c->launches++;
   CK(cudaEventRecord(c->ev_packed, c->stream));
   CK(cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
+  CK(run_project(c, u, (int64_t)c->plan.interior.size(), c->d_interior, wt));
+  if (c->timing) {
+    cudaEventRecord(te.b, c->stream);
+    c->tev.push_back(te);
+  }
   return ES_OK;
 }
 

@@ -36,13 +36,19 @@ __host__ __device__ constexpr bool k2_shfl() {
 #ifndef ES_K2_NWMAX
 #define ES_K2_NWMAX 16  // warps per flux-kernel CTA (4 per SM sub-partition at <= 128 registers)
 #endif
+// tetrahedra at N = 9 (C5): 12 warps at 168 registers (35.56 ms per RHS) beat 16 at 128 (36.14 ms) once
+// the shared-memory bank conflicts were removed (tools/gpu_k2sweep.sh; 14 warps: 47.0 ms)
+#ifndef ES_K2_NW9
+#define ES_K2_NW9 12
+#endif
 template <int DIM, int N>
 struct Lw {  // line-group layout
   using S = Sz<DIM, N>;
   static constexpr int LPW = 32 / N;                         // lines per warp slot
   static constexpr int NL = DIM == 2 ? N : N * N;            // lines per direction
   static constexpr int SLOTS = (NL + LPW - 1) / LPW;         // warp slots per direction
-  static constexpr int NW = SLOTS <= ES_K2_NWMAX ? SLOTS : ES_K2_NWMAX;
+  static constexpr int NWM = (DIM == 3 && N == 9) ? ES_K2_NW9 : ES_K2_NWMAX;
+  static constexpr int NW = SLOTS <= NWM ? SLOTS : NWM;
   static constexpr int NT = NW * 32;
   static constexpr int NS = N / 2;                            // shifts
 #ifndef ES_K2_VB
