@@ -72,6 +72,8 @@ def lib():
         L.ora_mesh_destroy.argtypes = [ctypes.c_void_p]
         L.ora_mesh_geometry.argtypes = [ctypes.c_void_p, ctypes.c_int64, _dp, _dp, _dp, _dp, _dp]
         L.ora_mesh_conn.argtypes = [ctypes.c_void_p, _lp, _ip, _ip]
+        L.ora_metric_modal.argtypes = [ctypes.c_void_p, ctypes.c_int64, _dp]
+        L.ora_mesh_use_modal_metrics.argtypes = [ctypes.c_void_p]
         L.ora_project.argtypes = [ctypes.c_void_p, ctypes.c_int64, _lp, _dp, _dp]
         L.ora_rhs.argtypes = [ctypes.c_void_p, _dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _lp,
                               ctypes.c_int, ctypes.POINTER(Stats)]
@@ -252,7 +254,7 @@ class Mesh:
     """Oracle mesh + geometry.  `mesh` is an es_inputs.split_cartesian dict, `warp` a callable
     [n,d] -> [n,d] (the user map).  `active`: optional element subset (plus neighbours)."""
 
-    def __init__(self, mesh, p, warp=None, gamma=1.4, active=None, nodes=0):
+    def __init__(self, mesh, p, warp=None, gamma=1.4, active=None, nodes=0, metric_storage=0):
         self.d = mesh["d"]
         self.p = p
         self.gamma = gamma
@@ -286,6 +288,8 @@ class Mesh:
         if not h:
             raise RuntimeError("oracle mesh creation failed")
         self.h = h
+        if metric_storage:  # modal metric storage: G -> V V^T W G
+            lib().ora_mesh_use_modal_metrics(self.h)
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -303,6 +307,13 @@ class Mesh:
         if rc:
             raise KeyError(e)
         return dict(G=G, Gf=Gf, Jt=Jt, Jn=Jn, xq=xq)
+
+    def metric_modal(self, e):
+        """PKD coefficients of the volume metric of element e: [d*d][Np], row l*d + m = V^T W G_lm"""
+        gm = np.zeros((self.d * self.d, self.Np))
+        if lib().ora_metric_modal(self.h, e, _d(gm)):
+            raise KeyError(e)
+        return gm
 
     def conn(self):
         nbr = np.zeros((self.ne, self.Nf), np.int64)

@@ -1375,6 +1375,45 @@ int ora_mesh_geometry(const ora_mesh* m, int64_t el, double* G, double* Gf, doub
   return 0;
 }
 
+// Modal (compressed) metric storage ("the only necessary storage being
+// geometric information", stored here as PKD coefficients instead of nodal values).  The metric
+// terms are polynomials of degree <= p in the reference coordinates: in 2D the exact metrics of the
+// degree-p_g = p map have degree p - 1, in 3D the conservative curl form differentiates
+// the degree-(q+1) interpolant once (R4), degree q = p.  With M = V^T W V = I the
+// L2 projection g~ = V^T W G is therefore exact and V g~ reproduces G at the volume nodes (up to
+// rounding).  g~ [d*d][Np]: row l*d + m holds G_lm.
+int ora_metric_modal(const ora_mesh* m, int64_t el, double* gm) {
+  if (el < 0 || el >= m->ne || !m->has_geom[el]) return -1;
+  const Ref& r = m->ref;
+  const int d = m->d, Nq = r.Nq, Np = r.Np;
+  const vector<double>& G = m->G[el];  // [Nq][d][d]
+  for (int lm = 0; lm < d * d; ++lm)
+    for (int k = 0; k < Np; ++k) {
+      double s = 0.0;  // (V^T W G_lm)_k
+      for (int i = 0; i < Nq; ++i) s += r.V[(size_t)i * Np + k] * r.W[i] * G[(size_t)i * d * d + lm];
+      gm[(size_t)lm * Np + k] = s;
+    }
+  return 0;
+}
+
+int ora_mesh_use_modal_metrics(ora_mesh* m) {
+  const Ref& r = m->ref;
+  const int d = m->d, Nq = r.Nq, Np = r.Np;
+  vector<double> gm((size_t)d * d * Np);
+  for (int64_t el = 0; el < m->ne; ++el) {
+    if (!m->has_geom[el]) continue;
+    ora_metric_modal(m, el, gm.data());
+    vector<double>& G = m->G[el];
+    for (int i = 0; i < Nq; ++i)
+      for (int lm = 0; lm < d * d; ++lm) {
+        double s = 0.0;  // (V g~_lm)_i
+        for (int k = 0; k < Np; ++k) s += r.V[(size_t)i * Np + k] * gm[(size_t)lm * Np + k];
+        G[(size_t)i * d * d + lm] = s;
+      }
+  }
+  return 0;
+}
+
 void ora_mesh_conn(const ora_mesh* m, int64_t* nbr, int* nbr_face, int* reflect) {
   size_t N = m->nbr.size();
   for (size_t i = 0; i < N; ++i) {

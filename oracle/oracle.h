@@ -99,6 +99,13 @@ void ora_mesh_destroy(ora_mesh* m);
  * [Nf][Nqf][d], xq [Nq][d]; any pointer may be NULL. Returns 0, or -1 if geometry not built. */
 int ora_mesh_geometry(const ora_mesh* m, int64_t elem, double* G, double* Gf, double* Jt,
                       double* Jn, double* xq);
+/* modal (compressed) metric storage, SURVEY 8(f) rank 4 / P:595: gm [d*d][Np] = V^T W G_lm of one
+ * element (row l*d + m; exact L2 projection, the metric terms being polynomials of degree <= p).
+ * Returns 0, or -1 if geometry not built. */
+int ora_metric_modal(const ora_mesh* m, int64_t elem, double* gm);
+/* replaces the volume metric G of every element by V (V^T W G), i.e. the values a modal store
+ * reproduces at the volume nodes (facet metrics unchanged); afterwards ora_rhs runs on them. */
+int ora_mesh_use_modal_metrics(ora_mesh* m);
 /* connectivity: nbr[ne][Nf], nbr_face[ne][Nf], reflect[ne][Nf] */
 void ora_mesh_conn(const ora_mesh* m, int64_t* nbr, int* nbr_face, int* reflect);
 /* modal L2 projection u_modal = V^T W u_nodal (R18) for the listed elements.
