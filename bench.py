@@ -351,7 +351,10 @@ def run(args):
     stream = torch.cuda.Stream()
     t_setup = time.perf_counter()
     ctx = es.Context(mesh, p, warp=w, interface_flux=fm, rank=rank, world=world, nccl_id=nccl_id,
-                     stream=stream.cuda_stream, device=local, volume_mode=args.volume_mode)
+                     stream=stream.cuda_stream, device=local, volume_mode=args.volume_mode,
+                     metric_storage=args.metric_storage)
+    if args.metric_storage:
+        desc = f"{desc} [modal metric storage: G = V g~ expanded in the flux kernel]"
     if args.volume_mode == 1:
         desc = f"{desc} [ablation: Eq. num_fluxes per-operator fluxes]"
     elif args.volume_mode == 2:
@@ -525,6 +528,8 @@ def main():
     ap.add_argument("--volume-mode", type=int, default=0,
                     help="1: ablation, one flux per operator S^(l) (the paper's Eq. num_fluxes iteration); "
                          "2: ablation, brute force over all node pairs (small configurations only)")
+    ap.add_argument("--metric-storage", type=int, default=0,
+                    help="1: modal (compressed) metric storage, PKD coefficients of G expanded in the flux kernel")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -90,6 +90,16 @@ typedef struct {
                                            default); 1: warp & blend -- Gauss-Lobatto-Legendre points
                                            on the edges, Warburton's blend with alpha = 0 inside
                                            (R32); other values: ES_ERR_CONFIG */
+  int metric_storage;                   /* volume metric terms G_lm read by the flux kernel (P:595:
+                                           "geometric information at each volume and facet
+                                           quadrature node"): 0: nodal values
+                                           (the default); 1: modal -- PKD coefficients V^T W G_lm
+                                           (N_p* instead of N_q doubles per entry, 4.4x fewer bytes at
+                                           p = 8 in 3D), expanded to G = V g~ in the flux kernel's
+                                           prologue; exact up to rounding, the metric terms being
+                                           polynomials of degree <= p (R33).  Applies to
+                                           volume_mode 0 (the ablation kernels read the nodal copy,
+                                           which setup keeps); other values: ES_ERR_CONFIG */
 } es_options;
 
 /* Builds tables, geometry (exact metrics in 2D, conservative curl metrics in 3D, P:345-364;

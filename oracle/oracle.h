@@ -10,7 +10,7 @@
  * paper_2312_07874_b200/ and neither includes the other.
  *
  * Citation format: P:<line> = /root/reference/PAPER.md line, followed by the equation label.
- * Readings of the paper where it is silent/garbled are numbered as in DESIGN.md section 3 (R1..R24).
+ * Readings of the paper where it is silent/garbled are numbered as in DESIGN.md section 3 (R1..R33).
  *
  * All reals are IEEE FP64, compiled with -O2 -ffp-contract=off (no FMA contraction).
  * Layout of modal arrays (same as the product ABI, include/es.h): u[element][variable e][mode k],

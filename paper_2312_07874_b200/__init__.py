@@ -42,7 +42,7 @@ class es_options(ctypes.Structure):
     _fields_ = [("gamma", ctypes.c_double), ("interface_flux", ctypes.c_int), ("rank", ctypes.c_int),
                 ("world", ctypes.c_int), ("nccl_unique_id", ctypes.c_char_p), ("cuda_stream", _vp),
                 ("device", ctypes.c_int), ("check_admissibility", ctypes.c_int), ("volume_mode", ctypes.c_int),
-                ("mapping_nodes", ctypes.c_int)]
+                ("mapping_nodes", ctypes.c_int), ("metric_storage", ctypes.c_int)]
 
 
 def _sig(name, res, *args):
@@ -222,7 +222,8 @@ class Context:
     (e.g. es_inputs.split_cartesian); `warp` a callable [n,d] -> [n,d] (the geometry map)."""
 
     def __init__(self, mesh, p, warp=None, gamma=1.4, interface_flux=1, rank=0, world=1, nccl_id=None,
-                 stream=None, device=0, check_admissibility=0, volume_mode=0, mapping_nodes=0):
+                 stream=None, device=0, check_admissibility=0, volume_mode=0, mapping_nodes=0,
+                 metric_storage=0):
         self.d = int(mesh["d"]) if "d" in mesh else int(np.asarray(mesh["period"]).size)
         self._ev = np.ascontiguousarray(mesh["elem_vertices"], dtype=np.int64)
         self._evx = np.ascontiguousarray(mesh["elem_vertex_coords"], dtype=np.float64)
@@ -244,7 +245,7 @@ class Context:
                     self._per.ctypes.data_as(_dp))
         self._nccl_id = nccl_id
         o = es_options(gamma, interface_flux, rank, world, nccl_id, stream, device, check_admissibility, volume_mode,
-                       mapping_nodes)
+                       mapping_nodes, metric_storage)
         h = _vp()
         rc = es_setup(ctypes.byref(h), ctypes.byref(m), p, self._cb, None, ctypes.byref(o))
         self.h = h

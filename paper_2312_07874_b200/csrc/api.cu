@@ -84,6 +84,8 @@ struct es_context {
   bool external = false;
   int eq56 = 0;   // volume_mode 1: per-operator fluxes (Eq. num_fluxes ablation)
   int dense = 0;  // volume_mode 2: brute force over all node pairs (dense operators)
+  int metric_modal = 0;    // es_options.metric_storage 1: volume metric as PKD coefficients
+  double* gmod = nullptr;  // [nloc][even(NG Np)] PKD coefficients of G_lm (metric_modal)
   double *sdense = nullptr, *rbdense = nullptr;
   int64_t *face_slot = nullptr, *d_interior = nullptr, *d_boundary = nullptr, *d_send = nullptr;
   int* face_reflect = nullptr;
@@ -286,6 +288,7 @@ RhsArgs base_rhs_args(es_context* c) {
   A.rbdense = c->rbdense;
   A.nhat = c->R.nhat;
   A.rbuf = c->rbuf;
+  A.gmod = c->gmod;
   return A;
 }
 
@@ -431,7 +434,7 @@ void es_destroy(es_context* c) {
                   (void*)c->hin, (void*)c->hout, (void*)c->send_buf, (void*)c->dbg,
                   (void*)c->dpy, (void*)c->dppart, (void*)c->sdense, (void*)c->rbdense, (void*)c->rbuf,
                   (void*)c->wjk3, (void*)c->dcounts, (void*)c->xmapv, (void*)c->adv_unod, (void*)c->adv_trace,
-                  (void*)c->adv_X, (void*)c->adv_acc, (void*)c->adv_us, (void*)c->adv_part})
+                  (void*)c->adv_X, (void*)c->adv_acc, (void*)c->adv_us, (void*)c->adv_part, (void*)c->gmod})
     if (p) cudaFree(p);
   for (double* p : c->dpk)
     if (p) cudaFree(p);
@@ -477,6 +480,8 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
   c->external = c->world > 1 && !opt->nccl_unique_id;
   std::string err;
   if (opt->mapping_nodes != 0 && opt->mapping_nodes != 1) return fail(c, ES_ERR_CONFIG, "mapping_nodes must be 0 or 1");
+  if (opt->metric_storage != 0 && opt->metric_storage != 1) return fail(c, ES_ERR_CONFIG, "metric_storage must be 0 or 1");
+  c->metric_modal = opt->metric_storage;
   if (!build_ref_tables(c->d, p, c->T, err, opt->mapping_nodes)) return fail(c, ES_ERR_CONFIG, err);
   c->n = c->T.n;
   c->Nq = c->T.Nq;
@@ -614,6 +619,15 @@ es_status es_setup(es_context** out, const es_mesh* mesh, int p, es_map_fn map, 
     CK(launch_wjinv_permute_3d(c->n, c->geo_vol, even_up((NG + 2) * c->Nq), NG + 1, c->nloc, c->wjk3, c->stream));
     CK(upload_psi_3d(c->n, c->T.psi1.data(), c->T.psi2.data(), c->T.psi3.data()));
     CK(upload_psi_3d_k1(c->n, c->T.psi1.data(), c->T.psi2.data(), c->T.psi3.data()));
+    c->launches++;
+  }
+  if (c->metric_modal) {  // modal metric storage: g~ = V^T W G per element
+    const int gms = even_up(NG * c->Np);
+    CK(cudaMalloc((void**)&c->gmod, (size_t)c->nloc * gms * sizeof(double)));
+    MetricModalArgs mm{d, c->n, c->Nq, c->Np, even_up((NG + 2) * c->Nq), gms, c->nloc, c->geo_vol,
+                       c->R.psi1, c->R.psi2, c->R.psi3, c->R.Wvol, c->R.mode_pr, c->R.pair_a1, c->R.pair_a2,
+                       c->R.pair_off, c->gmod};
+    CK(launch_metric_modal(mm, c->stream));
     c->launches++;
   }
   if (std::getenv("ES_PHASE_TIMING")) {

@@ -263,6 +263,36 @@ cudaError_t launch_geometry(const GeoArgs& g, int64_t ne, cudaStream_t st) {
   geometry_kernel<<<(unsigned)ne, 128, sm, st>>>(g);
   return cudaGetLastError();
 }
+__global__ void __launch_bounds__(256) metric_modal_kernel(MetricModalArgs a) {
+  const int NG = a.dim * a.dim, n = a.n;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.ne * NG * a.Np) return;
+  const int64_t e = t / (NG * a.Np);
+  const int r = (int)(t - e * NG * a.Np), lm = r / a.Np, k = r - lm * a.Np;
+  const int pr = a.mode_pr[k], a1 = a.pair_a1[pr];
+  const int a2 = a.dim == 2 ? k - a.pair_off[pr] : a.pair_a2[pr];
+  const int a3 = a.dim == 3 ? k - a.pair_off[pr] : 0, s = a1 + a2;
+  const double* G = a.geo_vol + (size_t)e * a.gv_stride + (size_t)lm * a.Nq;
+  const int nc = a.dim == 3 ? n : 1;
+  double acc = 0.0;
+  for (int c = 0; c < nc; ++c) {
+    const double p3 = a.dim == 3 ? a.psi3[(s * n + a3) * n + c] : 1.0;
+    for (int b = 0; b < n; ++b) {
+      const double p23 = a.psi2[(a1 * n + a2) * n + b] * p3;
+      for (int q = 0; q < n; ++q) {
+        const int i = q + n * b + n * n * c;  // volume node order: eta1 fastest (R9)
+        acc = fma(a.psi1[a1 * n + q] * p23 * a.Wvol[i], G[i], acc);
+      }
+    }
+  }
+  a.gmod[(size_t)e * a.gm_stride + (size_t)lm * a.Np + k] = acc;
+}
+cudaError_t launch_metric_modal(const MetricModalArgs& a, cudaStream_t st) {
+  const int64_t n = a.ne * a.dim * a.dim * a.Np;
+  if (n <= 0) return cudaSuccess;
+  metric_modal_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
 cudaError_t launch_face_check(const FaceCheckArgs& a, cudaStream_t st) {
   if (a.nloc <= 0) return cudaSuccess;
   face_check_kernel<<<(unsigned)a.nloc, 128, 0, st>>>(a);

@@ -51,6 +51,18 @@ struct EvalPtsArgs {
   double* jac;         // optional [ne][npts]
 };
 cudaError_t launch_eval_points(const EvalPtsArgs& a, cudaStream_t st);
+
+// modal (compressed) metric storage, setup: g~_lm = V^T W G_lm per element
+// (exact: the metric terms have degree <= p, R33); one thread per (element, lm, mode)
+struct MetricModalArgs {
+  int dim, n, Nq, Np, gv_stride, gm_stride;
+  int64_t ne;
+  const double* geo_vol;                   // [ne][gv_stride]: G rows [NG][Nq] first
+  const double *psi1, *psi2, *psi3, *Wvol;  // PKD principal functions [a1][a], [a1][a2][b], [s][a3][c]; weights
+  const int *mode_pr, *pair_a1, *pair_a2, *pair_off;
+  double* gmod;                            // [ne][gm_stride]: [NG][Np] (+ pad)
+};
+cudaError_t launch_metric_modal(const MetricModalArgs& a, cudaStream_t st);
 cudaError_t launch_reduce_parts(const double* part, int64_t ne, int w, double* out, cudaStream_t st);
 
 // explicit Runge-Kutta combinations over the modal state (HBM-bound streams)

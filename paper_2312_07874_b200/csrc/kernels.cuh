@@ -94,6 +94,7 @@ struct RhsArgs {
   const double* nhat;         // [Nf][3] reference outward normals
   double* rbuf;               // 3D: nodal residual [nloc][NC][N(b)][N(a)][N(c)] for the batched K3
   unsigned long long* counts; // counting launch: [nloc][4] volume / facet-correction / issued flux evaluations
+  const double* gmod;         // modal metric storage: [nloc][ev2(NG Np)] PKD coefficients of G (else null)
 };
 
 

@@ -458,11 +458,67 @@ __device__ __forceinline__ void line_coords(int L, int pos, int& ca, int& cb, in
   if constexpr (DIM == 2) cc = 0;
 }
 
+// ---- modal (compressed) metric storage (es_options.metric_storage = 1) ----
+// The element's metric arrives as PKD coefficients g~ [NG][Np] (bulk copy into the head of the G
+// region) and is expanded here to G = V g~ at the volume nodes -- exact, the metric terms being
+// polynomials of degree <= p (R33) -- by the sum-factorised steps of u = V u~:
+//   X[v][pr][c] = sum_a3 psi3[s][a3][c] g~[v][off(pr) + a3]                  items (pr, v), pr-major
+//   G[v][a + N b + N^2 c] = sum_a1 psi1[a1][a] sum_a2 psi2[a1][a2][b] X[v][pr(a1, a2)][c]   items (b, v, c)
+// with the tables from constant memory (this unit's c_psi<N>, uploaded for K1), so the table reads of
+// a warp touch at most a few distinct rows.  X is scratch in the residual / facet-4 regions, both free
+// before the passes.  The caller's barrier completes the second step.
+template <int N>
+__device__ __forceinline__ void metric_expand_3d(double* sG, double* X, int tid, int nt) {
+  constexpr int NG = 9, NPAIR = N * (N + 1) / 2, Np = N * (N + 1) * (N + 2) / 6, Nq = N * N * N;
+  for (int it = tid; it < NPAIR * NG; it += nt) {
+    const int pr = it / NG, v = it - pr * NG;
+    int a1 = 0, base = 0, off = 0;  // pr -> (a1, a2) and the first mode of the pair (a1-major nested, R9)
+    while (pr >= base + (N - a1)) {
+      base += N - a1;
+      off += (N - a1) * (N - a1 + 1) / 2;
+      ++a1;
+    }
+    const int a2 = pr - base, s = a1 + a2, n3 = N - s;
+    off += a2 * (N - a1) - a2 * (a2 - 1) / 2;
+    const double* gm = sG + v * Np + off;
+    double x[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) x[c] = 0.0;
+#pragma unroll
+    for (int a3 = 0; a3 < N; ++a3)
+      if (a3 < n3) {
+        const double gv = gm[a3];
+#pragma unroll
+        for (int c = 0; c < N; ++c) x[c] = fma(c_psi<N>.p3[(s * N + a3) * N + c], gv, x[c]);
+      }
+    double* xo = X + (v * NPAIR + pr) * N;
+#pragma unroll
+    for (int c = 0; c < N; ++c) xo[c] = x[c];
+  }
+  __syncthreads();
+  for (int q = tid; q < N * NG * N; q += nt) {
+    const int b = q / (NG * N), r = q - b * (NG * N), v = r / N, c = r - v * N;
+    double t2[N], y[N];
+#pragma unroll
+    for (int a1 = 0; a1 < N; ++a1) {
+      const int prs = a1 * N - a1 * (a1 - 1) / 2;
+      double t = 0.0;
+#pragma unroll
+      for (int a2 = 0; a2 < N - a1; ++a2) t = fma(c_psi<N>.p2[(a1 * N + a2) * N + b], X[(v * NPAIR + prs + a2) * N + c], t);
+      t2[a1] = t;
+    }
+    psi1_apply_eo<N>(t2, y);
+    double* go = sG + v * Nq + N * b + N * N * c;
+#pragma unroll
+    for (int a = 0; a < N; ++a) go[a] = y[a];
+  }
+}
+
 template <int DIM, int N>
 __device__ __forceinline__ void k2_epilogue_2d(const RhsArgs& A, int64_t e, unsigned it);
 
-// one element of the flux kernel (the body of the persistent loop)
-template <int DIM, int N, bool EQ, bool DN = false, bool CNT = false>
+// one element of the flux kernel (the body of the persistent loop); MM: modal metric storage
+template <int DIM, int N, bool EQ, bool DN = false, bool CNT = false, bool MM = false>
 __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsigned it) {
   using S = Sz<DIM, N>;
   using W = Lw<DIM, N>;
@@ -498,12 +554,15 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
   // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers
   auto issue_A = [&](int64_t e, unsigned buf) {
-    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8,
-                       bW = DIM == 2 ? L::WJN * 8 : 0;
+    constexpr unsigned bP = S::PRS * 8, bG = (MM ? ev2(S::NG * Np) : ev2(S::NG * Nq)) * 8, bF = L::FP * 8,
+                       bJ = L::FJ * 8, bW = DIM == 2 ? L::WJN * 8 : 0;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&k2_barA, bP + bG + bF + bJ + bW);
     bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &k2_barA);
-    bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &k2_barA);
+    if constexpr (MM)  // modal metric storage: the PKD coefficients g~ [NG][Np] (+ pad), expanded below
+      bulk_g2s(sG, A.gmod + (size_t)e * ev2(S::NG * Np), bG, &k2_barA);
+    else
+      bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &k2_barA);
     bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &k2_barA);
     bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &k2_barA);
     if constexpr (DIM == 2) bulk_g2s(smk2 + L::o_wj + buf * ev2(L::WJN), A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barA);
@@ -543,6 +602,15 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   int cv = 0, cf = 0, ci = 0, cI = 0;
   stamp(0);
   mbar_wait(&k2_barA, it & 1);
+  if constexpr (MM) {  // G = V g~ at the volume nodes (scratch: the residual and facet-4 regions)
+    static_assert(S::NG * S::NPAIR * N <= L::o_fp - L::o_r, "metric expansion scratch");
+    if constexpr (DIM == 3) {
+      metric_expand_3d<N>(sG, sR, tid, NT);
+    } else {
+      const PsiS T = psi_tables<DIM, N>(smk2 + L::o_ps);
+      modal_to_nodal<DIM, N, S::NG>(T, sG, sG, sR, nullptr);
+    }
+  }
   // facet beta = rho / p = (rho / (p/2)) / 2 (the volume beta rows and the element's all-Taylor flag
   // come from K1; the state rows hold p / 2)
   for (int fz = tid; fz < NF; fz += NT) {
@@ -1230,7 +1298,7 @@ __device__ __forceinline__ void k2_epilogue_2d(const RhsArgs& A, int64_t e, unsi
   stamp(11);
 }
 
-template <int DIM, int N, bool EQ, bool DN = false, bool CNT = false>
+template <int DIM, int N, bool EQ, bool DN = false, bool CNT = false, bool MM = false>
 __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   using S = Sz<DIM, N>;
   using W = Lw<DIM, N>;
@@ -1266,12 +1334,15 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   auto elem_of = [&](int64_t idx) { return A.elem_list ? A.elem_list[idx] : idx; };
   // bulk copies of one element's data (cp.async.bulk, TMA engine) onto the two mbarriers
   auto issue_A = [&](int64_t e, unsigned buf) {
-    constexpr unsigned bP = S::PRS * 8, bG = ev2(S::NG * Nq) * 8, bF = L::FP * 8, bJ = L::FJ * 8,
-                       bW = DIM == 2 ? L::WJN * 8 : 0;
+    constexpr unsigned bP = S::PRS * 8, bG = (MM ? ev2(S::NG * Np) : ev2(S::NG * Nq)) * 8, bF = L::FP * 8,
+                       bJ = L::FJ * 8, bW = DIM == 2 ? L::WJN * 8 : 0;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&k2_barA, bP + bG + bF + bJ + bW);
     bulk_g2s(sP, A.prim + (size_t)e * S::PRS, bP, &k2_barA);
-    bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &k2_barA);
+    if constexpr (MM)  // modal metric storage: the PKD coefficients g~ [NG][Np] (+ pad), expanded below
+      bulk_g2s(sG, A.gmod + (size_t)e * ev2(S::NG * Np), bG, &k2_barA);
+    else
+      bulk_g2s(sG, A.geo_vol + (size_t)e * S::GVS, bG, &k2_barA);
     bulk_g2s(fP, A.trace + (size_t)e * L::FP, bF, &k2_barA);
     bulk_g2s(fJ, A.geo_face + (size_t)e * L::FJ, bJ, &k2_barA);
     if constexpr (DIM == 2) bulk_g2s(smk2 + L::o_wj + buf * ev2(L::WJN), A.geo_vol + (size_t)e * S::GVS + L::WJ0, bW, &k2_barA);
@@ -1319,7 +1390,7 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   __syncthreads();  // mbarriers initialised and tables staged before anyone uses them
 
 #pragma unroll 1
-  for (int64_t idx = blockIdx.x, it = 0; idx < A.n_elem; idx += gridDim.x, ++it) k2_element<DIM, N, EQ, DN, CNT>(A, idx, (unsigned)it);
+  for (int64_t idx = blockIdx.x, it = 0; idx < A.n_elem; idx += gridDim.x, ++it) k2_element<DIM, N, EQ, DN, CNT, MM>(A, idx, (unsigned)it);
 }
 
 // resident CTAs per SM the register budget is sized for: about 18 warps per SM where shared memory
@@ -1335,6 +1406,11 @@ __host__ __device__ constexpr int k2_min_blocks() {
 template <int DIM, int N>
 __global__ void __launch_bounds__(Lw<DIM, N>::NT, k2_min_blocks<DIM, N>()) rhs2_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
   rhs2_body<DIM, N, false>(R, A);
+}
+// modal metric storage (es_options.metric_storage = 1): the production kernel reading g~ instead of G
+template <int DIM, int N>
+__global__ void __launch_bounds__(Lw<DIM, N>::NT, k2_min_blocks<DIM, N>()) rhs2_mm_kernel(DevRef R, const __grid_constant__ RhsArgs A) {
+  rhs2_body<DIM, N, false, false, false, true>(R, A);
 }
 // counting instantiation (es_count_fluxes): the production kernel with per-element flux counters
 template <int DIM, int N>
