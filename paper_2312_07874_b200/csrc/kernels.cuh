@@ -626,6 +626,8 @@ __host__ __device__ constexpr int k1_min_blocks() {
 
 template <int DIM, int N>
 __global__ void __launch_bounds__(k1_threads<DIM, N>(), k1_min_blocks<DIM, N>()) project_kernel(DevRef R, ProjArgs A) {
+  pdl_wait();
+  PDL_TRIGGER();
   using S = Sz<DIM, N>;
   using L = ProjSmem<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf;

@@ -5,7 +5,27 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <utility>
+
 namespace esb {
+
+// Programmatic dependent launch (PDL): the kernels of one RK stage chain (K1 -> K2 -> K3 -> K1 ...) are
+// launched with cudaLaunchAttributeProgrammaticStreamSerialization (launch_pdl), so a kernel's grid is
+// scheduled while its predecessor drains.  Every such kernel calls pdl_wait() (griddepcontrol.wait:
+// blocks until the predecessor grid has completed and its memory is visible) unconditionally before
+// touching any buffer another kernel writes or reads, and pdl_trigger() (launch_dependents) so that its
+// own successor may be scheduled as soon as all of its CTAs are running.  Both are no-ops for a normal
+// launch.  The chain is transitive: each kernel's completion implies its predecessor's.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#ifndef ES_PDL_TRIGGER  // explicit early trigger (1) or the implicit one at CTA exit (0)
+#define ES_PDL_TRIGGER 0
+#endif
+#define PDL_TRIGGER() \
+  do {                \
+    if (ES_PDL_TRIGGER) pdl_trigger(); \
+  } while (0)
 
 template <int N>
 struct PsiC {
@@ -60,6 +80,24 @@ __device__ __forceinline__ void psi1T_apply_eo(const double* y, double* s2) {  /
     }
     s2[a1] = t;
   }
+}
+
+// host: launch with the PDL attribute (see pdl_wait)
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool off = std::getenv("ES_NO_PDL") != nullptr;  // measurement switch: plain launches
+  cfg.attrs = at;
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace esb

@@ -1300,6 +1300,8 @@ __device__ __forceinline__ void k2_epilogue_2d(const RhsArgs& A, int64_t e, unsi
 
 template <int DIM, int N, bool EQ, bool DN = false, bool CNT = false, bool MM = false>
 __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
+  pdl_wait();
+  PDL_TRIGGER();
   using S = Sz<DIM, N>;
   using W = Lw<DIM, N>;
   using L = Rhs2Smem<DIM, N>;

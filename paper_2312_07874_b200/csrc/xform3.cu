@@ -35,8 +35,7 @@ cudaError_t do_wadj(const WadjArgs& A, cudaStream_t st) {
     attr[dev] = true;
   }
   const int64_t grid = (A.n_elem + Z::E - 1) / Z::E;
-  wadj3_kernel<N><<<(unsigned)grid, Z::NT, Z::SMEM, st>>>(A);
-  return cudaGetLastError();
+  return launch_pdl(wadj3_kernel<N>, dim3((unsigned)grid), dim3(Z::NT), Z::SMEM, st, A);
 }
 
 template <int N>

@@ -240,6 +240,8 @@ __device__ __forceinline__ void pr_by_rank(int rank, int& a1, int& a2) {
 
 template <int N>
 __global__ void __launch_bounds__(X3<N>::NT, X3<N>::MINB) wadj3_kernel(const WadjArgs A) {
+  pdl_wait();
+  PDL_TRIGGER();
   using Z = X3<N>;
   constexpr int NC = Z::NC, NPAIR = Z::NPAIR, Np = Z::Np, E = Z::E, NT = Z::NT, SPE = Z::SPE, UPE = Z::UPE;
   extern __shared__ __align__(16) double smx[];
