@@ -69,3 +69,27 @@ def test_setup_rejects_unknown_interface_flux_without_gpu(es):
         assert rc == es.ES_ERR_CONFIG
         assert b"interface_flux" in es.es_last_error(h)
         es.es_destroy(h)
+
+
+def test_struct_layouts_match_header(es, tmp_path):
+    # the ctypes mirrors of es_mesh / es_options have the field offsets and sizes the C compiler gives
+    # the declarations in include/es.h (an appended or reordered field breaks every caller silently)
+    structs = {"es_mesh": es.es_mesh, "es_options": es.es_options}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "es.h"', "int main(void) {"]
+    for name, py in structs.items():
+        lines.append(f'  printf("{name} size %zu\\n", sizeof({name}));')
+        for f, _ in py._fields_:
+            lines.append(f'  printf("{name} {f} %zu\\n", offsetof({name}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        s, f, v = ln.split()
+        got[(s, f)] = int(v)
+    for name, py in structs.items():
+        assert got[(name, "size")] == ctypes.sizeof(py), name
+        for f, _ in py._fields_:
+            assert got[(name, f)] == getattr(py, f).offset, (name, f)
