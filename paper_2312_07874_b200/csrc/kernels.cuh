@@ -11,6 +11,7 @@
 #include <stdint.h>
 
 #include "psi_const.cuh"
+#include "fastmath.cuh"
 
 namespace esb {
 
@@ -631,6 +632,12 @@ __global__ void __launch_bounds__(k1_threads<DIM, N>(), k1_min_blocks<DIM, N>())
   using S = Sz<DIM, N>;
   using L = ProjSmem<DIM, N>;
   constexpr int NC = S::NC, Nq = S::Nq, Np = S::Np, NF = S::NF, Nqf = S::Nqf;
+#ifndef ES_K1_PB
+#define ES_K1_PB 1
+#endif
+  // nodes per thread and round in the pointwise phases: 2 measured slower than 1 (C5 K1 18.15 vs 17.29 ms:
+  // registers, not latency, limit these phases)
+  constexpr int PB = ES_K1_PB;
   extern __shared__ __align__(16) double sm[];
   double* X = sm + L::o_x;    // [NC][Nq]
   double* T2 = sm + L::o_t2;  // [NC][Nq]
@@ -690,27 +697,60 @@ __global__ void __launch_bounds__(k1_threads<DIM, N>(), k1_min_blocks<DIM, N>())
     else
       modal_to_nodal<DIM, N, NC>(T, uin, X, T2, nullptr);
     stamp(2);
-    for (int i = tid; i < Nq; i += nt) {  // W J~ W(u)   (App. B formulas, R7)
-      double U[NC];
+    // W J~ W(u)   (App. B formulas, R7): PB nodes per thread as independent straight-line streams
+    // (branch-free log, fastmath.cuh)
+    for (int i0 = tid; i0 < Nq; i0 += PB * nt) {
+      double U[PB][NC], ir[PB], pp[PB], lr[PB], lp[PB];
+      int ii[PB];
+      bool nanj[PB] = {};
 #pragma unroll
-      for (int v = 0; v < NC; ++v) U[v] = X[v * Nq + i];
-      double r = U[0], ke = 0.0, vel[DIM];
-      const double ir = 1.0 / r;
+      for (int j = 0; j < PB; ++j) {
+        const int i = i0 + j * nt;
+        ii[j] = i < Nq ? i : i0;  // an absent node recomputes the first one and stores nothing
 #pragma unroll
-      for (int m = 0; m < DIM; ++m) {
-        vel[m] = U[1 + m] * ir;
-        ke += vel[m] * U[1 + m];
+        for (int v = 0; v < NC; ++v) U[j][v] = X[v * Nq + ii[j]];
       }
-      double p = gm1 * (U[DIM + 1] - 0.5 * ke);
-      if (!(r > 0.0) || !(p > 0.0)) bad = 1;
-      double s = log(p) - g * log(r), beta = r / p, v2 = 0.0;
 #pragma unroll
-      for (int m = 0; m < DIM; ++m) v2 += vel[m] * vel[m];
-      const double w = wj[i];
-      X[0 * Nq + i] = w * ((g - s) * gm1inv - 0.5 * beta * v2);
+      for (int j = 0; j < PB; ++j) {
+        if (!(U[j][0] > 0.0 && U[j][0] < 1e300)) {
+          bad = 1;
+          nanj[j] = true;
+          U[j][0] = 1.0;
+        }
+        ir[j] = es_fm_rcp(U[j][0]);
+        double ke = 0.0;
 #pragma unroll
-      for (int m = 0; m < DIM; ++m) X[(1 + m) * Nq + i] = w * beta * vel[m];
-      X[(DIM + 1) * Nq + i] = -w * beta;
+        for (int m = 0; m < DIM; ++m) {
+          const double vm = U[j][1 + m] * ir[j];  // velocity
+          ke += vm * U[j][1 + m];
+          U[j][1 + m] = vm;
+        }
+        pp[j] = gm1 * (U[j][DIM + 1] - 0.5 * ke);
+        if (!(pp[j] > 0.0 && pp[j] < 1e300)) {
+          bad = 1;
+          nanj[j] = true;
+          pp[j] = 1.0;  // keep the branch-free log inside its domain; the result is set to NaN below
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < PB; ++j) lr[j] = es_log_pos(U[j][0]);
+#pragma unroll
+      for (int j = 0; j < PB; ++j) lp[j] = nanj[j] ? __longlong_as_double(0x7ff8000000000000LL) : es_log_pos(pp[j]);
+#pragma unroll
+      for (int j = 0; j < PB; ++j) {
+        const double s = lp[j] - g * lr[j], beta = U[j][0] * es_fm_rcp(pp[j]);
+        double v2 = 0.0;
+#pragma unroll
+        for (int m = 0; m < DIM; ++m) v2 += U[j][1 + m] * U[j][1 + m];
+        if (j == 0 || i0 + j * nt < Nq) {
+          const int i = ii[j];
+          const double w = wj[i];
+          X[0 * Nq + i] = w * ((g - s) * gm1inv - 0.5 * beta * v2);
+#pragma unroll
+          for (int m = 0; m < DIM; ++m) X[(1 + m) * Nq + i] = w * beta * U[j][1 + m];
+          X[(DIM + 1) * Nq + i] = -w * beta;
+        }
+      }
     }
     __syncthreads();
     stamp(3);
@@ -750,11 +790,49 @@ __global__ void __launch_bounds__(k1_threads<DIM, N>(), k1_min_blocks<DIM, N>())
       }
       __syncthreads();
     }
-    for (int it = tid; it < NC * NF; it += nt) {
-      const int v = it / NF, fz = it - v * NF, z = fz / Nqf, f = fz - z * Nqf;
-      const double* x = X + v * Nq;
-      double s = 0.0;
-      if constexpr (DIM == 2) {
+    if constexpr (DIM == 3) {
+      // warp tasks (variable, kind, 32-node part): kind 0 = facet 1 (along eta2), kind 1 = facets 2 and 3
+      // (both along eta1, sharing the line's loads), kind 2 = facet 4 (eta2 contraction of y); the kind
+      // is warp-uniform, so the index arithmetic is a few integer instructions per item
+      constexpr int PARTS = (Nqf + 31) / 32;
+      const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+      for (int task = warp; task < NC * 3 * PARTS; task += nw) {
+        const int v = task / (3 * PARTS), rr = task - v * 3 * PARTS, kind = rr / PARTS, f = (rr - kind * PARTS) * 32 + lane;
+        if (f < Nqf) {
+          const int f1 = f % N, f2 = f / N;
+          double* fw = FW + v * NF + f;
+          if (kind == 0) {
+            const double* x = X + v * Nq + f1 + N * N * f2;
+            double s = 0.0;
+#pragma unroll
+            for (int b = 0; b < N; ++b) s = fma(tlL[b], x[N * b], s);
+            fw[0] = s;
+          } else if (kind == 1) {
+            const double* x = X + v * Nq + N * f1 + N * N * f2;
+            double sR = 0.0, sL = 0.0;
+#pragma unroll
+            for (int a = 0; a < N; ++a) {
+              const double xa = x[a];
+              sR = fma(tlR[a], xa, sR);
+              sL = fma(tlL[a], xa, sL);
+            }
+            fw[Nqf] = sR;
+            fw[2 * Nqf] = sL;
+          } else {
+            const double* y = T2 + v * N * N + f1;
+            const double* l = tli4 + f2 * N;
+            double s = 0.0;
+#pragma unroll
+            for (int b = 0; b < N; ++b) s = fma(l[b], y[N * b], s);
+            fw[3 * Nqf] = s;
+          }
+        }
+      }
+    } else {
+      for (int it = tid; it < NC * NF; it += nt) {
+        const int v = it / NF, fz = it - v * NF, z = fz / Nqf, f = fz - z * Nqf;
+        const double* x = X + v * Nq;
+        double s = 0.0;
         if (z == 0) {
 #pragma unroll
           for (int b = 0; b < N; ++b) s = fma(tlL[b], x[f + N * b], s);
@@ -763,22 +841,8 @@ __global__ void __launch_bounds__(k1_threads<DIM, N>(), k1_min_blocks<DIM, N>())
 #pragma unroll
           for (int a = 0; a < N; ++a) s = fma(l[a], x[a + N * f], s);
         }
-      } else {
-        const int f1 = f % N, f2 = f / N;
-        if (z == 0) {
-#pragma unroll
-          for (int b = 0; b < N; ++b) s = fma(tlL[b], x[f1 + N * b + N * N * f2], s);
-        } else if (z < 3) {
-          const double* l = z == 1 ? tlR : tlL;
-#pragma unroll
-          for (int a = 0; a < N; ++a) s = fma(l[a], x[a + N * f1 + N * N * f2], s);
-        } else {
-          const double* y = T2 + v * N * N + f1;
-#pragma unroll
-          for (int b = 0; b < N; ++b) s = fma(tli4[f2 * N + b], y[N * b], s);
-        }
+        FW[it] = s;
       }
-      FW[it] = s;
     }
     __syncthreads();
     stamp(9);
@@ -786,44 +850,78 @@ __global__ void __launch_bounds__(k1_threads<DIM, N>(), k1_min_blocks<DIM, N>())
     // beta = rho / p = -w_last (App. B); the spread of rho and beta over the element's volume and
     // facet nodes decides the all-Taylor flag ((max - min) < 0.0099 (max + min) for both implies
     // f2 = ((x - y)/(x + y))^2 < 1e-4 for every pair, reading R5)
-    auto Uofw = [&](const double* w, double* out) -> int {
-      const double b = -w[DIM + 1], ib = 1.0 / b;
-      double vel[DIM], v2 = 0.0;
-#pragma unroll
-      for (int m = 0; m < DIM; ++m) {
-        vel[m] = w[1 + m] * ib;
-        v2 += vel[m] * vel[m];
-      }
-      const double s = g - gm1 * (w[0] + 0.5 * b * v2);
-      const double r = exp((s + log(b)) * i1mg);  // (b e^s)^(1/(1-g))
-      out[0] = r;
-#pragma unroll
-      for (int m = 0; m < DIM; ++m) out[1 + m] = vel[m];
-      out[DIM + 1] = 0.5 * (r * ib);  // p / 2: the flux uses half pressures (exact scaling)
-      out[DIM + 2] = b;
-      return (b > 0.0 && r > 0.0) ? 0 : 1;
-    };
     double mm[4] = {1e300, -1e300, 1e300, -1e300};  // rho min, max, beta min, max
-    for (int i = tid; i < Nq + NF; i += nt) {
-      double w[NC], o[NC + 1];
-      if (i < Nq) {
+    // PB nodes per thread as independent straight-line streams (branch-free log / exp, fastmath.cuh)
+    for (int i0 = tid; i0 < Nq + NF; i0 += PB * nt) {
+      double w[PB][NC], b[PB], ib[PB], arg[PB], r[PB];
+      bool nanj[PB] = {};
 #pragma unroll
-        for (int v = 0; v < NC; ++v) w[v] = X[v * Nq + i];
-        bad |= Uofw(w, o);
+      for (int j = 0; j < PB; ++j) {
+        const int i = (j == 0 || i0 + j * nt < Nq + NF) ? i0 + j * nt : i0;  // an absent node repeats the first
+        if (i < Nq) {
 #pragma unroll
-        for (int v = 0; v <= NC; ++v) A.prim[(size_t)e * S::PRS + v * Nq + i] = o[v];
-      } else {
-        const int fz = i - Nq, z = fz / Nqf, f = fz - z * Nqf;
+          for (int v = 0; v < NC; ++v) w[j][v] = X[v * Nq + i];
+        } else {
 #pragma unroll
-        for (int v = 0; v < NC; ++v) w[v] = FW[v * NF + fz];
-        bad |= Uofw(w, o);
-#pragma unroll
-        for (int v = 0; v < NC; ++v) A.trace[(((size_t)e * S::Nf + z) * NC + v) * Nqf + f] = o[v];
+          for (int v = 0; v < NC; ++v) w[j][v] = FW[v * NF + (i - Nq)];
+        }
       }
-      mm[0] = o[0] < mm[0] ? o[0] : mm[0];
-      mm[1] = o[0] > mm[1] ? o[0] : mm[1];
-      mm[2] = o[NC] < mm[2] ? o[NC] : mm[2];
-      mm[3] = o[NC] > mm[3] ? o[NC] : mm[3];
+#pragma unroll
+      for (int j = 0; j < PB; ++j) {
+        b[j] = -w[j][DIM + 1];
+        if (!(b[j] > 0.0 && b[j] < 1e300)) {
+          nanj[j] = true;
+          b[j] = 1.0;
+        }
+        ib[j] = es_fm_rcp(b[j]);
+        double v2 = 0.0;
+#pragma unroll
+        for (int m = 0; m < DIM; ++m) {
+          w[j][1 + m] *= ib[j];  // velocity
+          v2 += w[j][1 + m] * w[j][1 + m];
+        }
+        arg[j] = g - gm1 * (w[j][0] + 0.5 * b[j] * v2);  // s
+      }
+#pragma unroll
+      for (int j = 0; j < PB; ++j) arg[j] = (arg[j] + es_log_pos(b[j])) * i1mg;
+#pragma unroll
+      for (int j = 0; j < PB; ++j) {
+        if (!(fabs(arg[j]) < 600.0)) {
+          nanj[j] = true;
+          arg[j] = 0.0;
+        }
+        r[j] = es_exp(arg[j]);  // (b e^s)^(1/(1-g))
+      }
+#pragma unroll
+      for (int j = 0; j < PB; ++j) {
+        if (nanj[j]) {  // inadmissible projected state: flag it and let NaN propagate (as log / exp would)
+          bad = 1;
+          r[j] = b[j] = ib[j] = __longlong_as_double(0x7ff8000000000000LL);
+        }
+        if (j == 0 || i0 + j * nt < Nq + NF) {
+          const int i = i0 + j * nt;
+          const double ph = 0.5 * (r[j] * ib[j]);  // p / 2: the flux uses half pressures (exact scaling)
+          if (i < Nq) {
+            double* o = A.prim + (size_t)e * S::PRS + i;
+            o[0] = r[j];
+#pragma unroll
+            for (int m = 0; m < DIM; ++m) o[(1 + m) * Nq] = w[j][1 + m];
+            o[(DIM + 1) * Nq] = ph;
+            o[(DIM + 2) * Nq] = b[j];
+          } else {
+            const int fz = i - Nq, z = fz / Nqf, f = fz - z * Nqf;
+            double* o = A.trace + (((size_t)e * S::Nf + z) * NC) * Nqf + f;
+            o[0] = r[j];
+#pragma unroll
+            for (int m = 0; m < DIM; ++m) o[(1 + m) * Nqf] = w[j][1 + m];
+            o[(DIM + 1) * Nqf] = ph;
+          }
+          mm[0] = r[j] < mm[0] ? r[j] : mm[0];
+          mm[1] = r[j] > mm[1] ? r[j] : mm[1];
+          mm[2] = b[j] < mm[2] ? b[j] : mm[2];
+          mm[3] = b[j] > mm[3] ? b[j] : mm[3];
+        }
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
