@@ -572,12 +572,15 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
   // previous element's passes
   auto prefetch_nbr = [&](int64_t e) {
     double* fN = smk2 + L::o_fn;
-    for (int q = tid; q < S::Nf * NC * Nqf; q += NT) {
-      const int z = q / (NC * Nqf), r = q - z * NC * Nqf, v = r / Nqf, f = r - v * Nqf;
+    for (int zf = tid; zf < S::Nf * Nqf; zf += NT) {  // one facet node per item, its NC variables in turn
+      const int z = zf / Nqf, f = zf - z * Nqf;
       const int64_t slot = A.face_slot[e * S::Nf + z];
       const int rf = A.face_reflect[e * S::Nf + z];
       const int fo = DIM == 2 ? (rf ? N - 1 - f : f) : (rf ? (N - 1 - f % N) + N * (f / N) : f);
-      cp_async8(fN + q, A.trace + (size_t)slot * NC * Nqf + v * Nqf + fo);
+      const double* src = A.trace + (size_t)slot * NC * Nqf + fo;
+      double* dst = fN + z * NC * Nqf + f;
+#pragma unroll
+      for (int v = 0; v < NC; ++v) cp_async8(dst + v * Nqf, src + v * Nqf);
     }
     cp_async_commit();
   };
@@ -1172,12 +1175,18 @@ __device__ __forceinline__ void k2_element(const RhsArgs& A, int64_t idx, unsign
     // weight-adjusted inverse K3 reads coalesced, xform3.cuh); K3 applies P:593 and the RK update
     const double* t4 = sU;
     double* rg = A.rbuf + (size_t)e * NC * Nq;
-    for (int q = tid; q < NC * Nq; q += NT) {
-      const int v = q / Nq, rq = q - v * Nq, b = rq / (N * N), a = (rq / N) % N, c = rq % N;
+    for (int rq = tid; rq < Nq; rq += NT) {  // one node per item (index decoded once), its NC variables in turn
+      const int b = rq / (N * N), a = (rq / N) % N, c = rq % N;
       const int i = a + N * b + N * N * c;
-      const double t = tlL[b] * fS[(0 * NC + v) * Nqf + a + N * c] + tlR[a] * fS[(1 * NC + v) * Nqf + b + N * c] +
-                       tlL[a] * fS[(2 * NC + v) * Nqf + b + N * c] + tl3[c] * t4[(v * N + b) * N + a];
-      rg[q] = sR[v * Nq + i] - t;
+      const double lb = tlL[b], ra = tlR[a], la = tlL[a], l3 = tl3[c];
+      const double* f0 = fS + a + N * c;
+      const double* f12 = fS + NC * Nqf + b + N * c;
+      const double* t4p = t4 + b * N + a;
+#pragma unroll
+      for (int v = 0; v < NC; ++v) {
+        const double t = lb * f0[v * Nqf] + ra * f12[v * Nqf] + la * f12[(NC + v) * Nqf] + l3 * t4p[v * N * N];
+        rg[v * Nq + rq] = sR[v * Nq + i] - t;
+      }
     }
     __syncthreads();
     stamp(7);
@@ -1354,12 +1363,15 @@ __device__ __forceinline__ void rhs2_body(DevRef R, const RhsArgs& A) {
   // previous element's passes
   auto prefetch_nbr = [&](int64_t e) {
     double* fN = smk2 + L::o_fn;
-    for (int q = tid; q < S::Nf * NC * Nqf; q += NT) {
-      const int z = q / (NC * Nqf), r = q - z * NC * Nqf, v = r / Nqf, f = r - v * Nqf;
+    for (int zf = tid; zf < S::Nf * Nqf; zf += NT) {  // one facet node per item, its NC variables in turn
+      const int z = zf / Nqf, f = zf - z * Nqf;
       const int64_t slot = A.face_slot[e * S::Nf + z];
       const int rf = A.face_reflect[e * S::Nf + z];
       const int fo = DIM == 2 ? (rf ? N - 1 - f : f) : (rf ? (N - 1 - f % N) + N * (f / N) : f);
-      cp_async8(fN + q, A.trace + (size_t)slot * NC * Nqf + v * Nqf + fo);
+      const double* src = A.trace + (size_t)slot * NC * Nqf + fo;
+      double* dst = fN + z * NC * Nqf + f;
+#pragma unroll
+      for (int v = 0; v < NC; ++v) cp_async8(dst + v * Nqf, src + v * Nqf);
     }
     cp_async_commit();
   };
